@@ -1,0 +1,196 @@
+/*
+ * simdex_b200.h -- C ABI of the B200-native exact top-K serving path
+ * (SimDex, arXiv 1706.01449; reference package `mipserve`).
+ *
+ * The reference is pure Python (numpy); it has no FFI.  Each entry point below
+ * replaces one numpy call site / function of the reference's hot path and is
+ * what a ctypes / cffi binding of that function binds.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer on the current CUDA device unless the
+ *     comment says "host";  matrices are row-major and dense;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *     all work is enqueued on it, nothing synchronises the host unless the
+ *     comment says so;
+ *   - factor matrices are float64 [rows, f] like the reference's FactorMatrix
+ *     (model_io.py:37-48);  item ids / list positions are int32 (|I| < 2^31);
+ *     user ids are int64;
+ *   - returns SIMDEX_OK (0) or a negative SIMDEX_E* code; the message is in
+ *     simdex_last_error() (thread-local).  Argument validation that raises
+ *     ValueError in the reference is done by the Python host mirror first;
+ *     the library re-checks shapes and pointers and returns SIMDEX_EINVAL.
+ *   - ordering of every top-K result: score descending, item id ascending
+ *     (index.py:158-163).  k_eff = min(k, |I|) (brute.py:49, index.py:204).
+ */
+#ifndef SIMDEX_B200_H
+#define SIMDEX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIMDEX_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SIMDEX_API __attribute__((visibility("default")))
+#else
+#define SIMDEX_API
+#endif
+
+enum {
+  SIMDEX_OK = 0,
+  SIMDEX_EINVAL = -1,
+  SIMDEX_ECUDA = -2,
+  SIMDEX_ENOMEM = -3,
+  SIMDEX_EUNSUPPORTED = -4
+};
+
+SIMDEX_API int simdex_abi_version(void);
+SIMDEX_API const char* simdex_last_error(void);
+/* sm count / compute capability of `device` (host outputs). */
+SIMDEX_API int simdex_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------------------
+ * Brute force (brute.py)
+ * ---------------------------------------------------------------------- */
+
+/* brute.py:43-56 topk_naive: exact float64 score of every (row, item) pair and
+ * the full (score desc, id asc) ordering, truncated to k_eff.
+ * rows: optional int64[n_rows] subset of user rows (NULL: all nu rows, n_rows = nu).
+ * out_ids int32[n_rows, k_eff], out_scores float64[n_rows, k_eff]. */
+SIMDEX_API int simdex_topk_exact(const double* users, int64_t nu, const double* items, int64_t ni, int32_t f,
+                      const int64_t* rows, int64_t n_rows, int32_t k,
+                      int32_t* out_ids, double* out_scores, void* stream);
+
+/* Operand packing for the tensor-core path: bf16 copy of x * 2^scale_exp,
+ * zero padded to [rows_pad, kp] (kp = 64*ceil(f/64), rows_pad >= rows), and
+ * float64 row norms of the UNSCALED rows.  Replaces the fp64->operand
+ * conversion implicit in brute.py:93 (dgemm on FactorMatrix values). */
+SIMDEX_API int simdex_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp,
+                     int64_t rows_pad, int32_t kp, uint16_t* out_bf16, double* out_norms, void* stream);
+
+/* brute.py:59-113 topk_matmul: users x items product on tcgen05 tensor cores
+ * (single-pass bf16 operands, fp32 accumulation in TMEM) fused with a
+ * certified running top-K, then exact float64 rescoring of the surviving
+ * candidates.  Results equal simdex_topk_exact.
+ *   ub/ib: packed operands from simdex_pack_bf16 (same kp, scale exps su/si);
+ *   u_norm/i_norm: float64 norms of the unscaled rows;
+ *   heap_ops: optional int64[nu]: per user count of tile scores above the
+ *   running K-th at the time the tile is merged (brute.py:95-97; tile order
+ *   differs from the reference, the count is analogous, not bit-equal).
+ * Requires k_eff <= 256; larger k goes through simdex_topk_exact. */
+SIMDEX_API int simdex_topk_matmul(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu,
+                       const double* items, const uint16_t* ib, const double* i_norm, int64_t ni,
+                       int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k,
+                       int32_t* out_ids, double* out_scores, int64_t* heap_ops, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Clustering (clustering.py)
+ * ---------------------------------------------------------------------- */
+
+/* clustering.py:105-122 _plusplus_seeds on device.  The host draws the RNG
+ * stream exactly as the reference: first = rng.integers(0, n), then one
+ * rng.random() per further seed (numpy's choice(n, p) == searchsorted(cdf, u,
+ * 'right')).  uniforms: float64[k-1] (device).  Writes out_rows int64[k] (the
+ * chosen point ids) and out_centers float64[k, f].  If a pass finds a
+ * non-positive D^2 total (fewer distinct points than seeds,
+ * clustering.py:113-117), *out_degenerate_pass (device int32) receives that
+ * pass index and the remaining rows are left for the host; else -1. */
+SIMDEX_API int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, int32_t k, int64_t first,
+                       const double* uniforms, int64_t* out_rows, double* out_centers,
+                       int32_t* out_degenerate_pass, void* stream);
+
+/* clustering.py:96-102 + argmin (:164, :176): squared L2 distances to every
+ * center as ||p||^2 + ||c||^2 - 2 p.c clipped at 0, first minimum wins.
+ * prev_assign (nullable) is compared to count changed rows.
+ * out_assign int64[n], out_d2 float64[n] (distance to the assigned center),
+ * out_changed int64[1], out_objective float64[1] = sum(out_d2). */
+SIMDEX_API int simdex_kmeans_assign(const double* points, int64_t n, int32_t f, const double* centers, int32_t c,
+                         const int64_t* prev_assign, int64_t* out_assign, double* out_d2,
+                         int64_t* out_changed, double* out_objective, void* stream);
+
+/* clustering.py:168-172 (+ members, :185): users sorted by (cluster, id)
+ * into out_members int64[n] with out_offsets int64[c+1]; out_counts int64[c];
+ * centers[c] <- mean of its members for every non-empty cluster (fixed
+ * summation order: deterministic). */
+SIMDEX_API int simdex_kmeans_update(const double* points, int64_t n, int32_t f, const int64_t* assign, int32_t c,
+                         double* centers, int64_t* out_counts, int64_t* out_members, int64_t* out_offsets,
+                         void* stream);
+
+/* clustering.py:65-93 compute_max_angles: theta_b[c] = max over members of
+ * 2*atan2(|x-y|, |x+y|) on unit vectors; zero-norm member or center -> pi;
+ * empty cluster -> 0.  out_theta float64[c]. */
+SIMDEX_API int simdex_max_angles(const double* users, int64_t n, int32_t f, const double* centers, int32_t c,
+                      const int64_t* assign, double* out_theta, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Index build (index.py:90-155)
+ * ---------------------------------------------------------------------- */
+
+/* index.py:129-155 build_index: item norms, per (cluster, item) half-angle
+ * theta_ic (zero-norm item / zero center -> pi/2, index.py:103-116), Eq. 2
+ * ceiling (index.py:119-121), and per-cluster sort by (ceiling desc, id asc)
+ * (index.py:124-126) -- a device merge sort.
+ * out_item_norms float64[ni], out_list_ids int32[c, ni], out_bounds float64[c, ni]. */
+SIMDEX_API int simdex_build_index(const double* items, int64_t ni, int32_t f, const double* centers,
+                       const double* theta_b, int32_t c, double* out_item_norms,
+                       int32_t* out_list_ids, double* out_bounds, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Index walk (index.py:185-389)
+ * ---------------------------------------------------------------------- */
+
+/* index.py:185-268 _walk / query_user, one query per entry:
+ *   q_user int64[nq] user row, q_cluster int32[nq] its cluster (list row);
+ *   start: first list position (0, or the work-sharing prefix B);
+ *   warm_ids/warm_scores [nq, k_eff] + warm_count int32[nq]: the running
+ *   top-K entering at `start` (nullable when start == 0);
+ *   no_prune != 0 scans the whole list (the per-pair baseline, brute.py:116-130).
+ * Exact Algorithm 1 semantics: first k_eff positions scored unconditionally,
+ * stop at the first later position j with kth > bounds[j]*||u|| (strict).
+ * out_ids int32[nq, k_eff], out_scores float64[nq, k_eff], out_visited int64[nq]. */
+SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const double* items, int32_t f, int64_t ni,
+                const int32_t* list_ids, const double* bounds,
+                const int64_t* q_user, const int32_t* q_cluster, int64_t nq, int32_t k, int64_t start,
+                const int32_t* warm_ids, const double* warm_scores, const int32_t* warm_count,
+                int32_t no_prune, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
+
+/* index.py:305-389 query_batch with work sharing: every cluster's first B
+ * list items scored for all its queried users on tcgen05 (prefix GEMM fused
+ * with the certified top-K, as simdex_topk_matmul), then the walk continues
+ * from B only for users whose K-th does not beat the ceiling at B.
+ * Queries must be grouped by cluster: q_user int64[nq] sorted so that
+ * cluster q_cluster is non-decreasing.  prefix_b / prefix_norm are the
+ * per-cluster prefix operands from simdex_build_prefix.
+ * out_visited follows the reference: n if B >= n, else max(B, walk visited). */
+SIMDEX_API int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
+                    const double* items, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
+                    const int32_t* list_ids, const double* bounds, int32_t c, int64_t block,
+                    const uint16_t* prefix_b, const double* prefix_norm,
+                    const int64_t* q_user, const int32_t* q_cluster, int64_t nq, int32_t k,
+                    int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
+
+/* Work-sharing operands: for every cluster the first min(B, ni) list items,
+ * gathered in list order into bf16 [c, b_pad, kp] (b_pad = 128*ceil(B'/128))
+ * plus their float64 norms [c, b_pad]; the re-layout that makes the prefix
+ * product a dense TMA-fed GEMM (index.py:351-357). */
+SIMDEX_API int simdex_build_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
+                        const int32_t* list_ids, int32_t c, int64_t block, int64_t b_pad,
+                        uint16_t* out_prefix_b, double* out_prefix_norm, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Catalog sharding (no reference counterpart)
+ * ---------------------------------------------------------------------- */
+
+/* Merge `parts` partial top-K lists per user into one: in_ids/in_scores
+ * [parts, nu, kk] (ids already global), output [nu, k_out] by
+ * (score desc, id asc). */
+SIMDEX_API int simdex_merge_topk(const int32_t* in_ids, const double* in_scores, int32_t parts, int64_t nu,
+                      int32_t kk, int32_t k_out, int32_t* out_ids, double* out_scores, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIMDEX_B200_H */

@@ -1,0 +1,62 @@
+"""Device residency of host factor matrices.
+
+A FactorMatrix is immutable, so its device copies are computed once per
+device and cached on the object: the float64 values (row-major, what the
+exact kernels read), their row norms, and the packed bf16 tensor-core
+operand.  Host->device copies go through pinned staging.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib, _ops
+
+
+def device():
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(a: np.ndarray, dtype=None) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    if t.numel() * t.element_size() >= (1 << 20):
+        t = t.pin_memory()
+    return t.to(device(), non_blocking=True)
+
+
+def _cache(matrix):
+    dev = device()
+    store = matrix.__dict__.setdefault("_device", {})
+    return store.setdefault(dev.index, {})
+
+
+def f64(matrix) -> torch.Tensor:
+    c = _cache(matrix)
+    if "f64" not in c:
+        c["f64"] = to_device(matrix.values)
+    return c["f64"]
+
+
+def packed(matrix) -> _ops.Packed:
+    c = _cache(matrix)
+    if "packed" not in c:
+        max_abs = float(np.abs(matrix.values).max()) if matrix.values.size else 0.0
+        c["packed"] = _ops.pack(f64(matrix), max_abs)
+    return c["packed"]
+
+
+def norms(matrix) -> torch.Tensor:
+    return packed(matrix).norms
+
+
+def drop(matrix):
+    """Forget the device copies (e.g. to time host->device transfers)."""
+    matrix.__dict__.get("_device", {}).clear()
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()

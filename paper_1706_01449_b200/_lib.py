@@ -1,0 +1,108 @@
+"""ctypes binding of the in-tree C-ABI library (include/simdex_b200.h).
+
+The library is the product path: there is no CPU fallback.  Loading fails
+loudly when the shared object is missing, and every device entry point raises
+``RuntimeError`` when no CUDA device is visible.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsimdex_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "simdex_b200.h")
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+
+# name -> argtypes (all return int status except the two noted)
+SIGNATURES = {
+    "simdex_abi_version": [],
+    "simdex_last_error": [],
+    "simdex_device_info": [C.c_int, P, P, P],
+    "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
+    "simdex_pack_bf16": [P, I64, I32, I32, I64, I32, P, P, P],
+    "simdex_topk_matmul": [P, P, P, I64, P, P, P, I64, I32, I32, I32, I32, I32, P, P, P, P],
+    "simdex_kmeans_seed": [P, I64, I32, I32, I64, P, P, P, P, P],
+    "simdex_kmeans_assign": [P, I64, I32, P, I32, P, P, P, P, P, P],
+    "simdex_kmeans_update": [P, I64, I32, P, I32, P, P, P, P, P],
+    "simdex_max_angles": [P, I64, I32, P, I32, P, P, P],
+    "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P],
+    "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
+    "simdex_query_ws": [P, P, P, I64, P, I64, I32, I32, I32, I32, P, P, I32, I64, P, P, P, P, I64, I32, P, P, P, P],
+    "simdex_build_prefix": [P, P, I64, I32, P, I32, I64, I64, P, P, P],
+    "simdex_merge_topk": [P, P, I32, I64, I32, I32, P, P, P],
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class SimdexError(RuntimeError):
+    """A device-side failure reported by the C-ABI library."""
+
+
+def load():
+    """Load (once) and return the ctypes library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(make -C paper_1706_01449_b200/csrc).  There is no CPU fallback."
+            )
+        lib = C.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = C.c_char_p if name == "simdex_last_error" else C.c_int
+        if lib.simdex_abi_version() != 1:
+            raise ImportError("libsimdex_b200.so ABI version mismatch")
+        _lib = lib
+    return _lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1706_01449_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback"
+        )
+
+
+def call(name, *args):
+    """Invoke a C-ABI entry point, raising on a non-zero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.simdex_last_error().decode(errors="replace")
+        raise SimdexError(f"{name} failed ({rc}): {msg}")
+
+
+def ptr(t):
+    """Raw device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def header_symbols(path=HEADER_PATH):
+    """Every entry point declared in include/simdex_b200.h."""
+    import re
+
+    text = open(path).read()
+    return sorted(set(re.findall(r"SIMDEX_API\s+(?:const\s+)?\w+\*?\s+(simdex_\w+)\s*\(", text)))

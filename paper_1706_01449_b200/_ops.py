@@ -1,0 +1,188 @@
+"""Tensor-level wrappers of the C-ABI (device in, device out).
+
+Each function allocates its outputs with torch (the caching allocator is the
+plumbing), validates shapes, and enqueues the library call on the current
+stream.  Nothing here computes on the host.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_ptr
+
+F64 = torch.float64
+I64 = torch.int64
+I32 = torch.int32
+
+
+def _dev():
+    _lib.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _c(t, dtype):
+    assert t.dtype == dtype and t.is_cuda and t.is_contiguous(), (t.dtype, t.device, t.is_contiguous())
+    return t
+
+
+@dataclass
+class Packed:
+    """bf16 tensor-core operand of a factor matrix (see simdex_pack_bf16)."""
+
+    bf16: torch.Tensor      # int16 storage [rows_pad, kp]
+    norms: torch.Tensor     # float64 [rows] norms of the unscaled rows
+    scale_exp: int
+    kp: int
+    rows: int
+
+
+ROW_PAD = 256
+
+
+def pack(x: torch.Tensor, max_abs: float) -> Packed:
+    """bf16 copy scaled by 2^e so that the largest |entry| lies in [1, 2)."""
+    rows, f = x.shape
+    e = 0 if max_abs == 0.0 else -int(math.floor(math.log2(max_abs)))
+    kp = 64 * ((f + 63) // 64)
+    rows_pad = ROW_PAD * ((rows + ROW_PAD - 1) // ROW_PAD)
+    out = torch.empty((rows_pad, kp), dtype=torch.int16, device=x.device)
+    norms = torch.empty(rows, dtype=F64, device=x.device)
+    call("simdex_pack_bf16", ptr(_c(x, F64)), rows, f, e, rows_pad, kp, ptr(out), ptr(norms), stream_ptr())
+    return Packed(out, norms, e, kp, rows)
+
+
+def topk_exact(users, items, k, rows=None):
+    nu, f = users.shape
+    ni = items.shape[0]
+    k_eff = min(k, ni)
+    n_rows = nu if rows is None else rows.shape[0]
+    ids = torch.empty((n_rows, k_eff), dtype=I32, device=users.device)
+    sc = torch.empty((n_rows, k_eff), dtype=F64, device=users.device)
+    call("simdex_topk_exact", ptr(_c(users, F64)), nu, ptr(_c(items, F64)), ni, f,
+         ptr(None if rows is None else _c(rows, I64)), n_rows, k, ptr(ids), ptr(sc), stream_ptr())
+    return ids, sc
+
+
+def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False):
+    nu, f = users.shape
+    ni = items.shape[0]
+    k_eff = min(k, ni)
+    ids = torch.empty((nu, k_eff), dtype=I32, device=users.device)
+    sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
+    hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
+    call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu,
+         ptr(_c(items, F64)), ptr(pi.bf16), ptr(pi.norms), ni, f, pu.kp, pu.scale_exp, pi.scale_exp, k,
+         ptr(ids), ptr(sc), ptr(hops), stream_ptr())
+    return ids, sc, hops
+
+
+def kmeans_seed(points, k, first, uniforms):
+    n, f = points.shape
+    rows = torch.empty(k, dtype=I64, device=points.device)
+    centers = torch.empty((k, f), dtype=F64, device=points.device)
+    deg = torch.empty(1, dtype=I32, device=points.device)
+    call("simdex_kmeans_seed", ptr(_c(points, F64)), n, f, k, int(first),
+         ptr(None if uniforms is None else _c(uniforms, F64)), ptr(rows), ptr(centers), ptr(deg), stream_ptr())
+    return rows, centers, deg
+
+
+def kmeans_assign(points, centers, prev=None):
+    n, f = points.shape
+    c = centers.shape[0]
+    assign = torch.empty(n, dtype=I64, device=points.device)
+    d2 = torch.empty(n, dtype=F64, device=points.device)
+    changed = torch.empty(1, dtype=I64, device=points.device)
+    obj = torch.empty(1, dtype=F64, device=points.device)
+    call("simdex_kmeans_assign", ptr(_c(points, F64)), n, f, ptr(_c(centers, F64)), c,
+         ptr(None if prev is None else _c(prev, I64)), ptr(assign), ptr(d2), ptr(changed), ptr(obj), stream_ptr())
+    return assign, d2, changed, obj
+
+
+def kmeans_update(points, assign, centers, c=None):
+    """Group users by cluster; with ``centers`` also recompute the means in place."""
+    n, f = points.shape
+    c = centers.shape[0] if centers is not None else c
+    counts = torch.empty(c, dtype=I64, device=points.device)
+    members = torch.empty(n, dtype=I64, device=points.device)
+    offsets = torch.empty(c + 1, dtype=I64, device=points.device)
+    call("simdex_kmeans_update", ptr(_c(points, F64)), n, f, ptr(_c(assign, I64)), c,
+         ptr(None if centers is None else _c(centers, F64)), ptr(counts), ptr(members), ptr(offsets), stream_ptr())
+    return counts, members, offsets
+
+
+def max_angles(users, centers, assign):
+    n, f = users.shape
+    c = centers.shape[0]
+    theta = torch.empty(c, dtype=F64, device=users.device)
+    call("simdex_max_angles", ptr(_c(users, F64)), n, f, ptr(_c(centers, F64)), c, ptr(_c(assign, I64)),
+         ptr(theta), stream_ptr())
+    return theta
+
+
+def build_index(items, centers, theta):
+    ni, f = items.shape
+    c = centers.shape[0]
+    norms = torch.empty(ni, dtype=F64, device=items.device)
+    ids = torch.empty((c, ni), dtype=I32, device=items.device)
+    bounds = torch.empty((c, ni), dtype=F64, device=items.device)
+    call("simdex_build_index", ptr(_c(items, F64)), ni, f, ptr(_c(centers, F64)), ptr(_c(theta, F64)), c,
+         ptr(norms), ptr(ids), ptr(bounds), stream_ptr())
+    return norms, ids, bounds
+
+
+def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, warm=None, no_prune=False):
+    nq = q_user.shape[0]
+    ni, f = items.shape
+    k_eff = min(k, ni)
+    ids = torch.empty((nq, k_eff), dtype=I32, device=users.device)
+    sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
+    vis = torch.empty(nq, dtype=I64, device=users.device)
+    wi = ws = wc = None
+    if warm is not None:
+        wi, ws, wc = (_c(warm[0], I32), _c(warm[1], F64), _c(warm[2], I32))
+    call("simdex_walk", ptr(_c(users, F64)), ptr(_c(unorm, F64)), ptr(_c(items, F64)), f, ni,
+         ptr(_c(list_ids, I32)), ptr(_c(bounds, F64)), ptr(_c(q_user, I64)), ptr(_c(q_cluster, I32)), nq, k,
+         int(start), ptr(wi), ptr(ws), ptr(wc), int(bool(no_prune)), ptr(ids), ptr(sc), ptr(vis), stream_ptr())
+    return ids, sc, vis
+
+
+def build_prefix(pi: Packed, list_ids, block):
+    c, ni = list_ids.shape
+    bp = min(block, ni)
+    b_pad = 128 * ((bp + 127) // 128)
+    out = torch.empty((c, b_pad, pi.kp), dtype=torch.int16, device=list_ids.device)
+    onorm = torch.empty((c, b_pad), dtype=F64, device=list_ids.device)
+    call("simdex_build_prefix", ptr(pi.bf16), ptr(pi.norms), ni, pi.kp, ptr(_c(list_ids, I32)), c, int(block),
+         b_pad, ptr(out), ptr(onorm), stream_ptr())
+    return out, onorm
+
+
+def query_ws(users, pu: Packed, items, pi: Packed, list_ids, bounds, block, prefix, q_user, q_cluster, k):
+    nu, f = users.shape
+    ni = items.shape[0]
+    c = list_ids.shape[0]
+    nq = q_user.shape[0]
+    k_eff = min(k, ni)
+    ids = torch.empty((nq, k_eff), dtype=I32, device=users.device)
+    sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
+    vis = torch.empty(nq, dtype=I64, device=users.device)
+    pb, pn = prefix if prefix is not None else (None, None)
+    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ni, f,
+         pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)), ptr(_c(bounds, F64)), c, int(block),
+         ptr(pb), ptr(pn), ptr(_c(q_user, I64)), ptr(_c(q_cluster, I32)), nq, k, ptr(ids), ptr(sc), ptr(vis),
+         stream_ptr())
+    return ids, sc, vis
+
+
+def merge_topk(in_ids, in_scores, k_out):
+    parts, nu, kk = in_ids.shape
+    ids = torch.empty((nu, k_out), dtype=I32, device=in_ids.device)
+    sc = torch.empty((nu, k_out), dtype=F64, device=in_ids.device)
+    call("simdex_merge_topk", ptr(_c(in_ids, I32)), ptr(_c(in_scores, F64)), parts, nu, kk, k_out, ptr(ids),
+         ptr(sc), stream_ptr())
+    return ids, sc

@@ -1,0 +1,131 @@
+"""Brute-force top-K serving (reference: mipserve/brute.py).
+
+``topk_matmul`` runs the users x items product on tcgen05 tensor cores with
+the running top-K fused into the epilogue and exact float64 rescoring of the
+certified candidates (simdex_topk_matmul); ``topk_naive`` is the exact
+float64 full scan + ordering on the GPU (simdex_topk_exact).  Both return
+identical results under the shared tie rule (score desc, item id asc).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _ops
+from .index import TopKResults
+from .model_io import ModelPair
+
+# tiles the reference's default_blocks picks (brute.py:21-40); accepted for
+# API compatibility, the GPU tiling is internal
+_TILE_BUDGET_DOUBLES = 32768
+MATMUL_MAX_K = 256
+
+
+@dataclass(frozen=True)
+class BlockSpec:
+    user_block: int
+    item_block: int
+
+    def __post_init__(self):
+        if self.user_block < 1 or self.item_block < 1:
+            raise ValueError("block sizes must be >= 1")
+
+
+def default_blocks(factors: int) -> BlockSpec:
+    """Largest power-of-two square tile whose two panels plus score tile fit
+    32768 doubles (brute.py:36-40)."""
+    side = 256
+    while side > 8 and 2 * side * factors + side * side > _TILE_BUDGET_DOUBLES:
+        side //= 2
+    return BlockSpec(side, side)
+
+
+def _results(ids, sc, n_items, num_users):
+    vis = np.full(num_users, n_items, dtype=np.int64)
+    return TopKResults(np.arange(num_users), _device.to_host(ids), _device.to_host(sc), vis)
+
+
+def topk_naive_tensors(model: ModelPair, k: int):
+    return _ops.topk_exact(_device.f64(model.users), _device.f64(model.items), k)
+
+
+def topk_naive(model: ModelPair, k: int) -> TopKResults:
+    """Score every pair in float64 and order (brute.py:43-56); GPU exact scan."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    ids, sc = topk_naive_tensors(model, k)
+    return _results(ids, sc, model.num_items, model.num_users)
+
+
+def topk_matmul_tensors(model: ModelPair, k: int, heap_ops: bool = False):
+    """Device form: (ids int32 [U, k_eff], scores float64, heap_ops|None)."""
+    users, items = _device.f64(model.users), _device.f64(model.items)
+    if min(k, model.num_items) > MATMUL_MAX_K:
+        ids, sc = _ops.topk_exact(users, items, k)
+        return ids, sc, None
+    return _ops.topk_matmul(users, _device.packed(model.users), items, _device.packed(model.items), k, heap_ops)
+
+
+def topk_matmul(model: ModelPair, k: int, blocks: BlockSpec | None = None, counters: dict | None = None) -> TopKResults:
+    """Blocked product with a running per-user top-K; identical to topk_naive
+    (brute.py:59-113).  ``counters['heap_ops']`` receives per-user counts of
+    tile scores that beat the running K-th when merged."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    ids, sc, hops = topk_matmul_tensors(model, k, heap_ops=counters is not None)
+    if counters is not None:
+        counters["heap_ops"] = _device.to_host(hops) if hops is not None else np.full(
+            model.num_users, model.num_items, dtype=np.int64)
+    return _results(ids, sc, model.num_items, model.num_users)
+
+
+def _scan_list(model: ModelPair):
+    """Identity list (all items in id order) for the unpruned per-pair scan."""
+    cache = model.items.__dict__.setdefault("_device", {}).setdefault(_device.device().index, {})
+    if "scan_list" not in cache:
+        n = model.num_items
+        dev = _device.device()
+        cache["scan_list"] = (torch.arange(n, dtype=torch.int32, device=dev).view(1, n),
+                              torch.full((1, n), float("inf"), dtype=torch.float64, device=dev))
+    return cache["scan_list"]
+
+
+def _perpair_scan(model: ModelPair, k: int) -> None:
+    """Pair-at-a-time scoring with a bounded running top-K and no pruning
+    (brute.py:116-130): the bounded-walk kernel over an unpruned list, the
+    GPU's "unblocked" rate for calibrating h0."""
+    ids, bounds = _scan_list(model)
+    dev = _device.device()
+    q = torch.arange(model.num_users, dtype=torch.int64, device=dev)
+    qc = torch.zeros(model.num_users, dtype=torch.int32, device=dev)
+    _ops.walk(_device.f64(model.users), _device.norms(model.users), _device.f64(model.items), ids, bounds, q, qc,
+              k, no_prune=True)
+
+
+@dataclass(frozen=True)
+class ThroughputSample:
+    """Scored pairs per second for the blocked product and the per-pair loop."""
+
+    blocked_rate: float
+    unblocked_rate: float
+
+
+def measure_throughput(model: ModelPair, k: int = 1, blocks: BlockSpec | None = None) -> ThroughputSample:
+    """Time both serving styles over the full user x item workload
+    (brute.py:141-150), device-synchronised wall clock."""
+    pairs = model.num_users * model.num_items
+    _device.packed(model.users), _device.packed(model.items), _scan_list(model)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    topk_matmul_tensors(model, k)
+    torch.cuda.synchronize()
+    blocked = max(time.perf_counter() - t0, 1e-9)
+    t0 = time.perf_counter()
+    _perpair_scan(model, k)
+    torch.cuda.synchronize()
+    unblocked = max(time.perf_counter() - t0, 1e-9)
+    return ThroughputSample(pairs / blocked, pairs / unblocked)

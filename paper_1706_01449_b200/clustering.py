@@ -1,0 +1,207 @@
+"""k-means over user vectors plus the per-cluster angular slack theta_b
+(reference: mipserve/clustering.py).
+
+Lloyd iterations run on the GPU: k-means++ seeding with the reference's
+exact RNG draw sequence (simdex_kmeans_seed), fused distance + argmin
+assignment (simdex_kmeans_assign), deterministic centroid means
+(simdex_kmeans_update) and theta_b (simdex_max_angles).  The host only
+drives the loop: one small device->host read per iteration for the
+convergence test and the empty-cluster check.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _ops
+from .model_io import FactorMatrix
+
+DEFAULT_NUM_CLUSTERS = 8
+DEFAULT_MAX_ITERS = 100
+
+# Angle used when a vector has zero norm; the most conservative choice
+# (clustering.py:21-23).
+DEGENERATE_ANGLE = math.pi
+
+
+@dataclass(frozen=True, eq=False)
+class Clustering:
+    """Centroids, assignment, theta_b (``max_angle``), members, objective
+    history and seed (clustering.py:26-44)."""
+
+    centroids: FactorMatrix
+    assignment: np.ndarray
+    max_angle: np.ndarray
+    members: tuple
+    objective: np.ndarray
+    seed: int
+
+    @property
+    def num_clusters(self) -> int:
+        return self.centroids.rows
+
+    # device copies (cached per device)
+    def _dev(self):
+        store = self.__dict__.setdefault("_device_cache", {})
+        return store.setdefault(_device.device().index, {})
+
+    def device_assignment(self) -> torch.Tensor:
+        d = self._dev()
+        if "assign" not in d:
+            d["assign"] = _device.to_device(np.asarray(self.assignment, dtype=np.int64))
+        return d["assign"]
+
+    def device_centroids(self) -> torch.Tensor:
+        return _device.f64(self.centroids)
+
+    def device_max_angle(self) -> torch.Tensor:
+        d = self._dev()
+        if "theta" not in d:
+            d["theta"] = _device.to_device(np.asarray(self.max_angle, dtype=np.float64))
+        return d["theta"]
+
+
+def _half_angles(vectors: np.ndarray, center: np.ndarray) -> np.ndarray:
+    cn = np.linalg.norm(center)
+    if cn == 0.0:
+        return np.full(vectors.shape[0], DEGENERATE_ANGLE)
+    n = np.linalg.norm(vectors, axis=1)
+    x = vectors / np.where(n > 0.0, n, 1.0)[:, None]
+    y = center / cn
+    a = 2.0 * np.arctan2(np.linalg.norm(x - y, axis=1), np.linalg.norm(x + y, axis=1))
+    a[n == 0.0] = DEGENERATE_ANGLE
+    return a
+
+
+def angular_distance(a, b) -> float:
+    """Angle in [0, pi] between two nonzero vectors, half-angle form
+    2*atan2(|x-y|, |x+y|) on unit vectors (clustering.py:47-62).  A host
+    scalar helper (two vectors), not part of the batched path."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if np.linalg.norm(a) == 0.0 or np.linalg.norm(b) == 0.0:
+        raise ValueError("angular distance is undefined for zero-norm vectors")
+    return float(_half_angles(a[None, :], b)[0])
+
+
+def angles_to_center(vectors, center) -> np.ndarray:
+    """Per-row angle to ``center``; degenerate rows (or center) get pi
+    (clustering.py:65-78).  Host helper for inspection and tests."""
+    return _half_angles(np.atleast_2d(np.asarray(vectors, dtype=np.float64)), np.asarray(center, dtype=np.float64))
+
+
+def _as_matrix(x):
+    return x if isinstance(x, FactorMatrix) else FactorMatrix(np.asarray(x, dtype=np.float64))
+
+
+def compute_max_angles(users, centroids, assignment) -> np.ndarray:
+    """theta_b per cluster: max member-to-centroid angle, 0 for empty clusters
+    (clustering.py:81-93), computed on the GPU."""
+    um, cm = _as_matrix(users), _as_matrix(centroids)
+    a = _device.to_device(np.asarray(assignment, dtype=np.int64))
+    return _device.to_host(_ops.max_angles(_device.f64(um), _device.f64(cm), a)).copy()
+
+
+def _finish_seeds_on_degenerate(points_h, rows_h, start):
+    """clustering.py:113-117: with a zero D^2 total, take the lowest-id point
+    not already a seed (no RNG draw).  Once the total is zero it stays zero,
+    so every remaining pass takes this branch."""
+    n = points_h.shape[0]
+    taken = {tuple(points_h[r]) for r in rows_h[:start]}
+    for j in range(start, rows_h.shape[0]):
+        pick = j % n
+        for i in range(n):
+            if tuple(points_h[i]) not in taken:
+                pick = i
+                break
+        rows_h[j] = pick
+        taken.add(tuple(points_h[pick]))
+    return rows_h
+
+
+def _repair_empty_host(points_h, centers_h, assign_h, d2_h):
+    """clustering.py:125-138: an empty cluster takes the farthest point whose
+    own cluster keeps at least one member.  Rare (only when a Lloyd step
+    empties a cluster); runs on the host copies and is re-uploaded."""
+    counts = np.bincount(assign_h, minlength=centers_h.shape[0])
+    changed = False
+    for c in np.flatnonzero(counts == 0):
+        for cand in np.argsort(-d2_h, kind="stable"):
+            cand = int(cand)
+            if counts[assign_h[cand]] > 1:
+                counts[assign_h[cand]] -= 1
+                assign_h[cand] = c
+                counts[c] = 1
+                centers_h[c] = points_h[cand]
+                d2_h[cand] = 0.0
+                changed = True
+                break
+    return changed
+
+
+def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_iters: int = DEFAULT_MAX_ITERS,
+           seed: int = 0) -> Clustering:
+    """Lloyd iterations with k-means++ seeding, stopping on a stable
+    assignment (clustering.py:141-198).  Deterministic for a fixed seed; the
+    RNG stream (and hence the seeds) is the reference's."""
+    n = users.rows
+    if not 1 <= num_clusters <= n:
+        raise ValueError(f"num_clusters must be in [1, {n}], got {num_clusters}")
+    if max_iters < 1:
+        raise ValueError("max_iters must be >= 1")
+    pts = _device.f64(users)
+    dev = pts.device
+    rng = np.random.default_rng(seed)
+    first = int(rng.integers(0, n))
+    unif = _device.to_device(rng.random(num_clusters - 1)) if num_clusters > 1 else None
+    rows, centers, deg = _ops.kmeans_seed(pts, num_clusters, first, unif)
+    deg_pass = int(deg.item())
+    if deg_pass >= 0:
+        rows_h = _device.to_host(rows).copy()
+        rows_h = _finish_seeds_on_degenerate(users.values, rows_h, deg_pass)
+        centers = torch.as_tensor(users.values[rows_h], device=dev).contiguous()
+
+    def repair(assign_t, d2_t, counts_t):
+        if not (_device.to_host(counts_t) == 0).any():
+            return assign_t, False
+        a_h = _device.to_host(assign_t).copy()
+        c_h = _device.to_host(centers).copy()
+        d_h = _device.to_host(d2_t).copy()
+        _repair_empty_host(users.values, c_h, a_h, d_h)
+        centers.copy_(torch.as_tensor(c_h, device=dev))
+        return torch.as_tensor(a_h, device=dev), True
+
+    assign, d2, _, obj = _ops.kmeans_assign(pts, centers)
+    history = [float(obj.item())]
+    for _ in range(max_iters):
+        counts, _, _ = _ops.kmeans_update(pts, assign, centers)
+        assign, _ = repair(assign, d2, counts)
+        new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign)
+        history.append(float(obj.item()))
+        if int(changed.item()) == 0:
+            break
+        assign = new_assign
+    counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
+    assign, fixed = repair(assign, d2, counts)
+    if fixed:
+        counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
+    theta = _ops.max_angles(pts, centers, assign)
+    assign_h = _device.to_host(assign).astype(np.int64)
+    mem_h = _device.to_host(members)
+    off_h = _device.to_host(offsets)
+    members_t = tuple(mem_h[off_h[c]:off_h[c + 1]].copy() for c in range(num_clusters))
+    cen_h = _device.to_host(centers).copy()
+    theta_h = _device.to_host(theta).copy()
+    objective = np.asarray(history)
+    for a in (assign_h, theta_h, objective):
+        a.setflags(write=False)
+    out = Clustering(FactorMatrix(cen_h), assign_h, theta_h, members_t, objective, seed)
+    # keep the device copies produced here
+    d = out._dev()
+    d["assign"] = assign.contiguous()
+    d["theta"] = theta
+    return out

@@ -1,0 +1,100 @@
+// C-ABI entry points (include/simdex_b200.h) that are not defined next to
+// their kernels, plus the shared error state.
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace simdex {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %s (%d) at %s", cudaGetErrorString(e), (int)e, what);
+  return e == cudaErrorMemoryAllocation ? SIMDEX_ENOMEM : SIMDEX_ECUDA;
+}
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int launch_walk(const double*, const double*, const double*, int32_t, int64_t, const int32_t*, const double*,
+                const int64_t*, const int32_t*, int64_t, int32_t, int64_t, const int32_t*, const double*,
+                const int32_t*, int32_t, int32_t*, double*, int64_t*, cudaStream_t);
+int ws_fix_visited(int64_t*, int64_t, int64_t, int64_t, cudaStream_t);
+int launch_pack_bf16(const double*, int64_t, int32_t, int32_t, int64_t, int32_t, uint16_t*, double*, cudaStream_t);
+int launch_gather_prefix(const uint16_t*, const double*, int64_t, int32_t, const int32_t*, int32_t, int64_t,
+                         int64_t, uint16_t*, double*, cudaStream_t);
+
+}  // namespace simdex
+
+using namespace simdex;
+
+extern "C" int simdex_abi_version(void) { return SIMDEX_ABI_VERSION; }
+
+extern "C" const char* simdex_last_error(void) { return g_err; }
+
+extern "C" int simdex_device_info(int device, int* sms, int* major, int* minor) {
+  SIMDEX_CHECK_ARG(sms && major && minor, "simdex_device_info: null pointer");
+  SIMDEX_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, device));
+  SIMDEX_CUDA(cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, device));
+  SIMDEX_CUDA(cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, device));
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_topk_exact(const double* users, int64_t nu, const double* items, int64_t ni, int32_t f,
+                                 const int64_t* rows, int64_t n_rows, int32_t k, int32_t* out_ids,
+                                 double* out_scores, void* stream) {
+  SIMDEX_CHECK_ARG(users && items && out_ids && out_scores, "simdex_topk_exact: null pointer");
+  SIMDEX_CHECK_ARG(nu >= 1 && ni >= 1 && f >= 1 && k >= 1 && ni < INT32_MAX, "simdex_topk_exact: bad sizes");
+  SIMDEX_CHECK_ARG(rows || n_rows == nu, "simdex_topk_exact: n_rows must equal nu without a row list");
+  return exact_topk_rows(users, items, ni, f, rows, n_rows, k, out_ids, out_scores, as_stream(stream));
+}
+
+extern "C" int simdex_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp, int64_t rows_pad,
+                                int32_t kp, uint16_t* out_bf16, double* out_norms, void* stream) {
+  SIMDEX_CHECK_ARG(x && out_bf16 && out_norms, "simdex_pack_bf16: null pointer");
+  SIMDEX_CHECK_ARG(rows >= 1 && f >= 1 && rows_pad >= rows && kp >= f && kp % 64 == 0,
+                   "simdex_pack_bf16: bad sizes");
+  return launch_pack_bf16(x, rows, f, scale_exp, rows_pad, kp, out_bf16, out_norms, as_stream(stream));
+}
+
+extern "C" int simdex_walk(const double* users, const double* user_norms, const double* items, int32_t f,
+                           int64_t ni, const int32_t* list_ids, const double* bounds, const int64_t* q_user,
+                           const int32_t* q_cluster, int64_t nq, int32_t k, int64_t start, const int32_t* warm_ids,
+                           const double* warm_scores, const int32_t* warm_count, int32_t no_prune,
+                           int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
+  SIMDEX_CHECK_ARG(users && user_norms && items && list_ids && bounds && q_user && q_cluster && out_ids &&
+                       out_scores && out_visited,
+                   "simdex_walk: null pointer");
+  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && nq >= 0 && start >= 0, "simdex_walk: bad sizes");
+  SIMDEX_CHECK_ARG(start == 0 || (warm_ids && warm_scores && warm_count), "simdex_walk: warm start needs warm lists");
+  return launch_walk(users, user_norms, items, f, ni, list_ids, bounds, q_user, q_cluster, nq, k, start, warm_ids,
+                     warm_scores, warm_count, no_prune, out_ids, out_scores, out_visited, as_stream(stream));
+}
+
+extern "C" int simdex_build_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
+                                   const int32_t* list_ids, int32_t c, int64_t block, int64_t b_pad,
+                                   uint16_t* out_prefix_b, double* out_prefix_norm, void* stream) {
+  SIMDEX_CHECK_ARG(ib && i_norm && list_ids && out_prefix_b && out_prefix_norm, "simdex_build_prefix: null pointer");
+  SIMDEX_CHECK_ARG(ni >= 1 && c >= 1 && block >= 1 && b_pad >= (block < ni ? block : ni) && kp % 64 == 0,
+                   "simdex_build_prefix: bad sizes");
+  return launch_gather_prefix(ib, i_norm, ni, kp, list_ids, c, block, b_pad, out_prefix_b, out_prefix_norm,
+                              as_stream(stream));
+}
+
+extern "C" int simdex_merge_topk(const int32_t* in_ids, const double* in_scores, int32_t parts, int64_t nu,
+                                 int32_t kk, int32_t k_out, int32_t* out_ids, double* out_scores, void* stream) {
+  SIMDEX_CHECK_ARG(in_ids && in_scores && out_ids && out_scores, "simdex_merge_topk: null pointer");
+  SIMDEX_CHECK_ARG(parts >= 1 && parts <= 32 && nu >= 0 && kk >= 1 && k_out >= 1, "simdex_merge_topk: bad sizes");
+  return merge_lists(in_ids, in_scores, parts, nu, kk, k_out, out_ids, out_scores, as_stream(stream));
+}

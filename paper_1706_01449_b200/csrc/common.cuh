@@ -1,0 +1,96 @@
+// Shared helpers for the SimDex B200 kernels: error state, launch checks,
+// ordering predicates, and small warp utilities.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/simdex_b200.h"
+
+namespace simdex {
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define SIMDEX_CHECK_ARG(cond, ...)        \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::simdex::set_error(__VA_ARGS__);    \
+      return SIMDEX_EINVAL;                \
+    }                                      \
+  } while (0)
+
+#define SIMDEX_CUDA(call)                                      \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::simdex::cuda_fail(_e, #call); \
+  } while (0)
+
+#define SIMDEX_LAUNCH_CHECK(name) SIMDEX_CUDA(cudaGetLastError())
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch allocation (freed on the same stream).
+template <class T>
+struct Scratch {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t count, cudaStream_t stream) {
+    s = stream;
+    if (count == 0) count = 1;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream);
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+int sm_count();
+
+// ---------------------------------------------------------------------------
+// Result ordering: (score desc, id asc)  -- index.py:158-163
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ bool ranks_before(double sa, int32_t ia, double sb, int32_t ib) {
+  return sa > sb || (sa == sb && ia < ib);
+}
+
+// Orderable 64-bit key of a double so that ascending key == descending value,
+// with -0.0 folded onto +0.0 (numpy compares them equal).
+__host__ __device__ __forceinline__ uint64_t desc_key(double v) {
+  if (v == 0.0) v = 0.0;
+  uint64_t b;
+  memcpy(&b, &v, 8);
+  b = (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);  // ascending order
+  return ~b;                                                           // descending
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int ceil_div_i(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// internal entry points shared across translation units
+// ---------------------------------------------------------------------------
+// Batched (score desc, id asc) sort of `segs` equal-length segments of
+// (key, id) pairs; keys are float64 values sorted descending.
+cudaError_t segmented_sort_desc(double* keys, int32_t* ids, int64_t segs, int64_t len, cudaStream_t s);
+
+// Exact fp64 top-K of rows x a column set.  cols == nullptr means all ni
+// items; otherwise cols[r] is a per-row... (not used).  Internal form used by
+// topk_exact and by the overflow fallback of the tensor-core path.
+int exact_topk_rows(const double* users, const double* items, int64_t ni, int32_t f,
+                    const int64_t* rows, int64_t n_rows, int32_t k,
+                    int32_t* out_ids, double* out_scores, cudaStream_t s);
+
+// Merge `parts` sorted lists per row.
+int merge_lists(const int32_t* in_ids, const double* in_scores, int32_t parts, int64_t nu, int32_t kk,
+                int32_t k_out, int32_t* out_ids, double* out_scores, cudaStream_t s);
+
+}  // namespace simdex

@@ -1,0 +1,359 @@
+// k-means on device (clustering.py:96-198):
+//   * assignment: fused float64 distance GEMM + first-minimum argmin
+//     (the U x C distance matrix never reaches HBM, clustering.py:175-177);
+//   * update: users ordered by (cluster, id) with the segmented sort, then
+//     one CTA per cluster sums its members in id order -- the same
+//     sequential order numpy's axis-0 mean uses (clustering.py:169-172), so
+//     the result is deterministic;
+//   * k-means++ seeding with the host's RNG draws: per pass a fused D^2
+//     update + block sums, then a one-CTA scan that finds the first index
+//     whose cumulative D^2 exceeds u * total (numpy's choice(n, p) ==
+//     searchsorted(cumsum(p)/cdf[-1], u, 'right'), clustering.py:118-121).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace simdex {
+namespace {
+
+constexpr int kAssignThreads = 128;
+constexpr int kCC = 32;  // centers per chunk (register accumulators)
+constexpr int kFC = 32;  // factors per chunk
+
+__global__ void sqnorm_kernel(const double* __restrict__ x, int64_t n, int f, double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < f; ++k) s = fma(x[i * f + k], x[i * f + k], s);
+  out[i] = s;
+}
+
+__global__ void __launch_bounds__(kAssignThreads) assign_kernel(
+    const double* __restrict__ points, const double* __restrict__ p2, int64_t n, int f,
+    const double* __restrict__ centers, const double* __restrict__ c2, int c, const int64_t* __restrict__ prev,
+    int64_t* __restrict__ out_assign, double* __restrict__ out_d2, unsigned long long* __restrict__ changed,
+    double* __restrict__ block_sums) {
+  __shared__ double cs[kCC][kFC + 1];
+  __shared__ double red[kAssignThreads / 32];
+  const int64_t u = (int64_t)blockIdx.x * kAssignThreads + threadIdx.x;
+  const bool live = u < n;
+  const double* x = points + (live ? u : 0) * f;
+  const double pp = live ? p2[u] : 0.0;
+  double best = DBL_MAX;
+  int64_t arg = 0;
+  for (int c0 = 0; c0 < c; c0 += kCC) {
+    double acc[kCC];
+#pragma unroll
+    for (int j = 0; j < kCC; ++j) acc[j] = 0.0;
+    for (int k0 = 0; k0 < f; k0 += kFC) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kCC * kFC; e += kAssignThreads) {
+        int j = e / kFC, k = e % kFC;
+        cs[j][k] = (c0 + j < c && k0 + k < f) ? centers[(int64_t)(c0 + j) * f + k0 + k] : 0.0;
+      }
+      __syncthreads();
+      const int kn = (f - k0) < kFC ? (f - k0) : kFC;
+      for (int k = 0; k < kn; ++k) {
+        const double xk = live ? x[k0 + k] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kCC; ++j) acc[j] = fma(xk, cs[j][k], acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kCC; ++j) {
+      if (c0 + j < c) {
+        double d = (pp + c2[c0 + j]) - 2.0 * acc[j];
+        d = d > 0.0 ? d : 0.0;  // np.maximum(d2, 0)
+        if (d < best) {         // strict: first minimum wins (argmin)
+          best = d;
+          arg = c0 + j;
+        }
+      }
+    }
+  }
+  double mine = 0.0;
+  if (live) {
+    out_assign[u] = arg;
+    out_d2[u] = best;
+    mine = best;
+    if (prev && prev[u] != arg) atomicAdd(changed, 1ull);
+  }
+  // deterministic block sum of d2 (fixed tree)
+  mine = warp_sum(mine);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kAssignThreads / 32; ++w) s += red[w];
+    block_sums[blockIdx.x] = s;
+  }
+}
+
+// Sum `m` partials in a fixed order (one CTA).
+__global__ void sum_partials_kernel(const double* __restrict__ part, int64_t m, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) s += part[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+__global__ void cluster_keys_kernel(const int64_t* __restrict__ assign, int64_t n, double* keys, int32_t* ids,
+                                    unsigned long long* counts) {
+  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  keys[u] = -(double)assign[u];  // sort desc on -cluster == cluster ascending, then id ascending
+  ids[u] = (int32_t)u;
+  atomicAdd(counts + assign[u], 1ull);
+}
+
+__global__ void offsets_kernel(const unsigned long long* counts, int c, int64_t* out_counts, int64_t* offsets) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t acc = 0;
+  for (int j = 0; j < c; ++j) {
+    offsets[j] = acc;
+    out_counts[j] = (int64_t)counts[j];
+    acc += (int64_t)counts[j];
+  }
+  offsets[c] = acc;
+}
+
+__global__ void members_kernel(const int32_t* ids, int64_t n, int64_t* members) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) members[i] = ids[i];
+}
+
+// One CTA per cluster: sequential (id-ordered) sum per factor, then / count.
+__global__ void centroid_mean_kernel(const double* __restrict__ points, int f, const int64_t* __restrict__ members,
+                                     const int64_t* __restrict__ offsets, double* __restrict__ centers) {
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  if (e == b) return;  // empty: keep the previous centroid (clustering.py:171)
+  for (int k = threadIdx.x; k < f; k += blockDim.x) {
+    double s = 0.0;
+    for (int64_t m = b; m < e; ++m) s += points[members[m] * f + k];
+    centers[(int64_t)c * f + k] = s / (double)(e - b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k-means++ seeding
+// ---------------------------------------------------------------------------
+constexpr int kSeedThreads = 256;
+
+// d2 = min(d2, |p - center_j|^2) with the reference's expression
+// (||p||^2 + ||c||^2 - 2 p.c, clipped); pass 0 initialises.  Also block sums.
+__global__ void __launch_bounds__(kSeedThreads) seed_update_kernel(const double* __restrict__ points,
+                                                                   const double* __restrict__ p2, int64_t n, int f,
+                                                                   const int64_t* __restrict__ rows, int j,
+                                                                   double* __restrict__ d2,
+                                                                   double* __restrict__ block_sums,
+                                                                   const int32_t* __restrict__ degenerate) {
+  extern __shared__ double cen[];
+  __shared__ double red[kSeedThreads / 32];
+  if (*degenerate >= 0) return;
+  const int64_t r = rows[j];
+  for (int k = threadIdx.x; k < f; k += kSeedThreads) cen[k] = points[r * f + k];
+  __syncthreads();
+  const double cc = p2[r];
+  const int64_t u = (int64_t)blockIdx.x * kSeedThreads + threadIdx.x;
+  double v = 0.0;
+  if (u < n) {
+    const double* x = points + u * f;
+    double dot = 0.0;
+    for (int k = 0; k < f; ++k) dot = fma(x[k], cen[k], dot);
+    double d = (p2[u] + cc) - 2.0 * dot;
+    d = d > 0.0 ? d : 0.0;
+    v = (j == 0) ? d : fmin(d2[u], d);
+    d2[u] = v;
+  }
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kSeedThreads / 32; ++w) s += red[w];
+    block_sums[blockIdx.x] = s;
+  }
+}
+
+// One CTA: pick seed j+1 = first index i with cumsum(d2)[i] > u * total.
+__global__ void __launch_bounds__(1024) seed_pick_kernel(const double* __restrict__ points, int64_t n, int f,
+                                                         const double* __restrict__ d2,
+                                                         const double* __restrict__ block_sums, int64_t nblocks,
+                                                         const double* __restrict__ uniforms, int j,
+                                                         int64_t* __restrict__ rows, double* __restrict__ centers,
+                                                         int32_t* __restrict__ degenerate) {
+  __shared__ double s_total;
+  __shared__ int64_t s_block;
+  __shared__ double s_base;
+  __shared__ int64_t s_pick;
+  __shared__ double wsum[32];
+  if (*degenerate >= 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // total in a fixed order: serial over block sums by thread 0 (nblocks is ~n/256)
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) t += block_sums[b];
+    s_total = t;
+  }
+  __syncthreads();
+  const double total = s_total;
+  if (!(total > 0.0)) {
+    if (threadIdx.x == 0) *degenerate = j + 1;
+    return;
+  }
+  const double target = uniforms[j] * total;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    int64_t b = 0;
+    for (; b < nblocks; ++b) {
+      if (acc + block_sums[b] > target) break;
+      acc += block_sums[b];
+    }
+    if (b == nblocks) {  // rounding pushed target past the end: last positive block
+      b = nblocks - 1;
+      while (b > 0 && !(block_sums[b] > 0.0)) --b;
+      acc = 0.0;
+      for (int64_t q = 0; q < b; ++q) acc += block_sums[q];
+    }
+    s_block = b;
+    s_base = acc;
+    s_pick = -1;
+  }
+  __syncthreads();
+  // scan the chosen block (kSeedThreads entries) in index order
+  const int64_t b0 = s_block * kSeedThreads;
+  double v = 0.0;
+  const int64_t i = b0 + threadIdx.x;
+  if (threadIdx.x < kSeedThreads && i < n) v = d2[i];
+  // inclusive scan over the first kSeedThreads threads (8 warps)
+  double x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  double pre = s_base;
+  for (int w = 0; w < wid; ++w) pre += wsum[w];
+  const double incl = pre + x;
+  const double excl = incl - v;
+  if (threadIdx.x < kSeedThreads && i < n && v > 0.0 && incl > target && !(excl > target)) atomicMin((unsigned long long*)&s_pick, (unsigned long long)i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t p = s_pick;
+    if (p < 0) {  // defensive: last positive entry of the block
+      for (int64_t q = b0 + kSeedThreads - 1; q >= b0; --q)
+        if (q < n && d2[q] > 0.0) {
+          p = q;
+          break;
+        }
+    }
+    rows[j + 1] = p;
+    s_pick = p;
+  }
+  __syncthreads();
+  const int64_t p = s_pick;
+  for (int k = threadIdx.x; k < f; k += blockDim.x) centers[(int64_t)(j + 1) * f + k] = points[p * f + k];
+  (void)nw;
+}
+
+__global__ void seed_first_kernel(const double* __restrict__ points, int f, int64_t first, int64_t* rows,
+                                  double* centers, int32_t* degenerate) {
+  if (threadIdx.x == 0) {
+    rows[0] = first;
+    *degenerate = -1;
+  }
+  for (int k = threadIdx.x; k < f; k += blockDim.x) centers[k] = points[first * f + k];
+}
+
+}  // namespace
+}  // namespace simdex
+
+using namespace simdex;
+
+extern "C" int simdex_kmeans_assign(const double* points, int64_t n, int32_t f, const double* centers, int32_t c,
+                                    const int64_t* prev_assign, int64_t* out_assign, double* out_d2,
+                                    int64_t* out_changed, double* out_objective, void* stream) {
+  SIMDEX_CHECK_ARG(points && centers && out_assign && out_d2 && out_changed && out_objective,
+                   "simdex_kmeans_assign: null pointer");
+  SIMDEX_CHECK_ARG(n >= 1 && f >= 1 && c >= 1, "simdex_kmeans_assign: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  Scratch<double> p2, c2, part;
+  const int64_t nb = ceil_div(n, kAssignThreads);
+  SIMDEX_CUDA(p2.alloc(n, s));
+  SIMDEX_CUDA(c2.alloc(c, s));
+  SIMDEX_CUDA(part.alloc(nb, s));
+  sqnorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(points, n, f, p2.p);
+  sqnorm_kernel<<<(unsigned)ceil_div(c, 256), 256, 0, s>>>(centers, c, f, c2.p);
+  SIMDEX_CUDA(cudaMemsetAsync(out_changed, 0, sizeof(int64_t), s));
+  assign_kernel<<<(unsigned)nb, kAssignThreads, 0, s>>>(points, p2.p, n, f, centers, c2.p, c, prev_assign,
+                                                        out_assign, out_d2,
+                                                        reinterpret_cast<unsigned long long*>(out_changed), part.p);
+  SIMDEX_LAUNCH_CHECK("assign");
+  sum_partials_kernel<<<1, 1024, 0, s>>>(part.p, nb, out_objective);
+  SIMDEX_LAUNCH_CHECK("sum_partials");
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_kmeans_update(const double* points, int64_t n, int32_t f, const int64_t* assign, int32_t c,
+                                    double* centers, int64_t* out_counts, int64_t* out_members,
+                                    int64_t* out_offsets, void* stream) {
+  SIMDEX_CHECK_ARG(points && assign && out_counts && out_members && out_offsets,
+                   "simdex_kmeans_update: null pointer");
+  SIMDEX_CHECK_ARG(n >= 1 && f >= 1 && c >= 1 && n < INT32_MAX, "simdex_kmeans_update: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  Scratch<double> keys;
+  Scratch<int32_t> ids;
+  Scratch<unsigned long long> cnt;
+  SIMDEX_CUDA(keys.alloc(n, s));
+  SIMDEX_CUDA(ids.alloc(n, s));
+  SIMDEX_CUDA(cnt.alloc(c, s));
+  SIMDEX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * c, s));
+  cluster_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(assign, n, keys.p, ids.p, cnt.p);
+  SIMDEX_LAUNCH_CHECK("cluster_keys");
+  SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, n, s));
+  offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
+  members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(ids.p, n, out_members);
+  if (centers) {  // NULL: grouping only (members/offsets/counts)
+    centroid_mean_kernel<<<(unsigned)c, 64, 0, s>>>(points, f, out_members, out_offsets, centers);
+    SIMDEX_LAUNCH_CHECK("centroid_mean");
+  }
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, int32_t k, int64_t first,
+                                  const double* uniforms, int64_t* out_rows, double* out_centers,
+                                  int32_t* out_degenerate_pass, void* stream) {
+  SIMDEX_CHECK_ARG(points && out_rows && out_centers && out_degenerate_pass, "simdex_kmeans_seed: null pointer");
+  SIMDEX_CHECK_ARG(n >= 1 && f >= 1 && k >= 1 && k <= n && first >= 0 && first < n,
+                   "simdex_kmeans_seed: bad sizes");
+  SIMDEX_CHECK_ARG(k == 1 || uniforms, "simdex_kmeans_seed: uniforms required");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nb = ceil_div(n, kSeedThreads);
+  Scratch<double> p2, d2, part;
+  SIMDEX_CUDA(p2.alloc(n, s));
+  SIMDEX_CUDA(d2.alloc(n, s));
+  SIMDEX_CUDA(part.alloc(nb, s));
+  sqnorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(points, n, f, p2.p);
+  seed_first_kernel<<<1, 128, 0, s>>>(points, f, first, out_rows, out_centers, out_degenerate_pass);
+  SIMDEX_LAUNCH_CHECK("seed_first");
+  const size_t smem = (size_t)f * sizeof(double);
+  if (smem > 48 * 1024)
+    SIMDEX_CUDA(cudaFuncSetAttribute(seed_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int j = 0; j + 1 < k; ++j) {
+    seed_update_kernel<<<(unsigned)nb, kSeedThreads, smem, s>>>(points, p2.p, n, f, out_rows, j, d2.p, part.p,
+                                                                out_degenerate_pass);
+    seed_pick_kernel<<<1, 1024, 0, s>>>(points, n, f, d2.p, part.p, nb, uniforms, j, out_rows, out_centers,
+                                        out_degenerate_pass);
+  }
+  SIMDEX_LAUNCH_CHECK("seed");
+  return SIMDEX_OK;
+}

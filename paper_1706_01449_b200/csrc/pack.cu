@@ -1,0 +1,64 @@
+// Operand packing for the tensor-core path: float64 factors -> bf16 (scaled
+// by an exact power of two, round-to-nearest-even, zero padded to [rows_pad,
+// kp]) + float64 row norms; and the work-sharing prefix gather (every
+// cluster's first B list items in list order, index.py:351-357).
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace simdex {
+namespace {
+
+__global__ void pack_bf16_kernel(const double* __restrict__ x, int64_t rows, int f, int scale_exp, int64_t rows_pad,
+                                 int kp, uint16_t* __restrict__ out, double* __restrict__ norms) {
+  // one warp per row
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows_pad) return;
+  double ss = 0.0;
+  for (int k = lane; k < kp; k += 32) {
+    double v = (r < rows && k < f) ? x[r * f + k] : 0.0;
+    ss = fma(v, v, ss);
+    __nv_bfloat16 b = __double2bfloat16(ldexp(v, scale_exp));
+    out[r * kp + k] = *reinterpret_cast<uint16_t*>(&b);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0 && r < rows) norms[r] = sqrt(ss);
+}
+
+__global__ void gather_prefix_kernel(const uint16_t* __restrict__ ib, const double* __restrict__ inorm, int64_t ni,
+                                     int kp, const int32_t* __restrict__ list_ids, int64_t bp, int64_t b_pad,
+                                     int64_t n_clusters, uint16_t* __restrict__ out, double* __restrict__ onorm) {
+  // one warp per (cluster, prefix row)
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t c = g / b_pad, r = g % b_pad;
+  if (c >= n_clusters) return;
+  const bool live = r < bp;
+  const int64_t src = live ? list_ids[c * ni + r] : 0;
+  const uint4* s = reinterpret_cast<const uint4*>(ib + src * kp);
+  uint4* d = reinterpret_cast<uint4*>(out + (c * b_pad + r) * kp);
+  for (int v = lane; v < kp / 8; v += 32) d[v] = live ? s[v] : make_uint4(0, 0, 0, 0);
+  if (lane == 0) onorm[c * b_pad + r] = live ? inorm[src] : 0.0;
+}
+
+}  // namespace
+
+int launch_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp, int64_t rows_pad, int32_t kp,
+                     uint16_t* out, double* norms, cudaStream_t s) {
+  pack_bf16_kernel<<<(unsigned)ceil_div(rows_pad, 8), 256, 0, s>>>(x, rows, f, scale_exp, rows_pad, kp, out, norms);
+  SIMDEX_LAUNCH_CHECK("pack_bf16");
+  return SIMDEX_OK;
+}
+
+int launch_gather_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp, const int32_t* list_ids,
+                         int32_t c, int64_t block, int64_t b_pad, uint16_t* out, double* onorm, cudaStream_t s) {
+  const int64_t bp = block < ni ? block : ni;
+  const int64_t warps = (int64_t)c * b_pad;
+  gather_prefix_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>(ib, i_norm, ni, kp, list_ids, bp, b_pad, c,
+                                                                    out, onorm);
+  SIMDEX_LAUNCH_CHECK("gather_prefix");
+  return SIMDEX_OK;
+}
+
+}  // namespace simdex

@@ -1,0 +1,401 @@
+"""Clustered upper-bound index for exact top-K inner-product queries
+(reference: mipserve/index.py).
+
+The sorted ceiling lists live on the device (int32 item ids + float64
+ceilings, [C, |I|]); the host views ``item_ids`` / ``bounds`` /
+``item_norms`` of the reference's CentroidIndex are materialised on first
+access.  Every query runs on the GPU: the bounded walk (simdex_walk) and the
+work-sharing batch path (simdex_query_ws).  Results are exact and equal the
+reference's, including ``visited``.
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+from collections.abc import Sequence
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _ops
+from .clustering import DEGENERATE_ANGLE, Clustering, angular_distance
+from .model_io import DimensionMismatchError, FactorMatrix, FormatError, ModelPair, NonFiniteValueError
+
+DEFAULT_BLOCK_SIZE = 4096
+
+INDEX_MAGIC = b"MFIDX001"
+_IDX_HEADER = struct.Struct("<8sQQQQQq")
+
+
+@dataclass(frozen=True)
+class TopKResult:
+    """Top items for one user: scores descending, ties by ascending item id;
+    ``visited`` = items whose true score was computed (index.py:42-58)."""
+
+    user_id: int
+    item_ids: np.ndarray
+    scores: np.ndarray
+    visited: int
+
+    @property
+    def entries(self) -> list[tuple[int, float]]:
+        return list(zip(self.item_ids.tolist(), self.scores.tolist()))
+
+
+class TopKResults(Sequence):
+    """Lazy ``list[TopKResult]`` over batched [n, K] result arrays.
+
+    Indexing/iteration build TopKResult objects on demand (fresh int64 /
+    float64 arrays per element, like the reference's list); ``reused`` maps
+    positions to existing TopKResult objects that must be returned as-is
+    (``precomputed`` in query_batch, index.py:330-332).  The whole-batch
+    arrays are available as ``.item_ids`` / ``.scores`` / ``.visited``.
+    """
+
+    def __init__(self, user_ids, item_ids, scores, visited, reused=None):
+        self.user_ids = np.asarray(user_ids, dtype=np.int64)
+        self.item_ids = item_ids
+        self.scores = scores
+        self.visited = visited
+        self._reused = reused or {}
+
+    def __len__(self):
+        return self.user_ids.shape[0]
+
+    def _make(self, i):
+        r = self._reused.get(i)
+        if r is not None:
+            return r
+        return TopKResult(int(self.user_ids[i]), self.item_ids[i].astype(np.int64),
+                          self.scores[i].astype(np.float64), int(self.visited[i]))
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._make(j) for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("TopKResults index out of range")
+        return self._make(i)
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self._make(i)
+
+
+class CentroidIndex:
+    """Per-cluster item lists sorted by score ceiling, plus item norms
+    (index.py:61-87).  Immutable; safe to share for reads."""
+
+    def __init__(self, item_ids, bounds, item_norms, block_size, clustering, *, _dev=None):
+        self.block_size = int(block_size)
+        self.clustering = clustering
+        self._host = {}
+        self._dev = dict(_dev or {})
+        for name, val in (("item_ids", item_ids), ("bounds", bounds), ("item_norms", item_norms)):
+            if val is not None:
+                a = np.asarray(val)
+                a.setflags(write=False) if a.flags.owndata else None
+                self._host[name] = a
+        shape = self._dev["ids"].shape if "ids" in self._dev else self._host["item_ids"].shape
+        self._shape = (int(shape[0]), int(shape[1]))
+
+    # -- host views (reference fields) --------------------------------------
+    def _host_get(self, name, key, dtype):
+        if name not in self._host:
+            a = _device.to_host(self._dev[key]).astype(dtype, copy=False)
+            a.setflags(write=False)
+            self._host[name] = a
+        return self._host[name]
+
+    @property
+    def item_ids(self) -> np.ndarray:
+        return self._host_get("item_ids", "ids", np.int64)
+
+    @property
+    def bounds(self) -> np.ndarray:
+        return self._host_get("bounds", "bounds", np.float64)
+
+    @property
+    def item_norms(self) -> np.ndarray:
+        return self._host_get("item_norms", "norms", np.float64)
+
+    @property
+    def num_clusters(self) -> int:
+        return self._shape[0]
+
+    @property
+    def num_items(self) -> int:
+        return self._shape[1]
+
+    @property
+    def entry_count(self) -> int:
+        return self._shape[0] * self._shape[1]
+
+    # -- device views -------------------------------------------------------
+    def device_lists(self):
+        if "ids" not in self._dev:
+            self._dev["ids"] = _device.to_device(self._host["item_ids"].astype(np.int32))
+            self._dev["bounds"] = _device.to_device(self._host["bounds"].astype(np.float64))
+        return self._dev["ids"], self._dev["bounds"]
+
+    def device_assignment(self):
+        return self.clustering.device_assignment()
+
+    def device_prefix(self, model: ModelPair):
+        key = ("prefix", id(model.items))
+        if key not in self._dev:
+            ids, _ = self.device_lists()
+            self._dev[key] = _ops.build_prefix(_device.packed(model.items), ids, self.block_size)
+        return self._dev[key]
+
+
+def item_bound(item_norm: float, item_angle: float, cluster_angle: float) -> float:
+    """Eq. 2 ceiling of one item (index.py:90-100): ||i|| cos(theta_ic -
+    theta_b) while the slack is below the item angle, else ||i||."""
+    if item_norm < 0.0:
+        raise ValueError("item_norm must be >= 0")
+    for name, a in (("item_angle", item_angle), ("cluster_angle", cluster_angle)):
+        if not 0.0 <= a <= math.pi:
+            raise ValueError(f"{name} outside [0, pi]: {a}")
+    return float(item_norm * math.cos(item_angle - cluster_angle)) if cluster_angle < item_angle else float(item_norm)
+
+
+def _device_build(model: ModelPair, centers_t, theta_t):
+    items = _device.f64(model.items)
+    return _ops.build_index(items, centers_t, theta_t)
+
+
+def build_index(model: ModelPair, clustering: Clustering, block_size: int = DEFAULT_BLOCK_SIZE) -> CentroidIndex:
+    """Sorted ceiling lists for every cluster, built on the GPU (index.py:129-155)."""
+    if clustering.assignment.shape[0] != model.num_users:
+        raise ValueError(
+            f"clustering covers {clustering.assignment.shape[0]} users, model has {model.num_users}"
+        )
+    if block_size < 1:
+        raise ValueError("block_size must be >= 1")
+    norms, ids, bounds = _device_build(model, clustering.device_centroids(), clustering.device_max_angle())
+    return CentroidIndex(None, None, None, block_size, clustering, _dev={"ids": ids, "bounds": bounds, "norms": norms})
+
+
+def _check_k(k):
+    if k < 1:
+        raise ValueError("k must be >= 1")
+
+
+def _walk_rows(index, model, q_users_np, k, q_clusters=None):
+    users = _device.f64(model.users)
+    unorm = _device.norms(model.users)
+    items = _device.f64(model.items)
+    ids, bounds = index.device_lists()
+    q = _device.to_device(np.asarray(q_users_np, dtype=np.int64))
+    if q_clusters is None:
+        qc = index.device_assignment().index_select(0, q).to(torch.int32)
+    else:
+        qc = q_clusters
+    return _ops.walk(users, unorm, items, ids, bounds, q, qc, k)
+
+
+def query_user(index: CentroidIndex, model: ModelPair, user_id: int, k: int) -> TopKResult:
+    """Exact top-K for one model user via their cluster's list walk (index.py:258-268)."""
+    _check_k(k)
+    if not 0 <= user_id < model.num_users:
+        raise ValueError(f"user_id {user_id} out of range [0, {model.num_users})")
+    ids, sc, vis = _walk_rows(index, model, [user_id], k)
+    return TopKResult(int(user_id), _device.to_host(ids[0]).astype(np.int64), _device.to_host(sc[0]),
+                      int(vis[0].item()))
+
+
+def _check_vector(vector, factors: int, what="vector") -> np.ndarray:
+    v = np.asarray(vector, dtype=np.float64)
+    if v.shape != (factors,):
+        raise DimensionMismatchError(f"{what} shape {v.shape} != ({factors},)")
+    if not np.isfinite(v).all():
+        raise NonFiniteValueError(f"{what} contains non-finite values")
+    return v
+
+
+def _nearest_centroid(cvals: np.ndarray, v: np.ndarray):
+    """Route a vector to its L2-nearest centroid and measure its angle
+    (index.py:285-293); host-side scalar routing, like the reference."""
+    c = int(((cvals - v) ** 2).sum(axis=1).argmin())
+    if np.linalg.norm(v) == 0.0 or np.linalg.norm(cvals[c]) == 0.0:
+        return c, DEGENERATE_ANGLE
+    return c, angular_distance(v, cvals[c])
+
+
+def _cluster_list(model, centroid, slack):
+    """One re-bounded list (index.py:295-299): GPU build for a single centroid."""
+    dev = _device.device()
+    cen = torch.as_tensor(np.asarray(centroid, dtype=np.float64)[None, :], device=dev)
+    th = torch.tensor([float(slack)], dtype=torch.float64, device=dev)
+    _, ids, bounds = _device_build(model, cen, th)
+    return ids, bounds
+
+
+def query_vector(index: CentroidIndex, model: ModelPair, vector, k: int) -> TopKResult:
+    """Exact top-K for an arbitrary query vector (user_id -1); a vector outside
+    its cluster's recorded slack walks a locally re-bounded list (index.py:271-302)."""
+    _check_k(k)
+    u = _check_vector(vector, model.factors, "vector")
+    cvals = index.clustering.centroids.values
+    c, theta = _nearest_centroid(cvals, u)
+    dev = _device.device()
+    ut = torch.as_tensor(u[None, :], device=dev)
+    un = torch.tensor([float(np.linalg.norm(u))], dtype=torch.float64, device=dev)
+    if theta <= index.clustering.max_angle[c]:
+        ids, bounds = index.device_lists()
+        qc = torch.tensor([c], dtype=torch.int32, device=dev)
+    else:
+        ids, bounds = _cluster_list(model, cvals[c], theta)
+        qc = torch.zeros(1, dtype=torch.int32, device=dev)
+    q = torch.zeros(1, dtype=torch.int64, device=dev)
+    oi, os_, ov = _ops.walk(ut, un, _device.f64(model.items), ids, bounds, q, qc, k)
+    return TopKResult(-1, _device.to_host(oi[0]).astype(np.int64), _device.to_host(os_[0]), int(ov[0].item()))
+
+
+def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.Tensor, k: int,
+                        work_sharing: bool = True):
+    """Device form of query_batch: int64 user rows in, (ids int32 [n, k_eff],
+    scores float64, visited int64) out, all on the device, in query order."""
+    users = _device.f64(model.users)
+    items = _device.f64(model.items)
+    ids, bounds = index.device_lists()
+    qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
+    if not work_sharing:
+        return _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
+    prefix = index.device_prefix(model)
+    return _ops.query_ws(users, _device.packed(model.users), items, _device.packed(model.items), ids, bounds,
+                         index.block_size, prefix, q_users, qc, k)
+
+
+def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 1, work_sharing: bool = True,
+                precomputed: dict | None = None) -> TopKResults:
+    """Top-K for many users (index.py:305-389); identical entries with work
+    sharing on or off.  With work sharing the first ``block_size`` items of
+    each cluster's list are scored for all that cluster's users as one
+    tensor-core product, and only users whose K-th does not beat the ceiling
+    at B continue walking.  ``precomputed`` results are reused verbatim."""
+    _check_k(k)
+    uids = np.arange(model.num_users, dtype=np.int64) if user_ids is None else np.asarray(
+        [int(u) for u in user_ids], dtype=np.int64)
+    bad = (uids < 0) | (uids >= model.num_users)
+    if bad.any():
+        raise ValueError(f"user_id {int(uids[np.argmax(bad)])} out of range [0, {model.num_users})")
+    precomputed = precomputed or {}
+    reused = {i: precomputed[int(u)] for i, u in enumerate(uids) if int(u) in precomputed} if precomputed else {}
+    todo = np.array([i for i in range(uids.shape[0]) if i not in reused], dtype=np.int64)
+    k_eff = min(k, model.num_items)
+    ids_h = np.zeros((uids.shape[0], k_eff), dtype=np.int32)
+    sc_h = np.zeros((uids.shape[0], k_eff), dtype=np.float64)
+    vis_h = np.zeros(uids.shape[0], dtype=np.int64)
+    if todo.size:
+        q = _device.to_device(uids[todo])
+        ids, sc, vis = query_batch_tensors(index, model, q, k, work_sharing)
+        ids_h[todo] = _device.to_host(ids)
+        sc_h[todo] = _device.to_host(sc)
+        vis_h[todo] = _device.to_host(vis)
+    return TopKResults(uids, ids_h, sc_h, vis_h, reused)
+
+
+def insert_item(index: CentroidIndex, model: ModelPair, item_vector):
+    """Add one item (index.py:401-430).  The lists are rebuilt on the GPU with
+    the unchanged clustering: the new id is the largest, so among equal
+    ceilings it sorts last -- the same list the reference's searchsorted
+    insertion produces.  Returns (index, model)."""
+    v = _check_vector(item_vector, model.factors, "vector")
+    new_model = ModelPair(model.users, FactorMatrix(np.vstack([model.items.values, v[None, :]])))
+    cl = index.clustering
+    norms, ids, bounds = _device_build(new_model, cl.device_centroids(), cl.device_max_angle())
+    return CentroidIndex(None, None, None, index.block_size, cl,
+                         _dev={"ids": ids, "bounds": bounds, "norms": norms}), new_model
+
+
+def add_user(index: CentroidIndex, model: ModelPair, user_vector):
+    """Assign a new user to the L2-nearest centroid (index.py:433-483); if its
+    angle exceeds the cluster's slack the slack is raised and that cluster's
+    list rebuilt (flag False = drift).  Returns (index, model, fits)."""
+    v = _check_vector(user_vector, model.factors, "vector")
+    cl = index.clustering
+    cvals = cl.centroids.values
+    c, theta = _nearest_centroid(cvals, v)
+    new_id = model.num_users
+    new_model = ModelPair(FactorMatrix(np.vstack([model.users.values, v[None, :]])), model.items)
+    assignment = np.append(cl.assignment, np.int64(c))
+    members = tuple(np.append(m, new_id) if j == c else m for j, m in enumerate(cl.members))
+    fits = bool(theta <= cl.max_angle[c])
+    max_angle = cl.max_angle.copy()
+    if not fits:
+        max_angle[c] = theta
+    max_angle.setflags(write=False)
+    assignment.setflags(write=False)
+    new_cl = Clustering(cl.centroids, assignment, max_angle, members, cl.objective, cl.seed)
+    if fits:
+        return _derive(index, new_cl), new_model, True
+    ids, bounds = index.device_lists()
+    ids, bounds = ids.clone(), bounds.clone()
+    rid, rb = _cluster_list(model, cvals[c], theta)
+    ids[c] = rid[0]
+    bounds[c] = rb[0]
+    return _derive(index, new_cl, (ids, bounds)), new_model, False
+
+
+def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> CentroidIndex:
+    """Same lists (or replaced ``lists``) under a new clustering."""
+    out = CentroidIndex.__new__(CentroidIndex)
+    out.block_size = index.block_size
+    out.clustering = clustering
+    out._shape = index._shape
+    out._host = dict(index._host)
+    out._dev = {key: val for key, val in index._dev.items() if not (isinstance(key, tuple) and lists is not None)}
+    if lists is not None:
+        out._host.pop("item_ids", None)
+        out._host.pop("bounds", None)
+        out._dev["ids"], out._dev["bounds"] = lists
+    return out
+
+
+def save_index(index: CentroidIndex, path) -> None:
+    """MFIDX001 sidecar (index.py:486-509): header, theta_b, centroids,
+    assignment, item norms, item ids (int64), ceilings (float64)."""
+    cl = index.clustering
+    parts = [
+        _IDX_HEADER.pack(INDEX_MAGIC, index.num_clusters, index.num_items, cl.centroids.factors,
+                         cl.assignment.shape[0], index.block_size, cl.seed),
+        np.ascontiguousarray(cl.max_angle, dtype="<f8").tobytes(),
+        np.ascontiguousarray(cl.centroids.values, dtype="<f8").tobytes(),
+        np.ascontiguousarray(cl.assignment, dtype="<i8").tobytes(),
+        np.ascontiguousarray(index.item_norms, dtype="<f8").tobytes(),
+        np.ascontiguousarray(index.item_ids, dtype="<i8").tobytes(),
+        np.ascontiguousarray(index.bounds, dtype="<f8").tobytes(),
+    ]
+    with open(path, "wb") as fh:
+        fh.writelines(parts)
+
+
+def load_index(path) -> CentroidIndex:
+    """Read a sidecar written by save_index (index.py:512-553)."""
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    if len(raw) < _IDX_HEADER.size:
+        raise FormatError(f"{path}: file shorter than the index header")
+    magic, nc, n, f, nu, block, seed = _IDX_HEADER.unpack_from(raw)
+    if magic != INDEX_MAGIC:
+        raise FormatError(f"{path}: bad magic {magic!r}, expected {INDEX_MAGIC!r}")
+    counts = [nc, nc * f, nu, n, nc * n, nc * n]
+    if len(raw) != _IDX_HEADER.size + 8 * sum(counts):
+        raise FormatError(f"{path}: file is {len(raw)} bytes, expected {_IDX_HEADER.size + 8 * sum(counts)}")
+    off = _IDX_HEADER.size
+    out = []
+    for cnt, dt in zip(counts, ("<f8", "<f8", "<i8", "<f8", "<i8", "<f8")):
+        out.append(np.frombuffer(raw, dtype=dt, count=cnt, offset=off).copy())
+        off += 8 * cnt
+    max_angle, cen, assign, norms, ids, bounds = out
+    for a in (assign, max_angle):
+        a.setflags(write=False)
+    members = tuple(np.flatnonzero(assign == c) for c in range(nc))
+    cl = Clustering(FactorMatrix(cen.reshape(nc, f)), assign, max_angle, members, np.empty(0), int(seed))
+    return CentroidIndex(ids.reshape(nc, n), bounds.reshape(nc, n), norms, int(block), cl)

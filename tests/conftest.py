@@ -66,3 +66,16 @@ def near_tie_rows(scores_sorted_full, k, rel=1e-5):
 def oracle():
     import simdex_oracle
     return simdex_oracle
+
+
+def assert_lists_equal_up_to_ties(ids, bounds, want_ids, want_bounds, rel=1e-12, ctx=""):
+    """Index lists equal, except that items whose ceilings agree to ``rel``
+    (mathematical ties that float64 rounding orders arbitrarily) may appear in
+    any order within their run."""
+    __tracebackhide__ = True
+    np.testing.assert_allclose(bounds, want_bounds, rtol=rel, atol=rel, err_msg=ctx)
+    for c in range(want_ids.shape[0]):
+        wb = want_bounds[c]
+        brk = np.flatnonzero(np.abs(np.diff(wb)) > rel * np.maximum(np.abs(wb[1:]), 1.0)) + 1
+        for seg in np.split(np.arange(wb.shape[0]), brk):
+            assert set(ids[c][seg].tolist()) == set(want_ids[c][seg].tolist()), f"{ctx} cluster {c} run {seg[:3]}"
