@@ -49,6 +49,8 @@ enum {
 
 SIMDEX_API int simdex_abi_version(void);
 SIMDEX_API const char* simdex_last_error(void);
+/* Number of kernels this library has launched in the process (monotone). */
+SIMDEX_API int64_t simdex_launch_count(void);
 /* sm count / compute capability of `device` (host outputs). */
 SIMDEX_API int simdex_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 

@@ -25,6 +25,7 @@ I64 = C.c_int64
 SIGNATURES = {
     "simdex_abi_version": [],
     "simdex_last_error": [],
+    "simdex_launch_count": [],
     "simdex_device_info": [C.c_int, P, P, P],
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
     "simdex_pack_bf16": [P, I64, I32, I32, I64, I32, P, P, P],
@@ -65,7 +66,7 @@ def load():
         for name, args in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.argtypes = args
-            fn.restype = C.c_char_p if name == "simdex_last_error" else C.c_int
+            fn.restype = {"simdex_last_error": C.c_char_p, "simdex_launch_count": C.c_int64}.get(name, C.c_int)
         if lib.simdex_abi_version() != 1:
             raise ImportError("libsimdex_b200.so ABI version mismatch")
         _lib = lib
@@ -86,6 +87,11 @@ def call(name, *args):
     if rc != 0:
         msg = lib.simdex_last_error().decode(errors="replace")
         raise SimdexError(f"{name} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    """Kernels launched by the library so far in this process."""
+    return int(load().simdex_launch_count())
 
 
 def ptr(t):

@@ -1,5 +1,6 @@
 // C-ABI entry points (include/simdex_b200.h) that are not defined next to
 // their kernels, plus the shared error state.
+#include <atomic>
 #include <cstdarg>
 #include <cstring>
 
@@ -8,6 +9,9 @@
 namespace simdex {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -42,6 +46,8 @@ using namespace simdex;
 extern "C" int simdex_abi_version(void) { return SIMDEX_ABI_VERSION; }
 
 extern "C" const char* simdex_last_error(void) { return g_err; }
+
+extern "C" int64_t simdex_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int simdex_device_info(int device, int* sms, int* major, int* minor) {
   SIMDEX_CHECK_ARG(sms && major && minor, "simdex_device_info: null pointer");

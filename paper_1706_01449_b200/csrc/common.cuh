@@ -29,7 +29,14 @@ int cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::simdex::cuda_fail(_e, #call); \
   } while (0)
 
-#define SIMDEX_LAUNCH_CHECK(name) SIMDEX_CUDA(cudaGetLastError())
+// Every kernel launch site ends with SIMDEX_LAUNCH_CHECK (or count_launches
+// for loops), which also feeds simdex_launch_count().
+void count_launches(int64_t n);
+#define SIMDEX_LAUNCH_CHECK(name)      \
+  do {                                 \
+    ::simdex::count_launches(1);       \
+    SIMDEX_CUDA(cudaGetLastError());   \
+  } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -218,6 +218,7 @@ cudaError_t segmented_sort_desc(double* keys, int32_t* ids, int64_t segs, int64_
   if (segs == 0 || len <= 1) return cudaSuccess;
   const int64_t tiles = ceil_div(len, kSortTile);
   tile_sort_kernel<<<(unsigned)(segs * tiles), kSortThreads, 0, s>>>(keys, ids, len, tiles);
+  count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || len <= kSortTile) return e;
   double* k2 = nullptr;
@@ -233,6 +234,7 @@ cudaError_t segmented_sort_desc(double* keys, int32_t* ids, int64_t segs, int64_
     const int64_t threads = segs * chunks;
     merge_pass_kernel<<<(unsigned)ceil_div(threads, kSortThreads), kSortThreads, 0, s>>>(srck, srci, dstk, dsti,
                                                                                           len, w, chunks, segs);
+    count_launches(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     double* tk = srck;
     srck = dstk;

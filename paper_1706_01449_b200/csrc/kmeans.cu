@@ -293,6 +293,7 @@ extern "C" int simdex_kmeans_assign(const double* points, int64_t n, int32_t f, 
   SIMDEX_CUDA(part.alloc(nb, s));
   sqnorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(points, n, f, p2.p);
   sqnorm_kernel<<<(unsigned)ceil_div(c, 256), 256, 0, s>>>(centers, c, f, c2.p);
+  count_launches(2);
   SIMDEX_CUDA(cudaMemsetAsync(out_changed, 0, sizeof(int64_t), s));
   assign_kernel<<<(unsigned)nb, kAssignThreads, 0, s>>>(points, p2.p, n, f, centers, c2.p, c, prev_assign,
                                                         out_assign, out_d2,
@@ -318,6 +319,7 @@ extern "C" int simdex_kmeans_update(const double* points, int64_t n, int32_t f, 
   SIMDEX_CUDA(cnt.alloc(c, s));
   SIMDEX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * c, s));
   cluster_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(assign, n, keys.p, ids.p, cnt.p);
+  count_launches(2);  // + offsets/members below
   SIMDEX_LAUNCH_CHECK("cluster_keys");
   SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, n, s));
   offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
@@ -343,6 +345,7 @@ extern "C" int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, in
   SIMDEX_CUDA(d2.alloc(n, s));
   SIMDEX_CUDA(part.alloc(nb, s));
   sqnorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(points, n, f, p2.p);
+  count_launches(1);
   seed_first_kernel<<<1, 128, 0, s>>>(points, f, first, out_rows, out_centers, out_degenerate_pass);
   SIMDEX_LAUNCH_CHECK("seed_first");
   const size_t smem = (size_t)f * sizeof(double);
@@ -353,6 +356,7 @@ extern "C" int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, in
                                                                 out_degenerate_pass);
     seed_pick_kernel<<<1, 1024, 0, s>>>(points, n, f, d2.p, part.p, nb, uniforms, j, out_rows, out_centers,
                                         out_degenerate_pass);
+    count_launches(2);
   }
   SIMDEX_LAUNCH_CHECK("seed");
   return SIMDEX_OK;

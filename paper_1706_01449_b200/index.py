@@ -285,9 +285,14 @@ def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 
     bad = (uids < 0) | (uids >= model.num_users)
     if bad.any():
         raise ValueError(f"user_id {int(uids[np.argmax(bad)])} out of range [0, {model.num_users})")
-    precomputed = precomputed or {}
-    reused = {i: precomputed[int(u)] for i, u in enumerate(uids) if int(u) in precomputed} if precomputed else {}
-    todo = np.array([i for i in range(uids.shape[0]) if i not in reused], dtype=np.int64)
+    reused = {}
+    if precomputed:
+        keys = np.fromiter(precomputed.keys(), dtype=np.int64, count=len(precomputed))
+        hit = np.isin(uids, keys)
+        reused = {int(i): precomputed[int(uids[i])] for i in np.flatnonzero(hit)}
+        todo = np.flatnonzero(~hit)
+    else:
+        todo = np.arange(uids.shape[0], dtype=np.int64)
     k_eff = min(k, model.num_items)
     ids_h = np.zeros((uids.shape[0], k_eff), dtype=np.int32)
     sc_h = np.zeros((uids.shape[0], k_eff), dtype=np.float64)
