@@ -163,16 +163,30 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
  * list items scored for all its queried users on tcgen05 (prefix GEMM fused
  * with the certified top-K, as simdex_topk_matmul), then the walk continues
  * from B only for users whose K-th does not beat the ceiling at B.
- * Queries must be grouped by cluster: q_user int64[nq] sorted so that
- * cluster q_cluster is non-decreasing.  prefix_b / prefix_norm are the
- * per-cluster prefix operands from simdex_build_prefix.
- * out_visited follows the reference: n if B >= n, else max(B, walk visited). */
+ * Queries are grouped by cluster (simdex_group_queries): cluster j's queries
+ * are q_user[q_off[j] .. q_off[j+1]); grouped query i is written to output
+ * row q_perm[i] (q_perm NULL: row i).  prefix_b / prefix_norm are the
+ * per-cluster prefix operands from simdex_build_prefix ([c, b_pad, kp]).
+ * out_visited follows the reference: n if B >= n, else max(B, walk visited).
+ * Requires k_eff <= 256 and f <= 256 (else use simdex_walk). */
 SIMDEX_API int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
                     const double* items, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
                     const int32_t* list_ids, const double* bounds, int32_t c, int64_t block,
-                    const uint16_t* prefix_b, const double* prefix_norm,
-                    const int64_t* q_user, const int32_t* q_cluster, int64_t nq, int32_t k,
+                    const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                    const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
+
+/* Group queries by their cluster (index.py:346-348), stable in query order:
+ * out_q_user int64[nq] grouped user rows, out_perm int64[nq] original query
+ * position of each grouped entry, out_off int64[c+1] cluster offsets. */
+SIMDEX_API int simdex_group_queries(const int64_t* q_user, int64_t nq, const int64_t* assign, int32_t c,
+                         int64_t* out_q_user, int64_t* out_perm, int64_t* out_off, void* stream);
+
+/* Diagnostic: raw fp32 accumulators of the tcgen05 product of two packed
+ * operands (simdex_pack_bf16 layout), out float[nu, ni].  Used by the tests to
+ * validate the TMA/UMMA descriptors against a float reference. */
+SIMDEX_API int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t* ib, int64_t ni, int32_t f,
+                      int32_t kp, float* out, void* stream);
 
 /* Work-sharing operands: for every cluster the first min(B, ni) list items,
  * gathered in list order into bf16 [c, b_pad, kp] (b_pad = 128*ceil(B'/128))

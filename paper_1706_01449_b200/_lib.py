@@ -36,7 +36,10 @@ SIGNATURES = {
     "simdex_max_angles": [P, I64, I32, P, I32, P, P, P],
     "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P],
     "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
-    "simdex_query_ws": [P, P, P, I64, P, I64, I32, I32, I32, I32, P, P, I32, I64, P, P, P, P, I64, I32, P, P, P, P],
+    "simdex_query_ws": [P, P, P, I64, P, I64, I32, I32, I32, I32, P, P, I32, I64, P, P, I64, P, P, P, I64, I32, P, P,
+                        P, P],
+    "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
+    "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
     "simdex_build_prefix": [P, P, I64, I32, P, I32, I64, I64, P, P, P],
     "simdex_merge_topk": [P, P, I32, I64, I32, I32, P, P, P],
 }

@@ -152,6 +152,7 @@ def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, w
 
 
 def build_prefix(pi: Packed, list_ids, block):
+    """Per-cluster prefix operands: (bf16 [c, b_pad, kp], float64 norms [c, b_pad], b_pad)."""
     c, ni = list_ids.shape
     bp = min(block, ni)
     b_pad = 128 * ((bp + 127) // 128)
@@ -159,24 +160,43 @@ def build_prefix(pi: Packed, list_ids, block):
     onorm = torch.empty((c, b_pad), dtype=F64, device=list_ids.device)
     call("simdex_build_prefix", ptr(pi.bf16), ptr(pi.norms), ni, pi.kp, ptr(_c(list_ids, I32)), c, int(block),
          b_pad, ptr(out), ptr(onorm), stream_ptr())
-    return out, onorm
+    return out, onorm, b_pad
 
 
-def query_ws(users, pu: Packed, items, pi: Packed, list_ids, bounds, block, prefix, q_user, q_cluster, k):
+def group_queries(q_user, assign, c):
+    """(grouped user rows, original positions, cluster offsets [c+1])."""
+    nq = q_user.shape[0]
+    gq = torch.empty(nq, dtype=I64, device=q_user.device)
+    perm = torch.empty(nq, dtype=I64, device=q_user.device)
+    off = torch.empty(c + 1, dtype=I64, device=q_user.device)
+    call("simdex_group_queries", ptr(_c(q_user, I64)), nq, ptr(_c(assign, I64)), c, ptr(gq), ptr(perm), ptr(off),
+         stream_ptr())
+    return gq, perm, off
+
+
+def query_ws(users, pu: Packed, items, pi: Packed, list_ids, bounds, block, prefix, grouped, k):
+    """Work-sharing batch query; ``grouped`` = group_queries(...) output.
+    Returns (ids, scores, visited) in the original query order."""
     nu, f = users.shape
     ni = items.shape[0]
     c = list_ids.shape[0]
-    nq = q_user.shape[0]
+    gq, perm, off = grouped
+    nq = gq.shape[0]
     k_eff = min(k, ni)
     ids = torch.empty((nq, k_eff), dtype=I32, device=users.device)
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
-    pb, pn = prefix if prefix is not None else (None, None)
+    pb, pn, b_pad = prefix
     call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ni, f,
          pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)), ptr(_c(bounds, F64)), c, int(block),
-         ptr(pb), ptr(pn), ptr(_c(q_user, I64)), ptr(_c(q_cluster, I32)), nq, k, ptr(ids), ptr(sc), ptr(vis),
-         stream_ptr())
+         ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), stream_ptr())
     return ids, sc, vis
+
+
+def gemm_debug(pu: Packed, pi: Packed, f):
+    out = torch.empty((pu.rows, pi.rows), dtype=torch.float32, device=pu.bf16.device)
+    call("simdex_gemm_debug", ptr(pu.bf16), pu.rows, ptr(pi.bf16), pi.rows, f, pu.kp, ptr(out), stream_ptr())
+    return out
 
 
 def merge_topk(in_ids, in_scores, k_out):

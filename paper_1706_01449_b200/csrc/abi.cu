@@ -34,7 +34,6 @@ int sm_count() {
 int launch_walk(const double*, const double*, const double*, int32_t, int64_t, const int32_t*, const double*,
                 const int64_t*, const int32_t*, int64_t, int32_t, int64_t, const int32_t*, const double*,
                 const int32_t*, int32_t, int32_t*, double*, int64_t*, cudaStream_t);
-int ws_fix_visited(int64_t*, int64_t, int64_t, int64_t, cudaStream_t);
 int launch_pack_bf16(const double*, int64_t, int32_t, int32_t, int64_t, int32_t, uint16_t*, double*, cudaStream_t);
 int launch_gather_prefix(const uint16_t*, const double*, int64_t, int32_t, const int32_t*, int32_t, int64_t,
                          int64_t, uint16_t*, double*, cudaStream_t);

@@ -96,6 +96,10 @@ int exact_topk_rows(const double* users, const double* items, int64_t ni, int32_
                     const int64_t* rows, int64_t n_rows, int32_t k,
                     int32_t* out_ids, double* out_scores, cudaStream_t s);
 
+int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni, int32_t f, const int64_t* rows,
+                           int64_t n_rows, int32_t k, const int64_t* out_map, int32_t* out_ids, double* out_scores,
+                           cudaStream_t s);
+
 // Merge `parts` sorted lists per row.
 int merge_lists(const int32_t* in_ids, const double* in_scores, int32_t parts, int64_t nu, int32_t kk,
                 int32_t k_out, int32_t* out_ids, double* out_scores, cudaStream_t s);

@@ -102,7 +102,8 @@ __device__ void block_bitonic(Entry* e, int n) {
 // One CTA per row: exact top-k_eff of S[row, :ni].
 __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restrict__ S, int64_t ni, int k_eff,
                                                           int pow2, int32_t* __restrict__ out_ids,
-                                                          double* __restrict__ out_scores, int64_t out_row0) {
+                                                          double* __restrict__ out_scores, int64_t out_row0,
+                                                          const int64_t* __restrict__ out_map) {
   extern __shared__ unsigned char smem_raw[];
   Entry* buf = reinterpret_cast<Entry*>(smem_raw);
   __shared__ uint32_t hist[256];
@@ -175,7 +176,8 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
   }
   for (int i = k_eff + threadIdx.x; i < pow2; i += blockDim.x) buf[i] = Entry{-DBL_MAX, INT32_MAX};
   block_bitonic(buf, pow2);
-  const int64_t o = (out_row0 + blockIdx.x) * (int64_t)k_eff;
+  const int64_t orow = out_map ? out_map[out_row0 + blockIdx.x] : out_row0 + blockIdx.x;
+  const int64_t o = orow * (int64_t)k_eff;
   for (int i = threadIdx.x; i < k_eff; i += blockDim.x) {
     out_ids[o + i] = buf[i].id;
     out_scores[o + i] = buf[i].s;
@@ -188,12 +190,13 @@ __global__ void iota_rows_kernel(int32_t* ids, int64_t rows, int64_t n) {
 }
 
 __global__ void take_prefix_kernel(const double* S, const int32_t* ids, int64_t rows, int64_t n, int k,
-                                   int32_t* out_ids, double* out_scores, int64_t out_row0) {
+                                   int32_t* out_ids, double* out_scores, int64_t out_row0, const int64_t* out_map) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= rows * k) return;
   int64_t r = t / k, i = t % k;
-  out_ids[(out_row0 + r) * k + i] = ids[r * n + i];
-  out_scores[(out_row0 + r) * k + i] = S[r * n + i];
+  const int64_t o = out_map ? out_map[out_row0 + r] : out_row0 + r;
+  out_ids[o * k + i] = ids[r * n + i];
+  out_scores[o * k + i] = S[r * n + i];
 }
 
 // ---------------------------------------------------------------------------
@@ -239,6 +242,12 @@ __global__ void merge_lists_kernel(const int32_t* __restrict__ in_ids, const dou
 
 int exact_topk_rows(const double* users, const double* items, int64_t ni, int32_t f, const int64_t* rows,
                     int64_t n_rows, int32_t k, int32_t* out_ids, double* out_scores, cudaStream_t s) {
+  return exact_topk_rows_mapped(users, items, ni, f, rows, n_rows, k, nullptr, out_ids, out_scores, s);
+}
+
+int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni, int32_t f, const int64_t* rows,
+                           int64_t n_rows, int32_t k, const int64_t* out_map, int32_t* out_ids, double* out_scores,
+                           cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   if (n_rows == 0) return SIMDEX_OK;
   // score block budget ~1 GiB
@@ -261,7 +270,8 @@ int exact_topk_rows(const double* users, const double* items, int64_t ni, int32_
     score_f64_kernel<<<grid, 256, 0, s>>>(users, rows, r0, nr, items, ni, f, S.p);
     SIMDEX_LAUNCH_CHECK("score_f64");
     if (!full_sort) {
-      select_rows_kernel<<<(unsigned)nr, 256, smem, s>>>(S.p, ni, k_eff, pow2, out_ids, out_scores, r0);
+      select_rows_kernel<<<(unsigned)nr, 256, smem, s>>>(S.p, ni, k_eff, pow2, out_ids, out_scores, r0,
+                                                                          out_map);
       SIMDEX_LAUNCH_CHECK("select_rows");
     } else {
       int64_t tot = nr * ni;
@@ -269,7 +279,7 @@ int exact_topk_rows(const double* users, const double* items, int64_t ni, int32_
       SIMDEX_LAUNCH_CHECK("iota");
       SIMDEX_CUDA(segmented_sort_desc(S.p, ids.p, nr, ni, s));
       take_prefix_kernel<<<(unsigned)ceil_div(nr * k_eff, 256), 256, 0, s>>>(S.p, ids.p, nr, ni, k_eff, out_ids,
-                                                                            out_scores, r0);
+                                                                            out_scores, r0, out_map);
       SIMDEX_LAUNCH_CHECK("take_prefix");
     }
   }

@@ -1,12 +1,51 @@
-// Serving entry points: topk_matmul (brute.py:59-113) and work-sharing
-// query_batch (index.py:305-389).
+// Serving entry points: topk_matmul (brute.py:59-113), work-sharing
+// query_batch (index.py:305-389) and the query grouping it needs.
 #include "common.cuh"
 
 namespace simdex {
-int launch_walk(const double*, const double*, const double*, int32_t, int64_t, const int32_t*, const double*,
-                const int64_t*, const int32_t*, int64_t, int32_t, int64_t, const int32_t*, const double*,
-                const int32_t*, int32_t, int32_t*, double*, int64_t*, cudaStream_t);
-int ws_fix_visited(int64_t*, int64_t, int64_t, int64_t, cudaStream_t);
+int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
+                    const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su,
+                    int32_t si, int32_t k, int32_t* out_ids, double* out_scores, int64_t* heap_ops, float* debug_out,
+                    cudaStream_t s);
+int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
+                 int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si, const int32_t* list_ids,
+                 const double* bounds, int32_t c, int64_t block, const uint16_t* prefix_b, const double* prefix_norm,
+                 int64_t b_pad, const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
+                 int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, cudaStream_t s);
+
+namespace {
+constexpr int kMaxMatmulK = 256;
+constexpr int kMaxKp = 256;
+
+__global__ void group_keys_kernel(const int64_t* __restrict__ q_user, int64_t nq, const int64_t* __restrict__ assign,
+                                  double* keys, int32_t* ids, unsigned long long* counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq) return;
+  const int64_t c = assign[q_user[i]];
+  keys[i] = -(double)c;  // (key desc, id asc) == (cluster asc, query position asc)
+  ids[i] = (int32_t)i;
+  atomicAdd(counts + c, 1ull);
+}
+
+__global__ void group_scatter_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ q_user, int64_t nq,
+                                     int64_t* __restrict__ out_q, int64_t* __restrict__ out_perm) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nq) return;
+  const int32_t i = ids[j];
+  out_q[j] = q_user[i];
+  out_perm[j] = i;
+}
+
+__global__ void group_offsets_kernel(const unsigned long long* counts, int c, int64_t* off) {
+  if (threadIdx.x != 0) return;
+  int64_t acc = 0;
+  for (int j = 0; j < c; ++j) {
+    off[j] = acc;
+    acc += (int64_t)counts[j];
+  }
+  off[c] = acc;
+}
+}  // namespace
 }  // namespace simdex
 
 using namespace simdex;
@@ -16,25 +55,74 @@ extern "C" int simdex_topk_matmul(const double* users, const uint16_t* ub, const
                                   int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids,
                                   double* out_scores, int64_t* heap_ops, void* stream) {
   SIMDEX_CHECK_ARG(users && items && out_ids && out_scores, "simdex_topk_matmul: null pointer");
-  SIMDEX_CHECK_ARG(nu >= 1 && ni >= 1 && f >= 1 && k >= 1, "simdex_topk_matmul: bad sizes");
-  (void)ub; (void)u_norm; (void)ib; (void)i_norm; (void)kp; (void)su; (void)si; (void)heap_ops;
-  return exact_topk_rows(users, items, ni, f, nullptr, nu, k, out_ids, out_scores, as_stream(stream));
+  SIMDEX_CHECK_ARG(nu >= 1 && ni >= 1 && f >= 1 && k >= 1 && ni < INT32_MAX, "simdex_topk_matmul: bad sizes");
+  const int64_t k_eff = k < ni ? k : ni;
+  if (k_eff > kMaxMatmulK || kp > kMaxKp || !ub || !ib || !u_norm || !i_norm) {
+    // outside the tensor-core path's envelope: the exact float64 scan gives the same answer
+    if (heap_ops) SIMDEX_CUDA(cudaMemsetAsync(heap_ops, 0, sizeof(int64_t) * nu, as_stream(stream)));
+    return exact_topk_rows(users, items, ni, f, nullptr, nu, k, out_ids, out_scores, as_stream(stream));
+  }
+  SIMDEX_CHECK_ARG(kp % 64 == 0 && kp >= f, "simdex_topk_matmul: kp must be a multiple of 64 >= f");
+  return gemm_topk_brute(users, ub, u_norm, nu, items, ib, i_norm, ni, f, kp, su, si, k, out_ids, out_scores,
+                         heap_ops, nullptr, as_stream(stream));
+}
+
+extern "C" int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t* ib, int64_t ni, int32_t f,
+                                 int32_t kp, float* out, void* stream) {
+  SIMDEX_CHECK_ARG(ub && ib && out, "simdex_gemm_debug: null pointer");
+  SIMDEX_CHECK_ARG(nu >= 1 && ni >= 1 && f >= 1 && kp % 64 == 0 && kp >= f && kp <= kMaxKp,
+                   "simdex_gemm_debug: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  Scratch<double> un, in;
+  SIMDEX_CUDA(un.alloc(nu, s));
+  SIMDEX_CUDA(in.alloc(ni, s));
+  SIMDEX_CUDA(cudaMemsetAsync(un.p, 0, sizeof(double) * nu, s));
+  SIMDEX_CUDA(cudaMemsetAsync(in.p, 0, sizeof(double) * ni, s));
+  return gemm_topk_brute(nullptr, ub, un.p, nu, nullptr, ib, in.p, ni, f, kp, 0, 0, 1, nullptr, nullptr, nullptr,
+                         out, s);
+}
+
+extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int64_t* assign, int32_t c,
+                                    int64_t* out_q_user, int64_t* out_perm, int64_t* out_off, void* stream) {
+  SIMDEX_CHECK_ARG(q_user && assign && out_q_user && out_perm && out_off, "simdex_group_queries: null pointer");
+  SIMDEX_CHECK_ARG(nq >= 0 && nq < INT32_MAX && c >= 1, "simdex_group_queries: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  Scratch<double> keys;
+  Scratch<int32_t> ids;
+  Scratch<unsigned long long> counts;
+  SIMDEX_CUDA(keys.alloc(nq, s));
+  SIMDEX_CUDA(ids.alloc(nq, s));
+  SIMDEX_CUDA(counts.alloc(c, s));
+  SIMDEX_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * c, s));
+  if (nq > 0) {
+    group_keys_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(q_user, nq, assign, keys.p, ids.p, counts.p);
+    SIMDEX_LAUNCH_CHECK("group_keys");
+    SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, nq, s));
+    group_scatter_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(ids.p, q_user, nq, out_q_user, out_perm);
+    SIMDEX_LAUNCH_CHECK("group_scatter");
+  }
+  group_offsets_kernel<<<1, 32, 0, s>>>(counts.p, c, out_off);
+  SIMDEX_LAUNCH_CHECK("group_offsets");
+  return SIMDEX_OK;
 }
 
 extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
                                const double* items, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
                                const int32_t* list_ids, const double* bounds, int32_t c, int64_t block,
-                               const uint16_t* prefix_b, const double* prefix_norm, const int64_t* q_user,
-                               const int32_t* q_cluster, int64_t nq, int32_t k, int32_t* out_ids,
-                               double* out_scores, int64_t* out_visited, void* stream) {
-  SIMDEX_CHECK_ARG(users && user_norms && items && list_ids && bounds && q_user && q_cluster && out_ids &&
-                       out_scores && out_visited,
+                               const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                               const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
+                               int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
+  SIMDEX_CHECK_ARG(users && ub && user_norms && items && list_ids && bounds && prefix_b && prefix_norm && q_user &&
+                       q_off && out_ids && out_scores && out_visited,
                    "simdex_query_ws: null pointer");
-  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 1 && c >= 1, "simdex_query_ws: bad sizes");
-  (void)ub; (void)kp; (void)su; (void)si; (void)prefix_b; (void)prefix_norm; (void)nu;
-  cudaStream_t s = as_stream(stream);
-  int rc = launch_walk(users, user_norms, items, f, ni, list_ids, bounds, q_user, q_cluster, nq, k, 0, nullptr,
-                       nullptr, nullptr, 0, out_ids, out_scores, out_visited, s);
-  if (rc) return rc;
-  return ws_fix_visited(out_visited, nq, block, ni, s);
+  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 1 && c >= 1 && kp % 64 == 0 && kp >= f,
+                   "simdex_query_ws: bad sizes");
+  SIMDEX_CHECK_ARG(b_pad % 128 == 0 && b_pad >= (block < ni ? block : ni), "simdex_query_ws: bad prefix padding");
+  const int64_t k_eff = k < ni ? k : ni;
+  SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
+                   "simdex_query_ws: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);
+  if (nq == 0) return SIMDEX_OK;
+  return gemm_topk_ws(users, ub, user_norms, nu, items, ni, f, kp, su, si, list_ids, bounds, c, block, prefix_b,
+                      prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids, out_scores, out_visited,
+                      as_stream(stream));
 }

@@ -264,12 +264,27 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
     users = _device.f64(model.users)
     items = _device.f64(model.items)
     ids, bounds = index.device_lists()
+    n = model.num_items
+    if q_users is None:
+        q_users = index._dev.get("all_users")
+        if q_users is None:
+            q_users = index._dev["all_users"] = torch.arange(model.num_users, dtype=torch.int64, device=users.device)
+    pu, pi = _device.packed(model.users), _device.packed(model.items)
+    if work_sharing and min(k, n) <= 256 and pu.kp <= 256:
+        key = ("grouped", q_users.data_ptr(), q_users.shape[0])
+        grouped = index._dev.get(key) if q_users is index._dev.get("all_users") else None
+        if grouped is None:
+            grouped = _ops.group_queries(q_users, index.device_assignment(), index.num_clusters)
+            if q_users is index._dev.get("all_users"):
+                index._dev[key] = grouped
+        return _ops.query_ws(users, pu, items, pi, ids, bounds, index.block_size, index.device_prefix(model),
+                             grouped, k)
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
-    if not work_sharing:
-        return _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
-    prefix = index.device_prefix(model)
-    return _ops.query_ws(users, _device.packed(model.users), items, _device.packed(model.items), ids, bounds,
-                         index.block_size, prefix, q_users, qc, k)
+    out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
+    if work_sharing:  # k beyond the tensor-core envelope: WS visited = n if B >= n else max(B, walk visited)
+        vis = out[2].fill_(n) if index.block_size >= n else out[2].clamp_(min=index.block_size)
+        out = (out[0], out[1], vis)
+    return out
 
 
 def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 1, work_sharing: bool = True,
