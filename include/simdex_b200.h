@@ -51,6 +51,14 @@ SIMDEX_API int simdex_abi_version(void);
 SIMDEX_API const char* simdex_last_error(void);
 /* Number of kernels this library has launched in the process (monotone). */
 SIMDEX_API int64_t simdex_launch_count(void);
+/* Optional per-kernel timing: with profiling on, the library records a CUDA
+ * event pair on the launching stream around its main kernels (gemm_topk,
+ * finalize, walk, kmeans_assign, ...); simdex_profile_read(name, ...) returns
+ * the accumulated milliseconds and launch count for that kernel name (it
+ * synchronises on the recorded events). */
+SIMDEX_API int simdex_profile_enable(int on);
+SIMDEX_API int simdex_profile_read(const char* name, double* total_ms, int64_t* launches);
+SIMDEX_API int simdex_profile_reset(void);
 /* sm count / compute capability of `device` (host outputs). */
 SIMDEX_API int simdex_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 
@@ -135,10 +143,14 @@ SIMDEX_API int simdex_max_angles(const double* users, int64_t n, int32_t f, cons
  * theta_ic (zero-norm item / zero center -> pi/2, index.py:103-116), Eq. 2
  * ceiling (index.py:119-121), and per-cluster sort by (ceiling desc, id asc)
  * (index.py:124-126) -- a device merge sort.
- * out_item_norms float64[ni], out_list_ids int32[c, ni], out_bounds float64[c, ni]. */
+ * out_item_norms float64[ni], out_list_ids int32[c, ni], out_bounds float64[c, ni],
+ * out_list_pos int32[c, ni] (nullable): position of item i in cluster c's list. */
 SIMDEX_API int simdex_build_index(const double* items, int64_t ni, int32_t f, const double* centers,
                        const double* theta_b, int32_t c, double* out_item_norms,
-                       int32_t* out_list_ids, double* out_bounds, void* stream);
+                       int32_t* out_list_ids, double* out_bounds, int32_t* out_list_pos, void* stream);
+
+/* Inverse list permutation: out_pos[c, list_ids[c, j]] = j (int32[c, ni]). */
+SIMDEX_API int simdex_list_positions(const int32_t* list_ids, int32_t c, int64_t ni, int32_t* out_pos, void* stream);
 
 /* ------------------------------------------------------------------------
  * Index walk (index.py:185-389)
@@ -167,11 +179,17 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
  * are q_user[q_off[j] .. q_off[j+1]); grouped query i is written to output
  * row q_perm[i] (q_perm NULL: row i).  prefix_b / prefix_norm are the
  * per-cluster prefix operands from simdex_build_prefix ([c, b_pad, kp]).
+ * Users whose K-th does not beat the ceiling at B are finished by a second
+ * certified tensor-core pass over the whole catalogue (ib / item_norms, the
+ * simdex_pack_bf16 operand of the items); their Algorithm 1 stop position
+ * then follows in closed form from the exact top-K (list_pos = inverse of
+ * list_ids, from simdex_build_index).
  * out_visited follows the reference: n if B >= n, else max(B, walk visited).
  * Requires k_eff <= 256 and f <= 256 (else use simdex_walk). */
 SIMDEX_API int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
-                    const double* items, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
-                    const int32_t* list_ids, const double* bounds, int32_t c, int64_t block,
+                    const double* items, const uint16_t* ib, const double* item_norms, int64_t ni,
+                    int32_t f, int32_t kp, int32_t su, int32_t si,
+                    const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                     const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);

@@ -26,6 +26,9 @@ SIGNATURES = {
     "simdex_abi_version": [],
     "simdex_last_error": [],
     "simdex_launch_count": [],
+    "simdex_profile_enable": [C.c_int],
+    "simdex_profile_read": [C.c_char_p, P, P],
+    "simdex_profile_reset": [],
     "simdex_device_info": [C.c_int, P, P, P],
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
     "simdex_pack_bf16": [P, I64, I32, I32, I64, I32, P, P, P],
@@ -34,10 +37,11 @@ SIGNATURES = {
     "simdex_kmeans_assign": [P, I64, I32, P, I32, P, P, P, P, P, P],
     "simdex_kmeans_update": [P, I64, I32, P, I32, P, P, P, P, P],
     "simdex_max_angles": [P, I64, I32, P, I32, P, P, P],
-    "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P],
+    "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P, P],
+    "simdex_list_positions": [P, I32, I64, P, P],
     "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
-    "simdex_query_ws": [P, P, P, I64, P, I64, I32, I32, I32, I32, P, P, I32, I64, P, P, I64, P, P, P, I64, I32, P, P,
-                        P, P],
+    "simdex_query_ws": [P, P, P, I64, P, P, P, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64, P, P, P, I64,
+                        I32, P, P, P, P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
     "simdex_build_prefix": [P, P, I64, I32, P, I32, I64, I64, P, P, P],
@@ -95,6 +99,20 @@ def call(name, *args):
 def launch_count() -> int:
     """Kernels launched by the library so far in this process."""
     return int(load().simdex_launch_count())
+
+
+def profile(on: bool = True) -> None:
+    """Record CUDA events around the library's main kernels (simdex_profile_*)."""
+    call("simdex_profile_reset")
+    call("simdex_profile_enable", 1 if on else 0)
+
+
+def profile_read(name: str):
+    """(total milliseconds, launches) recorded for kernel ``name``."""
+    ms = C.c_double(0.0)
+    n = C.c_int64(0)
+    call("simdex_profile_read", name.encode(), C.byref(ms), C.byref(n))
+    return ms.value, n.value
 
 
 def ptr(t):

@@ -124,15 +124,24 @@ def max_angles(users, centers, assign):
     return theta
 
 
-def build_index(items, centers, theta):
+def build_index(items, centers, theta, with_pos=False):
+    """(item norms, list ids [c, n], ceilings [c, n][, inverse positions [c, n]])."""
     ni, f = items.shape
     c = centers.shape[0]
     norms = torch.empty(ni, dtype=F64, device=items.device)
     ids = torch.empty((c, ni), dtype=I32, device=items.device)
     bounds = torch.empty((c, ni), dtype=F64, device=items.device)
+    pos = torch.empty((c, ni), dtype=I32, device=items.device) if with_pos else None
     call("simdex_build_index", ptr(_c(items, F64)), ni, f, ptr(_c(centers, F64)), ptr(_c(theta, F64)), c,
-         ptr(norms), ptr(ids), ptr(bounds), stream_ptr())
-    return norms, ids, bounds
+         ptr(norms), ptr(ids), ptr(bounds), ptr(pos), stream_ptr())
+    return (norms, ids, bounds, pos) if with_pos else (norms, ids, bounds)
+
+
+def list_positions(list_ids):
+    c, ni = list_ids.shape
+    pos = torch.empty((c, ni), dtype=I32, device=list_ids.device)
+    call("simdex_list_positions", ptr(_c(list_ids, I32)), c, ni, ptr(pos), stream_ptr())
+    return pos
 
 
 def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, warm=None, no_prune=False):
@@ -174,7 +183,7 @@ def group_queries(q_user, assign, c):
     return gq, perm, off
 
 
-def query_ws(users, pu: Packed, items, pi: Packed, list_ids, bounds, block, prefix, grouped, k):
+def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k):
     """Work-sharing batch query; ``grouped`` = group_queries(...) output.
     Returns (ids, scores, visited) in the original query order."""
     nu, f = users.shape
@@ -187,8 +196,9 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, bounds, block, pref
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
-    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ni, f,
-         pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)), ptr(_c(bounds, F64)), c, int(block),
+    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(pi.bf16),
+         ptr(pi.norms), ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)), ptr(_c(list_pos, I32)),
+         ptr(_c(bounds, F64)), c, int(block),
          ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), stream_ptr())
     return ids, sc, vis
 

@@ -1,6 +1,10 @@
 // C-ABI entry points (include/simdex_b200.h) that are not defined next to
 // their kernels, plus the shared error state.
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 #include <cstdarg>
 #include <cstring>
 
@@ -12,6 +16,38 @@ static thread_local char g_err[1024] = "";
 static std::atomic<int64_t> g_launches{0};
 
 void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------
+// optional per-kernel event timing (simdex_profile_*): events are recorded on
+// the launching stream around the named kernels, read back on demand.
+// ---------------------------------------------------------------------------
+namespace {
+struct Pending {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<Pending> g_pending;
+std::map<std::string, std::pair<double, int64_t>> g_prof_acc;
+}  // namespace
+
+ProfileScope::ProfileScope(const char* name, cudaStream_t s) : s_(s) {
+  if (!g_prof_on) return;
+  name_ = name;
+  cudaEventCreate(&a_);
+  cudaEventCreate(&b_);
+  cudaEventRecord(a_, s);
+  on_ = true;
+}
+
+void ProfileScope::end() {
+  if (!on_) return;
+  on_ = false;
+  cudaEventRecord(b_, s_);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_pending.push_back(Pending{name_, a_, b_});
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -47,6 +83,44 @@ extern "C" int simdex_abi_version(void) { return SIMDEX_ABI_VERSION; }
 extern "C" const char* simdex_last_error(void) { return g_err; }
 
 extern "C" int64_t simdex_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+extern "C" int simdex_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_profile_read(const char* name, double* total_ms, int64_t* launches) {
+  SIMDEX_CHECK_ARG(name && total_ms && launches, "simdex_profile_read: null pointer");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& p : g_pending) {
+    float ms = 0.f;
+    SIMDEX_CUDA(cudaEventSynchronize(p.b));
+    SIMDEX_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto& acc = g_prof_acc[p.name];
+    acc.first += ms;
+    acc.second += 1;
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  g_pending.clear();
+  auto it = g_prof_acc.find(name);
+  *total_ms = it == g_prof_acc.end() ? 0.0 : it->second.first;
+  *launches = it == g_prof_acc.end() ? 0 : it->second.second;
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& p : g_pending) {
+    cudaEventSynchronize(p.b);
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  g_pending.clear();
+  g_prof_acc.clear();
+  return SIMDEX_OK;
+}
 
 extern "C" int simdex_device_info(int device, int* sms, int* major, int* minor) {
   SIMDEX_CHECK_ARG(sms && major && minor, "simdex_device_info: null pointer");

@@ -40,6 +40,20 @@ void count_launches(int64_t n);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// RAII event pair around a kernel launch when simdex_profile_enable(1) is set.
+class ProfileScope {
+ public:
+  ProfileScope(const char* name, cudaStream_t s);
+  ~ProfileScope() { end(); }
+  void end();
+
+ private:
+  std::string name_;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+  cudaStream_t s_;
+  bool on_ = false;
+};
+
 // Stream-ordered scratch allocation (freed on the same stream).
 template <class T>
 struct Scratch {

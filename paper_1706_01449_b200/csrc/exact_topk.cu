@@ -267,11 +267,15 @@ int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni,
   for (int64_t r0 = 0; r0 < n_rows; r0 += rb) {
     int64_t nr = (n_rows - r0 < rb) ? n_rows - r0 : rb;
     dim3 grid((unsigned)ceil_div(ni, kTile), (unsigned)ceil_div(nr, kTile));
+    ProfileScope _prof("score_f64", s);
     score_f64_kernel<<<grid, 256, 0, s>>>(users, rows, r0, nr, items, ni, f, S.p);
+    _prof.end();
     SIMDEX_LAUNCH_CHECK("score_f64");
     if (!full_sort) {
+      ProfileScope _prof("select_rows", s);
       select_rows_kernel<<<(unsigned)nr, 256, smem, s>>>(S.p, ni, k_eff, pow2, out_ids, out_scores, r0,
                                                                           out_map);
+      _prof.end();
       SIMDEX_LAUNCH_CHECK("select_rows");
     } else {
       int64_t tot = nr * ni;

@@ -1,6 +1,5 @@
 // Fused users x items tensor-core product + certified running top-K
-// (brute.py:59-113 topk_matmul; the work-sharing prefix product of
-// index.py:351-371).
+// (brute.py:59-113 topk_matmul; the work-sharing product of index.py:351-371).
 //
 // Persistent, warp-specialised sm_100a kernel.  A work unit is 256 users
 // (two 128-row M tiles that share every item tile) against one item
@@ -22,26 +21,24 @@
 // keeps candidates with hi = v + e_j >= T, where T is the k-th largest
 // lo = v - e_j seen so far (a valid lower bound on the exact k-th score);
 // items dropped or never kept have s <= hi < T <= s_k, so they cannot be in
-// the exact top-k (not even by the id tie rule).  The survivors are rescored
-// exactly in float64 and ordered (score desc, id asc) by the finalize kernel.
-// A row whose band outgrows its buffer is flagged and recomputed by the exact
-// float64 path.
+// the exact top-k (not even by the id tie rule).  For k <= 32 the top-k of
+// the lower bounds is held in registers (a branch-free insertion network), so
+// T is always exact-current and the buffer only needs a linear filter; larger
+// k keeps lower bounds in the buffer and re-selects T when it fills.  The
+// survivors are rescored exactly in float64 and ordered (score desc, id asc)
+// by the finalize kernel.  A row whose band outgrows its buffer is flagged and
+// recomputed by the exact float64 path.
 #include <cuda.h>
 
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
 
 namespace simdex {
 
-int launch_walk_tasks(const double* users, const double* unorm, const double* items, int32_t f, int64_t n,
-                      const int32_t* list_ids, const double* bounds, const int64_t* tasks, const int32_t* n_tasks_dev,
-                      int64_t n_tasks_max, const int64_t* q_user, const int32_t* q_cluster, const int64_t* q_out,
-                      int32_t k, int64_t start, const int32_t* warm_ids, const double* warm_scores,
-                      const int32_t* warm_count, int32_t no_prune, int64_t ws_floor, int32_t* out_ids,
-                      double* out_scores, int64_t* out_visited, cudaStream_t s);
 int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni, int32_t f, const int64_t* rows,
                            int64_t n_rows, int32_t k, const int64_t* out_map, int32_t* out_ids, double* out_scores,
                            cudaStream_t s);
@@ -56,7 +53,6 @@ constexpr int kSlab = kTileM * 128;  // one [128 rows x 64 bf16] swizzled slab: 
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kMaxCap = 512;
-constexpr int kMaxKB = 4;  // kp <= 256
 constexpr uint32_t kIdesc = idesc_bf16_f32(kTileM, kTileN);
 
 struct Unit {
@@ -78,9 +74,9 @@ struct TopkParams {
   int stages;
   int cap;
   int k_eff;
-  int32_t* cand_id;
-  float* cand_lo;
-  float* cand_hi;
+  int32_t* cand_id;  // [A rows, cap]
+  float* cand_lo;    // [A rows, cap] (k > 32 only)
+  float* cand_hi;    // [A rows, cap]
   int32_t* row_count;
   int32_t* row_flags;
   int64_t* heap_ops;
@@ -123,9 +119,9 @@ __device__ __noinline__ float kth_largest(float* a, int n, int k) {
   return a[lo];
 }
 
-// Raise T to the k-th largest lower bound in the buffer and drop every entry
+// k > 32: raise T to the k-th largest lower bound in the buffer, drop entries
 // whose upper bound falls below it.
-__device__ __noinline__ void compact_row(float* lo, float* hi, int32_t* id, int& cnt, float& T, int k_eff) {
+__device__ __noinline__ void compact_select(float* lo, float* hi, int32_t* id, int& cnt, float& T, int k_eff) {
   float tmp[kMaxCap];
   for (int e = 0; e < cnt; ++e) tmp[e] = lo[e];
   const float kth = kth_largest(tmp, cnt, k_eff);
@@ -142,6 +138,96 @@ __device__ __noinline__ void compact_row(float* lo, float* hi, int32_t* id, int&
   cnt = w;
 }
 
+// k > 32, warp-cooperative: the 32 lanes jointly re-select lane `who`'s
+// threshold T = k-th largest lower bound in its buffer (bitwise radix search
+// over order-preserving keys, one warp-wide count per bit) and compact the
+// buffer to the entries with hi >= T, preserving order.  Called with the whole
+// warp converged; returns the new (cnt, T) of that lane.
+__device__ __forceinline__ uint32_t f2key(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__device__ __noinline__ void warp_compact(float* lo, float* hi, int32_t* id, int cnt, int k_eff, float T_old,
+                                          int lane, int* cnt_out, float* T_out) {
+  constexpr int kPer = kMaxCap / 32;
+  uint32_t key[kPer];
+  float h[kPer];
+  int32_t ids[kPer];
+#pragma unroll
+  for (int t = 0; t < kPer; ++t) {
+    const int e = t * 32 + lane;
+    key[t] = 0u;
+    h[t] = -INFINITY;
+    ids[t] = 0;
+    if (e < cnt) {
+      key[t] = f2key(lo[e]);
+      h[t] = hi[e];
+      ids[t] = id[e];
+    }
+  }
+  uint32_t thr = 0;
+  for (int b = 31; b >= 0; --b) {
+    const uint32_t cand = thr | (1u << b);
+    int c = 0;
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) c += (t * 32 + lane < cnt && key[t] >= cand) ? 1 : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (c >= k_eff) thr = cand;
+  }
+  float T = key2f(thr);
+  if (T_old > T) T = T_old;
+  __syncwarp();
+  int w = 0;
+#pragma unroll
+  for (int t = 0; t < kPer; ++t) {
+    const bool keep = (t * 32 + lane < cnt) && h[t] >= T;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int dst = w + __popc(m & ((1u << lane) - 1u));
+      lo[dst] = key2f(key[t]);
+      hi[dst] = h[t];
+      id[dst] = ids[t];
+    }
+    w += __popc(m);
+  }
+  *cnt_out = w;
+  *T_out = T;
+}
+
+// k <= 32: drop entries whose upper bound is below the (current) T.
+__device__ __noinline__ void compact_filter(float* hi, int32_t* id, int& cnt, float T) {
+  int w = 0;
+  for (int e = 0; e < cnt; ++e) {
+    if (hi[e] >= T) {
+      hi[w] = hi[e];
+      id[w] = id[e];
+      ++w;
+    }
+  }
+  cnt = w;
+}
+
+// sorted-descending top-KT insertion network: t <- top-KT of t + {x}
+template <int KT>
+__device__ __forceinline__ void push_top(float (&t)[KT], float x) {
+#pragma unroll
+  for (int i = KT - 1; i > 0; --i) t[i] = fmaxf(t[i], fminf(t[i - 1], x));
+  t[0] = fmaxf(t[0], x);
+}
+
+template <int KT>
+__device__ __forceinline__ float top_at(const float (&t)[KT], int k) {
+  float r = t[0];
+#pragma unroll
+  for (int i = 1; i < KT; ++i) r = (i == k) ? t[i] : r;
+  return r;
+}
+
+template <int KT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_topk_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const TopkParams p) {
@@ -250,10 +336,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
-    const int h = ew >> 2;         // M tile of this warp
-    const int q = warp & 3;        // TMEM lane quarter this warp may access
+    const int h = ew >> 2;   // M tile of this warp
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_local = h * kTileM + q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int kk = p.k_eff - 1;
     uint32_t acc = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const Unit un = p.units[u];
@@ -262,6 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t grow = un.a_row0 + row_local;
       const float cu = live ? p.row_cu[grow] : 0.f;
       float T = -INFINITY;
+      float top[KT > 0 ? KT : 1];
+#pragma unroll
+      for (int i = 0; i < (KT > 0 ? KT : 1); ++i) top[i] = -INFINITY;
       int cnt = 0, flags = 0;
       int64_t hops = 0;
       int32_t* my_id = p.cand_id + grow * p.cap;
@@ -279,36 +369,64 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (nvalid <= 0) break;
             float v[32];
             tmem_ld32(tbase + lane_off + (buf * 2 + h) * kTileN + ch * 32, v);
-            if (!live) continue;
             if (p.debug_out) {
+              if (live) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < nvalid) p.debug_out[grow * p.debug_ld + un.b_row0 + c0 + i] = v[i];
+                for (int i = 0; i < 32; ++i)
+                  if (i < nvalid) p.debug_out[grow * p.debug_ld + un.b_row0 + c0 + i] = v[i];
+              }
               continue;
             }
-            if (flags) continue;
-            float mx = -INFINITY;
+            const bool act = live && !flags;
+            if (act) {
+              float mx = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, i < nvalid ? v[i] : -INFINITY);
-            const float nmax = __ldg(p.item_nmax32 + ((un.b_row0 + c0) >> 5));
-            if (fmaf(cu, nmax, mx) + p.e_abs >= T) {
-              const float* nrm = p.item_nrm + un.b_row0 + c0;
+              for (int i = 0; i < 32; ++i) mx = fmaxf(mx, i < nvalid ? v[i] : -INFINITY);
+              const float nmax = __ldg(p.item_nmax32 + ((un.b_row0 + c0) >> 5));
+              if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
+                const float* nrm = p.item_nrm + un.b_row0 + c0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                if (i < nvalid) {
-                  const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
-                  const float hi = v[i] + e;
-                  if (hi >= T && !flags) {
-                    my_lo[cnt] = v[i] - e;
-                    my_hi[cnt] = hi;
-                    my_id[cnt] = c0 + i;
-                    ++cnt;
-                    ++hops;
-                    if (cnt == p.cap) {
-                      compact_row(my_lo, my_hi, my_id, cnt, T, p.k_eff);
-                      if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
+                for (int i = 0; i < 32; ++i) {
+                  if (i < nvalid) {
+                    const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
+                    const float hi = v[i] + e;
+                    if (hi >= T && !flags) {
+                      my_hi[cnt] = hi;
+                      my_id[cnt] = c0 + i;
+                      ++cnt;
+                      ++hops;
+                      if constexpr (KT > 0) {
+                        push_top<KT>(top, v[i] - e);
+                        T = top_at<KT>(top, kk);
+                        if (cnt == p.cap) {
+                          compact_filter(my_hi, my_id, cnt, T);
+                          if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
+                        }
+                      } else {
+                        my_lo[cnt - 1] = v[i] - e;  // the buffer always has >= 32 free slots here
+                      }
                     }
                   }
+                }
+              }
+            }
+            if constexpr (KT == 0) {
+              // keep >= 32 free slots per row: re-select T for every full row, warp-cooperatively
+              unsigned need = __ballot_sync(0xffffffffu, act && cnt > p.cap - 32);
+              while (need) {
+                const int who = __ffs(need) - 1;
+                need &= need - 1;
+                const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+                const int c_w = __shfl_sync(0xffffffffu, cnt, who);
+                const float t_w = __shfl_sync(0xffffffffu, T, who);
+                int nc;
+                float nt;
+                warp_compact(p.cand_lo + g_w * p.cap, p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, c_w,
+                             p.k_eff, t_w, lane, &nc, &nt);
+                if (lane == who) {
+                  cnt = nc;
+                  T = nt;
+                  if (cnt > p.cap - 32 - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
                 }
               }
             }
@@ -318,8 +436,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(t_empty + buf);
       }
+      if constexpr (KT == 0) {
+        // final re-selection of T for every row of this warp (warp-cooperative)
+        if (h < ntile_a && !p.debug_out) {
+          unsigned need = __ballot_sync(0xffffffffu, live && !flags && cnt > p.k_eff);
+          while (need) {
+            const int who = __ffs(need) - 1;
+            need &= need - 1;
+            const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+            const int c_w = __shfl_sync(0xffffffffu, cnt, who);
+            const float t_w = __shfl_sync(0xffffffffu, T, who);
+            int nc;
+            float nt;
+            warp_compact(p.cand_lo + g_w * p.cap, p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, c_w, p.k_eff,
+                         t_w, lane, &nc, &nt);
+            if (lane == who) {
+              cnt = nc;
+              T = nt;
+            }
+          }
+        }
+      }
       if (live && h < ntile_a) {
-        if (!flags && !p.debug_out && cnt > p.k_eff) compact_row(my_lo, my_hi, my_id, cnt, T, p.k_eff);
+        if constexpr (KT > 0) {
+          if (!flags && !p.debug_out && cnt > p.k_eff) compact_filter(my_hi, my_id, cnt, T);
+        }
         p.row_count[grow] = cnt;
         p.row_flags[grow] = flags;
         if (p.heap_ops) p.heap_ops[grow] = hops;
@@ -360,16 +501,21 @@ __global__ void item_nrm_kernel(const double* __restrict__ norms, int64_t rows, 
 // ---------------------------------------------------------------------------
 // finalize: exact float64 rescoring of the certified candidates (warp per row)
 // ---------------------------------------------------------------------------
+enum FinalizeMode { kBrute = 0, kPrefix = 1, kFullList = 2 };
+
 struct FinalizeParams {
+  int mode;
   int64_t total_rows;
+  const int32_t* n_rows_dev;   // device row count (stage 2); null: total_rows
   const int64_t* row_user;     // packed row -> user row (-1 = padding); null = identity (< nu)
   const int64_t* row_out;      // packed row -> output row; null = identity
-  const int32_t* row_cluster;  // packed row -> cluster (work sharing); null = brute force
+  const int32_t* row_cluster;  // packed row -> cluster
   int64_t nu;
   const double* users;
   const double* items;
   int f;
-  const int32_t* list_ids;  // [C, n] (work sharing)
+  const int32_t* list_ids;  // [C, n]
+  const int32_t* list_pos;  // [C, n] inverse of list_ids (full-list mode)
   const double* bounds;     // [C, n]
   const double* unorm;      // [nu]
   int64_t n;                // list length (= items)
@@ -381,15 +527,27 @@ struct FinalizeParams {
   const int32_t* row_flags;
   int32_t* out_ids;
   double* out_scores;
-  int64_t* out_visited;  // work sharing
-  int32_t* warm_count;   // work sharing: entries held at B
-  int64_t* walk_list;
-  int32_t* walk_n;
+  int64_t* out_visited;
+  int64_t* cont_list;  // prefix mode: rows that continue past B
+  int32_t* cont_n;
   int64_t* over_list;
   int64_t* over_out;
   int32_t* over_n;
   int pow2;
 };
+
+// First list position j with bounds[j] * unorm < s (ceilings are non-increasing).
+__device__ int64_t ceiling_count(const double* b, int64_t n, double unorm, double s) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (b[mid] * unorm >= s)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
 
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   extern __shared__ unsigned char smem[];
@@ -400,16 +558,21 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   double* us = reinterpret_cast<double*>(mine);
   double* ss = us + p.f;
   int32_t* si = reinterpret_cast<int32_t*>(ss + p.pow2);
-  if (r >= p.total_rows) return;
+  const int64_t total = p.n_rows_dev ? (int64_t)*p.n_rows_dev : p.total_rows;
+  if (r >= total) return;
   const int64_t user = p.row_user ? p.row_user[r] : r;
   if (user < 0 || user >= p.nu) return;
   const int64_t out = p.row_out ? p.row_out[r] : r;
-  const int c = p.row_cluster ? p.row_cluster[r] : 0;
+  const int c = p.mode != kBrute ? p.row_cluster[r] : 0;
   if (p.row_flags[r]) {
     if (lane == 0) {
-      const int slot = atomicAdd(p.over_n, 1);
-      p.over_list[slot] = p.row_cluster ? r : user;
-      p.over_out[slot] = out;
+      if (p.mode == kPrefix) {  // band overflow on the prefix: redo it on the full list
+        p.cont_list[atomicAdd(p.cont_n, 1)] = r;
+      } else {
+        const int slot = atomicAdd(p.over_n, 1);
+        p.over_list[slot] = p.mode == kBrute ? user : r;
+        p.over_out[slot] = out;
+      }
     }
     return;
   }
@@ -420,7 +583,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   for (int e = lane; e < p.pow2; e += 32) {
     if (e < cnt) {
       const int32_t pos = cid[e];
-      const int32_t item = p.row_cluster ? p.list_ids[(int64_t)c * p.n + pos] : pos;
+      const int32_t item = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : pos;
       const double* x = p.items + (int64_t)item * p.f;
       double s = 0.0;
       for (int t = 0; t < p.f; ++t) s = fma(x[t], us[t], s);
@@ -455,22 +618,65 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     p.out_ids[out * p.k_eff + i] = i < held ? si[i] : -1;
     p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
   }
-  if (p.row_cluster && lane == 0) {
-    // index.py:372-387: the prefix covers the list -> n; K-th beats the next
-    // ceiling -> B; otherwise continue the walk from B with this top-K.
+  if (p.mode == kPrefix && lane == 0) {
+    // index.py:372-387: the prefix covers the list -> n; the K-th beats the
+    // ceiling at B -> B; otherwise the user continues past B.
     if (p.prefix >= p.n) {
       p.out_visited[out] = p.n;
     } else if (held == p.k_eff && ss[p.k_eff - 1] > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
       p.out_visited[out] = p.prefix;
     } else {
-      p.warm_count[out] = held;
-      p.walk_list[atomicAdd(p.walk_n, 1)] = r;
+      p.cont_list[atomicAdd(p.cont_n, 1)] = r;
+    }
+  }
+  if (p.mode == kFullList) {
+    // Exact top-K over the whole list is known, so Algorithm 1's sequential
+    // stop position follows in closed form ("visited"): with P =
+    // 1 + the largest list position of a top-K item and s_K the K-th score,
+    //   visited = min(n, max(P, k_eff, #{j : bounds[j]*||u|| >= s_K})),
+    // floored at B for work sharing (index.py:372-387).
+    int64_t mp = -1;
+    for (int i = lane; i < held; i += 32) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
+    for (int o = 16; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+    if (lane == 0) {
+      const int64_t q = ceiling_count(p.bounds + (int64_t)c * p.n, p.n, p.unorm[user], ss[p.k_eff - 1]);
+      int64_t v = max(max(mp + 1, (int64_t)p.k_eff), q);
+      if (v > p.n) v = p.n;
+      if (v < p.prefix) v = p.prefix;
+      p.out_visited[out] = v;
     }
   }
 }
 
+// visited for rows the exact fallback handled on the full list (same closed form)
+__global__ void fallback_visited_kernel(const int64_t* __restrict__ rows, const int32_t* n_rows,
+                                        const int64_t* __restrict__ row_user, const int64_t* __restrict__ row_out,
+                                        const int32_t* __restrict__ row_cluster, const int32_t* __restrict__ list_pos,
+                                        const double* __restrict__ bounds, const double* __restrict__ unorm, int64_t n,
+                                        int64_t prefix, int k_eff, const int32_t* __restrict__ out_ids,
+                                        const double* __restrict__ out_scores, int64_t* __restrict__ out_visited) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *n_rows) return;
+  const int64_t r = rows[i];
+  const int64_t user = row_user[r], out = row_out[r];
+  const int c = row_cluster[r];
+  int64_t mp = -1;
+  for (int t = 0; t < k_eff; ++t) mp = max(mp, (int64_t)list_pos[(int64_t)c * n + out_ids[out * k_eff + t]]);
+  const int64_t q = ceiling_count(bounds + (int64_t)c * n, n, unorm[user], out_scores[out * k_eff + k_eff - 1]);
+  int64_t v = max(max(mp + 1, (int64_t)k_eff), q);
+  if (v > n) v = n;
+  if (v < prefix) v = prefix;
+  out_visited[out] = v;
+}
+
+__global__ void fallback_users_kernel(const int64_t* __restrict__ rows, const int32_t* n_rows,
+                                      const int64_t* __restrict__ row_user, int64_t* __restrict__ users_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *n_rows) users_out[i] = row_user[rows[i]];
+}
+
 // ---------------------------------------------------------------------------
-// work-sharing setup: grouped queries -> 256-aligned packed rows and units
+// work-sharing setup
 // ---------------------------------------------------------------------------
 // single CTA: per-cluster aligned offsets and the unit list
 __global__ void ws_units_kernel(const int64_t* __restrict__ q_off, int c, int64_t b_pad, int64_t bp,
@@ -502,7 +708,6 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
                                const float* __restrict__ u_cu, uint16_t* __restrict__ a_pk, float* __restrict__ cu,
                                int64_t* __restrict__ row_user, int64_t* __restrict__ row_out,
                                int32_t* __restrict__ row_cluster) {
-  // one warp per packed row
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows_max || r >= a_off[c]) return;
@@ -529,15 +734,41 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
   }
 }
 
-__global__ void brute_units_kernel(int64_t nu, int64_t ni, Unit* units, int32_t* n_units) {
+// stage 2: pack the continuing rows densely (rows past the count are zero)
+__global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
+                                 int64_t rows_max, const int64_t* __restrict__ row_user,
+                                 const int64_t* __restrict__ row_out, const int32_t* __restrict__ row_cluster,
+                                 const float* __restrict__ cu_in, const uint16_t* __restrict__ a_in, int kp,
+                                 uint16_t* __restrict__ a2, float* __restrict__ cu2, int64_t* __restrict__ user2,
+                                 int64_t* __restrict__ out2, int32_t* __restrict__ clus2) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t nc = *n_cont;
+  if (r >= rows_max || r >= ((nc + kUnitRows - 1) / kUnitRows) * kUnitRows) return;
+  const bool live = r < nc;
+  const int64_t src_row = live ? cont[r] : 0;
+  const uint4* s = reinterpret_cast<const uint4*>(a_in + src_row * kp);
+  uint4* d = reinterpret_cast<uint4*>(a2 + r * kp);
+  for (int v = lane; v < kp / 8; v += 32) d[v] = live ? s[v] : make_uint4(0, 0, 0, 0);
+  if (lane == 0) {
+    cu2[r] = live ? cu_in[src_row] : 0.f;
+    user2[r] = live ? row_user[src_row] : -1;
+    out2[r] = live ? row_out[src_row] : -1;
+    clus2[r] = live ? row_cluster[src_row] : 0;
+  }
+}
+
+__global__ void units_from_count_kernel(const int32_t* __restrict__ n_rows_dev, int64_t n_rows_host, int64_t ni,
+                                        Unit* __restrict__ units, int32_t* __restrict__ n_units, int64_t units_max) {
+  const int64_t nr = n_rows_dev ? (int64_t)*n_rows_dev : n_rows_host;
+  const int64_t nunits = (nr + kUnitRows - 1) / kUnitRows;
   const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nunits = (nu + kUnitRows - 1) / kUnitRows;
   if (u == 0) *n_units = (int32_t)nunits;
-  if (u >= nunits) return;
+  if (u >= nunits || u >= units_max) return;
   Unit un;
   un.a_row0 = u * kUnitRows;
   un.b_row0 = 0;
-  un.rows = (int32_t)min((int64_t)kUnitRows, nu - u * kUnitRows);
+  un.rows = (int32_t)min((int64_t)kUnitRows, nr - u * kUnitRows);
   un.n_items = (int32_t)ni;
   units[u] = un;
 }
@@ -575,10 +806,24 @@ int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int kp) {
   return SIMDEX_OK;
 }
 
-double eps_for(int kp) { return std::ldexp(1.0, -7) + std::ldexp(1.0, -16) + (kp + 16) * std::ldexp(1.0, -22) + std::ldexp(1.0, -20); }
+double eps_for(int kp) {
+  return std::ldexp(1.0, -7) + std::ldexp(1.0, -16) + (kp + 16) * std::ldexp(1.0, -22) + std::ldexp(1.0, -20);
+}
+
+int kt_for(int k_eff) {
+  if (k_eff <= 1) return 1;
+  if (k_eff <= 2) return 2;
+  if (k_eff <= 4) return 4;
+  if (k_eff <= 8) return 8;
+  if (k_eff <= 16) return 16;
+  if (k_eff <= 32) return 32;
+  return 0;
+}
 
 int cap_for(int k_eff) {
-  int c = 2 * k_eff + 32;
+  const int kt = kt_for(k_eff);
+  if (kt > 0) return kt <= 16 ? 64 : 128;  // T is exact-current: the buffer only holds the band
+  int c = 4 * k_eff + 64;
   int p = 64;
   while (p < c) p <<= 1;
   return p > kMaxCap ? kMaxCap : p;
@@ -604,22 +849,87 @@ int geometry(int kp, GemmGeometry* g) {
   return SIMDEX_OK;
 }
 
-int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
-                cudaStream_t s) {
-  SIMDEX_CUDA(cudaFuncSetAttribute(gemm_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
-  gemm_topk_kernel<<<grid, kThreads, g.smem, s>>>(ma, mb, p);
+template <int KT>
+int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
+                   cudaStream_t s) {
+  SIMDEX_CUDA(cudaFuncSetAttribute(gemm_topk_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  ProfileScope _prof("gemm_topk", s);
+  gemm_topk_kernel<KT><<<grid, kThreads, g.smem, s>>>(ma, mb, p);
+  _prof.end();
   SIMDEX_LAUNCH_CHECK("gemm_topk");
   return SIMDEX_OK;
 }
 
-int finalize_smem(int pow2, int f, size_t* out) {
-  const size_t per_warp = ((size_t)pow2 * 12 + (size_t)f * 8 + 15) & ~size_t(15);
-  *out = per_warp * 8;
-  if (*out > 200 * 1024) {
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
+                cudaStream_t s) {
+  switch (p.debug_out ? 1 : kt_for(p.k_eff)) {
+    case 1: return launch_gemm_kt<1>(ma, mb, p, g, grid, s);
+    case 2: return launch_gemm_kt<2>(ma, mb, p, g, grid, s);
+    case 4: return launch_gemm_kt<4>(ma, mb, p, g, grid, s);
+    case 8: return launch_gemm_kt<8>(ma, mb, p, g, grid, s);
+    case 16: return launch_gemm_kt<16>(ma, mb, p, g, grid, s);
+    case 32: return launch_gemm_kt<32>(ma, mb, p, g, grid, s);
+    default: return launch_gemm_kt<0>(ma, mb, p, g, grid, s);
+  }
+}
+
+int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
+  const size_t per_warp = ((size_t)fp.pow2 * 12 + (size_t)fp.f * 8 + 15) & ~size_t(15);
+  const size_t smem = per_warp * 8;
+  if (smem > 200 * 1024) {
     set_error("finalize: candidate buffer too large");
     return SIMDEX_EUNSUPPORTED;
   }
+  SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfileScope _prof("finalize", s);
+  finalize_kernel<<<(unsigned)ceil_div(rows, 8), 256, smem, s>>>(fp);
+  _prof.end();
+  SIMDEX_LAUNCH_CHECK("finalize");
   return SIMDEX_OK;
+}
+
+// Candidate buffers + per-row state for up to `rows` packed rows.
+struct RowState {
+  Scratch<int32_t> cid, cnt, flags;
+  Scratch<float> lo, hi;
+  int cap;
+  int alloc(int64_t rows, int k_eff, cudaStream_t s) {
+    cap = cap_for(k_eff);
+    SIMDEX_CUDA(cid.alloc((size_t)rows * cap, s));
+    SIMDEX_CUDA(hi.alloc((size_t)rows * cap, s));
+    SIMDEX_CUDA(lo.alloc(kt_for(k_eff) > 0 ? 1 : (size_t)rows * cap, s));
+    SIMDEX_CUDA(cnt.alloc(rows, s));
+    SIMDEX_CUDA(flags.alloc(rows, s));
+    return SIMDEX_OK;
+  }
+};
+
+TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_units, const float* inrm,
+                       const float* inmax, const float* cu, const GemmGeometry& g, int f, int k_eff) {
+  TopkParams p{};
+  p.units = units;
+  p.n_units = n_units;
+  p.item_nrm = inrm;
+  p.item_nmax32 = inmax;
+  p.row_cu = cu;
+  p.e_abs = (float)std::ldexp((double)(f + 1), -124);
+  p.kb = g.kb;
+  p.k_steps = (f + 15) / 16;
+  p.stages = g.stages;
+  p.cap = st.cap;
+  p.k_eff = k_eff;
+  p.cand_id = st.cid.p;
+  p.cand_lo = st.lo.p;
+  p.cand_hi = st.hi.p;
+  p.row_count = st.cnt.p;
+  p.row_flags = st.flags.p;
+  return p;
+}
+
+int pow2_at_least(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
 }
 
 }  // namespace
@@ -634,29 +944,25 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   int rc = geometry(kp, &g);
   if (rc) return rc;
   const int64_t nu_pad = ceil_div(nu, 256) * 256, ni_pad = ceil_div(ni, 256) * 256;
-  const int cap = cap_for(k_eff);
   const int64_t nunits = ceil_div(nu, kUnitRows);
+  RowState st;
+  if ((rc = st.alloc(nu_pad, k_eff, s))) return rc;
   Scratch<Unit> units;
-  Scratch<int32_t> n_units, cnt, flags, cid, over_n, walk_n;
-  Scratch<float> lo, hi, cu, inrm, inmax;
+  Scratch<int32_t> n_units, over_n;
+  Scratch<float> cu, inrm, inmax;
   Scratch<int64_t> over_list, over_out;
   SIMDEX_CUDA(units.alloc(nunits, s));
   SIMDEX_CUDA(n_units.alloc(1, s));
-  SIMDEX_CUDA(cnt.alloc(nu_pad, s));
-  SIMDEX_CUDA(flags.alloc(nu_pad, s));
-  SIMDEX_CUDA(cid.alloc((size_t)nu_pad * cap, s));
-  SIMDEX_CUDA(lo.alloc((size_t)nu_pad * cap, s));
-  SIMDEX_CUDA(hi.alloc((size_t)nu_pad * cap, s));
   SIMDEX_CUDA(cu.alloc(nu_pad, s));
   SIMDEX_CUDA(inrm.alloc(ni_pad, s));
   SIMDEX_CUDA(inmax.alloc(ni_pad / 32, s));
   SIMDEX_CUDA(over_n.alloc(1, s));
-  SIMDEX_CUDA(walk_n.alloc(1, s));
   SIMDEX_CUDA(over_list.alloc(nu, s));
   SIMDEX_CUDA(over_out.alloc(nu, s));
   const double eps = eps_for(kp);
-  brute_units_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nu, ni, units.p, n_units.p);
-  SIMDEX_LAUNCH_CHECK("brute_units");
+  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, nu, ni, units.p, n_units.p,
+                                                                          nunits);
+  SIMDEX_LAUNCH_CHECK("units");
   row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(u_norm, nu, nu_pad, eps * std::ldexp(1.0, su), cu.p);
   SIMDEX_LAUNCH_CHECK("row_cu");
   item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm.p,
@@ -665,35 +971,16 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   CUtensorMap ma, mb;
   if ((rc = make_map(&ma, ub, nu_pad, kp))) return rc;
   if ((rc = make_map(&mb, ib, ni_pad, kp))) return rc;
-  TopkParams p{};
-  p.units = units.p;
-  p.n_units = n_units.p;
-  p.item_nrm = inrm.p;
-  p.item_nmax32 = inmax.p;
-  p.row_cu = cu.p;
-  p.e_abs = (float)std::ldexp((double)(f + 1), -124);
-  p.kb = g.kb;
-  p.k_steps = (f + 15) / 16;
-  p.stages = g.stages;
-  p.cap = cap;
-  p.k_eff = k_eff;
-  p.cand_id = cid.p;
-  p.cand_lo = lo.p;
-  p.cand_hi = hi.p;
-  p.row_count = cnt.p;
-  p.row_flags = flags.p;
+  TopkParams p = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu.p, g, f, k_eff);
   p.heap_ops = heap_ops;
   p.debug_out = debug_out;
   p.debug_ld = ni;
   const int grid = (int)(nunits < sm_count() ? nunits : sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
   if (debug_out) return SIMDEX_OK;
-  int pow2 = 1;
-  while (pow2 < cap) pow2 <<= 1;
-  size_t fsm;
-  if ((rc = finalize_smem(pow2, f, &fsm))) return rc;
   SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
+  fp.mode = kBrute;
   fp.total_rows = nu;
   fp.nu = nu;
   fp.users = users;
@@ -701,19 +988,17 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   fp.f = f;
   fp.n = ni;
   fp.k_eff = k_eff;
-  fp.cap = cap;
-  fp.cand_id = cid.p;
-  fp.row_count = cnt.p;
-  fp.row_flags = flags.p;
+  fp.cap = st.cap;
+  fp.cand_id = st.cid.p;
+  fp.row_count = st.cnt.p;
+  fp.row_flags = st.flags.p;
   fp.out_ids = out_ids;
   fp.out_scores = out_scores;
   fp.over_list = over_list.p;
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
-  fp.pow2 = pow2;
-  SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-  finalize_kernel<<<(unsigned)ceil_div(nu, 8), 256, fsm, s>>>(fp);
-  SIMDEX_LAUNCH_CHECK("finalize");
+  fp.pow2 = pow2_at_least(st.cap);
+  if ((rc = launch_finalize(fp, nu, s))) return rc;
   int32_t n_over = 0;
   SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SIMDEX_CUDA(cudaStreamSynchronize(s));
@@ -722,12 +1007,18 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   return SIMDEX_OK;
 }
 
-// Work-sharing prefix path (query_batch with work sharing).
+// Work-sharing path (query_batch, work_sharing=True):
+//   stage 1  every cluster's first B' list items x that cluster's queried
+//            users (segmented tensor-core product, certified top-K); users
+//            whose K-th beats the ceiling at B' are done (visited = B');
+//   stage 2  the remaining users x the whole catalogue (certified top-K), and
+//            visited from the closed form of Algorithm 1's stop position.
 int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
-                 int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si, const int32_t* list_ids,
-                 const double* bounds, int32_t c, int64_t block, const uint16_t* prefix_b, const double* prefix_norm,
-                 int64_t b_pad, const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
-                 int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, cudaStream_t s) {
+                 const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
+                 const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
+                 const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
+                 const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
+                 double* out_scores, int64_t* out_visited, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   const int64_t bp = block < ni ? block : ni;
   GemmGeometry g;
@@ -735,35 +1026,31 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if (rc) return rc;
   const int64_t rows_max = nq + (int64_t)c * kUnitRows;
   const int64_t units_max = ceil_div(nq, kUnitRows) + c;
-  const int cap = cap_for(k_eff);
+  const int64_t ni_pad = ceil_div(ni, 256) * 256;
+  const double eps = eps_for(kp);
+  RowState st;
+  if ((rc = st.alloc(rows_max, k_eff, s))) return rc;
   Scratch<Unit> units;
-  Scratch<int32_t> n_units, cnt, flags, cid, over_n, walk_n, warm_cnt, rclus;
-  Scratch<float> lo, hi, cu, ucu, inrm, inmax;
-  Scratch<int64_t> a_off, row_user, row_out, walk_list, over_list, over_out;
-  Scratch<uint16_t> a_pk;
+  Scratch<int32_t> n_units, cont_n, over_n, rclus, clus2;
+  Scratch<float> cu, ucu, pnrm, pnmax, inrm, inmax, cu2;
+  Scratch<int64_t> a_off, row_user, row_out, cont, over_list, over_out, user2, out2, fb_users;
+  Scratch<uint16_t> a_pk, a2;
   SIMDEX_CUDA(units.alloc(units_max, s));
   SIMDEX_CUDA(n_units.alloc(1, s));
   SIMDEX_CUDA(a_off.alloc(c + 1, s));
   SIMDEX_CUDA(a_pk.alloc((size_t)rows_max * kp, s));
   SIMDEX_CUDA(cu.alloc(rows_max, s));
-  SIMDEX_CUDA(ucu.alloc(ceil_div(nu, 256) * 256, s));
+  SIMDEX_CUDA(ucu.alloc(nu, s));
   SIMDEX_CUDA(row_user.alloc(rows_max, s));
   SIMDEX_CUDA(row_out.alloc(rows_max, s));
   SIMDEX_CUDA(rclus.alloc(rows_max, s));
-  SIMDEX_CUDA(cnt.alloc(rows_max, s));
-  SIMDEX_CUDA(flags.alloc(rows_max, s));
-  SIMDEX_CUDA(cid.alloc((size_t)rows_max * cap, s));
-  SIMDEX_CUDA(lo.alloc((size_t)rows_max * cap, s));
-  SIMDEX_CUDA(hi.alloc((size_t)rows_max * cap, s));
-  SIMDEX_CUDA(inrm.alloc((size_t)c * b_pad, s));
-  SIMDEX_CUDA(inmax.alloc((size_t)c * b_pad / 32, s));
-  SIMDEX_CUDA(walk_list.alloc(rows_max, s));
+  SIMDEX_CUDA(pnrm.alloc((size_t)c * b_pad, s));
+  SIMDEX_CUDA(pnmax.alloc((size_t)c * b_pad / 32, s));
+  SIMDEX_CUDA(cont.alloc(rows_max, s));
+  SIMDEX_CUDA(cont_n.alloc(1, s));
+  SIMDEX_CUDA(over_n.alloc(1, s));
   SIMDEX_CUDA(over_list.alloc(rows_max, s));
   SIMDEX_CUDA(over_out.alloc(rows_max, s));
-  SIMDEX_CUDA(walk_n.alloc(1, s));
-  SIMDEX_CUDA(over_n.alloc(1, s));
-  SIMDEX_CUDA(warm_cnt.alloc(nq, s));
-  const double eps = eps_for(kp);
   ws_units_kernel<<<1, 32, 0, s>>>(q_off, c, b_pad, bp, a_off.p, units.p, n_units.p);
   SIMDEX_LAUNCH_CHECK("ws_units");
   row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu.p);
@@ -775,37 +1062,19 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
                                                                    rclus.p);
   SIMDEX_LAUNCH_CHECK("ws_rows");
   item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
-      prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), inrm.p, inmax.p);
+      prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm.p, pnmax.p);
   SIMDEX_LAUNCH_CHECK("item_nrm");
   CUtensorMap ma, mb;
   if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
   if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
-  TopkParams p{};
-  p.units = units.p;
-  p.n_units = n_units.p;
-  p.item_nrm = inrm.p;
-  p.item_nmax32 = inmax.p;
-  p.row_cu = cu.p;
-  p.e_abs = (float)std::ldexp((double)(f + 1), -124);
-  p.kb = g.kb;
-  p.k_steps = (f + 15) / 16;
-  p.stages = g.stages;
-  p.cap = cap;
-  p.k_eff = k_eff;
-  p.cand_id = cid.p;
-  p.cand_lo = lo.p;
-  p.cand_hi = hi.p;
-  p.row_count = cnt.p;
-  p.row_flags = flags.p;
-  const int grid = (int)(units_max < sm_count() ? units_max : sm_count());
+  TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
+  int grid = (int)(units_max < sm_count() ? units_max : sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
-  int pow2 = 1;
-  while (pow2 < cap) pow2 <<= 1;
-  size_t fsm;
-  if ((rc = finalize_smem(pow2, f, &fsm))) return rc;
+
+  SIMDEX_CUDA(cudaMemsetAsync(cont_n.p, 0, sizeof(int32_t), s));
   SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
-  SIMDEX_CUDA(cudaMemsetAsync(walk_n.p, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
+  fp.mode = kPrefix;
   fp.total_rows = rows_max;
   fp.row_user = row_user.p;
   fp.row_out = row_out.p;
@@ -815,37 +1084,84 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   fp.items = items;
   fp.f = f;
   fp.list_ids = list_ids;
+  fp.list_pos = list_pos;
   fp.bounds = bounds;
   fp.unorm = unorm;
   fp.n = ni;
   fp.prefix = bp;
   fp.k_eff = k_eff;
-  fp.cap = cap;
-  fp.cand_id = cid.p;
-  fp.row_count = cnt.p;
-  fp.row_flags = flags.p;
+  fp.cap = st.cap;
+  fp.cand_id = st.cid.p;
+  fp.row_count = st.cnt.p;
+  fp.row_flags = st.flags.p;
   fp.out_ids = out_ids;
   fp.out_scores = out_scores;
   fp.out_visited = out_visited;
-  fp.warm_count = warm_cnt.p;
-  fp.walk_list = walk_list.p;
-  fp.walk_n = walk_n.p;
+  fp.cont_list = cont.p;
+  fp.cont_n = cont_n.p;
   fp.over_list = over_list.p;
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
-  fp.pow2 = pow2;
-  SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-  finalize_kernel<<<(unsigned)ceil_div(rows_max, 8), 256, fsm, s>>>(fp);
-  SIMDEX_LAUNCH_CHECK("finalize");
-  // continue from B with the warm top-K (index.py:376-387)
-  rc = launch_walk_tasks(users, unorm, items, f, ni, list_ids, bounds, walk_list.p, walk_n.p, rows_max, row_user.p,
-                         rclus.p, row_out.p, k, bp, out_ids, out_scores, warm_cnt.p, 0, -1, out_ids, out_scores,
-                         out_visited, s);
-  if (rc) return rc;
-  // rows whose certified band overflowed: exact walk from 0, visited floored at B
-  return launch_walk_tasks(users, unorm, items, f, ni, list_ids, bounds, over_list.p, over_n.p, rows_max, row_user.p,
-                           rclus.p, row_out.p, k, 0, nullptr, nullptr, nullptr, 0, bp, out_ids, out_scores,
-                           out_visited, s);
+  fp.pow2 = pow2_at_least(st.cap);
+  if ((rc = launch_finalize(fp, rows_max, s))) return rc;
+  if (bp >= ni) return SIMDEX_OK;  // the prefix was the whole list
+
+  // ---- stage 2: continuing users x the whole catalogue
+  int32_t n_cont = 0;
+  SIMDEX_CUDA(cudaMemcpyAsync(&n_cont, cont_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SIMDEX_CUDA(cudaStreamSynchronize(s));
+  if (getenv("SIMDEX_STATS")) fprintf(stderr, "[simdex] query_ws nq=%lld continue_past_B=%d\n", (long long)nq, n_cont);
+  if (n_cont == 0) return SIMDEX_OK;
+  const int64_t rows2 = ceil_div(n_cont, kUnitRows) * kUnitRows;
+  const int64_t units2 = rows2 / kUnitRows;
+  SIMDEX_CUDA(a2.alloc((size_t)rows2 * kp, s));
+  SIMDEX_CUDA(cu2.alloc(rows2, s));
+  SIMDEX_CUDA(user2.alloc(rows2, s));
+  SIMDEX_CUDA(out2.alloc(rows2, s));
+  SIMDEX_CUDA(clus2.alloc(rows2, s));
+  SIMDEX_CUDA(inrm.alloc(ni_pad, s));
+  SIMDEX_CUDA(inmax.alloc(ni_pad / 32, s));
+  cont_rows_kernel<<<(unsigned)ceil_div(rows2, 8), 256, 0, s>>>(cont.p, cont_n.p, rows2, row_user.p, row_out.p, rclus.p,
+                                                                 cu.p, a_pk.p, kp, a2.p, cu2.p, user2.p, out2.p,
+                                                                 clus2.p);
+  SIMDEX_LAUNCH_CHECK("cont_rows");
+  units_from_count_kernel<<<(unsigned)ceil_div(units2, 256), 256, 0, s>>>(cont_n.p, 0, ni, units.p, n_units.p,
+                                                                          units2);
+  SIMDEX_LAUNCH_CHECK("units");
+  item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm.p,
+                                                                      inmax.p);
+  SIMDEX_LAUNCH_CHECK("item_nrm");
+  CUtensorMap ma2, mb2;
+  if ((rc = make_map(&ma2, a2.p, rows2, kp))) return rc;
+  if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
+  TopkParams p2 = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu2.p, g, f, k_eff);
+  grid = (int)(units2 < sm_count() ? units2 : sm_count());
+  if ((rc = launch_gemm(ma2, mb2, p2, g, grid, s))) return rc;
+  FinalizeParams f2 = fp;
+  f2.mode = kFullList;
+  f2.total_rows = rows2;
+  f2.n_rows_dev = nullptr;
+  f2.row_user = user2.p;
+  f2.row_out = out2.p;
+  f2.row_cluster = clus2.p;
+  f2.cont_list = nullptr;
+  f2.cont_n = nullptr;
+  if ((rc = launch_finalize(f2, rows2, s))) return rc;
+  int32_t n_over = 0;
+  SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SIMDEX_CUDA(cudaStreamSynchronize(s));
+  if (n_over == 0) return SIMDEX_OK;
+  // band overflow on the full list: exact float64 scan for those users, same visited closed form
+  SIMDEX_CUDA(fb_users.alloc(n_over, s));
+  fallback_users_kernel<<<(unsigned)ceil_div(n_over, 256), 256, 0, s>>>(over_list.p, over_n.p, user2.p, fb_users.p);
+  SIMDEX_LAUNCH_CHECK("fallback_users");
+  if ((rc = exact_topk_rows_mapped(users, items, ni, f, fb_users.p, n_over, k, over_out.p, out_ids, out_scores, s)))
+    return rc;
+  fallback_visited_kernel<<<(unsigned)ceil_div(n_over, 256), 256, 0, s>>>(
+      over_list.p, over_n.p, user2.p, out2.p, clus2.p, list_pos, bounds, unorm, ni, bp, k_eff, out_ids, out_scores,
+      out_visited);
+  SIMDEX_LAUNCH_CHECK("fallback_visited");
+  return SIMDEX_OK;
 }
 
 }  // namespace simdex

@@ -204,6 +204,14 @@ __global__ void max_angles_kernel(const double* __restrict__ users, int64_t n, i
   atomicMax(theta_bits + c, (unsigned long long)__double_as_longlong(ang));
 }
 
+// pos[c, list_ids[c, j]] = j  (inverse permutation of every cluster's list)
+__global__ void list_pos_kernel(const int32_t* __restrict__ ids, int64_t c, int64_t n, int32_t* __restrict__ pos) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= c * n) return;
+  const int64_t row = t / n;
+  pos[row * n + ids[t]] = (int32_t)(t - row * n);
+}
+
 __global__ void center_norms_kernel(const double* __restrict__ centers, int c, int f, double* __restrict__ out) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= c) return;
@@ -258,7 +266,7 @@ using namespace simdex;
 
 extern "C" int simdex_build_index(const double* items, int64_t ni, int32_t f, const double* centers,
                                   const double* theta_b, int32_t c, double* out_item_norms, int32_t* out_list_ids,
-                                  double* out_bounds, void* stream) {
+                                  double* out_bounds, int32_t* out_list_pos, void* stream) {
   SIMDEX_CHECK_ARG(items && centers && theta_b && out_item_norms && out_list_ids && out_bounds,
                    "simdex_build_index: null pointer");
   SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && c >= 1 && ni < INT32_MAX, "simdex_build_index: bad sizes");
@@ -268,9 +276,25 @@ extern "C" int simdex_build_index(const double* items, int64_t ni, int32_t f, co
   dim3 grid((unsigned)ceil_div(ni, 256), (unsigned)c);
   const size_t smem = (size_t)f * sizeof(double);
   if (smem > 48 * 1024) SIMDEX_CUDA(cudaFuncSetAttribute(bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfileScope _prof("bounds", s);
   bounds_kernel<<<grid, 256, smem, s>>>(items, out_item_norms, ni, f, centers, theta_b, out_bounds, out_list_ids);
+  _prof.end();
   SIMDEX_LAUNCH_CHECK("bounds");
   SIMDEX_CUDA(segmented_sort_desc(out_bounds, out_list_ids, c, ni, s));
+  if (out_list_pos) {
+    const int64_t tot = (int64_t)c * ni;
+    list_pos_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(out_list_ids, (int64_t)c, ni, out_list_pos);
+    SIMDEX_LAUNCH_CHECK("list_pos");
+  }
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_list_positions(const int32_t* list_ids, int32_t c, int64_t ni, int32_t* out_pos, void* stream) {
+  SIMDEX_CHECK_ARG(list_ids && out_pos, "simdex_list_positions: null pointer");
+  SIMDEX_CHECK_ARG(c >= 1 && ni >= 1, "simdex_list_positions: bad sizes");
+  const int64_t tot = (int64_t)c * ni;
+  list_pos_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, as_stream(stream)>>>(list_ids, (int64_t)c, ni, out_pos);
+  SIMDEX_LAUNCH_CHECK("list_pos");
   return SIMDEX_OK;
 }
 

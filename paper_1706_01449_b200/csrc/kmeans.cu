@@ -295,9 +295,11 @@ extern "C" int simdex_kmeans_assign(const double* points, int64_t n, int32_t f, 
   sqnorm_kernel<<<(unsigned)ceil_div(c, 256), 256, 0, s>>>(centers, c, f, c2.p);
   count_launches(2);
   SIMDEX_CUDA(cudaMemsetAsync(out_changed, 0, sizeof(int64_t), s));
+  ProfileScope _prof("kmeans_assign", s);
   assign_kernel<<<(unsigned)nb, kAssignThreads, 0, s>>>(points, p2.p, n, f, centers, c2.p, c, prev_assign,
                                                         out_assign, out_d2,
                                                         reinterpret_cast<unsigned long long*>(out_changed), part.p);
+  _prof.end();
   SIMDEX_LAUNCH_CHECK("assign");
   sum_partials_kernel<<<1, 1024, 0, s>>>(part.p, nb, out_objective);
   SIMDEX_LAUNCH_CHECK("sum_partials");
@@ -325,7 +327,9 @@ extern "C" int simdex_kmeans_update(const double* points, int64_t n, int32_t f, 
   offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
   members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(ids.p, n, out_members);
   if (centers) {  // NULL: grouping only (members/offsets/counts)
+    ProfileScope _prof("centroid_mean", s);
     centroid_mean_kernel<<<(unsigned)c, 64, 0, s>>>(points, f, out_members, out_offsets, centers);
+    _prof.end();
     SIMDEX_LAUNCH_CHECK("centroid_mean");
   }
   return SIMDEX_OK;
@@ -352,8 +356,10 @@ extern "C" int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, in
   if (smem > 48 * 1024)
     SIMDEX_CUDA(cudaFuncSetAttribute(seed_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int j = 0; j + 1 < k; ++j) {
+    ProfileScope _prof("seed_update", s);
     seed_update_kernel<<<(unsigned)nb, kSeedThreads, smem, s>>>(points, p2.p, n, f, out_rows, j, d2.p, part.p,
                                                                 out_degenerate_pass);
+    _prof.end();
     seed_pick_kernel<<<1, 1024, 0, s>>>(points, n, f, d2.p, part.p, nb, uniforms, j, out_rows, out_centers,
                                         out_degenerate_pass);
     count_launches(2);

@@ -8,10 +8,11 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
                     int32_t si, int32_t k, int32_t* out_ids, double* out_scores, int64_t* heap_ops, float* debug_out,
                     cudaStream_t s);
 int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
-                 int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si, const int32_t* list_ids,
-                 const double* bounds, int32_t c, int64_t block, const uint16_t* prefix_b, const double* prefix_norm,
-                 int64_t b_pad, const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
-                 int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, cudaStream_t s);
+                 const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
+                 const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
+                 const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
+                 const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
+                 double* out_scores, int64_t* out_visited, cudaStream_t s);
 
 namespace {
 constexpr int kMaxMatmulK = 256;
@@ -107,13 +108,14 @@ extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int
 }
 
 extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
-                               const double* items, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
-                               const int32_t* list_ids, const double* bounds, int32_t c, int64_t block,
+                               const double* items, const uint16_t* ib, const double* item_norms, int64_t ni,
+                               int32_t f, int32_t kp, int32_t su, int32_t si, const int32_t* list_ids,
+                               const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                                const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
                                const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
                                int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
-  SIMDEX_CHECK_ARG(users && ub && user_norms && items && list_ids && bounds && prefix_b && prefix_norm && q_user &&
-                       q_off && out_ids && out_scores && out_visited,
+  SIMDEX_CHECK_ARG(users && ub && user_norms && items && ib && item_norms && list_ids && list_pos && bounds &&
+                       prefix_b && prefix_norm && q_user && q_off && out_ids && out_scores && out_visited,
                    "simdex_query_ws: null pointer");
   SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 1 && c >= 1 && kp % 64 == 0 && kp >= f,
                    "simdex_query_ws: bad sizes");
@@ -122,7 +124,7 @@ extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const do
   SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
                    "simdex_query_ws: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);
   if (nq == 0) return SIMDEX_OK;
-  return gemm_topk_ws(users, ub, user_norms, nu, items, ni, f, kp, su, si, list_ids, bounds, c, block, prefix_b,
-                      prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids, out_scores, out_visited,
-                      as_stream(stream));
+  return gemm_topk_ws(users, ub, user_norms, nu, items, ib, item_norms, ni, f, kp, su, si, list_ids, list_pos,
+                      bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
+                      out_scores, out_visited, as_stream(stream));
 }

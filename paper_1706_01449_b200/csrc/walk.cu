@@ -206,7 +206,9 @@ int launch_walk_tasks(const double* users, const double* unorm, const double* it
   WalkArgs a{users, unorm, items, f, n, list_ids, bounds, tasks, n_tasks_dev, n_tasks_max, q_user, q_cluster, q_out,
              k_eff, start, warm_ids, warm_scores, warm_count, no_prune, ws_floor, out_ids, out_scores, out_visited,
              wpc, queue.p};
+  ProfileScope _prof("walk", s);
   walk_kernel<<<(unsigned)grid, 32 * wpc, smem, s>>>(a);
+  _prof.end();
   SIMDEX_LAUNCH_CHECK("walk");
   return SIMDEX_OK;
 }

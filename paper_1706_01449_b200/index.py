@@ -142,6 +142,13 @@ class CentroidIndex:
             self._dev["bounds"] = _device.to_device(self._host["bounds"].astype(np.float64))
         return self._dev["ids"], self._dev["bounds"]
 
+    def device_list_pos(self):
+        """int32 [C, n]: position of each item in each cluster's list."""
+        if "pos" not in self._dev:
+            ids, _ = self.device_lists()
+            self._dev["pos"] = _ops.list_positions(ids)
+        return self._dev["pos"]
+
     def device_assignment(self):
         return self.clustering.device_assignment()
 
@@ -277,8 +284,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
             grouped = _ops.group_queries(q_users, index.device_assignment(), index.num_clusters)
             if q_users is index._dev.get("all_users"):
                 index._dev[key] = grouped
-        return _ops.query_ws(users, pu, items, pi, ids, bounds, index.block_size, index.device_prefix(model),
-                             grouped, k)
+        return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, index.block_size,
+                             index.device_prefix(model), grouped, k)
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
     out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
     if work_sharing:  # k beyond the tensor-core envelope: WS visited = n if B >= n else max(B, walk visited)
@@ -375,6 +382,7 @@ def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> Centroi
         out._host.pop("item_ids", None)
         out._host.pop("bounds", None)
         out._dev["ids"], out._dev["bounds"] = lists
+        out._dev.pop("pos", None)
     return out
 
 
