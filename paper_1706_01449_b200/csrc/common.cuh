@@ -54,12 +54,18 @@ class ProfileScope {
   bool on_ = false;
 };
 
+// Keep the device's stream-ordered pool warm: without this the pool returns
+// freed scratch to the driver at every synchronisation and the next call pays
+// for re-mapping it.
+void keep_pool_warm();
+
 // Stream-ordered scratch allocation (freed on the same stream).
 template <class T>
 struct Scratch {
   T* p = nullptr;
   cudaStream_t s = nullptr;
   cudaError_t alloc(size_t count, cudaStream_t stream) {
+    keep_pool_warm();
     s = stream;
     if (count == 0) count = 1;
     return cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream);

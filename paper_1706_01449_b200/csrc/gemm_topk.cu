@@ -68,6 +68,7 @@ struct TopkParams {
   const float* item_nrm;     // [B rows] ||i|| 2^si rounded up (0 on padding)
   const float* item_nmax32;  // [B rows / 32]
   const float* row_cu;       // [A rows] eps ||u|| 2^su rounded up
+  const float* row_T0;       // [A rows] initial certified threshold (scaled domain) or null
   float e_abs;
   int kb;
   int k_steps;
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool live = row_local < un.rows;
       const int64_t grow = un.a_row0 + row_local;
       const float cu = live ? p.row_cu[grow] : 0.f;
-      float T = -INFINITY;
+      float T = (live && p.row_T0) ? p.row_T0[grow] : -INFINITY;
       float top[KT > 0 ? KT : 1];
 #pragma unroll
       for (int i = 0; i < (KT > 0 ? KT : 1); ++i) top[i] = -INFINITY;
@@ -378,34 +379,55 @@ __global__ void __launch_bounds__(kThreads, 1)
               continue;
             }
             const bool act = live && !flags;
+            unsigned mask = 0;  // items of this chunk whose upper bound reaches T
+            const float* nrm = p.item_nrm + un.b_row0 + c0;
             if (act) {
-              float mx = -INFINITY;
+              if (nvalid < 32) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) mx = fmaxf(mx, i < nvalid ? v[i] : -INFINITY);
+                for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? v[i] : -INFINITY;
+              }
+              // chunk max as a tree (no serial dependency chain)
+              float m[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) m[i] = fmaxf(v[i], v[i + 16]);
+#pragma unroll
+              for (int w2 = 8; w2 > 0; w2 >>= 1)
+#pragma unroll
+                for (int i = 0; i < w2; ++i) m[i] = fmaxf(m[i], m[i + w2]);
               const float nmax = __ldg(p.item_nmax32 + ((un.b_row0 + c0) >> 5));
-              if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
-                const float* nrm = p.item_nrm + un.b_row0 + c0;
+              if (fmaf(cu, nmax, m[0]) + p.e_abs >= T) {  // else nothing in this chunk can qualify
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                  if (i < nvalid) {
-                    const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
-                    const float hi = v[i] + e;
-                    if (hi >= T && !flags) {
-                      my_hi[cnt] = hi;
-                      my_id[cnt] = c0 + i;
-                      ++cnt;
-                      ++hops;
-                      if constexpr (KT > 0) {
-                        push_top<KT>(top, v[i] - e);
-                        T = top_at<KT>(top, kk);
-                        if (cnt == p.cap) {
-                          compact_filter(my_hi, my_id, cnt, T);
-                          if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
-                        }
-                      } else {
-                        my_lo[cnt - 1] = v[i] - e;  // the buffer always has >= 32 free slots here
-                      }
+                  const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
+                  mask |= (v[i] + e >= T) ? (1u << i) : 0u;
+                }
+                if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
+              }
+            }
+            // converged append loop: every lane with pending items takes one per round
+            while (__any_sync(0xffffffffu, mask != 0u)) {
+              if (mask) {
+                const int i = __ffs(mask) - 1;
+                mask &= mask - 1;
+                float vi = v[0];
+#pragma unroll
+                for (int j = 1; j < 32; ++j) vi = (i == j) ? v[j] : vi;
+                const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
+                const float hi = vi + e;
+                if (hi >= T && !flags) {  // T may have risen within this chunk
+                  my_hi[cnt] = hi;
+                  my_id[cnt] = c0 + i;
+                  ++cnt;
+                  ++hops;
+                  if constexpr (KT > 0) {
+                    push_top<KT>(top, vi - e);
+                    T = fmaxf(T, top_at<KT>(top, kk));
+                    if (cnt == p.cap) {
+                      compact_filter(my_hi, my_id, cnt, T);
+                      if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
                     }
+                  } else {
+                    my_lo[cnt - 1] = vi - e;  // the buffer always has >= 32 free slots here
                   }
                 }
               }
@@ -528,6 +550,8 @@ struct FinalizeParams {
   int32_t* out_ids;
   double* out_scores;
   int64_t* out_visited;
+  float* row_T0_out;   // prefix mode: certified lower bound for the full-list pass (scaled)
+  double t0_scale;     // 2^(su+si)
   int64_t* cont_list;  // prefix mode: rows that continue past B
   int32_t* cont_n;
   int64_t* over_list;
@@ -567,6 +591,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   if (p.row_flags[r]) {
     if (lane == 0) {
       if (p.mode == kPrefix) {  // band overflow on the prefix: redo it on the full list
+        p.row_T0_out[r] = -INFINITY;
         p.cont_list[atomicAdd(p.cont_n, 1)] = r;
       } else {
         const int slot = atomicAdd(p.over_n, 1);
@@ -577,28 +602,43 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     return;
   }
   const int cnt = p.row_count[r];
-  for (int i = lane; i < p.f; i += 32) us[i] = p.users[user * p.f + i];
-  __syncwarp();
+  int np2 = 2;  // sort size for this row (warp-uniform)
+  while (np2 < cnt) np2 <<= 1;
+  (void)us;
+  // exact float64 rescoring, one candidate at a time across the warp:
+  // coalesced item-row loads, fixed shuffle-tree reduction (deterministic)
+  double ur[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int q = lane + 32 * t;
+    ur[t] = q < p.f ? p.users[user * p.f + q] : 0.0;
+  }
   const int32_t* cid = p.cand_id + r * p.cap;
-  for (int e = lane; e < p.pow2; e += 32) {
-    if (e < cnt) {
-      const int32_t pos = cid[e];
-      const int32_t item = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : pos;
-      const double* x = p.items + (int64_t)item * p.f;
-      double s = 0.0;
-      for (int t = 0; t < p.f; ++t) s = fma(x[t], us[t], s);
-      ss[e] = s;
+  for (int e = 0; e < cnt; ++e) {
+    const int32_t pos = cid[e];
+    const int32_t item = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : pos;
+    const double* x = p.items + (int64_t)item * p.f;
+    double part = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int q = lane + 32 * t;
+      if (q < p.f) part = fma(x[q], ur[t], part);
+    }
+    part = warp_sum(part);
+    if (lane == 0) {
+      ss[e] = part;
       si[e] = item;
-    } else {
-      ss[e] = -DBL_MAX;
-      si[e] = INT32_MAX;
     }
   }
+  for (int e = cnt + lane; e < np2; e += 32) {
+    ss[e] = -DBL_MAX;
+    si[e] = INT32_MAX;
+  }
   // warp bitonic sort by (score desc, id asc)
-  for (int size = 2; size <= p.pow2; size <<= 1) {
+  for (int size = 2; size <= np2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncwarp();
-      for (int i = lane; i < p.pow2 / 2; i += 32) {
+      for (int i = lane; i < np2 / 2; i += 32) {
         const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
         const bool up = (lo & size) == 0;
         const double a = ss[lo], b = ss[hi];
@@ -626,6 +666,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     } else if (held == p.k_eff && ss[p.k_eff - 1] > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
       p.out_visited[out] = p.prefix;
     } else {
+      // the prefix's exact K-th score lower-bounds the catalogue's: start the
+      // full-list pass from it (rounded down, with a 2^-40 relative guard)
+      float t0 = -INFINITY;
+      if (held == p.k_eff) {
+        const double sk = ss[p.k_eff - 1] * p.t0_scale;
+        t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
+      }
+      p.row_T0_out[r] = t0;
       p.cont_list[atomicAdd(p.cont_n, 1)] = r;
     }
   }
@@ -678,13 +726,38 @@ __global__ void fallback_users_kernel(const int64_t* __restrict__ rows, const in
 // ---------------------------------------------------------------------------
 // work-sharing setup
 // ---------------------------------------------------------------------------
-// single CTA: per-cluster aligned offsets and the unit list
-__global__ void ws_units_kernel(const int64_t* __restrict__ q_off, int c, int64_t b_pad, int64_t bp,
-                                int64_t* __restrict__ a_off, Unit* __restrict__ units, int32_t* __restrict__ n_units) {
-  if (threadIdx.x != 0) return;
-  int64_t acc = 0;
-  int nu = 0;
-  for (int j = 0; j < c; ++j) {
+// one CTA (1024 threads): per-cluster 256-aligned row offsets and the unit
+// list; thread t owns a contiguous run of clusters, runs are scanned in order
+__global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restrict__ q_off, int c, int64_t b_pad,
+                                                        int64_t bp, int64_t* __restrict__ a_off,
+                                                        Unit* __restrict__ units, int32_t* __restrict__ n_units) {
+  __shared__ int64_t s_rows[1024];
+  __shared__ int s_units[1024];
+  const int t = threadIdx.x;
+  const int per = (c + 1023) / 1024;
+  const int j0 = min(c, t * per), j1 = min(c, j0 + per);
+  int64_t rows = 0;
+  int nun = 0;
+  for (int j = j0; j < j1; ++j) {
+    const int64_t cnt = q_off[j + 1] - q_off[j];
+    const int64_t u = (cnt + kUnitRows - 1) / kUnitRows;
+    rows += u * kUnitRows;
+    nun += (int)u;
+  }
+  s_rows[t] = rows;
+  s_units[t] = nun;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
+    const int64_t r2 = t >= off ? s_rows[t - off] : 0;
+    const int u2 = t >= off ? s_units[t - off] : 0;
+    __syncthreads();
+    s_rows[t] += r2;
+    s_units[t] += u2;
+    __syncthreads();
+  }
+  int64_t acc = s_rows[t] - rows;
+  int nu = s_units[t] - nun;
+  for (int j = j0; j < j1; ++j) {
     const int64_t cnt = q_off[j + 1] - q_off[j];
     a_off[j] = acc;
     for (int64_t r = 0; r < cnt; r += kUnitRows) {
@@ -697,19 +770,24 @@ __global__ void ws_units_kernel(const int64_t* __restrict__ q_off, int c, int64_
     }
     acc += ((cnt + kUnitRows - 1) / kUnitRows) * kUnitRows;
   }
-  a_off[c] = acc;
-  *n_units = nu;
+  if (t == 1023) {
+    a_off[c] = s_rows[1023];
+    *n_units = s_units[1023];
+  }
 }
 
-// packed row r of cluster j: user q_user[q_off[j] + (r - a_off[j])] or padding
+// packed row r of cluster j: user q_user[q_off[j] + (r - a_off[j])] or padding;
+// one thread per 16-byte vector of the packed row
 __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t* __restrict__ q_perm,
                                const int64_t* __restrict__ q_off, const int64_t* __restrict__ a_off, int c,
                                int64_t rows_max, const uint16_t* __restrict__ ub, int kp,
                                const float* __restrict__ u_cu, uint16_t* __restrict__ a_pk, float* __restrict__ cu,
                                int64_t* __restrict__ row_user, int64_t* __restrict__ row_out,
                                int32_t* __restrict__ row_cluster) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int vpr = kp / 8;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = g / vpr;
+  const int v = (int)(g - r * vpr);
   if (r >= rows_max || r >= a_off[c]) return;
   int lo = 0, hi = c - 1;  // last j with a_off[j] <= r
   while (lo < hi) {
@@ -723,10 +801,9 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
   const int64_t i = r - a_off[j];
   const bool live = i < q_off[j + 1] - q_off[j];
   const int64_t user = live ? q_user[q_off[j] + i] : -1;
-  const uint4* src = reinterpret_cast<const uint4*>(ub + (live ? user : 0) * kp);
-  uint4* dst = reinterpret_cast<uint4*>(a_pk + r * kp);
-  for (int v = lane; v < kp / 8; v += 32) dst[v] = live ? src[v] : make_uint4(0, 0, 0, 0);
-  if (lane == 0) {
+  reinterpret_cast<uint4*>(a_pk + r * kp)[v] =
+      live ? reinterpret_cast<const uint4*>(ub + user * kp)[v] : make_uint4(0, 0, 0, 0);
+  if (v == 0) {
     cu[r] = live ? u_cu[user] : 0.f;
     row_user[r] = user;
     row_out[r] = live ? (q_perm ? q_perm[q_off[j] + i] : q_off[j] + i) : -1;
@@ -738,8 +815,9 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
 __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
                                  int64_t rows_max, const int64_t* __restrict__ row_user,
                                  const int64_t* __restrict__ row_out, const int32_t* __restrict__ row_cluster,
-                                 const float* __restrict__ cu_in, const uint16_t* __restrict__ a_in, int kp,
-                                 uint16_t* __restrict__ a2, float* __restrict__ cu2, int64_t* __restrict__ user2,
+                                 const float* __restrict__ cu_in, const float* __restrict__ t0_in,
+                                 const uint16_t* __restrict__ a_in, int kp, uint16_t* __restrict__ a2,
+                                 float* __restrict__ cu2, float* __restrict__ t02, int64_t* __restrict__ user2,
                                  int64_t* __restrict__ out2, int32_t* __restrict__ clus2) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -752,6 +830,7 @@ __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t
   for (int v = lane; v < kp / 8; v += 32) d[v] = live ? s[v] : make_uint4(0, 0, 0, 0);
   if (lane == 0) {
     cu2[r] = live ? cu_in[src_row] : 0.f;
+    t02[r] = live ? t0_in[src_row] : -INFINITY;
     user2[r] = live ? row_user[src_row] : -1;
     out2[r] = live ? row_out[src_row] : -1;
     clus2[r] = live ? row_cluster[src_row] : 0;
@@ -1032,7 +1111,7 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if ((rc = st.alloc(rows_max, k_eff, s))) return rc;
   Scratch<Unit> units;
   Scratch<int32_t> n_units, cont_n, over_n, rclus, clus2;
-  Scratch<float> cu, ucu, pnrm, pnmax, inrm, inmax, cu2;
+  Scratch<float> cu, ucu, pnrm, pnmax, inrm, inmax, cu2, t0, t02;
   Scratch<int64_t> a_off, row_user, row_out, cont, over_list, over_out, user2, out2, fb_users;
   Scratch<uint16_t> a_pk, a2;
   SIMDEX_CUDA(units.alloc(units_max, s));
@@ -1047,17 +1126,18 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   SIMDEX_CUDA(pnrm.alloc((size_t)c * b_pad, s));
   SIMDEX_CUDA(pnmax.alloc((size_t)c * b_pad / 32, s));
   SIMDEX_CUDA(cont.alloc(rows_max, s));
+  SIMDEX_CUDA(t0.alloc(rows_max, s));
   SIMDEX_CUDA(cont_n.alloc(1, s));
   SIMDEX_CUDA(over_n.alloc(1, s));
   SIMDEX_CUDA(over_list.alloc(rows_max, s));
   SIMDEX_CUDA(over_out.alloc(rows_max, s));
-  ws_units_kernel<<<1, 32, 0, s>>>(q_off, c, b_pad, bp, a_off.p, units.p, n_units.p);
+  ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off.p, units.p, n_units.p);
   SIMDEX_LAUNCH_CHECK("ws_units");
   row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu.p);
   SIMDEX_LAUNCH_CHECK("row_cu");
   // rows past a_off[c] stay "padding" (row_user = -1) and are skipped by finalize
   SIMDEX_CUDA(cudaMemsetAsync(row_user.p, 0xff, sizeof(int64_t) * rows_max, s));
-  ws_rows_kernel<<<(unsigned)ceil_div(rows_max, 8), 256, 0, s>>>(q_user, q_perm, q_off, a_off.p, c, rows_max, ub, kp,
+  ws_rows_kernel<<<(unsigned)ceil_div(rows_max * (kp / 8), 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off.p, c, rows_max, ub, kp,
                                                                    ucu.p, a_pk.p, cu.p, row_user.p, row_out.p,
                                                                    rclus.p);
   SIMDEX_LAUNCH_CHECK("ws_rows");
@@ -1097,6 +1177,8 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   fp.out_ids = out_ids;
   fp.out_scores = out_scores;
   fp.out_visited = out_visited;
+  fp.row_T0_out = t0.p;
+  fp.t0_scale = std::ldexp(1.0, su + si);
   fp.cont_list = cont.p;
   fp.cont_n = cont_n.p;
   fp.over_list = over_list.p;
@@ -1116,14 +1198,15 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   const int64_t units2 = rows2 / kUnitRows;
   SIMDEX_CUDA(a2.alloc((size_t)rows2 * kp, s));
   SIMDEX_CUDA(cu2.alloc(rows2, s));
+  SIMDEX_CUDA(t02.alloc(rows2, s));
   SIMDEX_CUDA(user2.alloc(rows2, s));
   SIMDEX_CUDA(out2.alloc(rows2, s));
   SIMDEX_CUDA(clus2.alloc(rows2, s));
   SIMDEX_CUDA(inrm.alloc(ni_pad, s));
   SIMDEX_CUDA(inmax.alloc(ni_pad / 32, s));
   cont_rows_kernel<<<(unsigned)ceil_div(rows2, 8), 256, 0, s>>>(cont.p, cont_n.p, rows2, row_user.p, row_out.p, rclus.p,
-                                                                 cu.p, a_pk.p, kp, a2.p, cu2.p, user2.p, out2.p,
-                                                                 clus2.p);
+                                                                 cu.p, t0.p, a_pk.p, kp, a2.p, cu2.p, t02.p, user2.p,
+                                                                 out2.p, clus2.p);
   SIMDEX_LAUNCH_CHECK("cont_rows");
   units_from_count_kernel<<<(unsigned)ceil_div(units2, 256), 256, 0, s>>>(cont_n.p, 0, ni, units.p, n_units.p,
                                                                           units2);
@@ -1135,6 +1218,7 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if ((rc = make_map(&ma2, a2.p, rows2, kp))) return rc;
   if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
   TopkParams p2 = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu2.p, g, f, k_eff);
+  p2.row_T0 = t02.p;
   grid = (int)(units2 < sm_count() ? units2 : sm_count());
   if ((rc = launch_gemm(ma2, mb2, p2, g, grid, s))) return rc;
   FinalizeParams f2 = fp;
