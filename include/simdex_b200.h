@@ -74,6 +74,9 @@ SIMDEX_API int simdex_topk_exact(const double* users, int64_t nu, const double* 
                       const int64_t* rows, int64_t n_rows, int32_t k,
                       int32_t* out_ids, double* out_scores, void* stream);
 
+/* max |x[i]| over n values into *out (device float64); picks the packing scale. */
+SIMDEX_API int simdex_max_abs(const double* x, int64_t n, double* out, void* stream);
+
 /* Operand packing for the tensor-core path: bf16 copy of x * 2^scale_exp,
  * zero padded to [rows_pad, kp] (kp = 64*ceil(f/64), rows_pad >= rows), and
  * float64 row norms of the UNSCALED rows.  Replaces the fp64->operand
@@ -98,7 +101,15 @@ SIMDEX_API int simdex_topk_matmul(const double* users, const uint16_t* ub, const
 
 /* ------------------------------------------------------------------------
  * Clustering (clustering.py)
+ *
+ * The k-means entry points take the points as float64 (`points`) or, when
+ * the caller has verified the values are exactly representable (BASELINE
+ * inputs are float32 upcast), as the float32 copy `points32` (non-NULL wins):
+ * the arithmetic is float64 either way, the float32 copy halves the bytes.
  * ---------------------------------------------------------------------- */
+
+/* float32 copy of x[n]; *inexact (device int32) = 1 if any value changed. */
+SIMDEX_API int simdex_to_f32(const double* x, int64_t n, float* out, int32_t* inexact, void* stream);
 
 /* clustering.py:105-122 _plusplus_seeds on device.  The host draws the RNG
  * stream exactly as the reference: first = rng.integers(0, n), then one
@@ -108,7 +119,8 @@ SIMDEX_API int simdex_topk_matmul(const double* users, const uint16_t* ub, const
  * non-positive D^2 total (fewer distinct points than seeds,
  * clustering.py:113-117), *out_degenerate_pass (device int32) receives that
  * pass index and the remaining rows are left for the host; else -1. */
-SIMDEX_API int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, int32_t k, int64_t first,
+SIMDEX_API int simdex_kmeans_seed(const double* points, const float* points32, int64_t n, int32_t f, int32_t k,
+                       int64_t first,
                        const double* uniforms, int64_t* out_rows, double* out_centers,
                        int32_t* out_degenerate_pass, void* stream);
 
@@ -117,7 +129,8 @@ SIMDEX_API int simdex_kmeans_seed(const double* points, int64_t n, int32_t f, in
  * prev_assign (nullable) is compared to count changed rows.
  * out_assign int64[n], out_d2 float64[n] (distance to the assigned center),
  * out_changed int64[1], out_objective float64[1] = sum(out_d2). */
-SIMDEX_API int simdex_kmeans_assign(const double* points, int64_t n, int32_t f, const double* centers, int32_t c,
+SIMDEX_API int simdex_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f,
+                         const double* centers, int32_t c,
                          const int64_t* prev_assign, int64_t* out_assign, double* out_d2,
                          int64_t* out_changed, double* out_objective, void* stream);
 
@@ -125,7 +138,8 @@ SIMDEX_API int simdex_kmeans_assign(const double* points, int64_t n, int32_t f, 
  * into out_members int64[n] with out_offsets int64[c+1]; out_counts int64[c];
  * centers[c] <- mean of its members for every non-empty cluster (fixed
  * summation order: deterministic). */
-SIMDEX_API int simdex_kmeans_update(const double* points, int64_t n, int32_t f, const int64_t* assign, int32_t c,
+SIMDEX_API int simdex_kmeans_update(const double* points, const float* points32, int64_t n, int32_t f,
+                         const int64_t* assign, int32_t c,
                          double* centers, int64_t* out_counts, int64_t* out_members, int64_t* out_offsets,
                          void* stream);
 

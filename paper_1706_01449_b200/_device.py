@@ -41,11 +41,21 @@ def f64(matrix) -> torch.Tensor:
     return c["f64"]
 
 
+def f32_exact(matrix):
+    """float32 device copy when every value is exactly representable
+    (BASELINE inputs are float32 upcast), else None."""
+    c = _cache(matrix)
+    if "f32" not in c:
+        t, exact = _ops.to_f32(f64(matrix))
+        c["f32"] = t if exact else None
+    return c["f32"]
+
+
 def packed(matrix) -> _ops.Packed:
     c = _cache(matrix)
     if "packed" not in c:
-        max_abs = float(np.abs(matrix.values).max()) if matrix.values.size else 0.0
-        c["packed"] = _ops.pack(f64(matrix), max_abs)
+        x = f64(matrix)
+        c["packed"] = _ops.pack(x, _ops.max_abs(x))
     return c["packed"]
 
 
@@ -60,3 +70,13 @@ def drop(matrix):
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy()
+
+
+def to_host_pinned(t: torch.Tensor) -> np.ndarray:
+    """Device -> pinned host copy (DMA at full PCIe rate), returned as numpy."""
+    if t.numel() * t.element_size() < (1 << 20):
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()

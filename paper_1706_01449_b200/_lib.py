@@ -31,11 +31,13 @@ SIGNATURES = {
     "simdex_profile_reset": [],
     "simdex_device_info": [C.c_int, P, P, P],
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
+    "simdex_max_abs": [P, I64, P, P],
     "simdex_pack_bf16": [P, I64, I32, I32, I64, I32, P, P, P],
     "simdex_topk_matmul": [P, P, P, I64, P, P, P, I64, I32, I32, I32, I32, I32, P, P, P, P],
-    "simdex_kmeans_seed": [P, I64, I32, I32, I64, P, P, P, P, P],
-    "simdex_kmeans_assign": [P, I64, I32, P, I32, P, P, P, P, P, P],
-    "simdex_kmeans_update": [P, I64, I32, P, I32, P, P, P, P, P],
+    "simdex_to_f32": [P, I64, P, P, P],
+    "simdex_kmeans_seed": [P, P, I64, I32, I32, I64, P, P, P, P, P],
+    "simdex_kmeans_assign": [P, P, I64, I32, P, I32, P, P, P, P, P, P],
+    "simdex_kmeans_update": [P, P, I64, I32, P, I32, P, P, P, P, P],
     "simdex_max_angles": [P, I64, I32, P, I32, P, P, P],
     "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P, P],
     "simdex_list_positions": [P, I32, I64, P, P],

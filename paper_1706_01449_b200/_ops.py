@@ -81,36 +81,50 @@ def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False):
     return ids, sc, hops
 
 
-def kmeans_seed(points, k, first, uniforms):
+def max_abs(x) -> float:
+    out = torch.empty(1, dtype=F64, device=x.device)
+    call("simdex_max_abs", ptr(_c(x, F64)), x.numel(), ptr(out), stream_ptr())
+    return float(out.item())
+
+
+def to_f32(x):
+    """(float32 copy, exact?) of a float64 tensor."""
+    out = torch.empty(x.shape, dtype=torch.float32, device=x.device)
+    flag = torch.empty(1, dtype=I32, device=x.device)
+    call("simdex_to_f32", ptr(_c(x, F64)), x.numel(), ptr(out), ptr(flag), stream_ptr())
+    return out, int(flag.item()) == 0
+
+
+def kmeans_seed(points, k, first, uniforms, points32=None):
     n, f = points.shape
     rows = torch.empty(k, dtype=I64, device=points.device)
     centers = torch.empty((k, f), dtype=F64, device=points.device)
     deg = torch.empty(1, dtype=I32, device=points.device)
-    call("simdex_kmeans_seed", ptr(_c(points, F64)), n, f, k, int(first),
+    call("simdex_kmeans_seed", ptr(_c(points, F64)), ptr(points32), n, f, k, int(first),
          ptr(None if uniforms is None else _c(uniforms, F64)), ptr(rows), ptr(centers), ptr(deg), stream_ptr())
     return rows, centers, deg
 
 
-def kmeans_assign(points, centers, prev=None):
+def kmeans_assign(points, centers, prev=None, points32=None):
     n, f = points.shape
     c = centers.shape[0]
     assign = torch.empty(n, dtype=I64, device=points.device)
     d2 = torch.empty(n, dtype=F64, device=points.device)
     changed = torch.empty(1, dtype=I64, device=points.device)
     obj = torch.empty(1, dtype=F64, device=points.device)
-    call("simdex_kmeans_assign", ptr(_c(points, F64)), n, f, ptr(_c(centers, F64)), c,
+    call("simdex_kmeans_assign", ptr(_c(points, F64)), ptr(points32), n, f, ptr(_c(centers, F64)), c,
          ptr(None if prev is None else _c(prev, I64)), ptr(assign), ptr(d2), ptr(changed), ptr(obj), stream_ptr())
     return assign, d2, changed, obj
 
 
-def kmeans_update(points, assign, centers, c=None):
+def kmeans_update(points, assign, centers, c=None, points32=None):
     """Group users by cluster; with ``centers`` also recompute the means in place."""
     n, f = points.shape
     c = centers.shape[0] if centers is not None else c
     counts = torch.empty(c, dtype=I64, device=points.device)
     members = torch.empty(n, dtype=I64, device=points.device)
     offsets = torch.empty(c + 1, dtype=I64, device=points.device)
-    call("simdex_kmeans_update", ptr(_c(points, F64)), n, f, ptr(_c(assign, I64)), c,
+    call("simdex_kmeans_update", ptr(_c(points, F64)), ptr(points32), n, f, ptr(_c(assign, I64)), c,
          ptr(None if centers is None else _c(centers, F64)), ptr(counts), ptr(members), ptr(offsets), stream_ptr())
     return counts, members, offsets
 

@@ -46,7 +46,7 @@ def default_blocks(factors: int) -> BlockSpec:
 
 def _results(ids, sc, n_items, num_users):
     vis = np.full(num_users, n_items, dtype=np.int64)
-    return TopKResults(np.arange(num_users), _device.to_host(ids), _device.to_host(sc), vis)
+    return TopKResults(np.arange(num_users), _device.to_host_pinned(ids), _device.to_host_pinned(sc), vis)
 
 
 def topk_naive_tensors(model: ModelPair, k: int):

@@ -154,11 +154,12 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
     if max_iters < 1:
         raise ValueError("max_iters must be >= 1")
     pts = _device.f64(users)
+    p32 = _device.f32_exact(users)  # exact float32 copy (half the bytes) or None
     dev = pts.device
     rng = np.random.default_rng(seed)
     first = int(rng.integers(0, n))
     unif = _device.to_device(rng.random(num_clusters - 1)) if num_clusters > 1 else None
-    rows, centers, deg = _ops.kmeans_seed(pts, num_clusters, first, unif)
+    rows, centers, deg = _ops.kmeans_seed(pts, num_clusters, first, unif, points32=p32)
     deg_pass = int(deg.item())
     if deg_pass >= 0:
         rows_h = _device.to_host(rows).copy()
@@ -175,12 +176,12 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
         centers.copy_(torch.as_tensor(c_h, device=dev))
         return torch.as_tensor(a_h, device=dev), True
 
-    assign, d2, _, obj = _ops.kmeans_assign(pts, centers)
+    assign, d2, _, obj = _ops.kmeans_assign(pts, centers, points32=p32)
     history = [float(obj.item())]
     for _ in range(max_iters):
-        counts, _, _ = _ops.kmeans_update(pts, assign, centers)
+        counts, _, _ = _ops.kmeans_update(pts, assign, centers, points32=p32)
         assign, _ = repair(assign, d2, counts)
-        new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign)
+        new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
         history.append(float(obj.item()))
         if int(changed.item()) == 0:
             break

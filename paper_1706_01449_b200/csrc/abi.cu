@@ -151,6 +151,16 @@ extern "C" int simdex_topk_exact(const double* users, int64_t nu, const double* 
   return exact_topk_rows(users, items, ni, f, rows, n_rows, k, out_ids, out_scores, as_stream(stream));
 }
 
+namespace simdex {
+int launch_max_abs(const double*, int64_t, double*, cudaStream_t);
+}
+
+extern "C" int simdex_max_abs(const double* x, int64_t n, double* out, void* stream) {
+  SIMDEX_CHECK_ARG(x && out, "simdex_max_abs: null pointer");
+  SIMDEX_CHECK_ARG(n >= 0, "simdex_max_abs: bad sizes");
+  return launch_max_abs(x, n, out, as_stream(stream));
+}
+
 extern "C" int simdex_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp, int64_t rows_pad,
                                 int32_t kp, uint16_t* out_bf16, double* out_norms, void* stream) {
   SIMDEX_CHECK_ARG(x && out_bf16 && out_norms, "simdex_pack_bf16: null pointer");

@@ -33,6 +33,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -573,72 +574,82 @@ __device__ int64_t ceiling_count(const double* b, int64_t n, double unorm, doubl
   return lo;
 }
 
+// 4 rows per warp, 8 lanes per row: exact float64 rescoring of the row's
+// certified candidates, (score desc, id asc) bitonic sort, output; plus the
+// work-sharing bookkeeping of the mode.
+constexpr int kFinRowsPerWarp = 4;
+
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   extern __shared__ unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t r = (int64_t)blockIdx.x * 8 + w;
-  const size_t per_warp = ((size_t)p.pow2 * 12 + (size_t)p.f * 8 + 15) & ~size_t(15);
-  unsigned char* mine = smem + w * per_warp;
+  const int grp = lane >> 3, gl = lane & 7;
+  const int slot = w * kFinRowsPerWarp + grp;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) * kFinRowsPerWarp + slot;
+  const size_t per_row = ((size_t)p.pow2 * 12 + (size_t)p.f * 8 + 15) & ~size_t(15);
+  unsigned char* mine = smem + slot * per_row;
   double* us = reinterpret_cast<double*>(mine);
   double* ss = us + p.f;
   int32_t* si = reinterpret_cast<int32_t*>(ss + p.pow2);
   const int64_t total = p.n_rows_dev ? (int64_t)*p.n_rows_dev : p.total_rows;
-  if (r >= total) return;
-  const int64_t user = p.row_user ? p.row_user[r] : r;
-  if (user < 0 || user >= p.nu) return;
-  const int64_t out = p.row_out ? p.row_out[r] : r;
-  const int c = p.mode != kBrute ? p.row_cluster[r] : 0;
-  if (p.row_flags[r]) {
-    if (lane == 0) {
-      if (p.mode == kPrefix) {  // band overflow on the prefix: redo it on the full list
-        p.row_T0_out[r] = -INFINITY;
-        p.cont_list[atomicAdd(p.cont_n, 1)] = r;
+  int64_t user = -1, out = -1;
+  int c = 0, cnt = 0;
+  bool act = false;
+  if (r < total) {
+    user = p.row_user ? p.row_user[r] : r;
+    if (user >= 0 && user < p.nu) {
+      out = p.row_out ? p.row_out[r] : r;
+      c = p.mode != kBrute ? p.row_cluster[r] : 0;
+      if (p.row_flags[r]) {
+        if (gl == 0) {
+          if (p.mode == kPrefix) {  // band overflow on the prefix: redo it on the full list
+            p.row_T0_out[r] = -INFINITY;
+            p.cont_list[atomicAdd(p.cont_n, 1)] = r;
+          } else {
+            const int sl = atomicAdd(p.over_n, 1);
+            p.over_list[sl] = p.mode == kBrute ? user : r;
+            p.over_out[sl] = out;
+          }
+        }
       } else {
-        const int slot = atomicAdd(p.over_n, 1);
-        p.over_list[slot] = p.mode == kBrute ? user : r;
-        p.over_out[slot] = out;
+        act = true;
+        cnt = p.row_count[r];
       }
     }
-    return;
   }
-  const int cnt = p.row_count[r];
-  int np2 = 2;  // sort size for this row (warp-uniform)
-  while (np2 < cnt) np2 <<= 1;
-  (void)us;
-  // exact float64 rescoring, one candidate at a time across the warp:
-  // coalesced item-row loads, fixed shuffle-tree reduction (deterministic)
-  double ur[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int q = lane + 32 * t;
-    ur[t] = q < p.f ? p.users[user * p.f + q] : 0.0;
-  }
+  // warp-uniform loop bounds (the four rows share every warp instruction)
+  const int cmax = __reduce_max_sync(0xffffffffu, cnt);
+  if (__all_sync(0xffffffffu, !act)) return;
+  int np2 = 2;
+  while (np2 < cmax) np2 <<= 1;
+  if (act)
+    for (int i = gl; i < p.f; i += 8) us[i] = p.users[user * p.f + i];
   const int32_t* cid = p.cand_id + r * p.cap;
-  for (int e = 0; e < cnt; ++e) {
-    const int32_t pos = cid[e];
-    const int32_t item = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : pos;
-    const double* x = p.items + (int64_t)item * p.f;
+  for (int e = gl; e < np2; e += 8) {
+    if (act && e < cnt) {
+      const int32_t pos = cid[e];
+      si[e] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : pos;
+    } else {
+      ss[e] = -DBL_MAX;
+      si[e] = INT32_MAX;
+    }
+  }
+  __syncwarp();
+  for (int e = 0; e < cmax; ++e) {
     double part = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int q = lane + 32 * t;
-      if (q < p.f) part = fma(x[q], ur[t], part);
+    if (act && e < cnt) {
+      const double* x = p.items + (int64_t)si[e] * p.f;
+      for (int q = gl; q < p.f; q += 8) part = fma(x[q], us[q], part);
     }
-    part = warp_sum(part);
-    if (lane == 0) {
-      ss[e] = part;
-      si[e] = item;
-    }
+    part += __shfl_xor_sync(0xffffffffu, part, 4);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    if (act && gl == 0 && e < cnt) ss[e] = part;
   }
-  for (int e = cnt + lane; e < np2; e += 32) {
-    ss[e] = -DBL_MAX;
-    si[e] = INT32_MAX;
-  }
-  // warp bitonic sort by (score desc, id asc)
+  // bitonic sort by (score desc, id asc), 8 lanes per row
   for (int size = 2; size <= np2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncwarp();
-      for (int i = lane; i < np2 / 2; i += 32) {
+      for (int i = gl; i < np2 / 2; i += 8) {
         const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
         const bool up = (lo & size) == 0;
         const double a = ss[lo], b = ss[hi];
@@ -653,12 +664,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     }
   }
   __syncwarp();
+  if (!act) return;
   const int held = cnt < p.k_eff ? cnt : p.k_eff;
-  for (int i = lane; i < p.k_eff; i += 32) {
+  for (int i = gl; i < p.k_eff; i += 8) {
     p.out_ids[out * p.k_eff + i] = i < held ? si[i] : -1;
     p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
   }
-  if (p.mode == kPrefix && lane == 0) {
+  if (p.mode == kPrefix && gl == 0) {
     // index.py:372-387: the prefix covers the list -> n; the K-th beats the
     // ceiling at B -> B; otherwise the user continues past B.
     if (p.prefix >= p.n) {
@@ -684,9 +696,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     //   visited = min(n, max(P, k_eff, #{j : bounds[j]*||u|| >= s_K})),
     // floored at B for work sharing (index.py:372-387).
     int64_t mp = -1;
-    for (int i = lane; i < held; i += 32) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
-    for (int o = 16; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
-    if (lane == 0) {
+    for (int i = gl; i < held; i += 8) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
+    for (int o = 4; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(0xffu << (grp * 8), mp, o));
+    if (gl == 0) {
       const int64_t q = ceiling_count(p.bounds + (int64_t)c * p.n, p.n, p.unorm[user], ss[p.k_eff - 1]);
       int64_t v = max(max(mp + 1, (int64_t)p.k_eff), q);
       if (v > p.n) v = p.n;
@@ -953,15 +965,17 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& 
 }
 
 int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
-  const size_t per_warp = ((size_t)fp.pow2 * 12 + (size_t)fp.f * 8 + 15) & ~size_t(15);
-  const size_t smem = per_warp * 8;
+  const size_t per_row = ((size_t)fp.pow2 * 12 + (size_t)fp.f * 8 + 15) & ~size_t(15);
+  int warps = 8;
+  while (warps > 1 && per_row * kFinRowsPerWarp * warps > 200 * 1024) warps >>= 1;
+  const size_t smem = per_row * kFinRowsPerWarp * warps;
   if (smem > 200 * 1024) {
     set_error("finalize: candidate buffer too large");
     return SIMDEX_EUNSUPPORTED;
   }
   SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileScope _prof("finalize", s);
-  finalize_kernel<<<(unsigned)ceil_div(rows, 8), 256, smem, s>>>(fp);
+  finalize_kernel<<<(unsigned)ceil_div(rows, kFinRowsPerWarp * warps), 32 * warps, smem, s>>>(fp);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("finalize");
   return SIMDEX_OK;
@@ -1192,7 +1206,25 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   int32_t n_cont = 0;
   SIMDEX_CUDA(cudaMemcpyAsync(&n_cont, cont_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SIMDEX_CUDA(cudaStreamSynchronize(s));
-  if (getenv("SIMDEX_STATS")) fprintf(stderr, "[simdex] query_ws nq=%lld continue_past_B=%d\n", (long long)nq, n_cont);
+  if (getenv("SIMDEX_STATS")) {
+    std::vector<int32_t> hc(rows_max);
+    SIMDEX_CUDA(cudaMemcpy(hc.data(), st.cnt.p, sizeof(int32_t) * rows_max, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> hu(rows_max);
+    SIMDEX_CUDA(cudaMemcpy(hu.data(), row_user.p, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
+    int64_t tot = 0, live = 0, mx = 0, hist[8] = {0};
+    for (int64_t r = 0; r < rows_max; ++r)
+      if (hu[r] >= 0) {
+        tot += hc[r];
+        ++live;
+        mx = hc[r] > mx ? hc[r] : mx;
+        hist[hc[r] < 16 ? 0 : hc[r] < 32 ? 1 : hc[r] < 64 ? 2 : 3]++;
+      }
+    fprintf(stderr,
+            "[simdex] query_ws nq=%lld continue_past_B=%d stage1 candidates mean=%.2f max=%lld "
+            "<16:%lld <32:%lld <64:%lld >=64:%lld\n",
+            (long long)nq, n_cont, live ? (double)tot / live : 0.0, (long long)mx, (long long)hist[0],
+            (long long)hist[1], (long long)hist[2], (long long)hist[3]);
+  }
   if (n_cont == 0) return SIMDEX_OK;
   const int64_t rows2 = ceil_div(n_cont, kUnitRows) * kUnitRows;
   const int64_t units2 = rows2 / kUnitRows;

@@ -42,7 +42,25 @@ __global__ void gather_prefix_kernel(const uint16_t* __restrict__ ib, const doub
   if (lane == 0) onorm[c * b_pad + r] = live ? inorm[src] : 0.0;
 }
 
+__global__ void max_abs_kernel(const double* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));  // m >= 0
+}
+
 }  // namespace
+
+int launch_max_abs(const double* x, int64_t n, double* out, cudaStream_t s) {
+  SIMDEX_CUDA(cudaMemsetAsync(out, 0, sizeof(double), s));
+  if (n == 0) return SIMDEX_OK;
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > 4 * 148) blocks = 4 * 148;
+  max_abs_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, n, reinterpret_cast<unsigned long long*>(out));
+  SIMDEX_LAUNCH_CHECK("max_abs");
+  return SIMDEX_OK;
+}
 
 int launch_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp, int64_t rows_pad, int32_t kp,
                      uint16_t* out, double* norms, cudaStream_t s) {

@@ -302,26 +302,32 @@ def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 
     tensor-core product, and only users whose K-th does not beat the ceiling
     at B continue walking.  ``precomputed`` results are reused verbatim."""
     _check_k(k)
-    uids = np.arange(model.num_users, dtype=np.int64) if user_ids is None else np.asarray(
+    all_users = user_ids is None
+    uids = np.arange(model.num_users, dtype=np.int64) if all_users else np.asarray(
         [int(u) for u in user_ids], dtype=np.int64)
     bad = (uids < 0) | (uids >= model.num_users)
     if bad.any():
         raise ValueError(f"user_id {int(uids[np.argmax(bad)])} out of range [0, {model.num_users})")
     reused = {}
+    hit = None
     if precomputed:
         keys = np.fromiter(precomputed.keys(), dtype=np.int64, count=len(precomputed))
         hit = np.isin(uids, keys)
         reused = {int(i): precomputed[int(uids[i])] for i in np.flatnonzero(hit)}
-        todo = np.flatnonzero(~hit)
-    else:
-        todo = np.arange(uids.shape[0], dtype=np.int64)
     k_eff = min(k, model.num_items)
+    if len(reused) * 2 <= uids.shape[0]:
+        # few reused entries: serve every position on the device (the reused
+        # positions still return the precomputed objects), no host gather
+        q = None if all_users else _device.to_device(uids)
+        ids, sc, vis = query_batch_tensors(index, model, q, k, work_sharing)
+        return TopKResults(uids, _device.to_host_pinned(ids), _device.to_host_pinned(sc),
+                           _device.to_host_pinned(vis), reused)
+    todo = np.flatnonzero(~hit)
     ids_h = np.zeros((uids.shape[0], k_eff), dtype=np.int32)
     sc_h = np.zeros((uids.shape[0], k_eff), dtype=np.float64)
     vis_h = np.zeros(uids.shape[0], dtype=np.int64)
     if todo.size:
-        q = _device.to_device(uids[todo])
-        ids, sc, vis = query_batch_tensors(index, model, q, k, work_sharing)
+        ids, sc, vis = query_batch_tensors(index, model, _device.to_device(uids[todo]), k, work_sharing)
         ids_h[todo] = _device.to_host(ids)
         sc_h[todo] = _device.to_host(sc)
         vis_h[todo] = _device.to_host(vis)
