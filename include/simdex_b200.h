@@ -208,6 +208,12 @@ SIMDEX_API int simdex_query_ws(const double* users, const uint16_t* ub, const do
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
 
+/* Host-side statistics of this thread's last simdex_query_ws call (host
+ * int64[5]): queries, queries that went on past B (second pass over the
+ * catalogue), B' = min(B, n), n, f.  Lets a caller count the algorithmic
+ * tensor work 2*f*(nq*B' + n_cont*n) of the call. */
+SIMDEX_API int simdex_ws_stats(int64_t* out5);
+
 /* Group queries by their cluster (index.py:346-348), stable in query order:
  * out_q_user int64[nq] grouped user rows, out_perm int64[nq] original query
  * position of each grouped entry, out_off int64[c+1] cluster offsets. */

@@ -44,6 +44,7 @@ SIGNATURES = {
     "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
     "simdex_query_ws": [P, P, P, I64, P, P, P, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64, P, P, P, I64,
                         I32, P, P, P, P],
+    "simdex_ws_stats": [P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
     "simdex_build_prefix": [P, P, I64, I32, P, I32, I64, I64, P, P, P],
@@ -115,6 +116,13 @@ def profile_read(name: str):
     n = C.c_int64(0)
     call("simdex_profile_read", name.encode(), C.byref(ms), C.byref(n))
     return ms.value, n.value
+
+
+def ws_stats():
+    """(queries, continued past B, B', n, f) of this thread's last work-sharing call."""
+    buf = (C.c_int64 * 5)()
+    call("simdex_ws_stats", C.cast(buf, C.c_void_p))
+    return tuple(int(x) for x in buf)
 
 
 def ptr(t):

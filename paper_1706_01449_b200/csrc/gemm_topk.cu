@@ -1027,6 +1027,21 @@ int pow2_at_least(int x) {
 
 }  // namespace
 
+// Work-sharing call statistics (simdex_ws_stats): queries, rows that went on
+// past B, prefix length, list length, factors -- enough for the caller to
+// count the algorithmic tensor work of the last call.
+static thread_local int64_t g_ws_stats[5] = {0, 0, 0, 0, 0};
+void record_ws_stats(int64_t nq, int64_t n_cont, int64_t bp, int64_t n, int64_t f) {
+  g_ws_stats[0] = nq;
+  g_ws_stats[1] = n_cont;
+  g_ws_stats[2] = bp;
+  g_ws_stats[3] = n;
+  g_ws_stats[4] = f;
+}
+void read_ws_stats(int64_t* out) {
+  for (int i = 0; i < 5; ++i) out[i] = g_ws_stats[i];
+}
+
 // Brute-force fused path (topk_matmul).
 int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
                     const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su,
@@ -1200,12 +1215,16 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   fp.over_n = over_n.p;
   fp.pow2 = pow2_at_least(st.cap);
   if ((rc = launch_finalize(fp, rows_max, s))) return rc;
-  if (bp >= ni) return SIMDEX_OK;  // the prefix was the whole list
+  if (bp >= ni) {  // the prefix was the whole list
+    record_ws_stats(nq, 0, bp, ni, f);
+    return SIMDEX_OK;
+  }
 
   // ---- stage 2: continuing users x the whole catalogue
   int32_t n_cont = 0;
   SIMDEX_CUDA(cudaMemcpyAsync(&n_cont, cont_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SIMDEX_CUDA(cudaStreamSynchronize(s));
+  record_ws_stats(nq, n_cont, bp, ni, f);
   if (getenv("SIMDEX_STATS")) {
     std::vector<int32_t> hc(rows_max);
     SIMDEX_CUDA(cudaMemcpy(hc.data(), st.cnt.p, sizeof(int32_t) * rows_max, cudaMemcpyDeviceToHost));

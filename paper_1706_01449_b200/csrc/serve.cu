@@ -14,6 +14,8 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
                  double* out_scores, int64_t* out_visited, cudaStream_t s);
 
+void read_ws_stats(int64_t* out);
+
 namespace {
 constexpr int kMaxMatmulK = 256;
 constexpr int kMaxKp = 256;
@@ -66,6 +68,12 @@ extern "C" int simdex_topk_matmul(const double* users, const uint16_t* ub, const
   SIMDEX_CHECK_ARG(kp % 64 == 0 && kp >= f, "simdex_topk_matmul: kp must be a multiple of 64 >= f");
   return gemm_topk_brute(users, ub, u_norm, nu, items, ib, i_norm, ni, f, kp, su, si, k, out_ids, out_scores,
                          heap_ops, nullptr, as_stream(stream));
+}
+
+extern "C" int simdex_ws_stats(int64_t* out5) {
+  SIMDEX_CHECK_ARG(out5, "simdex_ws_stats: null pointer");
+  read_ws_stats(out5);
+  return SIMDEX_OK;
 }
 
 extern "C" int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t* ib, int64_t ni, int32_t f,
