@@ -93,9 +93,12 @@ SIMDEX_API int simdex_pack_bf16(const double* x, int64_t rows, int32_t f, int32_
  *   heap_ops: optional int64[nu]: per user count of tile scores above the
  *   running K-th at the time the tile is merged (brute.py:95-97; tile order
  *   differs from the reference, the count is analogous, not bit-equal).
+ *   item_perm (nullable): the item operand ib / i_norm is in this row order
+ *   (e.g. simdex_norm_order), ib has ib_rows rows (0: 256*ceil(ni/256)).
  * Requires k_eff <= 256; larger k goes through simdex_topk_exact. */
 SIMDEX_API int simdex_topk_matmul(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu,
-                       const double* items, const uint16_t* ib, const double* i_norm, int64_t ni,
+                       const double* items, const uint16_t* ib, const double* i_norm,
+                       const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                        int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k,
                        int32_t* out_ids, double* out_scores, int64_t* heap_ops, void* stream);
 
@@ -163,6 +166,11 @@ SIMDEX_API int simdex_build_index(const double* items, int64_t ni, int32_t f, co
                        const double* theta_b, int32_t c, double* out_item_norms,
                        int32_t* out_list_ids, double* out_bounds, int32_t* out_list_pos, void* stream);
 
+/* Items by (norm desc, id asc): out_perm int32[n].  The brute-force pass
+ * streams the catalogue in this order so each row's threshold rises early and
+ * low-norm tiles are rejected by the norm bound (simdex_topk_matmul item_perm). */
+SIMDEX_API int simdex_norm_order(const double* norms, int64_t n, int32_t* out_perm, void* stream);
+
 /* Inverse list permutation: out_pos[c, list_ids[c, j]] = j (int32[c, ni]). */
 SIMDEX_API int simdex_list_positions(const int32_t* list_ids, int32_t c, int64_t ni, int32_t* out_pos, void* stream);
 
@@ -201,7 +209,8 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
  * out_visited follows the reference: n if B >= n, else max(B, walk visited).
  * Requires k_eff <= 256 and f <= 256 (else use simdex_walk). */
 SIMDEX_API int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
-                    const double* items, const uint16_t* ib, const double* item_norms, int64_t ni,
+                    const double* items, const uint16_t* ib, const double* item_norms,
+                    const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, int32_t si,
                     const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                     const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,

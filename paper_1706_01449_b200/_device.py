@@ -8,10 +8,15 @@ operand.  Host->device copies go through pinned staging.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
 from . import _lib, _ops
+
+# FactorMatrix values are read-only by contract; torch only ever reads them
+warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
 
 
 def device():
@@ -57,6 +62,14 @@ def packed(matrix) -> _ops.Packed:
         x = f64(matrix)
         c["packed"] = _ops.pack(x, _ops.max_abs(x))
     return c["packed"]
+
+
+def packed_sorted(matrix) -> _ops.Packed:
+    """The packed operand re-laid out by descending row norm (catalogue passes)."""
+    c = _cache(matrix)
+    if "packed_sorted" not in c:
+        c["packed_sorted"] = _ops.norm_sorted(packed(matrix))
+    return c["packed_sorted"]
 
 
 def norms(matrix) -> torch.Tensor:

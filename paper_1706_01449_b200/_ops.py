@@ -39,9 +39,25 @@ class Packed:
     scale_exp: int
     kp: int
     rows: int
+    perm: torch.Tensor | None = None   # operand row -> item id (norm-sorted operand), else None
+    rows_pad: int = 0                  # rows of the bf16 operand
 
 
 ROW_PAD = 256
+
+
+def norm_sorted(p: Packed) -> Packed:
+    """The item operand re-laid out by (norm desc, id asc) (simdex_norm_order):
+    the brute-force pass then meets high-norm items first, its thresholds rise
+    early and low-norm tiles fail the norm bound."""
+    perm = torch.empty(p.rows, dtype=I32, device=p.bf16.device)
+    call("simdex_norm_order", ptr(p.norms), p.rows, ptr(perm), stream_ptr())
+    rows_pad = ROW_PAD * ((p.rows + ROW_PAD - 1) // ROW_PAD)
+    out = torch.empty((1, rows_pad, p.kp), dtype=torch.int16, device=p.bf16.device)
+    onorm = torch.empty((1, rows_pad), dtype=F64, device=p.bf16.device)
+    call("simdex_build_prefix", ptr(p.bf16), ptr(p.norms), p.rows, p.kp, ptr(perm), 1, p.rows, rows_pad, ptr(out),
+         ptr(onorm), stream_ptr())
+    return Packed(out.view(rows_pad, p.kp), onorm.view(rows_pad), p.scale_exp, p.kp, p.rows, perm, rows_pad)
 
 
 def pack(x: torch.Tensor, max_abs: float) -> Packed:
@@ -76,8 +92,8 @@ def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False):
     sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
     call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu,
-         ptr(_c(items, F64)), ptr(pi.bf16), ptr(pi.norms), ni, f, pu.kp, pu.scale_exp, pi.scale_exp, k,
-         ptr(ids), ptr(sc), ptr(hops), stream_ptr())
+         ptr(_c(items, F64)), ptr(pi.bf16), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp,
+         pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), stream_ptr())
     return ids, sc, hops
 
 
@@ -211,7 +227,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
     call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(pi.bf16),
-         ptr(pi.norms), ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)), ptr(_c(list_pos, I32)),
+         ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),
+         ptr(_c(list_pos, I32)),
          ptr(_c(bounds, F64)), c, int(block),
          ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), stream_ptr())
     return ids, sc, vis

@@ -67,7 +67,8 @@ def topk_matmul_tensors(model: ModelPair, k: int, heap_ops: bool = False):
     if min(k, model.num_items) > MATMUL_MAX_K:
         ids, sc = _ops.topk_exact(users, items, k)
         return ids, sc, None
-    return _ops.topk_matmul(users, _device.packed(model.users), items, _device.packed(model.items), k, heap_ops)
+    return _ops.topk_matmul(users, _device.packed(model.users), items, _device.packed_sorted(model.items), k,
+                            heap_ops)
 
 
 def topk_matmul(model: ModelPair, k: int, blocks: BlockSpec | None = None, counters: dict | None = None) -> TopKResults:

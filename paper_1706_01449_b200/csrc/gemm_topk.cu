@@ -539,6 +539,7 @@ struct FinalizeParams {
   int f;
   const int32_t* list_ids;  // [C, n]
   const int32_t* list_pos;  // [C, n] inverse of list_ids (full-list mode)
+  const int32_t* item_perm; // item operand row -> item id (norm-sorted catalogue) or null
   const double* bounds;     // [C, n]
   const double* unorm;      // [nu]
   int64_t n;                // list length (= items)
@@ -627,7 +628,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   for (int e = gl; e < np2; e += 8) {
     if (act && e < cnt) {
       const int32_t pos = cid[e];
-      si[e] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : pos;
+      si[e] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
     } else {
       ss[e] = -DBL_MAX;
       si[e] = INT32_MAX;
@@ -1044,14 +1045,15 @@ void read_ws_stats(int64_t* out) {
 
 // Brute-force fused path (topk_matmul).
 int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
-                    const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su,
-                    int32_t si, int32_t k, int32_t* out_ids, double* out_scores, int64_t* heap_ops, float* debug_out,
-                    cudaStream_t s) {
+                    const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                    int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
+                    int64_t* heap_ops, float* debug_out, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   GemmGeometry g;
   int rc = geometry(kp, &g);
   if (rc) return rc;
-  const int64_t nu_pad = ceil_div(nu, 256) * 256, ni_pad = ceil_div(ni, 256) * 256;
+  const int64_t nu_pad = ceil_div(nu, 256) * 256;
+  const int64_t ni_pad = ib_rows > 0 ? ib_rows : ceil_div(ni, 256) * 256;  // rows of the item operand
   const int64_t nunits = ceil_div(nu, kUnitRows);
   RowState st;
   if ((rc = st.alloc(nu_pad, k_eff, s))) return rc;
@@ -1105,6 +1107,7 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   fp.over_list = over_list.p;
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
+  fp.item_perm = item_perm;
   fp.pow2 = pow2_at_least(st.cap);
   if ((rc = launch_finalize(fp, nu, s))) return rc;
   int32_t n_over = 0;
@@ -1122,7 +1125,8 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
 //   stage 2  the remaining users x the whole catalogue (certified top-K), and
 //            visited from the closed form of Algorithm 1's stop position.
 int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
-                 const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
+                 const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                 int32_t f, int32_t kp, int32_t su, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
@@ -1134,7 +1138,7 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if (rc) return rc;
   const int64_t rows_max = nq + (int64_t)c * kUnitRows;
   const int64_t units_max = ceil_div(nq, kUnitRows) + c;
-  const int64_t ni_pad = ceil_div(ni, 256) * 256;
+  const int64_t ni_pad = ib_rows > 0 ? ib_rows : ceil_div(ni, 256) * 256;
   const double eps = eps_for(kp);
   RowState st;
   if ((rc = st.alloc(rows_max, k_eff, s))) return rc;
@@ -1177,8 +1181,22 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
   if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
   TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
+  const bool stats = getenv("SIMDEX_STATS") != nullptr;
+  Scratch<int64_t> hops;
+  if (stats) {
+    SIMDEX_CUDA(hops.alloc(rows_max, s));
+    SIMDEX_CUDA(cudaMemsetAsync(hops.p, 0, sizeof(int64_t) * rows_max, s));
+    p.heap_ops = hops.p;
+  }
   int grid = (int)(units_max < sm_count() ? units_max : sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
+  if (stats) {
+    std::vector<int64_t> hh(rows_max);
+    SIMDEX_CUDA(cudaMemcpy(hh.data(), hops.p, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
+    int64_t tot = 0;
+    for (auto v : hh) tot += v;
+    fprintf(stderr, "[simdex] stage1 appends per query %.2f\n", (double)tot / (double)nq);
+  }
 
   SIMDEX_CUDA(cudaMemsetAsync(cont_n.p, 0, sizeof(int32_t), s));
   SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
@@ -1270,8 +1288,21 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
   TopkParams p2 = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu2.p, g, f, k_eff);
   p2.row_T0 = t02.p;
+  Scratch<int64_t> hops2;
+  if (stats) {
+    SIMDEX_CUDA(hops2.alloc(rows2, s));
+    SIMDEX_CUDA(cudaMemsetAsync(hops2.p, 0, sizeof(int64_t) * rows2, s));
+    p2.heap_ops = hops2.p;
+  }
   grid = (int)(units2 < sm_count() ? units2 : sm_count());
   if ((rc = launch_gemm(ma2, mb2, p2, g, grid, s))) return rc;
+  if (stats) {
+    std::vector<int64_t> hh(rows2);
+    SIMDEX_CUDA(cudaMemcpy(hh.data(), hops2.p, sizeof(int64_t) * rows2, cudaMemcpyDeviceToHost));
+    int64_t tot = 0;
+    for (auto v : hh) tot += v;
+    fprintf(stderr, "[simdex] stage2 appends per continuing query %.2f\n", (double)tot / (double)n_cont);
+  }
   FinalizeParams f2 = fp;
   f2.mode = kFullList;
   f2.total_rows = rows2;
@@ -1281,6 +1312,7 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   f2.row_cluster = clus2.p;
   f2.cont_list = nullptr;
   f2.cont_n = nullptr;
+  f2.item_perm = item_perm;
   if ((rc = launch_finalize(f2, rows2, s))) return rc;
   int32_t n_over = 0;
   SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

@@ -289,6 +289,29 @@ extern "C" int simdex_build_index(const double* items, int64_t ni, int32_t f, co
   return SIMDEX_OK;
 }
 
+namespace simdex {
+namespace {
+__global__ void norm_keys_kernel(const double* __restrict__ norms, int64_t n, double* keys, int32_t* ids) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = norms[i];
+  ids[i] = (int32_t)i;
+}
+}  // namespace
+}  // namespace simdex
+
+extern "C" int simdex_norm_order(const double* norms, int64_t n, int32_t* out_perm, void* stream) {
+  SIMDEX_CHECK_ARG(norms && out_perm, "simdex_norm_order: null pointer");
+  SIMDEX_CHECK_ARG(n >= 1 && n < INT32_MAX, "simdex_norm_order: bad sizes");
+  cudaStream_t s = as_stream(stream);
+  Scratch<double> keys;
+  SIMDEX_CUDA(keys.alloc(n, s));
+  norm_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(norms, n, keys.p, out_perm);
+  SIMDEX_LAUNCH_CHECK("norm_keys");
+  SIMDEX_CUDA(segmented_sort_desc(keys.p, out_perm, 1, n, s));
+  return SIMDEX_OK;
+}
+
 extern "C" int simdex_list_positions(const int32_t* list_ids, int32_t c, int64_t ni, int32_t* out_pos, void* stream) {
   SIMDEX_CHECK_ARG(list_ids && out_pos, "simdex_list_positions: null pointer");
   SIMDEX_CHECK_ARG(c >= 1 && ni >= 1, "simdex_list_positions: bad sizes");

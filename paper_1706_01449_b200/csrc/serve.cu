@@ -4,11 +4,12 @@
 
 namespace simdex {
 int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
-                    const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su,
-                    int32_t si, int32_t k, int32_t* out_ids, double* out_scores, int64_t* heap_ops, float* debug_out,
-                    cudaStream_t s);
+                    const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                    int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
+                    int64_t* heap_ops, float* debug_out, cudaStream_t s);
 int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
-                 const uint16_t* ib, const double* i_norm, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
+                 const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                 int32_t f, int32_t kp, int32_t su, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
@@ -54,9 +55,10 @@ __global__ void group_offsets_kernel(const unsigned long long* counts, int c, in
 using namespace simdex;
 
 extern "C" int simdex_topk_matmul(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu,
-                                  const double* items, const uint16_t* ib, const double* i_norm, int64_t ni,
-                                  int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids,
-                                  double* out_scores, int64_t* heap_ops, void* stream) {
+                                  const double* items, const uint16_t* ib, const double* i_norm,
+                                  const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
+                                  int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
+                                  int64_t* heap_ops, void* stream) {
   SIMDEX_CHECK_ARG(users && items && out_ids && out_scores, "simdex_topk_matmul: null pointer");
   SIMDEX_CHECK_ARG(nu >= 1 && ni >= 1 && f >= 1 && k >= 1 && ni < INT32_MAX, "simdex_topk_matmul: bad sizes");
   const int64_t k_eff = k < ni ? k : ni;
@@ -66,8 +68,8 @@ extern "C" int simdex_topk_matmul(const double* users, const uint16_t* ub, const
     return exact_topk_rows(users, items, ni, f, nullptr, nu, k, out_ids, out_scores, as_stream(stream));
   }
   SIMDEX_CHECK_ARG(kp % 64 == 0 && kp >= f, "simdex_topk_matmul: kp must be a multiple of 64 >= f");
-  return gemm_topk_brute(users, ub, u_norm, nu, items, ib, i_norm, ni, f, kp, su, si, k, out_ids, out_scores,
-                         heap_ops, nullptr, as_stream(stream));
+  return gemm_topk_brute(users, ub, u_norm, nu, items, ib, i_norm, item_perm, ib_rows, ni, f, kp, su, si, k, out_ids,
+                         out_scores, heap_ops, nullptr, as_stream(stream));
 }
 
 extern "C" int simdex_ws_stats(int64_t* out5) {
@@ -87,8 +89,8 @@ extern "C" int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t*
   SIMDEX_CUDA(in.alloc(ni, s));
   SIMDEX_CUDA(cudaMemsetAsync(un.p, 0, sizeof(double) * nu, s));
   SIMDEX_CUDA(cudaMemsetAsync(in.p, 0, sizeof(double) * ni, s));
-  return gemm_topk_brute(nullptr, ub, un.p, nu, nullptr, ib, in.p, ni, f, kp, 0, 0, 1, nullptr, nullptr, nullptr,
-                         out, s);
+  return gemm_topk_brute(nullptr, ub, un.p, nu, nullptr, ib, in.p, nullptr, 0, ni, f, kp, 0, 0, 1, nullptr, nullptr,
+                         nullptr, out, s);
 }
 
 extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int64_t* assign, int32_t c,
@@ -116,8 +118,9 @@ extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int
 }
 
 extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
-                               const double* items, const uint16_t* ib, const double* item_norms, int64_t ni,
-                               int32_t f, int32_t kp, int32_t su, int32_t si, const int32_t* list_ids,
+                               const double* items, const uint16_t* ib, const double* item_norms,
+                               const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
+                               int32_t su, int32_t si, const int32_t* list_ids,
                                const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                                const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
                                const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
@@ -132,7 +135,8 @@ extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const do
   SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
                    "simdex_query_ws: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);
   if (nq == 0) return SIMDEX_OK;
-  return gemm_topk_ws(users, ub, user_norms, nu, items, ib, item_norms, ni, f, kp, su, si, list_ids, list_pos,
+  return gemm_topk_ws(users, ub, user_norms, nu, items, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, si,
+                      list_ids, list_pos,
                       bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
                       out_scores, out_visited, as_stream(stream));
 }

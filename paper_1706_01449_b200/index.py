@@ -276,7 +276,7 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
         q_users = index._dev.get("all_users")
         if q_users is None:
             q_users = index._dev["all_users"] = torch.arange(model.num_users, dtype=torch.int64, device=users.device)
-    pu, pi = _device.packed(model.users), _device.packed(model.items)
+    pu, pi = _device.packed(model.users), _device.packed_sorted(model.items)
     if work_sharing and min(k, n) <= 256 and pu.kp <= 256:
         key = ("grouped", q_users.data_ptr(), q_users.shape[0])
         grouped = index._dev.get(key) if q_users is index._dev.get("all_users") else None
