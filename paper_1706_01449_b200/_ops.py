@@ -84,7 +84,7 @@ def topk_exact(users, items, k, rows=None):
     return ids, sc
 
 
-def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False):
+def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32=None):
     nu, f = users.shape
     ni = items.shape[0]
     k_eff = min(k, ni)
@@ -92,7 +92,8 @@ def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False):
     sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
     call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu,
-         ptr(_c(items, F64)), ptr(pi.bf16), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp,
+         ptr(_c(items, F64)), ptr(items32), ptr(pi.bf16), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
+         pu.scale_exp,
          pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), stream_ptr())
     return ids, sc, hops
 
@@ -213,7 +214,8 @@ def group_queries(q_user, assign, c):
     return gq, perm, off
 
 
-def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k):
+def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k,
+             items32=None):
     """Work-sharing batch query; ``grouped`` = group_queries(...) output.
     Returns (ids, scores, visited) in the original query order."""
     nu, f = users.shape
@@ -226,7 +228,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
-    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(pi.bf16),
+    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(items32),
+         ptr(pi.bf16),
          ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),
          ptr(_c(list_pos, I32)),
          ptr(_c(bounds, F64)), c, int(block),

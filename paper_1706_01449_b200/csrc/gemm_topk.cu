@@ -86,6 +86,13 @@ struct TopkParams {
   int64_t debug_ld;
 };
 
+// three-input max (sm_100 FMNMX3)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 __device__ __forceinline__ void swapf(float& a, float& b) {
   float t = a;
   a = b;
@@ -387,16 +394,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? v[i] : -INFINITY;
               }
-              // chunk max as a tree (no serial dependency chain)
-              float m[16];
+              // chunk max as a tree of 3-input FMNMX3 (17 instructions for 32 values)
+              float m[11];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) m[i] = fmaxf(v[i], v[i + 16]);
-#pragma unroll
-              for (int w2 = 8; w2 > 0; w2 >>= 1)
-#pragma unroll
-                for (int i = 0; i < w2; ++i) m[i] = fmaxf(m[i], m[i + w2]);
+              for (int i = 0; i < 10; ++i) m[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+              m[10] = fmaxf(v[30], v[31]);
+              const float m0 = fmax3(m[0], m[1], m[2]), m1 = fmax3(m[3], m[4], m[5]);
+              const float m2 = fmax3(m[6], m[7], m[8]), m3 = fmaxf(m[9], m[10]);
+              const float mx = fmaxf(fmax3(m0, m1, m2), m3);
               const float nmax = __ldg(p.item_nmax32 + ((un.b_row0 + c0) >> 5));
-              if (fmaf(cu, nmax, m[0]) + p.e_abs >= T) {  // else nothing in this chunk can qualify
+              if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
@@ -422,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   ++hops;
                   if constexpr (KT > 0) {
                     push_top<KT>(top, vi - e);
-                    T = fmaxf(T, top_at<KT>(top, kk));
+                    T = fmaxf(T, KT == kk + 1 ? top[KT - 1] : top_at<KT>(top, kk));
                     if (cnt == p.cap) {
                       compact_filter(my_hi, my_id, cnt, T);
                       if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
@@ -536,6 +543,7 @@ struct FinalizeParams {
   int64_t nu;
   const double* users;
   const double* items;
+  const float* items32;     // exact float32 copy of items (half the bytes) or null
   int f;
   const int32_t* list_ids;  // [C, n]
   const int32_t* list_pos;  // [C, n] inverse of list_ids (full-list mode)
@@ -578,14 +586,16 @@ __device__ int64_t ceiling_count(const double* b, int64_t n, double unorm, doubl
 // 4 rows per warp, 8 lanes per row: exact float64 rescoring of the row's
 // certified candidates, (score desc, id asc) bitonic sort, output; plus the
 // work-sharing bookkeeping of the mode.
-constexpr int kFinRowsPerWarp = 4;
-
+// LPR lanes per row: 8 (4 rows per warp) for small k, 32 for k > 32
+template <int LPR>
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
+  constexpr int RPW = 32 / LPR;
   extern __shared__ unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int grp = lane >> 3, gl = lane & 7;
-  const int slot = w * kFinRowsPerWarp + grp;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) * kFinRowsPerWarp + slot;
+  const int grp = lane / LPR, gl = lane % LPR;
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
+  const int slot = w * RPW + grp;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) * RPW + slot;
   const size_t per_row = ((size_t)p.pow2 * 12 + (size_t)p.f * 8 + 15) & ~size_t(15);
   unsigned char* mine = smem + slot * per_row;
   double* us = reinterpret_cast<double*>(mine);
@@ -623,9 +633,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   int np2 = 2;
   while (np2 < cmax) np2 <<= 1;
   if (act)
-    for (int i = gl; i < p.f; i += 8) us[i] = p.users[user * p.f + i];
+    for (int i = gl; i < p.f; i += LPR) us[i] = p.users[user * p.f + i];
   const int32_t* cid = p.cand_id + r * p.cap;
-  for (int e = gl; e < np2; e += 8) {
+  for (int e = gl; e < np2; e += LPR) {
     if (act && e < cnt) {
       const int32_t pos = cid[e];
       si[e] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
@@ -638,19 +648,23 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   for (int e = 0; e < cmax; ++e) {
     double part = 0.0;
     if (act && e < cnt) {
-      const double* x = p.items + (int64_t)si[e] * p.f;
-      for (int q = gl; q < p.f; q += 8) part = fma(x[q], us[q], part);
+      if (p.items32) {
+        const float* x = p.items32 + (int64_t)si[e] * p.f;
+        for (int q = gl; q < p.f; q += LPR) part = fma((double)x[q], us[q], part);
+      } else {
+        const double* x = p.items + (int64_t)si[e] * p.f;
+        for (int q = gl; q < p.f; q += LPR) part = fma(x[q], us[q], part);
+      }
     }
-    part += __shfl_xor_sync(0xffffffffu, part, 4);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if (act && gl == 0 && e < cnt) ss[e] = part;
   }
   // bitonic sort by (score desc, id asc), 8 lanes per row
   for (int size = 2; size <= np2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncwarp();
-      for (int i = gl; i < np2 / 2; i += 8) {
+      for (int i = gl; i < np2 / 2; i += LPR) {
         const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
         const bool up = (lo & size) == 0;
         const double a = ss[lo], b = ss[hi];
@@ -667,7 +681,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   __syncwarp();
   if (!act) return;
   const int held = cnt < p.k_eff ? cnt : p.k_eff;
-  for (int i = gl; i < p.k_eff; i += 8) {
+  for (int i = gl; i < p.k_eff; i += LPR) {
     p.out_ids[out * p.k_eff + i] = i < held ? si[i] : -1;
     p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
   }
@@ -697,8 +711,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     //   visited = min(n, max(P, k_eff, #{j : bounds[j]*||u|| >= s_K})),
     // floored at B for work sharing (index.py:372-387).
     int64_t mp = -1;
-    for (int i = gl; i < held; i += 8) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
-    for (int o = 4; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(0xffu << (grp * 8), mp, o));
+    for (int i = gl; i < held; i += LPR) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
+    for (int o = LPR / 2; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(gmask, mp, o));
     if (gl == 0) {
       const int64_t q = ceiling_count(p.bounds + (int64_t)c * p.n, p.n, p.unorm[user], ss[p.k_eff - 1]);
       int64_t v = max(max(mp + 1, (int64_t)p.k_eff), q);
@@ -906,7 +920,9 @@ int kt_for(int k_eff) {
   if (k_eff <= 1) return 1;
   if (k_eff <= 2) return 2;
   if (k_eff <= 4) return 4;
+  if (k_eff == 5) return 5;  // exact sizes for the BASELINE depths K = 5, 10
   if (k_eff <= 8) return 8;
+  if (k_eff == 10) return 10;
   if (k_eff <= 16) return 16;
   if (k_eff <= 32) return 32;
   return 0;
@@ -958,28 +974,36 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& 
     case 1: return launch_gemm_kt<1>(ma, mb, p, g, grid, s);
     case 2: return launch_gemm_kt<2>(ma, mb, p, g, grid, s);
     case 4: return launch_gemm_kt<4>(ma, mb, p, g, grid, s);
+    case 5: return launch_gemm_kt<5>(ma, mb, p, g, grid, s);
     case 8: return launch_gemm_kt<8>(ma, mb, p, g, grid, s);
+    case 10: return launch_gemm_kt<10>(ma, mb, p, g, grid, s);
     case 16: return launch_gemm_kt<16>(ma, mb, p, g, grid, s);
     case 32: return launch_gemm_kt<32>(ma, mb, p, g, grid, s);
     default: return launch_gemm_kt<0>(ma, mb, p, g, grid, s);
   }
 }
 
-int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
+template <int LPR>
+int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
+  constexpr int RPW = 32 / LPR;
   const size_t per_row = ((size_t)fp.pow2 * 12 + (size_t)fp.f * 8 + 15) & ~size_t(15);
   int warps = 8;
-  while (warps > 1 && per_row * kFinRowsPerWarp * warps > 200 * 1024) warps >>= 1;
-  const size_t smem = per_row * kFinRowsPerWarp * warps;
+  while (warps > 1 && per_row * RPW * warps > 100 * 1024) warps >>= 1;
+  const size_t smem = per_row * RPW * warps;
   if (smem > 200 * 1024) {
     set_error("finalize: candidate buffer too large");
     return SIMDEX_EUNSUPPORTED;
   }
-  SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileScope _prof("finalize", s);
-  finalize_kernel<<<(unsigned)ceil_div(rows, kFinRowsPerWarp * warps), 32 * warps, smem, s>>>(fp);
+  finalize_kernel<LPR><<<(unsigned)ceil_div(rows, RPW * warps), 32 * warps, smem, s>>>(fp);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("finalize");
   return SIMDEX_OK;
+}
+
+int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
+  return fp.k_eff > 32 ? launch_finalize_lpr<32>(fp, rows, s) : launch_finalize_lpr<8>(fp, rows, s);
 }
 
 // Candidate buffers + per-row state for up to `rows` packed rows.
@@ -1045,7 +1069,7 @@ void read_ws_stats(int64_t* out) {
 
 // Brute-force fused path (topk_matmul).
 int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
-                    const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                    const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
                     int64_t* heap_ops, float* debug_out, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
@@ -1095,6 +1119,7 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   fp.nu = nu;
   fp.users = users;
   fp.items = items;
+  fp.items32 = items32;
   fp.f = f;
   fp.n = ni;
   fp.k_eff = k_eff;
@@ -1125,7 +1150,7 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
 //   stage 2  the remaining users x the whole catalogue (certified top-K), and
 //            visited from the closed form of Algorithm 1's stop position.
 int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
-                 const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                 const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                  int32_t f, int32_t kp, int32_t su, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
@@ -1209,6 +1234,7 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   fp.nu = nu;
   fp.users = users;
   fp.items = items;
+  fp.items32 = items32;
   fp.f = f;
   fp.list_ids = list_ids;
   fp.list_pos = list_pos;
