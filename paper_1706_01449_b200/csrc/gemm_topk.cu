@@ -645,20 +645,25 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     }
   }
   __syncwarp();
-  for (int e = 0; e < cmax; ++e) {
+  // LPR/8 candidates per round, 8 lanes each (strided partials + xor tree)
+  constexpr int SG = LPR / 8;
+  const int sg = gl >> 3, sl = gl & 7;
+  for (int base = 0; base < cmax; base += SG) {
+    const int e = base + sg;
     double part = 0.0;
     if (act && e < cnt) {
       if (p.items32) {
         const float* x = p.items32 + (int64_t)si[e] * p.f;
-        for (int q = gl; q < p.f; q += LPR) part = fma((double)x[q], us[q], part);
+        for (int q = sl; q < p.f; q += 8) part = fma((double)x[q], us[q], part);
       } else {
         const double* x = p.items + (int64_t)si[e] * p.f;
-        for (int q = gl; q < p.f; q += LPR) part = fma(x[q], us[q], part);
+        for (int q = sl; q < p.f; q += 8) part = fma(x[q], us[q], part);
       }
     }
-#pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (act && gl == 0 && e < cnt) ss[e] = part;
+    part += __shfl_xor_sync(0xffffffffu, part, 4);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    if (act && sl == 0 && e < cnt) ss[e] = part;
   }
   // bitonic sort by (score desc, id asc), 8 lanes per row
   for (int size = 2; size <= np2; size <<= 1) {
@@ -925,12 +930,14 @@ int kt_for(int k_eff) {
   if (k_eff == 10) return 10;
   if (k_eff <= 16) return 16;
   if (k_eff <= 32) return 32;
+  if (k_eff == 50) return 50;  // BASELINE depth K = 50
+  if (k_eff <= 64) return 64;
   return 0;
 }
 
 int cap_for(int k_eff) {
   const int kt = kt_for(k_eff);
-  if (kt > 0) return kt <= 16 ? 64 : 128;  // T is exact-current: the buffer only holds the band
+  if (kt > 0) return kt <= 16 ? 64 : (kt <= 32 ? 128 : 256);  // T is exact-current: the buffer holds the band
   int c = 4 * k_eff + 64;
   int p = 64;
   while (p < c) p <<= 1;
@@ -979,6 +986,8 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& 
     case 10: return launch_gemm_kt<10>(ma, mb, p, g, grid, s);
     case 16: return launch_gemm_kt<16>(ma, mb, p, g, grid, s);
     case 32: return launch_gemm_kt<32>(ma, mb, p, g, grid, s);
+    case 50: return launch_gemm_kt<50>(ma, mb, p, g, grid, s);
+    case 64: return launch_gemm_kt<64>(ma, mb, p, g, grid, s);
     default: return launch_gemm_kt<0>(ma, mb, p, g, grid, s);
   }
 }

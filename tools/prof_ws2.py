@@ -2,15 +2,18 @@ import sys, os, time
 sys.path.insert(0, os.getcwd())
 import torch
 import paper_1706_01449_b200 as sx
-from paper_1706_01449_b200 import workloads as W, index as I
+from paper_1706_01449_b200 import workloads as W, index as I, _lib
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-w = W.cfg2()
+cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+w = W.CONFIGS[cfg]()
 m = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
-cl = sx.kmeans(m.users, 256, max_iters=3, seed=1)
+cl = sx.kmeans(m.users, w.clusters, max_iters=w.max_iters, seed=w.seed)
 idx = sx.build_index(m, cl, 4096)
 for _ in range(3):
     out = I.query_batch_tensors(idx, m, None, k, True)
 torch.cuda.synchronize()
-torch.cuda.nvtx.range_push("timed")
+_lib.profile(True)
 t = time.perf_counter(); out = I.query_batch_tensors(idx, m, None, k, True); torch.cuda.synchronize()
-print("k", k, "ms", 1000 * (time.perf_counter() - t), flush=True)
+dt = time.perf_counter() - t
+ks = {n: _lib.profile_read(n) for n in ("gemm_topk", "finalize", "walk", "select_rows")}
+print("k", k, "ms", 1000 * dt, " ".join(f"{n}={v[0]:.3f}ms/{v[1]}" for n, v in ks.items() if v[1]), "stats", _lib.ws_stats(), flush=True)
