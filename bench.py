@@ -297,8 +297,9 @@ def run_ours(args):
         host_u = torch.from_numpy(model.users.values).pin_memory()
         host_i = torch.from_numpy(model.items.values).pin_memory()
         e2e_steps = max(1, min(3, args.steps))
+        e2e_warm = 2  # first passes pay one-time costs (pinned host pools, tensor maps, allocator growth)
         times = []
-        for s in range(e2e_steps + 1):
+        for s in range(e2e_steps + e2e_warm):
             m2 = sx.ModelPair(sx.FactorMatrix(model.users.values), sx.FactorMatrix(model.items.values))
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -308,7 +309,7 @@ def run_ours(args):
                                        max_iters=w.max_iters, seed=w.seed, force=path)
             _ = res.item_ids  # results are host arrays [U, K] once run_pipeline returns
             torch.cuda.synchronize()
-            if s > 0:
+            if s >= e2e_warm:
                 times.append(time.perf_counter() - t0)
         t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
         if world > 1:

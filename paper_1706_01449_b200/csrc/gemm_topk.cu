@@ -32,8 +32,12 @@
 
 #include <cfloat>
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -404,6 +408,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float mx = fmaxf(fmax3(m0, m1, m2), m3);
               const float nmax = __ldg(p.item_nmax32 + ((un.b_row0 + c0) >> 5));
               if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
+                if constexpr (KT == 1) {
+                  // k = 1: the chunk's largest lower bound is a valid T before any append
+                  float lm = -INFINITY;
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) lm = fmaxf(lm, v[i] - fmaf(cu, __ldg(nrm + i), p.e_abs));
+                  top[0] = fmaxf(top[0], lm);
+                  T = fmaxf(T, top[0]);
+                }
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
@@ -528,10 +540,44 @@ __global__ void item_nrm_kernel(const double* __restrict__ norms, int64_t rows, 
   if (lane == 0) nmax32[chunk] = m;
 }
 
+// k-means assignment operands: argmin_j |p - c_j|^2 == argmax_j p'.c'_j with
+// p' = [p, 1] and c' = [c, -|c|^2/2] (one extra K column, free while f < kp).
+// Row norms for the certified band are guarded by alpha*(1 + |x|^2) per side:
+// the product's cross term eps*alpha^2*(1+p2)(1+c2) >= 2^-39 (p2 + c2) covers
+// the float64 rounding of d2 = (p2 + c2) - 2 p.c, so the exact float64 argmin
+// is always among the candidates.
+template <class P>
+__global__ void max_abs_any_kernel(const P* __restrict__ x, int64_t n, double mul,
+                                   unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs((double)x[i]) * mul);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+template <class P>
+__global__ void pack_aug_kernel(const P* __restrict__ x, const double* __restrict__ sq, int64_t rows, int f,
+                                int centers, int scale_exp, int64_t rows_pad, int kp, uint16_t* __restrict__ out,
+                                double* __restrict__ gnorm) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows_pad) return;
+  const bool live = r < rows;
+  const double q = live ? sq[r] : 0.0;
+  const double aug = live ? (centers ? -0.5 * q : 1.0) : 0.0;
+  for (int k = lane; k < kp; k += 32) {
+    const double v = live ? (k < f ? (double)x[r * f + k] : (k == f ? aug : 0.0)) : 0.0;
+    __nv_bfloat16 b = __double2bfloat16(ldexp(v, scale_exp));
+    out[r * kp + k] = *reinterpret_cast<uint16_t*>(&b);
+  }
+  if (lane == 0) gnorm[r] = live ? sqrt(q + aug * aug) * (1.0 + 0x1p-40) + 0x1p-16 * (1.0 + q) : 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // finalize: exact float64 rescoring of the certified candidates (warp per row)
 // ---------------------------------------------------------------------------
-enum FinalizeMode { kBrute = 0, kPrefix = 1, kFullList = 2 };
+enum FinalizeMode { kBrute = 0, kPrefix = 1, kFullList = 2, kAssign = 3 };
 
 struct FinalizeParams {
   int mode;
@@ -568,6 +614,15 @@ struct FinalizeParams {
   int64_t* over_out;
   int32_t* over_n;
   int pow2;
+  // k-means assignment mode (items = centers): d2 = (p2 + c2) - 2 p.c in
+  // float64, first minimum over the certified candidates
+  const float* users32;  // exact float32 copy of users or null
+  const double* p2;
+  const double* c2;
+  const int64_t* prev;
+  int64_t* out_assign;
+  double* out_d2;
+  unsigned long long* changed;
 };
 
 // First list position j with bounds[j] * unorm < s (ceilings are non-increasing).
@@ -609,7 +664,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     user = p.row_user ? p.row_user[r] : r;
     if (user >= 0 && user < p.nu) {
       out = p.row_out ? p.row_out[r] : r;
-      c = p.mode != kBrute ? p.row_cluster[r] : 0;
+      c = (p.mode == kPrefix || p.mode == kFullList) ? p.row_cluster[r] : 0;
       if (p.row_flags[r]) {
         if (gl == 0) {
           if (p.mode == kPrefix) {  // band overflow on the prefix: redo it on the full list
@@ -617,7 +672,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
             p.cont_list[atomicAdd(p.cont_n, 1)] = r;
           } else {
             const int sl = atomicAdd(p.over_n, 1);
-            p.over_list[sl] = p.mode == kBrute ? user : r;
+            p.over_list[sl] = (p.mode == kBrute || p.mode == kAssign) ? user : r;
             p.over_out[sl] = out;
           }
         }
@@ -633,7 +688,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   int np2 = 2;
   while (np2 < cmax) np2 <<= 1;
   if (act)
-    for (int i = gl; i < p.f; i += LPR) us[i] = p.users[user * p.f + i];
+    for (int i = gl; i < p.f; i += LPR) us[i] = p.users32 ? (double)p.users32[user * p.f + i] : p.users[user * p.f + i];
   const int32_t* cid = p.cand_id + r * p.cap;
   for (int e = gl; e < np2; e += LPR) {
     if (act && e < cnt) {
@@ -664,6 +719,36 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     part += __shfl_xor_sync(0xffffffffu, part, 2);
     part += __shfl_xor_sync(0xffffffffu, part, 1);
     if (act && sl == 0 && e < cnt) ss[e] = part;
+  }
+  if (p.mode == kAssign) {  // clustering.py:100 + argmin (first minimum) over the candidates
+    __syncwarp();
+    double bd = DBL_MAX;
+    int32_t bj = INT32_MAX;
+    if (act) {
+      const double pp = p.p2[user];
+      for (int e = gl; e < cnt; e += LPR) {
+        double d = (pp + p.c2[si[e]]) - 2.0 * ss[e];
+        d = d > 0.0 ? d : 0.0;
+        if (d < bd || (d == bd && si[e] < bj)) {
+          bd = d;
+          bj = si[e];
+        }
+      }
+    }
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (od < bd || (od == bd && oj < bj)) {
+        bd = od;
+        bj = oj;
+      }
+    }
+    if (act && gl == 0) {
+      p.out_assign[user] = bj;
+      p.out_d2[user] = bd;
+      if (p.prev && p.prev[user] != bj) atomicAdd(p.changed, 1ull);
+    }
+    return;
   }
   // bitonic sort by (score desc, id asc), 8 lanes per row
   for (int size = 2; size <= np2; size <<= 1) {
@@ -1364,6 +1449,123 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
       out_visited);
   SIMDEX_LAUNCH_CHECK("fallback_visited");
   return SIMDEX_OK;
+}
+
+// k-means assignment on the tensor cores (clustering.py:96-101, 175-177):
+// augmented product + certified top-1 band, exact float64 d2 over the band's
+// candidates.  Rows whose band overflows are returned in over_rows (count in
+// *n_over) for the float64 SIMT kernel.  Needs f + 1 <= 256.
+template <class P>
+int gemm_assign_impl(const double* points, const P* px, const float* points32, int64_t n, int32_t f,
+                     const double* p2, const double* centers, const double* c2, int32_t c, const int64_t* prev,
+                     int64_t* out_assign, double* out_d2, unsigned long long* changed, int64_t* over_rows,
+                     int32_t* n_over, cudaStream_t s) {
+  const int kp = ((f + 1 + 63) / 64) * 64;
+  GemmGeometry g;
+  int rc = geometry(kp, &g);
+  if (rc) return rc;
+  const int64_t nu_pad = ceil_div(n, 256) * 256, nc_pad = ceil_div(c, 256) * 256;
+  const int64_t nunits = nu_pad / kUnitRows;
+  Scratch<unsigned long long> mx;
+  SIMDEX_CUDA(mx.alloc(3, s));
+  SIMDEX_CUDA(cudaMemsetAsync(mx.p, 0, 3 * sizeof(unsigned long long), s));
+  const int64_t nf = n * (int64_t)f;
+  max_abs_any_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(nf, 256), 4 * 148), 256, 0, s>>>(px, nf, 1.0, mx.p);
+  max_abs_any_kernel<double><<<(unsigned)std::min<int64_t>(ceil_div((int64_t)c * f, 256), 64), 256, 0, s>>>(
+      centers, (int64_t)c * f, 1.0, mx.p + 1);
+  max_abs_any_kernel<double><<<1, 256, 0, s>>>(c2, c, 0.5, mx.p + 2);
+  SIMDEX_LAUNCH_CHECK("max_abs_any");
+  unsigned long long hm[3];
+  SIMDEX_CUDA(cudaMemcpyAsync(hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
+  SIMDEX_CUDA(cudaStreamSynchronize(s));
+  double m[3];
+  for (int i = 0; i < 3; ++i) std::memcpy(&m[i], &hm[i], sizeof(double));
+  const double mu = std::max(m[0], 1.0), mc = std::max(m[1], m[2]);
+  if (!std::isfinite(mu) || !std::isfinite(mc)) {
+    set_error("kmeans_assign: non-finite values");
+    return SIMDEX_EINVAL;
+  }
+  const int su = -std::ilogb(mu), sc = mc > 0.0 ? -std::ilogb(mc) : 0;
+  const int k_eff = 1;
+  RowState st;
+  if ((rc = st.alloc(nu_pad, k_eff, s))) return rc;
+  Scratch<uint16_t> ua, ca;
+  Scratch<double> un, cn;
+  Scratch<Unit> units;
+  Scratch<int32_t> n_units, over_n;
+  Scratch<float> cu, inrm, inmax;
+  Scratch<int64_t> over_out;
+  SIMDEX_CUDA(ua.alloc((size_t)nu_pad * kp, s));
+  SIMDEX_CUDA(ca.alloc((size_t)nc_pad * kp, s));
+  SIMDEX_CUDA(un.alloc(nu_pad, s));
+  SIMDEX_CUDA(cn.alloc(nc_pad, s));
+  SIMDEX_CUDA(units.alloc(nunits, s));
+  SIMDEX_CUDA(n_units.alloc(1, s));
+  SIMDEX_CUDA(over_n.alloc(1, s));
+  SIMDEX_CUDA(over_out.alloc(n, s));
+  SIMDEX_CUDA(cu.alloc(nu_pad, s));
+  SIMDEX_CUDA(inrm.alloc(nc_pad, s));
+  SIMDEX_CUDA(inmax.alloc(nc_pad / 32, s));
+  ProfileScope _prof("assign_pack", s);
+  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad, 8), 256, 0, s>>>(px, p2, n, f, 0, su, nu_pad, kp, ua.p, un.p);
+  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad, 8), 256, 0, s>>>(centers, c2, c, f, 1, sc, nc_pad, kp, ca.p,
+                                                                         cn.p);
+  _prof.end();
+  SIMDEX_LAUNCH_CHECK("pack_aug");
+  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units.p, n_units.p, nunits);
+  SIMDEX_LAUNCH_CHECK("units");
+  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un.p, n, nu_pad, eps_for(kp) * std::ldexp(1.0, su),
+                                                               cu.p);
+  SIMDEX_LAUNCH_CHECK("row_cu");
+  item_nrm_kernel<<<(unsigned)ceil_div(nc_pad / 32, 8), 256, 0, s>>>(cn.p, c, nc_pad, std::ldexp(1.0, sc), inrm.p,
+                                                                      inmax.p);
+  SIMDEX_LAUNCH_CHECK("item_nrm");
+  CUtensorMap ma, mb;
+  if ((rc = make_map(&ma, ua.p, nu_pad, kp))) return rc;
+  if ((rc = make_map(&mb, ca.p, nc_pad, kp))) return rc;
+  TopkParams tp = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu.p, g, f + 1, k_eff);
+  const int grid = (int)(nunits < sm_count() ? nunits : sm_count());
+  if ((rc = launch_gemm(ma, mb, tp, g, grid, s))) return rc;
+  SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
+  FinalizeParams fp{};
+  fp.mode = kAssign;
+  fp.total_rows = n;
+  fp.nu = n;
+  fp.users = points;
+  fp.users32 = points32;
+  fp.items = centers;
+  fp.f = f;
+  fp.n = c;
+  fp.k_eff = k_eff;
+  fp.cap = st.cap;
+  fp.cand_id = st.cid.p;
+  fp.row_count = st.cnt.p;
+  fp.row_flags = st.flags.p;
+  fp.over_list = over_rows;
+  fp.over_out = over_out.p;
+  fp.over_n = over_n.p;
+  fp.pow2 = pow2_at_least(st.cap);
+  fp.p2 = p2;
+  fp.c2 = c2;
+  fp.prev = prev;
+  fp.out_assign = out_assign;
+  fp.out_d2 = out_d2;
+  fp.changed = changed;
+  if ((rc = launch_finalize(fp, n, s))) return rc;
+  SIMDEX_CUDA(cudaMemcpyAsync(n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SIMDEX_CUDA(cudaStreamSynchronize(s));
+  return SIMDEX_OK;
+}
+
+int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, const double* p2,
+                       const double* centers, const double* c2, int32_t c, const int64_t* prev, int64_t* out_assign,
+                       double* out_d2, unsigned long long* changed, int64_t* over_rows, int32_t* n_over,
+                       cudaStream_t s) {
+  if (points32)
+    return gemm_assign_impl<float>(points, points32, points32, n, f, p2, centers, c2, c, prev, out_assign, out_d2,
+                                   changed, over_rows, n_over, s);
+  return gemm_assign_impl<double>(points, points, nullptr, n, f, p2, centers, c2, c, prev, out_assign, out_d2,
+                                  changed, over_rows, n_over, s);
 }
 
 }  // namespace simdex

@@ -14,10 +14,18 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace simdex {
+
+int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, const double* p2,
+                       const double* centers, const double* c2, int32_t c, const int64_t* prev, int64_t* out_assign,
+                       double* out_d2, unsigned long long* changed, int64_t* over_rows, int32_t* n_over,
+                       cudaStream_t s);
+
 namespace {
 
+constexpr int kAssignGemmMaxF = 256;  // augmented K (f + 1) the tensor-core path takes
 constexpr int kAssignThreads = 128;
 constexpr int kCC = 32;  // centers per chunk (register accumulators)
 constexpr int kFC = 32;  // factors per chunk
@@ -38,11 +46,13 @@ template <class P>
 __global__ void __launch_bounds__(kAssignThreads) assign_kernel(
     const P* __restrict__ points, const double* __restrict__ p2, int64_t n, int f, const double* __restrict__ centers,
     const double* __restrict__ c2, int c, const int64_t* __restrict__ prev, int64_t* __restrict__ out_assign,
-    double* __restrict__ out_d2, unsigned long long* __restrict__ changed, double* __restrict__ block_sums) {
+    double* __restrict__ out_d2, unsigned long long* __restrict__ changed, double* __restrict__ block_sums,
+    const int64_t* __restrict__ rows, int64_t n_rows) {
   __shared__ double cs[kCC][kFC + 1];
   __shared__ double red[kAssignThreads / 32];
-  const int64_t u = (int64_t)blockIdx.x * kAssignThreads + threadIdx.x;
-  const bool live = u < n;
+  const int64_t idx = (int64_t)blockIdx.x * kAssignThreads + threadIdx.x;
+  const bool live = rows ? idx < n_rows : idx < n;
+  const int64_t u = rows ? (live ? rows[idx] : 0) : idx;
   const P* x = points + (live ? u : 0) * f;
   const double pp = live ? p2[u] : 0.0;
   double best = DBL_MAX;
@@ -90,7 +100,22 @@ __global__ void __launch_bounds__(kAssignThreads) assign_kernel(
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < kAssignThreads / 32; ++w) s += red[w];
-    block_sums[blockIdx.x] = s;
+    if (block_sums) block_sums[blockIdx.x] = s;
+  }
+}
+
+// per-block sums of x (fixed tree): the objective from out_d2
+__global__ void block_sum_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double red[8];
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  double v = i < n ? x[i] : 0.0;
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    part[blockIdx.x] = s;
   }
 }
 
@@ -134,33 +159,58 @@ __global__ void members_kernel(const int32_t* ids, int64_t n, int64_t* members) 
   if (i < n) members[i] = ids[i];
 }
 
-// One CTA (256 threads) per cluster: thread (lane_m, k) sums members
-// lane_m, lane_m + L, ... of factor k; the L partials are then added in lane
-// order.  Fixed partition and order: deterministic.  Empty clusters keep
-// their centroid (clustering.py:170-172).
+// One CTA (8 warps) per cluster: warp w sums members w, w+8, ... with its
+// lanes on consecutive factors (coalesced row reads), then the 8 warp partials
+// are added in warp order.  Fixed partition and order: deterministic.  Empty
+// clusters keep their centroid (clustering.py:170-172).
+constexpr int kMeanWarps = 8;
+constexpr int kMeanRegs = 4;  // factors per lane per chunk (128-factor chunks)
+
 template <class P>
-__global__ void __launch_bounds__(256) centroid_mean_kernel(const P* __restrict__ points, int f,
-                                                            const int64_t* __restrict__ members,
-                                                            const int64_t* __restrict__ offsets,
-                                                            double* __restrict__ centers) {
-  __shared__ double part[256];
+__global__ void __launch_bounds__(kMeanWarps * 32) centroid_mean_kernel(const P* __restrict__ points, int f,
+                                                                        const int64_t* __restrict__ members,
+                                                                        const int64_t* __restrict__ offsets,
+                                                                        double* __restrict__ centers) {
+  __shared__ double part[kMeanWarps][kMeanRegs * 32];
   const int c = blockIdx.x;
   const int64_t b = offsets[c], e = offsets[c + 1];
   if (e == b) return;
-  const int L = f >= 256 ? 1 : 256 / f;
-  for (int k0 = 0; k0 < f; k0 += 256) {
-    const int fk = (f - k0) < 256 ? (f - k0) : 256;
-    const int t = threadIdx.x;
-    const int ml = f >= 256 ? 0 : t / fk, k = f >= 256 ? t : t % fk;
-    double s = 0.0;
-    if (ml < L && k < fk)
-      for (int64_t m = b + ml; m < e; m += L) s += (double)points[members[m] * f + k0 + k];
-    part[t] = s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k0 = 0; k0 < f; k0 += kMeanRegs * 32) {
+    double acc[kMeanRegs];
+#pragma unroll
+    for (int q = 0; q < kMeanRegs; ++q) acc[q] = 0.0;
+    int64_t m = b + w;
+    for (; m + 3 * kMeanWarps < e; m += 4 * kMeanWarps) {  // 4 independent rows in flight
+      const P* r0 = points + members[m] * f + k0;
+      const P* r1 = points + members[m + kMeanWarps] * f + k0;
+      const P* r2 = points + members[m + 2 * kMeanWarps] * f + k0;
+      const P* r3 = points + members[m + 3 * kMeanWarps] * f + k0;
+#pragma unroll
+      for (int q = 0; q < kMeanRegs; ++q) {
+        const int k = lane + 32 * q;
+        if (k0 + k < f) {
+          const double v0 = (double)r0[k], v1 = (double)r1[k], v2 = (double)r2[k], v3 = (double)r3[k];
+          acc[q] = (((acc[q] + v0) + v1) + v2) + v3;
+        }
+      }
+    }
+    for (; m < e; m += kMeanWarps) {
+      const P* r0 = points + members[m] * f + k0;
+#pragma unroll
+      for (int q = 0; q < kMeanRegs; ++q) {
+        const int k = lane + 32 * q;
+        if (k0 + k < f) acc[q] += (double)r0[k];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kMeanRegs; ++q) part[w][lane + 32 * q] = acc[q];
     __syncthreads();
-    if (t < fk) {
+    for (int k = threadIdx.x; k < kMeanRegs * 32 && k0 + k < f; k += blockDim.x) {
       double tot = 0.0;
-      for (int l = 0; l < L; ++l) tot += part[l * fk + t];
-      centers[(int64_t)c * f + k0 + t] = tot / (double)(e - b);
+#pragma unroll
+      for (int ww = 0; ww < kMeanWarps; ++ww) tot += part[ww][k];
+      centers[(int64_t)c * f + k0 + k] = tot / (double)(e - b);
     }
     __syncthreads();
   }
@@ -174,37 +224,126 @@ constexpr int kPickThreads = 1024;
 
 // d2 = min(d2, |p - center_j|^2) with the reference's expression
 // (||p||^2 + ||c||^2 - 2 p.c, clipped); pass 0 initialises.  Also block sums.
+// Points whose nearest seed a is far from the new center skip the distance:
+// |c_j - c_a|^2 >= 4 (d2 + eta)(1 + 2^-30), eta = 2^-40 (p2 + c2_j + c2_a)
+// bounds the float64 cancellation of the expression, so by the triangle
+// inequality the computed distance could not go below d2 and min() would keep
+// d2: the skip is bit-exact.  Each warp owns 32 consecutive points; the ones
+// that need the distance are taken 4 at a time, 8 lanes per point on strided
+// factors (coalesced row reads, all loads issued before the FMAs), reduced by
+// a fixed shuffle tree; the block sum adds the points in a fixed order.
+constexpr int kSeedWarps = kSeedThreads / 32;
+constexpr int kSeedBufBytes = 16384;  // per-warp row staging cap
+
+struct SeedSmem {  // dynamic shared layout of seed_update_kernel
+  int batch;       // rows staged per bulk copy (<= 32)
+  size_t buf;      // bytes per warp buffer
+  size_t cen_off, bar_off, buf_off, total;
+};
+
+__host__ __device__ inline SeedSmem seed_smem(int f, size_t esize) {
+  SeedSmem m;
+  const size_t row = (size_t)f * esize;
+  int b = (int)(kSeedBufBytes / row);
+  m.batch = b > 32 ? 32 : (b < 1 ? 1 : b);
+  m.buf = (((size_t)m.batch * row + 32) + 127) & ~size_t(127);
+  m.cen_off = 0;
+  m.bar_off = ((size_t)f * 8 + 15) & ~size_t(15);
+  m.buf_off = (m.bar_off + kSeedWarps * 8 + 127) & ~size_t(127);
+  m.total = m.buf_off + kSeedWarps * m.buf;
+  return m;
+}
+
 template <class P>
-__global__ void __launch_bounds__(kSeedThreads) seed_update_kernel(const P* __restrict__ points,
+__global__ void __launch_bounds__(kSeedThreads, 4) seed_update_kernel(const P* __restrict__ points,
                                                                    const double* __restrict__ p2, int64_t n, int f,
                                                                    const int64_t* __restrict__ rows, int j,
                                                                    double* __restrict__ d2,
+                                                                   int32_t* __restrict__ near,
+                                                                   const double* __restrict__ seed_c2,
+                                                                   const double* __restrict__ cd2,
                                                                    double* __restrict__ block_sums,
                                                                    const int32_t* __restrict__ degenerate) {
-  extern __shared__ double cen[];
-  __shared__ double red[kSeedThreads / 32];
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  __shared__ double red[kSeedWarps];
   if (*degenerate >= 0) return;
+  const SeedSmem L = seed_smem(f, sizeof(P));
+  double* cen = reinterpret_cast<double*>(sm_raw + L.cen_off);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + L.bar_off);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, sl = lane & 7, grp = lane >> 3;
+  unsigned char* buf = sm_raw + L.buf_off + w * L.buf;
+  const int64_t wbase = (int64_t)blockIdx.x * kSeedThreads + w * 32;
+  const int64_t me = wbase + lane;
+  const size_t row_bytes = (size_t)f * sizeof(P);
+  const size_t total_bytes = (size_t)n * row_bytes;
+  const unsigned char* gbase = reinterpret_cast<const unsigned char*>(points);
+  if (lane == 0) {
+    sm100::mbar_init(bars + w, 1);
+    sm100::fence_barrier_init();
+  }
+  double old = DBL_MAX, mp2 = 0.0;
+  int a = 0;
+  if (me < n) {
+    mp2 = p2[me];
+    if (j > 0) {
+      old = d2[me];
+      a = near[me];
+    }
+  }
   const int64_t r = rows[j];
   for (int k = threadIdx.x; k < f; k += kSeedThreads) cen[k] = (double)points[r * f + k];
   __syncthreads();
   const double cc = p2[r];
-  const int64_t u = (int64_t)blockIdx.x * kSeedThreads + threadIdx.x;
-  double v = 0.0;
-  if (u < n) {
-    const P* x = points + u * f;
-    double dot = 0.0;
-    for (int k = 0; k < f; ++k) dot = fma((double)x[k], cen[k], dot);
-    double d = (p2[u] + cc) - 2.0 * dot;
-    d = d > 0.0 ? d : 0.0;
-    v = (j == 0) ? d : fmin(d2[u], d);
-    d2[u] = v;
+  bool need = me < n;
+  if (need && j > 0) {
+    const double eta = 0x1p-40 * (mp2 + cc + seed_c2[a]);
+    need = !(cd2[a] >= 4.0 * (old + eta) * (1.0 + 0x1p-30));
   }
+  double fin = old;  // this lane's point's d2 after the pass
+  const unsigned needm = __ballot_sync(0xffffffffu, need);
+  uint32_t phase = 0;
+  for (int b0 = 0; b0 < 32; b0 += L.batch) {
+    const unsigned bm = L.batch >= 32 ? 0xffffffffu : (((1u << L.batch) - 1u) << b0);
+    unsigned pend = needm & bm;
+    if (!pend) continue;
+    // stage the batch's contiguous rows in shared memory with one bulk copy
+    const int64_t u0 = wbase + b0;
+    const int64_t u1 = (wbase + b0 + L.batch) < n ? (wbase + b0 + L.batch) : n;
+    const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
+    const size_t sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
+    const bool staged = a0 + sz <= total_bytes;  // else (buffer tail) read the rows from global
+    if (staged) {
+      __syncwarp();
+      if (lane == 0) {
+        sm100::fence_proxy_async_smem();
+        sm100::mbar_arrive_expect_tx(bars + w, (uint32_t)sz);
+        sm100::bulk_load_1d(buf, gbase + a0, (uint32_t)sz, bars + w);
+      }
+      sm100::mbar_wait(bars + w, phase);
+      phase ^= 1;
+    }
+    const unsigned char* sbase = buf + (start - a0);
+    if (need && lane >= b0 && lane < b0 + L.batch) {  // lane per point, row from shared memory
+      const P* x = staged ? reinterpret_cast<const P*>(sbase + (size_t)(lane - b0) * row_bytes) : points + me * f;
+      double dot = 0.0;
+#pragma unroll 5
+      for (int k = 0; k < f; ++k) dot = fma((double)x[k], cen[k], dot);
+      double d = (mp2 + cc) - 2.0 * dot;
+      d = d > 0.0 ? d : 0.0;
+      if (j == 0 || d < old) {
+        d2[me] = d;
+        near[me] = j;
+        fin = d;
+      }
+    }
+  }
+  double v = me < n ? fin : 0.0;
   v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  if (lane == 0) red[w] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < kSeedThreads / 32; ++w) s += red[w];
+    for (int ww = 0; ww < kSeedWarps; ++ww) s += red[ww];
     block_sums[blockIdx.x] = s;
   }
 }
@@ -220,6 +359,9 @@ __global__ void __launch_bounds__(kPickThreads) seed_pick_kernel(const P* __rest
                                                                  int64_t nblocks, const double* __restrict__ uniforms,
                                                                  int j, int64_t* __restrict__ rows,
                                                                  double* __restrict__ centers,
+                                                                 const double* __restrict__ p2,
+                                                                 double* __restrict__ seed_c2,
+                                                                 double* __restrict__ cd2,
                                                                  int32_t* __restrict__ degenerate) {
   __shared__ double scan[kPickThreads];
   __shared__ double wsum[kSeedThreads / 32];
@@ -312,14 +454,51 @@ __global__ void __launch_bounds__(kPickThreads) seed_pick_kernel(const P* __rest
   }
   __syncthreads();
   const int64_t p = (int64_t)s_pick;
-  for (int k = t; k < f; k += blockDim.x) centers[(int64_t)(j + 1) * f + k] = (double)points[p * f + k];
+  double* cnew = scan;  // reuse: the new center, then squared distances to the earlier seeds
+  for (int k = t; k < f; k += blockDim.x) {
+    const double v = (double)points[p * f + k];
+    centers[(int64_t)(j + 1) * f + k] = v;
+    cnew[k] = v;
+  }
+  if (t == 0) seed_c2[j + 1] = p2[p];
+  __syncthreads();
+  // squared distances new seed -> seeds 0..j: 4 lanes per seed, 8 seeds per warp
+  // per round, all loads of a round in flight together
+  const int g4 = lane >> 2, l4 = lane & 3;
+  for (int q0 = wid * 8; q0 <= j; q0 += kPickThreads / 4) {
+    const int q = q0 + g4;
+    double acc = 0.0;
+    if (q <= j) {
+      const double* cq = centers + (int64_t)q * f;
+      for (int k0 = 0; k0 < f; k0 += 64) {
+        double xv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int k = k0 + l4 + 4 * i;
+          xv[i] = k < f ? cq[k] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int k = k0 + l4 + 4 * i;
+          if (k < f) {
+            const double d = cnew[k] - xv[i];
+            acc = fma(d, d, acc);
+          }
+        }
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (q <= j && l4 == 0) cd2[q] = acc;
+  }
 }
 
 template <class P>
 __global__ void seed_first_kernel(const P* __restrict__ points, int f, int64_t first, int64_t* rows, double* centers,
-                                  int32_t* degenerate) {
+                                  const double* __restrict__ p2, double* __restrict__ seed_c2, int32_t* degenerate) {
   if (threadIdx.x == 0) {
     rows[0] = first;
+    seed_c2[0] = p2[first];
     *degenerate = -1;
   }
   for (int k = threadIdx.x; k < f; k += blockDim.x) centers[k] = (double)points[first * f + k];
@@ -341,24 +520,42 @@ __global__ void to_f32_kernel(const double* __restrict__ x, int64_t n, float* __
 // launchers (float64 or exact float32 points)
 // ---------------------------------------------------------------------------
 template <class P>
-int assign_impl(const P* points, int64_t n, int32_t f, const double* centers, int32_t c, const int64_t* prev,
-                int64_t* out_assign, double* out_d2, int64_t* out_changed, double* out_objective, cudaStream_t s) {
+int assign_impl(const double* points, const float* points32, const P* px, int64_t n, int32_t f,
+                const double* centers, int32_t c, const int64_t* prev, int64_t* out_assign, double* out_d2,
+                int64_t* out_changed, double* out_objective, cudaStream_t s) {
   Scratch<double> p2, c2, part;
-  const int64_t nb = ceil_div(n, kAssignThreads);
   SIMDEX_CUDA(p2.alloc(n, s));
   SIMDEX_CUDA(c2.alloc(c, s));
-  SIMDEX_CUDA(part.alloc(nb, s));
-  sqnorm_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(points, n, f, p2.p);
+  sqnorm_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(px, n, f, p2.p);
   SIMDEX_LAUNCH_CHECK("sqnorm");
   sqnorm_kernel<double><<<(unsigned)ceil_div(c, 256), 256, 0, s>>>(centers, c, f, c2.p);
   SIMDEX_LAUNCH_CHECK("sqnorm");
   SIMDEX_CUDA(cudaMemsetAsync(out_changed, 0, sizeof(int64_t), s));
-  ProfileScope _prof("kmeans_assign", s);
-  assign_kernel<P><<<(unsigned)nb, kAssignThreads, 0, s>>>(points, p2.p, n, f, centers, c2.p, c, prev, out_assign,
-                                                           out_d2, reinterpret_cast<unsigned long long*>(out_changed),
-                                                           part.p);
-  _prof.end();
-  SIMDEX_LAUNCH_CHECK("assign");
+  auto* changed = reinterpret_cast<unsigned long long*>(out_changed);
+  if (f + 1 <= kAssignGemmMaxF) {
+    // tensor-core candidates + exact float64 d2; overflowing bands go to the SIMT kernel
+    Scratch<int64_t> over;
+    SIMDEX_CUDA(over.alloc(n, s));
+    int32_t n_over = 0;
+    int rc = gemm_kmeans_assign(points, points32, n, f, p2.p, centers, c2.p, c, prev, out_assign, out_d2, changed,
+                                over.p, &n_over, s);
+    if (rc) return rc;
+    if (n_over > 0) {
+      assign_kernel<P><<<(unsigned)ceil_div(n_over, kAssignThreads), kAssignThreads, 0, s>>>(
+          px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, nullptr, over.p, n_over);
+      SIMDEX_LAUNCH_CHECK("assign");
+    }
+  } else {
+    ProfileScope _prof("kmeans_assign", s);
+    assign_kernel<P><<<(unsigned)ceil_div(n, kAssignThreads), kAssignThreads, 0, s>>>(
+        px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, nullptr, nullptr, 0);
+    _prof.end();
+    SIMDEX_LAUNCH_CHECK("assign");
+  }
+  const int64_t nb = ceil_div(n, 256);
+  SIMDEX_CUDA(part.alloc(nb, s));
+  block_sum_kernel<<<(unsigned)nb, 256, 0, s>>>(out_d2, n, part.p);
+  SIMDEX_LAUNCH_CHECK("block_sum");
   sum_partials_kernel<<<1, 1024, 0, s>>>(part.p, nb, out_objective);
   SIMDEX_LAUNCH_CHECK("sum_partials");
   return SIMDEX_OK;
@@ -367,26 +564,34 @@ int assign_impl(const P* points, int64_t n, int32_t f, const double* centers, in
 template <class P>
 int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, const double* uniforms,
               int64_t* out_rows, double* out_centers, int32_t* out_deg, cudaStream_t s) {
+  if (f > kPickThreads) {
+    set_error("kmeans_seed: f > %d", kPickThreads);
+    return SIMDEX_EUNSUPPORTED;
+  }
   const int64_t nb = ceil_div(n, kSeedThreads);
-  Scratch<double> p2, d2, part;
+  Scratch<double> p2, d2, part, seed_c2, cd2;
+  Scratch<int32_t> near;
   SIMDEX_CUDA(p2.alloc(n, s));
   SIMDEX_CUDA(d2.alloc(n, s));
+  SIMDEX_CUDA(near.alloc(n, s));
   SIMDEX_CUDA(part.alloc(nb, s));
+  SIMDEX_CUDA(seed_c2.alloc(k, s));
+  SIMDEX_CUDA(cd2.alloc(k, s));
   sqnorm_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(points, n, f, p2.p);
   SIMDEX_LAUNCH_CHECK("sqnorm");
-  seed_first_kernel<P><<<1, 128, 0, s>>>(points, f, first, out_rows, out_centers, out_deg);
+  seed_first_kernel<P><<<1, 128, 0, s>>>(points, f, first, out_rows, out_centers, p2.p, seed_c2.p, out_deg);
   SIMDEX_LAUNCH_CHECK("seed_first");
-  const size_t smem = (size_t)f * sizeof(double);
+  const size_t smem = seed_smem(f, sizeof(P)).total;
   if (smem > 48 * 1024)
     SIMDEX_CUDA(cudaFuncSetAttribute(seed_update_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int j = 0; j + 1 < k; ++j) {
     ProfileScope _prof("seed_update", s);
-    seed_update_kernel<P><<<(unsigned)nb, kSeedThreads, smem, s>>>(points, p2.p, n, f, out_rows, j, d2.p, part.p,
-                                                                   out_deg);
+    seed_update_kernel<P><<<(unsigned)nb, kSeedThreads, smem, s>>>(points, p2.p, n, f, out_rows, j, d2.p, near.p,
+                                                                   seed_c2.p, cd2.p, part.p, out_deg);
     _prof.end();
     ProfileScope _prof2("seed_pick", s);
     seed_pick_kernel<P><<<1, kPickThreads, 0, s>>>(points, n, f, d2.p, part.p, nb, uniforms, j, out_rows, out_centers,
-                                                   out_deg);
+                                                   p2.p, seed_c2.p, cd2.p, out_deg);
     _prof2.end();
     count_launches(2);
   }
@@ -398,7 +603,7 @@ template <class P>
 int mean_impl(const P* points, int32_t f, const int64_t* members, const int64_t* offsets, int32_t c,
               double* centers, cudaStream_t s) {
   ProfileScope _prof("centroid_mean", s);
-  centroid_mean_kernel<P><<<(unsigned)c, 256, 0, s>>>(points, f, members, offsets, centers);
+  centroid_mean_kernel<P><<<(unsigned)c, kMeanWarps * 32, 0, s>>>(points, f, members, offsets, centers);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("centroid_mean");
   return SIMDEX_OK;
@@ -428,9 +633,10 @@ extern "C" int simdex_kmeans_assign(const double* points, const float* points32,
   SIMDEX_CHECK_ARG(n >= 1 && f >= 1 && c >= 1, "simdex_kmeans_assign: bad sizes");
   cudaStream_t s = as_stream(stream);
   if (points32)
-    return assign_impl<float>(points32, n, f, centers, c, prev_assign, out_assign, out_d2, out_changed, out_objective,
-                              s);
-  return assign_impl<double>(points, n, f, centers, c, prev_assign, out_assign, out_d2, out_changed, out_objective, s);
+    return assign_impl<float>(points, points32, points32, n, f, centers, c, prev_assign, out_assign, out_d2,
+                              out_changed, out_objective, s);
+  return assign_impl<double>(points, nullptr, points, n, f, centers, c, prev_assign, out_assign, out_d2, out_changed,
+                             out_objective, s);
 }
 
 extern "C" int simdex_kmeans_update(const double* points, const float* points32, int64_t n, int32_t f,
