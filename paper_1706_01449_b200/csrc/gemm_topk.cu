@@ -37,7 +37,7 @@
 #include <cstring>
 #include <vector>
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -58,7 +58,7 @@ constexpr int kSlab = kTileM * 128;  // one [128 rows x 64 bf16] swizzled slab: 
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kMaxCap = 512;
-constexpr uint32_t kIdesc = idesc_bf16_f32(kTileM, kTileN);
+constexpr uint32_t kIdesc = idesc_f16_f32(kTileM, kTileN);
 
 struct Unit {
   int64_t a_row0;   // first packed user row (multiple of 256)
@@ -244,6 +244,8 @@ template <int KT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_topk_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const TopkParams p) {
+  constexpr bool kDebug = KT < 0;         // raw accumulators to p.debug_out, no selection
+  constexpr int KTT = KT > 0 ? KT : 1;    // register top-K size (KT = 0: buffer re-selection)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int KB = p.kb, S = p.stages;
@@ -362,9 +364,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t grow = un.a_row0 + row_local;
       const float cu = live ? p.row_cu[grow] : 0.f;
       float T = (live && p.row_T0) ? p.row_T0[grow] : -INFINITY;
-      float top[KT > 0 ? KT : 1];
+      float top[KTT];
 #pragma unroll
-      for (int i = 0; i < (KT > 0 ? KT : 1); ++i) top[i] = -INFINITY;
+      for (int i = 0; i < KTT; ++i) top[i] = -INFINITY;
       int cnt = 0, flags = 0;
       int64_t hops = 0;
       int32_t* my_id = p.cand_id + grow * p.cap;
@@ -375,112 +377,140 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t buf = acc & 1, use = acc >> 1;
         mbar_wait(t_full + buf, use & 1);
         tc_fence_after();
+        bool released = false;
         if (h < ntile_a) {
-          for (int ch = 0; ch < kTileN / 32; ++ch) {
-            const int c0 = t * kTileN + ch * 32;
-            const int nvalid = min(32, un.n_items - c0);
-            if (nvalid <= 0) break;
-            float v[32];
-            tmem_ld32(tbase + lane_off + (buf * 2 + h) * kTileN + ch * 32, v);
-            if (p.debug_out) {
-              if (live) {
+          const int tile_valid = min(kTileN, un.n_items - t * kTileN);
+          // the tile's four 32-item norm maxima in one load
+          const float4 nm4 = __ldg(reinterpret_cast<const float4*>(p.item_nmax32 + ((un.b_row0 + t * kTileN) >> 5)));
+          // two chunks of 32 columns per TMEM wait; once the whole tile is in
+          // registers the accumulator buffer goes back to the MMA warp
+          constexpr int LDC = 2;
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (i < nvalid) p.debug_out[grow * p.debug_ld + un.b_row0 + c0 + i] = v[i];
-              }
-              continue;
+          for (int cg = 0; cg < kTileN / 32; cg += LDC) {
+            if (cg * 32 >= tile_valid) break;
+            uint32_t raw[LDC][32];
+#pragma unroll
+            for (int c = 0; c < LDC; ++c)
+              tmem_ld32_nowait(tbase + lane_off + (buf * 2 + h) * kTileN + (cg + c) * 32, raw[c]);
+            tmem_wait_ld();
+            if (cg + LDC >= kTileN / 32) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(t_empty + buf);
+              released = true;
             }
-            const bool act = live && !flags;
-            unsigned mask = 0;  // items of this chunk whose upper bound reaches T
-            const float* nrm = p.item_nrm + un.b_row0 + c0;
-            if (act) {
-              if (nvalid < 32) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? v[i] : -INFINITY;
+            for (int c = 0; c < LDC; ++c) {
+              const int ch = cg + c;
+              const int c0 = t * kTileN + ch * 32;
+              const int nvalid = tile_valid - ch * 32;
+              if (nvalid <= 0) break;
+              if constexpr (kDebug) {
+                if (live)
+                  for (int i = 0; i < 32 && i < nvalid; ++i)
+                    p.debug_out[grow * p.debug_ld + un.b_row0 + c0 + i] = __uint_as_float(raw[c][i]);
+                continue;
               }
-              // chunk max as a tree of 3-input FMNMX3 (17 instructions for 32 values)
-              float m[11];
+              const bool act = live && !flags;
+              unsigned mask = 0;  // items of this chunk whose upper bound reaches T
+              const float* nrm = p.item_nrm + un.b_row0 + c0;
+              float vloc[32];  // the chunk, spilled for the (rare) appends: indexed dynamically
+              if (act) {
+                float v[32];
 #pragma unroll
-              for (int i = 0; i < 10; ++i) m[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
-              m[10] = fmaxf(v[30], v[31]);
-              const float m0 = fmax3(m[0], m[1], m[2]), m1 = fmax3(m[3], m[4], m[5]);
-              const float m2 = fmax3(m[6], m[7], m[8]), m3 = fmaxf(m[9], m[10]);
-              const float mx = fmaxf(fmax3(m0, m1, m2), m3);
-              const float nmax = __ldg(p.item_nmax32 + ((un.b_row0 + c0) >> 5));
-              if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
-                if constexpr (KT == 1) {
-                  // k = 1: the chunk's largest lower bound is a valid T before any append
-                  float lm = -INFINITY;
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[c][i]);
+                if (nvalid < 32) {
 #pragma unroll
-                  for (int i = 0; i < 32; ++i) lm = fmaxf(lm, v[i] - fmaf(cu, __ldg(nrm + i), p.e_abs));
-                  top[0] = fmaxf(top[0], lm);
-                  T = fmaxf(T, top[0]);
+                  for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? v[i] : -INFINITY;
                 }
+                // chunk max as a tree of 3-input FMNMX3 (17 instructions for 32 values)
+                float m[11];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
-                  mask |= (v[i] + e >= T) ? (1u << i) : 0u;
-                }
-                if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
-              }
-            }
-            // converged append loop: every lane with pending items takes one per round
-            while (__any_sync(0xffffffffu, mask != 0u)) {
-              if (mask) {
-                const int i = __ffs(mask) - 1;
-                mask &= mask - 1;
-                float vi = v[0];
+                for (int i = 0; i < 10; ++i) m[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+                m[10] = fmaxf(v[30], v[31]);
+                const float m0 = fmax3(m[0], m[1], m[2]), m1 = fmax3(m[3], m[4], m[5]);
+                const float m2 = fmax3(m[6], m[7], m[8]), m3 = fmaxf(m[9], m[10]);
+                const float mx = fmaxf(fmax3(m0, m1, m2), m3);
+                const float nmax = ch == 0 ? nm4.x : ch == 1 ? nm4.y : ch == 2 ? nm4.z : nm4.w;
+                if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
+                  if constexpr (KT == 1) {
+                    // k = 1: the chunk's largest lower bound is a valid T before any append
+                    float lm = -INFINITY;
 #pragma unroll
-                for (int j = 1; j < 32; ++j) vi = (i == j) ? v[j] : vi;
-                const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
-                const float hi = vi + e;
-                if (hi >= T && !flags) {  // T may have risen within this chunk
-                  my_hi[cnt] = hi;
-                  my_id[cnt] = c0 + i;
-                  ++cnt;
-                  ++hops;
-                  if constexpr (KT > 0) {
-                    push_top<KT>(top, vi - e);
-                    T = fmaxf(T, KT == kk + 1 ? top[KT - 1] : top_at<KT>(top, kk));
-                    if (cnt == p.cap) {
-                      compact_filter(my_hi, my_id, cnt, T);
-                      if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
-                    }
-                  } else {
-                    my_lo[cnt - 1] = vi - e;  // the buffer always has >= 32 free slots here
+                    for (int i = 0; i < 32; ++i) lm = fmaxf(lm, v[i] - fmaf(cu, __ldg(nrm + i), p.e_abs));
+                    top[0] = fmaxf(top[0], lm);
+                    T = fmaxf(T, top[0]);
+                  }
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) {
+                    const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
+                    mask |= (v[i] + e >= T) ? (1u << i) : 0u;
+                  }
+                  if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
+                  if (mask) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) vloc[i] = v[i];
                   }
                 }
               }
-            }
-            if constexpr (KT == 0) {
-              // keep >= 32 free slots per row: re-select T for every full row, warp-cooperatively
-              unsigned need = __ballot_sync(0xffffffffu, act && cnt > p.cap - 32);
-              while (need) {
-                const int who = __ffs(need) - 1;
-                need &= need - 1;
-                const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
-                const int c_w = __shfl_sync(0xffffffffu, cnt, who);
-                const float t_w = __shfl_sync(0xffffffffu, T, who);
-                int nc;
-                float nt;
-                warp_compact(p.cand_lo + g_w * p.cap, p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, c_w,
-                             p.k_eff, t_w, lane, &nc, &nt);
-                if (lane == who) {
-                  cnt = nc;
-                  T = nt;
-                  if (cnt > p.cap - 32 - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
+              // converged append loop: every lane with pending items takes one per round
+              while (__any_sync(0xffffffffu, mask != 0u)) {
+                if (mask) {
+                  const int i = __ffs(mask) - 1;
+                  mask &= mask - 1;
+                  const float vi = vloc[i];
+                  const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
+                  const float hi = vi + e;
+                  if (hi >= T && !flags) {  // T may have risen within this chunk
+                    my_hi[cnt] = hi;
+                    my_id[cnt] = c0 + i;
+                    ++cnt;
+                    ++hops;
+                    if constexpr (KT > 0) {
+                      push_top<KTT>(top, vi - e);
+                      T = fmaxf(T, KTT == kk + 1 ? top[KTT - 1] : top_at<KTT>(top, kk));
+                      if (cnt == p.cap) {
+                        compact_filter(my_hi, my_id, cnt, T);
+                        if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
+                      }
+                    } else {
+                      my_lo[cnt - 1] = vi - e;  // the buffer always has >= 32 free slots here
+                    }
+                  }
+                }
+              }
+              if constexpr (KT == 0) {
+                // keep >= 32 free slots per row: re-select T for every full row, warp-cooperatively
+                unsigned need = __ballot_sync(0xffffffffu, act && cnt > p.cap - 32);
+                while (need) {
+                  const int who = __ffs(need) - 1;
+                  need &= need - 1;
+                  const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+                  const int c_w = __shfl_sync(0xffffffffu, cnt, who);
+                  const float t_w = __shfl_sync(0xffffffffu, T, who);
+                  int nc;
+                  float nt;
+                  warp_compact(p.cand_lo + g_w * p.cap, p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, c_w,
+                               p.k_eff, t_w, lane, &nc, &nt);
+                  if (lane == who) {
+                    cnt = nc;
+                    T = nt;
+                    if (cnt > p.cap - 32 - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
+                  }
                 }
               }
             }
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(t_empty + buf);
+        if (!released) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(t_empty + buf);
+        }
       }
       if constexpr (KT == 0) {
         // final re-selection of T for every row of this warp (warp-cooperative)
-        if (h < ntile_a && !p.debug_out) {
+        if (h < ntile_a) {
           unsigned need = __ballot_sync(0xffffffffu, live && !flags && cnt > p.k_eff);
           while (need) {
             const int who = __ffs(need) - 1;
@@ -499,9 +529,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (live && h < ntile_a) {
+      if (live && h < ntile_a && !kDebug) {
         if constexpr (KT > 0) {
-          if (!flags && !p.debug_out && cnt > p.k_eff) compact_filter(my_hi, my_id, cnt, T);
+          if (!flags && cnt > p.k_eff) compact_filter(my_hi, my_id, cnt, T);
         }
         p.row_count[grow] = cnt;
         p.row_flags[grow] = flags;
@@ -568,7 +598,7 @@ __global__ void pack_aug_kernel(const P* __restrict__ x, const double* __restric
   const double aug = live ? (centers ? -0.5 * q : 1.0) : 0.0;
   for (int k = lane; k < kp; k += 32) {
     const double v = live ? (k < f ? (double)x[r * f + k] : (k == f ? aug : 0.0)) : 0.0;
-    __nv_bfloat16 b = __double2bfloat16(ldexp(v, scale_exp));
+    __half b = __double2half(ldexp(v, scale_exp));
     out[r * kp + k] = *reinterpret_cast<uint16_t*>(&b);
   }
   if (lane == 0) gnorm[r] = live ? sqrt(q + aug * aug) * (1.0 + 0x1p-40) + 0x1p-16 * (1.0 + q) : 0.0;
@@ -992,7 +1022,7 @@ int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int kp) {
   cuuint64_t strides[1] = {(cuuint64_t)kp * 2};
   cuuint32_t box[2] = {64, 128};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -1003,7 +1033,7 @@ int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int kp) {
 }
 
 double eps_for(int kp) {
-  return std::ldexp(1.0, -7) + std::ldexp(1.0, -16) + (kp + 16) * std::ldexp(1.0, -22) + std::ldexp(1.0, -20);
+  return std::ldexp(1.0, -10) + std::ldexp(1.0, -22) + (kp + 16) * std::ldexp(1.0, -22) + std::ldexp(1.0, -20);
 }
 
 int kt_for(int k_eff) {
@@ -1062,7 +1092,8 @@ int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParam
 
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
                 cudaStream_t s) {
-  switch (p.debug_out ? 1 : kt_for(p.k_eff)) {
+  if (p.debug_out) return launch_gemm_kt<-1>(ma, mb, p, g, grid, s);
+  switch (kt_for(p.k_eff)) {
     case 1: return launch_gemm_kt<1>(ma, mb, p, g, grid, s);
     case 2: return launch_gemm_kt<2>(ma, mb, p, g, grid, s);
     case 4: return launch_gemm_kt<4>(ma, mb, p, g, grid, s);
@@ -1124,7 +1155,7 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   p.item_nrm = inrm;
   p.item_nmax32 = inmax;
   p.row_cu = cu;
-  p.e_abs = (float)std::ldexp((double)(f + 1), -124);
+  p.e_abs = (float)(std::ldexp((double)(((f + 63) / 64) * 64), -22) + std::ldexp((double)(f + 1), -124));
   p.kb = g.kb;
   p.k_steps = (f + 15) / 16;
   p.stages = g.stages;

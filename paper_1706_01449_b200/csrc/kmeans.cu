@@ -12,6 +12,8 @@
 // an exact float32 copy (all BASELINE inputs are float32 upcast), as float32
 // converted back to float64 exactly: same arithmetic, half the bytes.
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -493,6 +495,411 @@ __global__ void __launch_bounds__(kPickThreads) seed_pick_kernel(const P* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// persistent k-means++ seeding: one cooperative launch runs every pass.
+// Per pass: (U) the D^2 update over 256-point chunks (as seed_update_kernel),
+// grid barrier, (P) every CTA locates the next seed redundantly from the
+// chunk sums (identical arithmetic in every CTA, so identical picks), CTA 0
+// records it, all CTAs split the new seed's distances to the earlier seeds,
+// grid barrier.  No launch or host round trip between passes.
+// ---------------------------------------------------------------------------
+struct SeedArgs {
+  int64_t n;
+  int f, k;
+  const double* p2;
+  const double* uniforms;
+  int64_t* rows;
+  double* centers;
+  double* d2;
+  int32_t* near;
+  double* seed_c2;
+  double* cd2;
+  double* chunk_sums;
+  double* range_sums;  // per CTA: sum of its contiguous chunk range
+  int64_t nchunks;
+  int32_t* degenerate;
+  unsigned* barrier;
+  unsigned long long* dbg;  // optional phase timers (ns): update, barrier 1, pick, barrier 2
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of the (co-resident) grid; `gen` counts barriers passed
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  ++gen;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const unsigned want = gen * gridDim.x;
+    while (ld_acquire_u32(bar) < want) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// inclusive scan of one double per thread over a 256-thread CTA (warp
+// shuffles + warp totals); returns the inclusive prefix, *total the CTA sum
+// inclusive scan of one double per thread over the CTA (warp shuffles +
+// warp totals in fixed order); *total = the CTA sum
+__device__ __forceinline__ double cta_scan(double x, double* wsum, double* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  double pre = 0.0, tot = 0.0;
+  for (int q = 0; q < nw; ++q) {
+    if (q < w) pre += wsum[q];
+    tot += wsum[q];
+  }
+  *total = tot;
+  __syncthreads();
+  return pre + x;
+}
+
+// dynamic shared layout of seed_persistent_kernel: new-seed center, cached
+// seed-seed distances and seed norms, per-warp double-buffered row staging
+struct PSeedSmem {
+  int kc;  // cached seeds (0: read cd2 / seed_c2 from global)
+  size_t buf, cen_off, cdc_off, scc_off, bar_off, buf_off, total;
+};
+
+__host__ __device__ inline PSeedSmem pseed_smem(int f, size_t esize, int k, int wpb) {
+  PSeedSmem m;
+  const size_t row = (size_t)f * esize;
+  m.buf = ((32 * row + 32) + 127) & ~size_t(127);
+  m.kc = k <= 2048 ? k : 0;
+  m.cen_off = 0;
+  m.cdc_off = ((size_t)f * 8 + 15) & ~size_t(15);
+  m.scc_off = m.cdc_off + (size_t)m.kc * 8;
+  m.bar_off = (m.scc_off + (size_t)m.kc * 8 + 15) & ~size_t(15);
+  m.buf_off = (m.bar_off + (size_t)wpb * 2 * 8 + 127) & ~size_t(127);
+  m.total = m.buf_off + (size_t)wpb * 2 * m.buf;
+  return m;
+}
+
+// First index i in [0, m) whose cumulative sum base + v[0] + ... + v[i]
+// exceeds target (numpy's searchsorted(cumsum, target, 'right')), scanned by
+// the whole CTA: contiguous per-thread runs (loads batched), a CTA scan, and
+// the crossing run walked by its owner.  If rounding puts the target beyond
+// the total, the last positive entry is taken.  Returns the index and the sum
+// before it in *before (every thread gets the same values).
+template <class Get>
+__device__ int64_t cta_crossing(Get get, int64_t m, double base, double target, double* wsum, double* s_val,
+                                int64_t* s_idx, double* before) {
+  const int t = threadIdx.x, CS = blockDim.x;
+  const int64_t per = (m + CS - 1) / CS;
+  const int64_t c0 = t * per < m ? t * per : m, c1 = (c0 + per) < m ? (c0 + per) : m;
+  double mine = 0.0;
+  for (int64_t b = c0; b < c1; b += 8) {
+    double vv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) vv[i] = b + i < c1 ? get(b + i) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mine += vv[i];
+  }
+  double total;
+  const double incl = base + cta_scan(mine, wsum, &total);
+  if (t == 0) *s_idx = -1;
+  __syncthreads();
+  const double excl = incl - mine;
+  if (c0 < c1 && incl > target && !(excl > target)) {
+    double acc = excl;
+    int64_t c = c1;
+    for (int64_t q = c0; q < c1; ++q) {
+      const double v = get(q);
+      if (v > 0.0 && acc + v > target) {
+        c = q;
+        break;
+      }
+      acc += v;
+    }
+    if (c == c1) {  // rounding between the summation orders: last positive entry of the run
+      c = c1 - 1;
+      while (c > c0 && !(get(c) > 0.0)) --c;
+      acc = excl;
+      for (int64_t q = c0; q < c; ++q) acc += get(q);
+    }
+    *s_idx = c;
+    *s_val = acc;
+  }
+  __syncthreads();
+  if (*s_idx < 0 && t == 0) {
+    // rounding put the target outside this level's sums: beyond the total ->
+    // last positive entry; before the base -> first positive entry
+    int64_t c;
+    if (target < base) {
+      c = 0;
+      while (c + 1 < m && !(get(c) > 0.0)) ++c;
+    } else {
+      c = m - 1;
+      while (c > 0 && !(get(c) > 0.0)) --c;
+    }
+    double acc = base;
+    for (int64_t q = 0; q < c; ++q) acc += get(q);
+    *s_idx = c;
+    *s_val = acc;
+  }
+  __syncthreads();
+  const int64_t r = *s_idx;
+  *before = *s_val;
+  __syncthreads();
+  return r;
+}
+
+template <class P>
+__global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restrict__ points, const SeedArgs a) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  __shared__ double red[2][8];
+  __shared__ double wsum[8];
+  __shared__ double s_base;
+  __shared__ int64_t s_block;
+  __shared__ unsigned long long s_pick;
+  const int f = a.f;
+  const int64_t n = a.n;
+  const int CS = blockDim.x, wpb = CS >> 5;  // chunk = one point per thread
+  const PSeedSmem L = pseed_smem(f, sizeof(P), a.k, wpb);
+  double* cen = reinterpret_cast<double*>(sm_raw + L.cen_off);
+  double* cdc = reinterpret_cast<double*>(sm_raw + L.cdc_off);
+  double* scc = reinterpret_cast<double*>(sm_raw + L.scc_off);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + L.bar_off);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (lane == 0) {
+    sm100::mbar_init(bars + 2 * w, 1);
+    sm100::mbar_init(bars + 2 * w + 1, 1);
+    sm100::fence_barrier_init();
+  }
+  const size_t row_bytes = (size_t)f * sizeof(P);
+  const size_t total_bytes = (size_t)n * row_bytes;
+  const unsigned char* gbase = reinterpret_cast<const unsigned char*>(points);
+  const int64_t G = gridDim.x;
+  uint32_t phbits = 0;  // mbarrier phase per staging buffer
+  unsigned gen = 0;
+  for (int q = t; q < f; q += CS) cen[q] = __ldcg(a.centers + q);
+  __syncthreads();
+  unsigned long long tm0 = 0, tm1 = 0;
+  const bool timing = a.dbg && blockIdx.x == 0 && t == 0;
+  for (int j = 0; j + 1 < a.k; ++j) {
+    if (timing) tm0 = gtimer();
+    if (L.kc)
+      for (int q = t; q <= j; q += CS) {
+        scc[q] = __ldcg(a.seed_c2 + q);
+        if (q < j) cdc[q] = __ldcg(a.cd2 + q);
+      }
+    __syncthreads();
+    const double cc = L.kc ? scc[j] : __ldcg(a.seed_c2 + j);
+    // chunks are dealt round-robin (concurrent CTAs stream neighbouring rows);
+    // the pick's CTA ranges are contiguous and summed after the barrier
+    const int64_t r0 = blockIdx.x, r1 = a.nchunks;
+    // ------------------------------------------------------------ (U) update
+    // per warp, a three-stage pipeline over this CTA's chunks: the test inputs
+    // of chunk C load while chunk B's rows stream into one staging buffer and
+    // chunk A (other buffer) is scored
+    auto load_regs = [&](int64_t ch, double& mp2, double& old, int& an) {
+      const int64_t me = ch * CS + w * 32 + lane;
+      mp2 = 0.0;
+      old = DBL_MAX;
+      an = 0;
+      if (ch < r1 && me < n) {
+        mp2 = a.p2[me];
+        if (j > 0) {
+          old = __ldcg(a.d2 + me);
+          an = __ldcg(a.near + me);
+        }
+      }
+    };
+    auto test = [&](int64_t ch, double mp2, double old, int an) -> bool {
+      const int64_t me = ch * CS + w * 32 + lane;
+      if (ch >= r1 || me >= n) return false;
+      if (j == 0) return true;
+      const double c2a = L.kc ? scc[an] : __ldcg(a.seed_c2 + an);
+      const double cda = L.kc ? cdc[an] : __ldcg(a.cd2 + an);
+      const double eta = 0x1p-40 * (mp2 + cc + c2a);
+      return !(cda >= 4.0 * (old + eta) * (1.0 + 0x1p-30));
+    };
+    // stage the warp's 32 rows with one bulk copy when any of them is needed
+    // (per-row copies of only the needed rows measured slower: TMA issue
+    // rate); returns false when the rows are read from global instead
+    auto issue = [&](int64_t ch, unsigned mask, int bsel) -> bool {
+      if (!mask) return false;
+      const int64_t u0 = ch * CS + w * 32;
+      const int64_t u1 = (u0 + 32) < n ? (u0 + 32) : n;
+      const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
+      const size_t sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
+      if (a0 + sz > total_bytes) return false;  // buffer tail: read from global
+      __syncwarp();
+      if (lane == 0) {
+        sm100::fence_proxy_async_smem();
+        sm100::mbar_arrive_expect_tx(bars + 2 * w + bsel, (uint32_t)sz);
+        sm100::bulk_load_1d(sm_raw + L.buf_off + (size_t)(2 * w + bsel) * L.buf, gbase + a0, (uint32_t)sz,
+                            bars + 2 * w + bsel);
+      }
+      return true;
+    };
+    int64_t chA = r0;
+    double mp2A, oldA, mp2B, oldB;
+    int anA, anB;
+    load_regs(chA, mp2A, oldA, anA);
+    bool needA = test(chA, mp2A, oldA, anA);
+    unsigned mA = __ballot_sync(0xffffffffu, needA);
+    int bA = 0;
+    bool sA = issue(chA, mA, bA);
+    int64_t chB = chA + G;
+    load_regs(chB, mp2B, oldB, anB);
+    int par = 0;
+    while (chA < r1) {
+      const int64_t chC = chB + G;
+      const bool needB = test(chB, mp2B, oldB, anB);
+      const unsigned mB = __ballot_sync(0xffffffffu, needB);
+      const bool sB = issue(chB, mB, bA ^ 1);
+      double mp2C, oldC;
+      int anC;
+      load_regs(chC, mp2C, oldC, anC);
+      // score chunk A
+      const int64_t meA = chA * CS + w * 32 + lane;
+      double fin = oldA;
+      if (mA) {
+        if (sA) {
+          sm100::mbar_wait(bars + 2 * w + bA, (phbits >> bA) & 1u);
+          phbits ^= 1u << bA;
+        }
+        if (needA) {
+          const size_t s0 = (size_t)(chA * CS + w * 32) * row_bytes;  // slice start
+          const P* x = sA ? reinterpret_cast<const P*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + (s0 & 15) +
+                                                       (size_t)lane * row_bytes)
+                          : points + meA * f;
+          double dot = 0.0;
+#pragma unroll 5
+          for (int q = 0; q < f; ++q) dot = fma((double)x[q], cen[q], dot);
+          double d = (mp2A + cc) - 2.0 * dot;
+          d = d > 0.0 ? d : 0.0;
+          if (j == 0 || d < oldA) {
+            a.d2[meA] = d;
+            a.near[meA] = j;
+            fin = d;
+          }
+        }
+      }
+      double v = meA < n ? fin : 0.0;
+      v = warp_sum(v);
+      if (lane == 0) red[par][w] = v;
+      __syncthreads();
+      if (t == 0) {
+        double sum = 0.0;
+        for (int q = 0; q < wpb; ++q) sum += red[par][q];
+        a.chunk_sums[chA] = sum;
+      }
+      par ^= 1;
+      chA = chB;
+      mp2A = mp2B;
+      oldA = oldB;
+      needA = needB;
+      mA = mB;
+      sA = sB;
+      bA ^= 1;
+      chB = chC;
+      mp2B = mp2C;
+      oldB = oldC;
+      anB = anC;
+    }
+    if (timing) {
+      tm1 = gtimer();
+      a.dbg[0] += tm1 - tm0;
+      tm0 = tm1;
+    }
+    grid_barrier(a.barrier, gen);
+    if (t == 0) {  // this CTA's contiguous range of chunk sums, in chunk order
+      const int64_t g0 = a.nchunks * blockIdx.x / G, g1 = a.nchunks * (blockIdx.x + 1) / G;
+      double rs = 0.0;
+      for (int64_t b = g0; b < g1; b += 8) {
+        double vv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vv[i] = b + i < g1 ? __ldcg(a.chunk_sums + b + i) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rs += vv[i];
+      }
+      a.range_sums[blockIdx.x] = rs;
+    }
+    grid_barrier(a.barrier, gen);
+    if (timing) {
+      tm1 = gtimer();
+      a.dbg[1] += tm1 - tm0;
+      tm0 = tm1;
+    }
+    // ---------------------------------------------------------- (P) pick seed j+1
+    // every CTA locates it (same arithmetic, same result): run sums of the
+    // chunk sums (loads batched), CTA scan, the crossing run, chunk, point
+    // three levels, one CTA-wide scan each: CTA ranges, chunks of the
+    // crossing range, points of the crossing chunk
+    double total = 0.0;
+    {
+      const int64_t per = (G + CS - 1) / CS;
+      const int64_t q0 = t * per < G ? t * per : G, q1 = (q0 + per) < G ? (q0 + per) : G;
+      double mine = 0.0;
+      for (int64_t q = q0; q < q1; ++q) mine += __ldcg(a.range_sums + q);
+      cta_scan(mine, wsum, &total);
+    }
+    if (!(total > 0.0)) {  // degenerate: every remaining pass takes the host branch
+      if (blockIdx.x == 0 && t == 0) *a.degenerate = j + 1;
+      break;
+    }
+    const double target = a.uniforms[j] * total;
+    double before;
+    const int64_t rg = cta_crossing([&](int64_t q) { return __ldcg(a.range_sums + q); }, G, 0.0, target, wsum,
+                                    &s_base, &s_block, &before);
+    const int64_t g0 = a.nchunks * rg / G, g1 = a.nchunks * (rg + 1) / G;
+    const int64_t chk = g0 + cta_crossing([&](int64_t q) { return __ldcg(a.chunk_sums + g0 + q); }, g1 - g0, before,
+                                          target, wsum, &s_base, &s_block, &before);
+    const int64_t pb = chk * CS, pe = (pb + CS) < n ? (pb + CS) : n;
+    const int64_t pp = pb + cta_crossing([&](int64_t q) { return __ldcg(a.d2 + pb + q); }, pe - pb, before, target,
+                                         wsum, &s_base, &s_block, &before);
+    if (t == 0) s_pick = (unsigned long long)pp;
+    __syncthreads();
+    const int64_t p = (int64_t)s_pick;
+    for (int q = t; q < f; q += CS) {
+      const double cv = (double)points[p * f + q];
+      cen[q] = cv;
+      if (blockIdx.x == 0) a.centers[(int64_t)(j + 1) * f + q] = cv;
+    }
+    if (blockIdx.x == 0 && t == 0) {
+      a.rows[j + 1] = p;
+      a.seed_c2[j + 1] = a.p2[p];
+    }
+    __syncthreads();
+    // squared distances new seed -> seeds 0..j, one warp per seed across the grid
+    for (int64_t q = (int64_t)blockIdx.x * wpb + w; q <= j; q += G * wpb) {
+      const double* cq = a.centers + q * f;
+      double acc = 0.0;
+      for (int r = lane; r < f; r += 32) {
+        const double d = cen[r] - __ldcg(cq + r);
+        acc = fma(d, d, acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) a.cd2[q] = acc;
+    }
+    if (timing) {
+      tm1 = gtimer();
+      a.dbg[2] += tm1 - tm0;
+      tm0 = tm1;
+    }
+    grid_barrier(a.barrier, gen);
+    if (timing) a.dbg[3] += gtimer() - tm0;
+  }
+}
+
 template <class P>
 __global__ void seed_first_kernel(const P* __restrict__ points, int f, int64_t first, int64_t* rows, double* centers,
                                   const double* __restrict__ p2, double* __restrict__ seed_c2, int32_t* degenerate) {
@@ -582,6 +989,79 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
   seed_first_kernel<P><<<1, 128, 0, s>>>(points, f, first, out_rows, out_centers, p2.p, seed_c2.p, out_deg);
   SIMDEX_LAUNCH_CHECK("seed_first");
   const size_t smem = seed_smem(f, sizeof(P)).total;
+  if (k == 1) return SIMDEX_OK;
+  {
+    // one cooperative launch for every pass (grid = co-resident CTAs, two per
+    // SM); the chunk is one point per thread, 32 per warp
+    // CTA size by resident warps per SM (staging buffers bound them)
+    int wpb = 0, occ = 0;
+    size_t psm = 0;
+    for (int cand = 8; cand >= 1; cand >>= 1) {
+      const size_t sm_c = pseed_smem(f, sizeof(P), k, cand).total;
+      if (sm_c > 200 * 1024) continue;
+      SIMDEX_CUDA(cudaFuncSetAttribute(seed_persistent_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm_c));
+      int o = 0;
+      SIMDEX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, seed_persistent_kernel<P>, 32 * cand, sm_c));
+      if (o * cand > occ * wpb) {
+        wpb = cand;
+        occ = o;
+        psm = sm_c;
+      }
+    }
+    if (occ >= 1) {
+      SIMDEX_CUDA(cudaFuncSetAttribute(seed_persistent_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)psm));
+      const int64_t cs = 32 * wpb, nch = ceil_div(n, cs);
+      Scratch<unsigned> bar;
+      Scratch<double> csum, rsum;
+      int64_t grid = (int64_t)occ * sm_count();
+      if (grid > nch) grid = nch;
+      SIMDEX_CUDA(bar.alloc(1, s));
+      SIMDEX_CUDA(csum.alloc(nch, s));
+      SIMDEX_CUDA(rsum.alloc(grid, s));
+      SIMDEX_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), s));
+      SeedArgs a{};
+      a.n = n;
+      a.f = f;
+      a.k = k;
+      a.p2 = p2.p;
+      a.uniforms = uniforms;
+      a.rows = out_rows;
+      a.centers = out_centers;
+      a.d2 = d2.p;
+      a.near = near.p;
+      a.seed_c2 = seed_c2.p;
+      a.cd2 = cd2.p;
+      a.chunk_sums = csum.p;
+      a.range_sums = rsum.p;
+      a.nchunks = nch;
+      a.degenerate = out_deg;
+      a.barrier = bar.p;
+      Scratch<unsigned long long> dbg;
+      const bool timing = std::getenv("SIMDEX_SEED_TIMING") != nullptr;
+      if (timing) {
+        SIMDEX_CUDA(dbg.alloc(4, s));
+        SIMDEX_CUDA(cudaMemsetAsync(dbg.p, 0, 4 * sizeof(unsigned long long), s));
+        a.dbg = dbg.p;
+      }
+      const P* pts = points;
+      void* args[] = {(void*)&pts, (void*)&a};
+      ProfileScope _prof("seed_persistent", s);
+      SIMDEX_CUDA(cudaLaunchCooperativeKernel((const void*)seed_persistent_kernel<P>, dim3((unsigned)grid),
+                                              dim3((unsigned)cs), args, psm, s));
+      _prof.end();
+      count_launches(1);
+      if (timing) {
+        unsigned long long h[4];
+        SIMDEX_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        SIMDEX_CUDA(cudaStreamSynchronize(s));
+        fprintf(stderr, "[simdex] seed grid %lld x %lld: update %.3f ms barrier %.3f ms pick %.3f ms barrier %.3f ms\n",
+                (long long)grid, (long long)cs, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6);
+      }
+      return SIMDEX_OK;
+    }
+  }
   if (smem > 48 * 1024)
     SIMDEX_CUDA(cudaFuncSetAttribute(seed_update_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int j = 0; j + 1 < k; ++j) {

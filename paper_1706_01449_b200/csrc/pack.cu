@@ -2,7 +2,7 @@
 // by an exact power of two, round-to-nearest-even, zero padded to [rows_pad,
 // kp]) + float64 row norms; and the work-sharing prefix gather (every
 // cluster's first B list items in list order, index.py:351-357).
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -19,7 +19,7 @@ __global__ void pack_bf16_kernel(const double* __restrict__ x, int64_t rows, int
   for (int k = lane; k < kp; k += 32) {
     double v = (r < rows && k < f) ? x[r * f + k] : 0.0;
     ss = fma(v, v, ss);
-    __nv_bfloat16 b = __double2bfloat16(ldexp(v, scale_exp));
+    __half b = __double2half(ldexp(v, scale_exp));
     out[r * kp + k] = *reinterpret_cast<uint16_t*>(&b);
   }
   ss = warp_sum(ss);

@@ -27,24 +27,24 @@ def _model(sx, users, items):
 @pytest.mark.parametrize("nu,ni,f", [(300, 500, 50), (256, 128, 64), (1000, 77, 5), (130, 1300, 100),
                                      (513, 260, 128), (40, 33, 1), (260, 300, 200)])
 def test_tcgen05_accumulators_match_float_reference(sx, nu, ni, f):
-    """The raw TMEM accumulators equal fp32 products of the bf16 operands."""
+    """The raw TMEM accumulators equal fp32 products of the fp16 operands."""
     import torch
     from paper_1706_01449_b200 import _device, _ops
     rng = np.random.default_rng(nu * 7 + f)
     m = _model(sx, rng.normal(size=(nu, f)), rng.normal(size=(ni, f)) * rng.lognormal(0, 1, (ni, 1)))
     pu, pi = _device.packed(m.users), _device.packed(m.items)
     got = _ops.gemm_debug(pu, pi, f)
-    a = _bf16_to_f32(pu.bf16[:nu, :f])
-    b = _bf16_to_f32(pi.bf16[:ni, :f])
+    a = _f16_to_f32(pu.bf16[:nu, :f])
+    b = _f16_to_f32(pi.bf16[:ni, :f])
     want = (a.double() @ b.double().T)
     scale = (a.double().abs() @ b.double().abs().T)
     err = (got.double() - want).abs()
     assert bool((err <= scale * (f + 2) * 2.0 ** -22 + 1e-30).all()), float((err / scale.clamp_min(1e-30)).max())
 
 
-def _bf16_to_f32(t16):
+def _f16_to_f32(t16):
     import torch
-    return (t16.to(torch.int32) << 16).view(torch.float32)
+    return t16.view(torch.float16).float()
 
 
 @pytest.mark.parametrize("nu,ni,f,k", [(700, 2000, 50, 10), (300, 129, 8, 1), (257, 4000, 32, 100), (100, 50, 3, 5),

@@ -1,0 +1,30 @@
+"""Instructions executed per CUDA source line: python tools/ncu_src_inst.py rep [N] [kernel-substring]"""
+import csv, subprocess, sys
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+ksub = sys.argv[3] if len(sys.argv) > 3 else None
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+cur_fn, agg, ii = None, {}, None
+for r in rows:
+    if len(r) >= 2 and r[0] == "Function Name":
+        cur_fn = r[1]
+        continue
+    if len(r) > 4 and r[0] == "Line No":
+        ii = r.index("Instructions Executed")
+        continue
+    if ii is None or len(r) <= ii or not r[0]:
+        continue
+    if ksub and (cur_fn is None or ksub not in cur_fn):
+        continue
+    try:
+        v = int(r[ii])
+    except ValueError:
+        continue
+    key = (r[0], r[1][:100])
+    agg[key] = agg.get(key, 0) + v
+tot = sum(agg.values()) or 1
+print("total warp instructions", tot)
+for (ln, src), v in sorted(agg.items(), key=lambda x: -x[1])[:n]:
+    print(f"{v:11d} {100 * v / tot:5.1f}%  L{ln:>5}  {src}")

@@ -13,5 +13,5 @@ for it in range(2):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t
     t = time.perf_counter(); idx = sx.build_index(m, cl, 4096); torch.cuda.synchronize(); bt = time.perf_counter() - t
-    ks = {n: _lib.profile_read(n) for n in ("seed_update", "seed_pick", "kmeans_assign", "assign_pack", "gemm_topk", "finalize", "centroid_mean", "bounds")}
+    ks = {n: _lib.profile_read(n) for n in ("seed_persistent", "seed_update", "seed_pick", "kmeans_assign", "assign_pack", "gemm_topk", "finalize", "centroid_mean", "bounds")}
     print(f"{cfg} kmeans {dt*1e3:.1f} ms build {bt*1e3:.1f} ms", " ".join(f"{n}={v[0]:.2f}ms/{v[1]}" for n, v in ks.items()), flush=True)
