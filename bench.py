@@ -284,8 +284,8 @@ def run_ours(args):
     roof = None
     if gemm_ms:
         achieved = flops / (gemm_ms / 1000.0) / 1e12
-        roof = {"kernel": "gemm_topk_kernel (tcgen05 bf16 x bf16 -> fp32 TMEM, fused certified top-K)",
-                "bound": "tensor", "achieved": achieved, "peak": bf16, "peak_kind": f"{peak_kind} bf16 dense (burst)",
+        roof = {"kernel": "gemm_topk_kernel (tcgen05 fp16 x fp16 -> fp32 TMEM, fused certified top-K)",
+                "bound": "tensor", "achieved": achieved, "peak": bf16, "peak_kind": f"{peak_kind} dense bf16 (= fp16 dense rate on B200; burst)",
                 "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
                 "algorithmic_flops_per_step": flops, "launch_ms_per_step": gemm_ms,
                 "launches_per_step": kernels["gemm_topk"]["launches_per_step"], "per_unit": per_unit,
@@ -333,7 +333,7 @@ def run_ours(args):
         line = {
             "metric": f"exact top-K users/sec (f={f}, K={k})", "value": value, "unit": "users/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (exact) / bf16 tensor-core candidates",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (exact) / fp16 tensor-core candidates",
             "data": "synthetic (seeded, BASELINE.json shapes; trained Netflix/R2 models unavailable)",
             "config": {"workload": f"{w.name}: {nu}x{ni}x{f}, K={k}, C={cl.num_clusters}, B=4096",
                        "path": path, "decision": decision, "mean_visited_sample": est.mean_visited,

@@ -77,18 +77,18 @@ SIMDEX_API int simdex_topk_exact(const double* users, int64_t nu, const double* 
 /* max |x[i]| over n values into *out (device float64); picks the packing scale. */
 SIMDEX_API int simdex_max_abs(const double* x, int64_t n, double* out, void* stream);
 
-/* Operand packing for the tensor-core path: bf16 copy of x * 2^scale_exp,
+/* Operand packing for the tensor-core path: fp16 copy of x * 2^scale_exp,
  * zero padded to [rows_pad, kp] (kp = 64*ceil(f/64), rows_pad >= rows), and
  * float64 row norms of the UNSCALED rows.  Replaces the fp64->operand
  * conversion implicit in brute.py:93 (dgemm on FactorMatrix values). */
-SIMDEX_API int simdex_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp,
-                     int64_t rows_pad, int32_t kp, uint16_t* out_bf16, double* out_norms, void* stream);
+SIMDEX_API int simdex_pack_f16(const double* x, int64_t rows, int32_t f, int32_t scale_exp,
+                     int64_t rows_pad, int32_t kp, uint16_t* out_f16, double* out_norms, void* stream);
 
 /* brute.py:59-113 topk_matmul: users x items product on tcgen05 tensor cores
- * (single-pass bf16 operands, fp32 accumulation in TMEM) fused with a
+ * (single-pass fp16 operands, fp32 accumulation in TMEM) fused with a
  * certified running top-K, then exact float64 rescoring of the surviving
  * candidates.  Results equal simdex_topk_exact.
- *   ub/ib: packed operands from simdex_pack_bf16 (same kp, scale exps su/si);
+ *   ub/ib: packed operands from simdex_pack_f16 (same kp, scale exps su/si);
  *   u_norm/i_norm: float64 norms of the unscaled rows;
  *   heap_ops: optional int64[nu]: per user count of tile scores above the
  *   running K-th at the time the tile is merged (brute.py:95-97; tile order
@@ -204,7 +204,7 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
  * per-cluster prefix operands from simdex_build_prefix ([c, b_pad, kp]).
  * Users whose K-th does not beat the ceiling at B are finished by a second
  * certified tensor-core pass over the whole catalogue (ib / item_norms, the
- * simdex_pack_bf16 operand of the items); their Algorithm 1 stop position
+ * simdex_pack_f16 operand of the items); their Algorithm 1 stop position
  * then follows in closed form from the exact top-K (list_pos = inverse of
  * list_ids, from simdex_build_index).
  * out_visited follows the reference: n if B >= n, else max(B, walk visited).
@@ -231,13 +231,13 @@ SIMDEX_API int simdex_group_queries(const int64_t* q_user, int64_t nq, const int
                          int64_t* out_q_user, int64_t* out_perm, int64_t* out_off, void* stream);
 
 /* Diagnostic: raw fp32 accumulators of the tcgen05 product of two packed
- * operands (simdex_pack_bf16 layout), out float[nu, ni].  Used by the tests to
+ * operands (simdex_pack_f16 layout), out float[nu, ni].  Used by the tests to
  * validate the TMA/UMMA descriptors against a float reference. */
 SIMDEX_API int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t* ib, int64_t ni, int32_t f,
                       int32_t kp, float* out, void* stream);
 
 /* Work-sharing operands: for every cluster the first min(B, ni) list items,
- * gathered in list order into bf16 [c, b_pad, kp] (b_pad = 128*ceil(B'/128))
+ * gathered in list order into fp16 [c, b_pad, kp] (b_pad = 128*ceil(B'/128))
  * plus their float64 norms [c, b_pad]; the re-layout that makes the prefix
  * product a dense TMA-fed GEMM (index.py:351-357). */
 SIMDEX_API int simdex_build_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,

@@ -2,7 +2,7 @@
 
 A FactorMatrix is immutable, so its device copies are computed once per
 device and cached on the object: the float64 values (row-major, what the
-exact kernels read), their row norms, and the packed bf16 tensor-core
+exact kernels read), their row norms, and the packed fp16 tensor-core
 operand.  Host->device copies go through pinned staging.
 """
 

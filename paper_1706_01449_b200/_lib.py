@@ -32,7 +32,7 @@ SIGNATURES = {
     "simdex_device_info": [C.c_int, P, P, P],
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
     "simdex_max_abs": [P, I64, P, P],
-    "simdex_pack_bf16": [P, I64, I32, I32, I64, I32, P, P, P],
+    "simdex_pack_f16": [P, I64, I32, I32, I64, I32, P, P, P],
     "simdex_topk_matmul": [P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, P],
     "simdex_norm_order": [P, I64, P, P],
     "simdex_to_f32": [P, I64, P, P, P],

@@ -32,15 +32,15 @@ def _c(t, dtype):
 
 @dataclass
 class Packed:
-    """bf16 tensor-core operand of a factor matrix (see simdex_pack_bf16)."""
+    """fp16 tensor-core operand of a factor matrix (see simdex_pack_f16)."""
 
-    bf16: torch.Tensor      # int16 storage [rows_pad, kp]
+    op: torch.Tensor        # fp16 bits in int16 storage [rows_pad, kp]
     norms: torch.Tensor     # float64 [rows] norms of the unscaled rows
     scale_exp: int
     kp: int
     rows: int
     perm: torch.Tensor | None = None   # operand row -> item id (norm-sorted operand), else None
-    rows_pad: int = 0                  # rows of the bf16 operand
+    rows_pad: int = 0                  # rows of the fp16 operand
 
 
 ROW_PAD = 256
@@ -50,25 +50,25 @@ def norm_sorted(p: Packed) -> Packed:
     """The item operand re-laid out by (norm desc, id asc) (simdex_norm_order):
     the brute-force pass then meets high-norm items first, its thresholds rise
     early and low-norm tiles fail the norm bound."""
-    perm = torch.empty(p.rows, dtype=I32, device=p.bf16.device)
+    perm = torch.empty(p.rows, dtype=I32, device=p.op.device)
     call("simdex_norm_order", ptr(p.norms), p.rows, ptr(perm), stream_ptr())
     rows_pad = ROW_PAD * ((p.rows + ROW_PAD - 1) // ROW_PAD)
-    out = torch.empty((1, rows_pad, p.kp), dtype=torch.int16, device=p.bf16.device)
-    onorm = torch.empty((1, rows_pad), dtype=F64, device=p.bf16.device)
-    call("simdex_build_prefix", ptr(p.bf16), ptr(p.norms), p.rows, p.kp, ptr(perm), 1, p.rows, rows_pad, ptr(out),
+    out = torch.empty((1, rows_pad, p.kp), dtype=torch.int16, device=p.op.device)
+    onorm = torch.empty((1, rows_pad), dtype=F64, device=p.op.device)
+    call("simdex_build_prefix", ptr(p.op), ptr(p.norms), p.rows, p.kp, ptr(perm), 1, p.rows, rows_pad, ptr(out),
          ptr(onorm), stream_ptr())
     return Packed(out.view(rows_pad, p.kp), onorm.view(rows_pad), p.scale_exp, p.kp, p.rows, perm, rows_pad)
 
 
 def pack(x: torch.Tensor, max_abs: float) -> Packed:
-    """bf16 copy scaled by 2^e so that the largest |entry| lies in [1, 2)."""
+    """fp16 copy scaled by 2^e so that the largest |entry| lies in [1, 2)."""
     rows, f = x.shape
     e = 0 if max_abs == 0.0 else -int(math.floor(math.log2(max_abs)))
     kp = 64 * ((f + 63) // 64)
     rows_pad = ROW_PAD * ((rows + ROW_PAD - 1) // ROW_PAD)
     out = torch.empty((rows_pad, kp), dtype=torch.int16, device=x.device)
     norms = torch.empty(rows, dtype=F64, device=x.device)
-    call("simdex_pack_bf16", ptr(_c(x, F64)), rows, f, e, rows_pad, kp, ptr(out), ptr(norms), stream_ptr())
+    call("simdex_pack_f16", ptr(_c(x, F64)), rows, f, e, rows_pad, kp, ptr(out), ptr(norms), stream_ptr())
     return Packed(out, norms, e, kp, rows)
 
 
@@ -91,8 +91,8 @@ def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32
     ids = torch.empty((nu, k_eff), dtype=I32, device=users.device)
     sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
-    call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu,
-         ptr(_c(items, F64)), ptr(items32), ptr(pi.bf16), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
+    call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(pu.op), ptr(pu.norms), nu,
+         ptr(_c(items, F64)), ptr(items32), ptr(pi.op), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
          pu.scale_exp,
          pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), stream_ptr())
     return ids, sc, hops
@@ -192,13 +192,13 @@ def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, w
 
 
 def build_prefix(pi: Packed, list_ids, block):
-    """Per-cluster prefix operands: (bf16 [c, b_pad, kp], float64 norms [c, b_pad], b_pad)."""
+    """Per-cluster prefix operands: (fp16 [c, b_pad, kp], float64 norms [c, b_pad], b_pad)."""
     c, ni = list_ids.shape
     bp = min(block, ni)
     b_pad = 128 * ((bp + 127) // 128)
     out = torch.empty((c, b_pad, pi.kp), dtype=torch.int16, device=list_ids.device)
     onorm = torch.empty((c, b_pad), dtype=F64, device=list_ids.device)
-    call("simdex_build_prefix", ptr(pi.bf16), ptr(pi.norms), ni, pi.kp, ptr(_c(list_ids, I32)), c, int(block),
+    call("simdex_build_prefix", ptr(pi.op), ptr(pi.norms), ni, pi.kp, ptr(_c(list_ids, I32)), c, int(block),
          b_pad, ptr(out), ptr(onorm), stream_ptr())
     return out, onorm, b_pad
 
@@ -228,8 +228,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
-    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.bf16), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(items32),
-         ptr(pi.bf16),
+    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(items32),
+         ptr(pi.op),
          ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),
          ptr(_c(list_pos, I32)),
          ptr(_c(bounds, F64)), c, int(block),
@@ -238,8 +238,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
 
 
 def gemm_debug(pu: Packed, pi: Packed, f):
-    out = torch.empty((pu.rows, pi.rows), dtype=torch.float32, device=pu.bf16.device)
-    call("simdex_gemm_debug", ptr(pu.bf16), pu.rows, ptr(pi.bf16), pi.rows, f, pu.kp, ptr(out), stream_ptr())
+    out = torch.empty((pu.rows, pi.rows), dtype=torch.float32, device=pu.op.device)
+    call("simdex_gemm_debug", ptr(pu.op), pu.rows, ptr(pi.op), pi.rows, f, pu.kp, ptr(out), stream_ptr())
     return out
 
 

@@ -6,18 +6,21 @@
 // segment, streamed in 128-item N tiles:
 //   warp 0      TMA producer: users tile once per unit, item tiles through a
 //               multi-stage ring (128-byte swizzled, mbarrier complete_tx);
-//   warp 1      MMA issuer: tcgen05.mma kind::f16 (bf16 x bf16 -> fp32) into
+//   warp 1      MMA issuer: tcgen05.mma kind::f16 (fp16 x fp16 -> fp32) into
 //               TMEM, 2 M tiles x 2 accumulator buffers x 128 columns = 512
 //               columns, so the next tile's MMAs overlap this tile's epilogue;
 //   warps 2..9  epilogue: one thread per user row, tcgen05.ld 32 columns at
 //               a time, a chunk-max filter against the row's certified
 //               threshold, and append of the rare surviving candidates.
 //
-// Certification (exactness from bf16): with operands rounded to bf16 (unit
-// roundoff 2^-8, exactly scaled by powers of two) and fp32 accumulation,
-// every approximate score v satisfies |v - s| <= e_j := eps*||u||*||i_j|| + e_abs
-// with eps = 2^-7 + 2^-16 + (kp+16)*2^-22 + 2^-20 (representation, product and
-// accumulation error, plus slack for the fp32 epilogue arithmetic).  Each row
+// Certification (exactness from fp16): with operands rounded to fp16 (unit
+// roundoff 2^-11; scaled by exact powers of two so max|x| is in [1, 2)) and
+// fp32 accumulation of the exact fp16 x fp16 products, every approximate
+// score v satisfies |v - s| <= e_j := eps*||u||*||i_j|| + e_abs with
+// eps = 2^-10 + 2^-22 + (kp+16)*2^-22 + 2^-20 (representation, accumulation,
+// slack for the fp32 epilogue arithmetic) and e_abs = kp*2^-22 covering
+// entries that land in fp16's subnormal range (absolute error <= 2^-25 each,
+// |scaled entry| < 2).  Each row
 // keeps candidates with hi = v + e_j >= T, where T is the k-th largest
 // lo = v - e_j seen so far (a valid lower bound on the exact k-th score);
 // items dropped or never kept have s <= hi < T <= s_k, so they cannot be in
@@ -54,7 +57,7 @@ using namespace sm100;
 constexpr int kUnitRows = 256;
 constexpr int kTileM = 128;
 constexpr int kTileN = 128;
-constexpr int kSlab = kTileM * 128;  // one [128 rows x 64 bf16] swizzled slab: 16 KB
+constexpr int kSlab = kTileM * 128;  // one [128 rows x 64 fp16] swizzled slab: 16 KB
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kMaxCap = 512;
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int kb = ks >> 2, kk = ks & 3;
               const uint64_t ad = umma_desc_sw128(smem_u32(a_sm + (h * KB + kb) * kSlab) + kk * 32);
               const uint64_t bd = umma_desc_sw128(smem_u32(b_sm + (stage * KB + kb) * kSlab) + kk * 32);
-              mma_bf16(d, ad, bd, kIdesc, ks > 0 ? 1u : 0u);
+              mma_f16(d, ad, bd, kIdesc, ks > 0 ? 1u : 0u);
             }
           }
           mma_commit(empty + stage);  // smem slot free once these MMAs retire

@@ -1,4 +1,4 @@
-// Operand packing for the tensor-core path: float64 factors -> bf16 (scaled
+// Operand packing for the tensor-core path: float64 factors -> fp16 (scaled
 // by an exact power of two, round-to-nearest-even, zero padded to [rows_pad,
 // kp]) + float64 row norms; and the work-sharing prefix gather (every
 // cluster's first B list items in list order, index.py:351-357).
@@ -9,7 +9,7 @@
 namespace simdex {
 namespace {
 
-__global__ void pack_bf16_kernel(const double* __restrict__ x, int64_t rows, int f, int scale_exp, int64_t rows_pad,
+__global__ void pack_f16_kernel(const double* __restrict__ x, int64_t rows, int f, int scale_exp, int64_t rows_pad,
                                  int kp, uint16_t* __restrict__ out, double* __restrict__ norms) {
   // one warp per row
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -62,10 +62,10 @@ int launch_max_abs(const double* x, int64_t n, double* out, cudaStream_t s) {
   return SIMDEX_OK;
 }
 
-int launch_pack_bf16(const double* x, int64_t rows, int32_t f, int32_t scale_exp, int64_t rows_pad, int32_t kp,
+int launch_pack_f16(const double* x, int64_t rows, int32_t f, int32_t scale_exp, int64_t rows_pad, int32_t kp,
                      uint16_t* out, double* norms, cudaStream_t s) {
-  pack_bf16_kernel<<<(unsigned)ceil_div(rows_pad, 8), 256, 0, s>>>(x, rows, f, scale_exp, rows_pad, kp, out, norms);
-  SIMDEX_LAUNCH_CHECK("pack_bf16");
+  pack_f16_kernel<<<(unsigned)ceil_div(rows_pad, 8), 256, 0, s>>>(x, rows, f, scale_exp, rows_pad, kp, out, norms);
+  SIMDEX_LAUNCH_CHECK("pack_f16");
   return SIMDEX_OK;
 }
 

@@ -34,8 +34,8 @@ def test_tcgen05_accumulators_match_float_reference(sx, nu, ni, f):
     m = _model(sx, rng.normal(size=(nu, f)), rng.normal(size=(ni, f)) * rng.lognormal(0, 1, (ni, 1)))
     pu, pi = _device.packed(m.users), _device.packed(m.items)
     got = _ops.gemm_debug(pu, pi, f)
-    a = _f16_to_f32(pu.bf16[:nu, :f])
-    b = _f16_to_f32(pi.bf16[:ni, :f])
+    a = _f16_to_f32(pu.op[:nu, :f])
+    b = _f16_to_f32(pi.op[:ni, :f])
     want = (a.double() @ b.double().T)
     scale = (a.double().abs() @ b.double().abs().T)
     err = (got.double() - want).abs()
