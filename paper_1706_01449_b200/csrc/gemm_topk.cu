@@ -88,9 +88,11 @@ struct TopkParams {
   float* cand_hi;    // [A rows, cap]
   int32_t* row_count;
   int32_t* row_flags;
+  float* row_T_out;  // [A rows] final certified threshold (finalize drops hi < T)
   int64_t* heap_ops;
   float* debug_out;
   int64_t debug_ld;
+  int skip_epi;  // timing experiments only: drain TMEM without filtering
 };
 
 // three-input max (sm_100 FMNMX3)
@@ -225,6 +227,33 @@ __device__ __noinline__ void compact_filter(float* hi, int32_t* id, int& cnt, fl
     }
   }
   cnt = w;
+}
+
+// k <= 64, warp-cooperative: drop lane `who`'s buffer entries whose upper
+// bound is below T, in place and order-preserving, 32 entries per step.
+// Called with the whole warp converged; returns the new count.
+__device__ __forceinline__ int warp_filter(float* hi, int32_t* id, int cnt, float T, int lane) {
+  int w = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    const int e = base + lane;
+    float h = -INFINITY;
+    int32_t i = 0;
+    if (e < cnt) {
+      h = hi[e];
+      i = id[e];
+    }
+    const bool keep = e < cnt && h >= T;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {  // destinations lie at or below this block: never a slot still to be read
+      const int dst = w + __popc(m & ((1u << lane) - 1u));
+      hi[dst] = h;
+      id[dst] = i;
+    }
+    w += __popc(m);
+    __syncwarp();
+  }
+  return w;
 }
 
 // sorted-descending top-KT insertion network: t <- top-KT of t + {x}
@@ -376,15 +405,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* my_lo = p.cand_lo + grow * p.cap;
       float* my_hi = p.cand_hi + grow * p.cap;
       const int n_tiles = (un.n_items + kTileN - 1) / kTileN;
+      // the tile's four 32-item norm maxima, loaded one tile ahead (off the critical path)
+      const float4* nm4p = reinterpret_cast<const float4*>(p.item_nmax32 + (un.b_row0 >> 5));
+      float4 nm4_next = __ldg(nm4p);
       for (int t = 0; t < n_tiles; ++t, ++acc) {
         const uint32_t buf = acc & 1, use = acc >> 1;
+        const float4 nm4 = nm4_next;
+        if (t + 1 < n_tiles) nm4_next = __ldg(nm4p + t + 1);
         mbar_wait(t_full + buf, use & 1);
         tc_fence_after();
         bool released = false;
         if (h < ntile_a) {
           const int tile_valid = min(kTileN, un.n_items - t * kTileN);
-          // the tile's four 32-item norm maxima in one load
-          const float4 nm4 = __ldg(reinterpret_cast<const float4*>(p.item_nmax32 + ((un.b_row0 + t * kTileN) >> 5)));
           // two chunks of 32 columns per TMEM wait; once the whole tile is in
           // registers the accumulator buffer goes back to the MMA warp
           constexpr int LDC = 2;
@@ -402,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == 0) mbar_arrive(t_empty + buf);
               released = true;
             }
+            if (p.skip_epi == 1) continue;
 #pragma unroll
             for (int c = 0; c < LDC; ++c) {
               const int ch = cg + c;
@@ -435,21 +468,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float m2 = fmax3(m[6], m[7], m[8]), m3 = fmaxf(m[9], m[10]);
                 const float mx = fmaxf(fmax3(m0, m1, m2), m3);
                 const float nmax = ch == 0 ? nm4.x : ch == 1 ? nm4.y : ch == 2 ? nm4.z : nm4.w;
-                if (fmaf(cu, nmax, mx) + p.e_abs >= T) {  // else nothing in this chunk can qualify
+                const float em = fmaf(cu, nmax, p.e_abs);  // the chunk's widest band
+                if (p.skip_epi != 2 && mx + em >= T) {  // else nothing in this chunk can qualify
                   if constexpr (KT == 1) {
-                    // k = 1: the chunk's largest lower bound is a valid T before any append
-                    float lm = -INFINITY;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) lm = fmaxf(lm, v[i] - fmaf(cu, __ldg(nrm + i), p.e_abs));
-                    top[0] = fmaxf(top[0], lm);
+                    // k = 1: the chunk max less the widest band lower-bounds its best item
+                    top[0] = fmaxf(top[0], mx - em);
                     T = fmaxf(T, top[0]);
                   }
+                  // coarse mask against the chunk-uniform band (a superset of the
+                  // per-item test, which the append loop applies): bit i set iff
+                  // v[i] - Tc >= 0, sign bits packed by funnel shifts
+                  const float Tc = (T - em) - fabsf(T) * 0x1p-22f - 0x1p-126f;
+                  unsigned neg = 0;
 #pragma unroll
-                  for (int i = 0; i < 32; ++i) {
-                    const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
-                    mask |= (v[i] + e >= T) ? (1u << i) : 0u;
-                  }
+                  for (int i = 31; i >= 0; --i) neg = __funnelshift_l(__float_as_uint(v[i] - Tc), neg, 1);
+                  mask = ~neg;
                   if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
+                  if (p.skip_epi == 3) mask = 0;
                   if (mask) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) vloc[i] = v[i];
@@ -472,12 +507,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (KT > 0) {
                       push_top<KTT>(top, vi - e);
                       T = fmaxf(T, KTT == kk + 1 ? top[KTT - 1] : top_at<KTT>(top, kk));
-                      if (cnt == p.cap) {
-                        compact_filter(my_hi, my_id, cnt, T);
-                        if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
-                      }
                     } else {
                       my_lo[cnt - 1] = vi - e;  // the buffer always has >= 32 free slots here
+                    }
+                  }
+                }
+                if constexpr (KT > 0) {
+                  // a full buffer is filtered against the current T by the whole warp
+                  unsigned full = __ballot_sync(0xffffffffu, cnt == p.cap);
+                  while (full) {
+                    const int who = __ffs(full) - 1;
+                    full &= full - 1;
+                    const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+                    const float t_w = __shfl_sync(0xffffffffu, T, who);
+                    const int nc = warp_filter(p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, p.cap, t_w, lane);
+                    if (lane == who) {
+                      cnt = nc;
+                      if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
                     }
                   }
                 }
@@ -533,11 +579,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (live && h < ntile_a && !kDebug) {
-        if constexpr (KT > 0) {
-          if (!flags && cnt > p.k_eff) compact_filter(my_hi, my_id, cnt, T);
-        }
+        // the buffer may still hold entries admitted before T reached its final
+        // value; finalize drops those against row_T_out in parallel
         p.row_count[grow] = cnt;
         p.row_flags[grow] = flags;
+        p.row_T_out[grow] = T;
         if (p.heap_ops) p.heap_ops[grow] = hops;
       }
     }
@@ -634,6 +680,8 @@ struct FinalizeParams {
   int k_eff;
   int cap;
   const int32_t* cand_id;
+  const float* cand_hi;   // upper bounds of the candidates (scaled domain)
+  const float* row_T;     // final certified threshold per row (scaled domain)
   const int32_t* row_count;
   const int32_t* row_flags;
   int32_t* out_ids;
@@ -723,20 +771,37 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   if (act)
     for (int i = gl; i < p.f; i += LPR) us[i] = p.users32 ? (double)p.users32[user * p.f + i] : p.users[user * p.f + i];
   const int32_t* cid = p.cand_id + r * p.cap;
-  for (int e = gl; e < np2; e += LPR) {
-    if (act && e < cnt) {
+  const float* chi = p.cand_hi + r * p.cap;
+  // keep the candidates whose upper bound reaches the row's final threshold
+  // (compacted to the front in buffer order), resolve them to item ids
+  const float Tr = act ? p.row_T[r] : 0.f;
+  int kept = 0;
+  for (int e0 = 0; e0 < cmax; e0 += LPR) {
+    const int e = e0 + gl;
+    const bool keep = act && e < cnt && chi[e] >= Tr;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const unsigned mine = (bal & gmask) >> (grp * LPR);
+    if (keep) {
+      const int dst = kept + __popc(mine & ((1u << gl) - 1u));
       const int32_t pos = cid[e];
-      si[e] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
-    } else {
-      ss[e] = -DBL_MAX;
-      si[e] = INT32_MAX;
+      si[dst] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
     }
+    kept += __popc(mine);
+  }
+  cnt = kept;
+  const int cmax2 = __reduce_max_sync(0xffffffffu, cnt);
+  np2 = 2;
+  while (np2 < cmax2) np2 <<= 1;
+  __syncwarp();
+  for (int e = cnt + gl; e < np2; e += LPR) {
+    ss[e] = -DBL_MAX;
+    si[e] = INT32_MAX;
   }
   __syncwarp();
   // LPR/8 candidates per round, 8 lanes each (strided partials + xor tree)
   constexpr int SG = LPR / 8;
   const int sg = gl >> 3, sl = gl & 7;
-  for (int base = 0; base < cmax; base += SG) {
+  for (int base = 0; base < cmax2; base += SG) {
     const int e = base + sg;
     double part = 0.0;
     if (act && e < cnt) {
@@ -961,6 +1026,39 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
   }
 }
 
+// stage 1: an initial certified threshold per row from the exact scores of
+// its cluster's first k list items (all inside the prefix, k <= B'): their
+// minimum lower-bounds the k-th best prefix score, so the row starts filtering
+// at once instead of admitting the first chunks wholesale.  One warp per row.
+template <class Q>
+__global__ void prefix_t0_kernel(const int64_t* __restrict__ row_user, const int32_t* __restrict__ row_cluster,
+                                 int64_t rows, const double* __restrict__ users, const Q* __restrict__ items,
+                                 const int32_t* __restrict__ list_ids, int64_t n, int f, int k, double scale,
+                                 float* __restrict__ t0) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int64_t user = row_user[r];
+  if (user < 0) {
+    if (lane == 0) t0[r] = -INFINITY;
+    return;
+  }
+  const int32_t* ids = list_ids + (int64_t)row_cluster[r] * n;
+  const double* u = users + user * f;
+  double mn = DBL_MAX;
+  for (int j = 0; j < k; ++j) {
+    const Q* x = items + (int64_t)ids[j] * f;
+    double s = 0.0;
+    for (int q = lane; q < f; q += 32) s = fma(u[q], (double)x[q], s);
+    s = warp_sum(s);
+    mn = fmin(mn, s);
+  }
+  if (lane == 0) {
+    const double v = mn * scale;
+    t0[r] = __double2float_rd(v - fabs(v) * 0x1p-40);
+  }
+}
+
 // stage 2: pack the continuing rows densely (rows past the count are zero)
 __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
                                  int64_t rows_max, const int64_t* __restrict__ row_user,
@@ -1137,7 +1235,7 @@ int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
 // Candidate buffers + per-row state for up to `rows` packed rows.
 struct RowState {
   Scratch<int32_t> cid, cnt, flags;
-  Scratch<float> lo, hi;
+  Scratch<float> lo, hi, rowT;
   int cap;
   int alloc(int64_t rows, int k_eff, cudaStream_t s) {
     cap = cap_for(k_eff);
@@ -1146,6 +1244,7 @@ struct RowState {
     SIMDEX_CUDA(lo.alloc(kt_for(k_eff) > 0 ? 1 : (size_t)rows * cap, s));
     SIMDEX_CUDA(cnt.alloc(rows, s));
     SIMDEX_CUDA(flags.alloc(rows, s));
+    SIMDEX_CUDA(rowT.alloc(rows, s));
     return SIMDEX_OK;
   }
 };
@@ -1164,11 +1263,13 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   p.stages = g.stages;
   p.cap = st.cap;
   p.k_eff = k_eff;
+  p.skip_epi = std::getenv("SIMDEX_SKIP_EPI") ? std::atoi(std::getenv("SIMDEX_SKIP_EPI")) : 0;
   p.cand_id = st.cid.p;
   p.cand_lo = st.lo.p;
   p.cand_hi = st.hi.p;
   p.row_count = st.cnt.p;
   p.row_flags = st.flags.p;
+  p.row_T_out = st.rowT.p;
   return p;
 }
 
@@ -1253,6 +1354,8 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   fp.k_eff = k_eff;
   fp.cap = st.cap;
   fp.cand_id = st.cid.p;
+  fp.cand_hi = st.hi.p;
+  fp.row_T = st.rowT.p;
   fp.row_count = st.cnt.p;
   fp.row_flags = st.flags.p;
   fp.out_ids = out_ids;
@@ -1334,6 +1437,19 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
   if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
   TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
+  Scratch<float> t0s;
+  if (k_eff <= bp) {
+    SIMDEX_CUDA(t0s.alloc(rows_max, s));
+    const double scale = std::ldexp(1.0, su + si);
+    if (items32)
+      prefix_t0_kernel<float><<<(unsigned)ceil_div(rows_max, 8), 256, 0, s>>>(
+          row_user.p, rclus.p, rows_max, users, items32, list_ids, ni, f, k_eff, scale, t0s.p);
+    else
+      prefix_t0_kernel<double><<<(unsigned)ceil_div(rows_max, 8), 256, 0, s>>>(
+          row_user.p, rclus.p, rows_max, users, items, list_ids, ni, f, k_eff, scale, t0s.p);
+    SIMDEX_LAUNCH_CHECK("prefix_t0");
+    p.row_T0 = t0s.p;
+  }
   const bool stats = getenv("SIMDEX_STATS") != nullptr;
   Scratch<int64_t> hops;
   if (stats) {
@@ -1373,6 +1489,8 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   fp.k_eff = k_eff;
   fp.cap = st.cap;
   fp.cand_id = st.cid.p;
+  fp.cand_hi = st.hi.p;
+  fp.row_T = st.rowT.p;
   fp.row_count = st.cnt.p;
   fp.row_flags = st.flags.p;
   fp.out_ids = out_ids;
@@ -1573,6 +1691,8 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   fp.k_eff = k_eff;
   fp.cap = st.cap;
   fp.cand_id = st.cid.p;
+  fp.cand_hi = st.hi.p;
+  fp.row_T = st.rowT.p;
   fp.row_count = st.cnt.p;
   fp.row_flags = st.flags.p;
   fp.over_list = over_rows;
