@@ -93,3 +93,14 @@ def to_host_pinned(t: torch.Tensor) -> np.ndarray:
     h.copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return h.numpy()
+
+
+def to_host_pinned_many(*ts: torch.Tensor):
+    """Several device -> pinned host copies behind one stream synchronisation."""
+    outs = []
+    for t in ts:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return tuple(h.numpy() for h in outs)

@@ -46,7 +46,8 @@ def default_blocks(factors: int) -> BlockSpec:
 
 def _results(ids, sc, n_items, num_users):
     vis = np.full(num_users, n_items, dtype=np.int64)
-    return TopKResults(np.arange(num_users), _device.to_host_pinned(ids), _device.to_host_pinned(sc), vis)
+    ids_h, sc_h = _device.to_host_pinned_many(ids, sc)
+    return TopKResults(np.arange(num_users), ids_h, sc_h, vis)
 
 
 def topk_naive_tensors(model: ModelPair, k: int):

@@ -191,12 +191,10 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
     if fixed:
         counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
     theta = _ops.max_angles(pts, centers, assign)
-    assign_h = _device.to_host(assign).astype(np.int64)
-    mem_h = _device.to_host(members)
-    off_h = _device.to_host(offsets)
+    assign_h, mem_h, off_h, cen_h, theta_h = (a.copy() for a in _device.to_host_pinned_many(
+        assign, members, offsets, centers, theta))
+    assign_h = assign_h.astype(np.int64, copy=False)
     members_t = tuple(mem_h[off_h[c]:off_h[c + 1]].copy() for c in range(num_clusters))
-    cen_h = _device.to_host(centers).copy()
-    theta_h = _device.to_host(theta).copy()
     objective = np.asarray(history)
     for a in (assign_h, theta_h, objective):
         a.setflags(write=False)

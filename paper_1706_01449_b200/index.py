@@ -312,16 +312,20 @@ def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 
     hit = None
     if precomputed:
         keys = np.fromiter(precomputed.keys(), dtype=np.int64, count=len(precomputed))
-        hit = np.isin(uids, keys)
-        reused = {int(i): precomputed[int(uids[i])] for i in np.flatnonzero(hit)}
+        keys = keys[(keys >= 0) & (keys < model.num_users)]
+        mark = np.zeros(model.num_users, dtype=bool)  # O(U) membership instead of a sort-based isin
+        mark[keys] = True
+        hit = mark if all_users else mark[uids]
+        pos = np.sort(keys) if all_users else np.flatnonzero(hit)
+        reused = {int(i): precomputed[int(uids[i])] for i in pos}
     k_eff = min(k, model.num_items)
     if len(reused) * 2 <= uids.shape[0]:
         # few reused entries: serve every position on the device (the reused
         # positions still return the precomputed objects), no host gather
         q = None if all_users else _device.to_device(uids)
         ids, sc, vis = query_batch_tensors(index, model, q, k, work_sharing)
-        return TopKResults(uids, _device.to_host_pinned(ids), _device.to_host_pinned(sc),
-                           _device.to_host_pinned(vis), reused)
+        ids_h, sc_h, vis_h = _device.to_host_pinned_many(ids, sc, vis)
+        return TopKResults(uids, ids_h, sc_h, vis_h, reused)
     todo = np.flatnonzero(~hit)
     ids_h = np.zeros((uids.shape[0], k_eff), dtype=np.int32)
     sc_h = np.zeros((uids.shape[0], k_eff), dtype=np.float64)
