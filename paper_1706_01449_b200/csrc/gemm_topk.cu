@@ -635,22 +635,30 @@ __global__ void max_abs_any_kernel(const P* __restrict__ x, int64_t n, double mu
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// eight threads per row, each writing 16-byte pieces (8 halves) of the row
 template <class P>
 __global__ void pack_aug_kernel(const P* __restrict__ x, const double* __restrict__ sq, int64_t rows, int f,
                                 int centers, int scale_exp, int64_t rows_pad, int kp, uint16_t* __restrict__ out,
                                 double* __restrict__ gnorm) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = g >> 3;
+  const int sub = (int)(g & 7);
   if (r >= rows_pad) return;
   const bool live = r < rows;
   const double q = live ? sq[r] : 0.0;
   const double aug = live ? (centers ? -0.5 * q : 1.0) : 0.0;
-  for (int k = lane; k < kp; k += 32) {
-    const double v = live ? (k < f ? (double)x[r * f + k] : (k == f ? aug : 0.0)) : 0.0;
-    __half b = __double2half(ldexp(v, scale_exp));
-    out[r * kp + k] = *reinterpret_cast<uint16_t*>(&b);
+  const double sc = ldexp(1.0, scale_exp);
+  for (int k0 = sub * 8; k0 < kp; k0 += 64) {
+    __align__(16) __half hv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = k0 + i;
+      const double v = live ? (k < f ? (double)x[r * f + k] : (k == f ? aug : 0.0)) : 0.0;
+      hv[i] = __double2half(v * sc);
+    }
+    *reinterpret_cast<uint4*>(out + r * kp + k0) = *reinterpret_cast<const uint4*>(hv);
   }
-  if (lane == 0) gnorm[r] = live ? sqrt(q + aug * aug) * (1.0 + 0x1p-40) + 0x1p-16 * (1.0 + q) : 0.0;
+  if (sub == 0) gnorm[r] = live ? sqrt(q + aug * aug) * (1.0 + 0x1p-40) + 0x1p-16 * (1.0 + q) : 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1659,9 +1667,10 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   SIMDEX_CUDA(inrm.alloc(nc_pad, s));
   SIMDEX_CUDA(inmax.alloc(nc_pad / 32, s));
   ProfileScope _prof("assign_pack", s);
-  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad, 8), 256, 0, s>>>(px, p2, n, f, 0, su, nu_pad, kp, ua.p, un.p);
-  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad, 8), 256, 0, s>>>(centers, c2, c, f, 1, sc, nc_pad, kp, ca.p,
-                                                                         cn.p);
+  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, su, nu_pad, kp, ua.p,
+                                                                          un.p);
+  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad * 8, 256), 256, 0, s>>>(centers, c2, c, f, 1, sc, nc_pad, kp,
+                                                                               ca.p, cn.p);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("pack_aug");
   units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units.p, n_units.p, nunits);

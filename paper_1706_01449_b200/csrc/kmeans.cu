@@ -11,9 +11,12 @@
 // Every kernel reads the points either as float64 or, when the caller passes
 // an exact float32 copy (all BASELINE inputs are float32 upcast), as float32
 // converted back to float64 exactly: same arithmetic, half the bytes.
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -168,15 +171,19 @@ __global__ void members_kernel(const int32_t* ids, int64_t n, int64_t* members) 
 constexpr int kMeanWarps = 8;
 constexpr int kMeanRegs = 4;  // factors per lane per chunk (128-factor chunks)
 
+// Cluster c's members are split into S contiguous parts (one CTA each,
+// blockIdx.x = c * S + s); part sums go to psum[c][s][f] and are combined in
+// part order by combine_mean_kernel.
 template <class P>
 __global__ void __launch_bounds__(kMeanWarps * 32) centroid_mean_kernel(const P* __restrict__ points, int f,
                                                                         const int64_t* __restrict__ members,
-                                                                        const int64_t* __restrict__ offsets,
-                                                                        double* __restrict__ centers) {
+                                                                        const int64_t* __restrict__ offsets, int S,
+                                                                        double* __restrict__ psum) {
   __shared__ double part[kMeanWarps][kMeanRegs * 32];
-  const int c = blockIdx.x;
-  const int64_t b = offsets[c], e = offsets[c + 1];
-  if (e == b) return;
+  const int c = blockIdx.x / S, sp = blockIdx.x % S;
+  const int64_t cb = offsets[c], ce = offsets[c + 1];
+  const int64_t b = cb + (ce - cb) * sp / S, e = cb + (ce - cb) * (sp + 1) / S;
+  double* out = psum + ((int64_t)c * S + sp) * f;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int k0 = 0; k0 < f; k0 += kMeanRegs * 32) {
     double acc[kMeanRegs];
@@ -212,9 +219,123 @@ __global__ void __launch_bounds__(kMeanWarps * 32) centroid_mean_kernel(const P*
       double tot = 0.0;
 #pragma unroll
       for (int ww = 0; ww < kMeanWarps; ++ww) tot += part[ww][k];
-      centers[(int64_t)c * f + k0 + k] = tot / (double)(e - b);
+      out[k0 + k] = tot;
     }
     __syncthreads();
+  }
+}
+
+// centroid = (sum of the S part sums, in part order) / count; empty clusters
+// keep their centroid (clustering.py:170-172)
+__global__ void combine_mean_kernel(const double* __restrict__ psum, const int64_t* __restrict__ offsets, int c,
+                                    int S, int f, double* __restrict__ centers) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)c * f) return;
+  const int cl = (int)(i / f), k = (int)(i % f);
+  const int64_t cnt = offsets[cl + 1] - offsets[cl];
+  if (cnt == 0) return;
+  double t = 0.0;
+  for (int sp = 0; sp < S; ++sp) t += psum[((int64_t)cl * S + sp) * f + k];
+  centers[i] = t / (double)cnt;
+}
+
+// Stable counting sort of points by cluster (members in (cluster, id)
+// order): per-block cluster histograms, cluster totals + offsets, per
+// (cluster, block) bases, then an in-order scatter per block.
+constexpr int kGroupBlock = 1024;  // points per histogram / scatter block
+
+__global__ void group_hist_kernel(const int64_t* __restrict__ assign, int64_t n, int c, int64_t nb,
+                                  int32_t* __restrict__ bcount) {
+  extern __shared__ int32_t h[];
+  for (int i = threadIdx.x; i < c; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t b0 = (int64_t)blockIdx.x * kGroupBlock;
+  for (int64_t i = b0 + threadIdx.x; i < n && i < b0 + kGroupBlock; i += blockDim.x) atomicAdd(h + assign[i], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < c; i += blockDim.x) bcount[(int64_t)i * nb + blockIdx.x] = h[i];
+}
+
+// one warp per cluster: exclusive scan of its block counts in block order
+__global__ void group_cluster_scan_kernel(int32_t* __restrict__ bcount, int64_t nb, int c,
+                                          int64_t* __restrict__ totals) {
+  const int cl = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (cl >= c) return;
+  int32_t* row = bcount + (int64_t)cl * nb;
+  int64_t carry = 0;
+  for (int64_t b0 = 0; b0 < nb; b0 += 32) {
+    const int64_t b = b0 + lane;
+    const int64_t v = b < nb ? row[b] : 0;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (b < nb) row[b] = (int32_t)(carry + x - v);
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) totals[cl] = carry;
+}
+
+__global__ void group_offsets_kernel(const int64_t* __restrict__ totals, int c, int64_t* __restrict__ out_counts,
+                                     int64_t* __restrict__ offsets) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) carry = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < c; c0 += blockDim.x) {
+    const int i = c0 + t;
+    const int64_t v = i < c ? totals[i] : 0;
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int64_t pre = carry;
+    for (int q = 0; q < w; ++q) pre += wsum[q];
+    if (i < c) {
+      offsets[i] = pre + x - v;
+      out_counts[i] = v;
+    }
+    __syncthreads();
+    if (t == 0)
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) carry += wsum[q];
+    __syncthreads();
+  }
+  if (t == 0) offsets[c] = carry;
+}
+
+// one warp per block of points, in point order: ranks among equal clusters
+// by match_any, a running per-cluster cursor in shared memory
+__global__ void group_scatter_kernel(const int64_t* __restrict__ assign, int64_t n, int c, int64_t nb,
+                                     const int32_t* __restrict__ bbase, const int64_t* __restrict__ offsets,
+                                     int64_t* __restrict__ members) {
+  extern __shared__ int32_t cur[];
+  const int lane = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  for (int i = lane; i < c; i += 32) cur[i] = 0;
+  __syncwarp();
+  const int64_t b0 = b * kGroupBlock;
+  for (int64_t i0 = b0; i0 < n && i0 < b0 + kGroupBlock; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool live = i < n && i < b0 + kGroupBlock;
+    const int cl = live ? (int)assign[i] : -1;
+    const unsigned live_m = __ballot_sync(0xffffffffu, live);
+    const unsigned peers = __match_any_sync(0xffffffffu, cl) & live_m;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (live && lane == leader) base = cur[cl];
+    base = __shfl_sync(0xffffffffu, base, live ? leader : lane);
+    if (live) {
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      members[offsets[cl] + bbase[(int64_t)cl * nb + b] + base + rank] = i;
+    }
+    __syncwarp();
+    if (live && lane == leader) cur[cl] = base + __popc(peers);
+    __syncwarp();
   }
 }
 
@@ -520,6 +641,8 @@ struct SeedArgs {
   int32_t* degenerate;
   unsigned* barrier;
   unsigned long long* dbg;  // optional phase timers (ns): update, barrier 1, pick, barrier 2
+  const __half* p16;        // compact fp16 copy of the points x 2^s16, rows padded to 32 (null: off)
+  const int* s16;           // its scale exponent (device scalar)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -574,7 +697,7 @@ __device__ __forceinline__ double cta_scan(double x, double* wsum, double* total
 // seed-seed distances and seed norms, per-warp double-buffered row staging
 struct PSeedSmem {
   int kc;  // cached seeds (0: read cd2 / seed_c2 from global)
-  size_t buf, cen_off, cdc_off, scc_off, bar_off, buf_off, total;
+  size_t buf, cen_off, cen32_off, cdc_off, scc_off, bar_off, buf_off, total;
 };
 
 __host__ __device__ inline PSeedSmem pseed_smem(int f, size_t esize, int k, int wpb) {
@@ -583,7 +706,8 @@ __host__ __device__ inline PSeedSmem pseed_smem(int f, size_t esize, int k, int 
   m.buf = ((32 * row + 32) + 127) & ~size_t(127);
   m.kc = k <= 2048 ? k : 0;
   m.cen_off = 0;
-  m.cdc_off = ((size_t)f * 8 + 15) & ~size_t(15);
+  m.cen32_off = ((size_t)f * 8 + 15) & ~size_t(15);
+  m.cdc_off = m.cen32_off + (((size_t)f * 4 + 15) & ~size_t(15));
   m.scc_off = m.cdc_off + (size_t)m.kc * 8;
   m.bar_off = (m.scc_off + (size_t)m.kc * 8 + 15) & ~size_t(15);
   m.buf_off = (m.bar_off + (size_t)wpb * 2 * 8 + 127) & ~size_t(127);
@@ -673,9 +797,11 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
   const int CS = blockDim.x, wpb = CS >> 5;  // chunk = one point per thread
   const PSeedSmem L = pseed_smem(f, sizeof(P), a.k, wpb);
   double* cen = reinterpret_cast<double*>(sm_raw + L.cen_off);
+  float* cen32 = reinterpret_cast<float*>(sm_raw + L.cen32_off);
   double* cdc = reinterpret_cast<double*>(sm_raw + L.cdc_off);
   double* scc = reinterpret_cast<double*>(sm_raw + L.scc_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + L.bar_off);
+  __shared__ double s_cl1;  // L1 norm of the pass's center (fp16 prefilter bound)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (lane == 0) {
     sm100::mbar_init(bars + 2 * w, 1);
@@ -688,8 +814,24 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
   const int64_t G = gridDim.x;
   uint32_t phbits = 0;  // mbarrier phase per staging buffer
   unsigned gen = 0;
+  const bool pre16 = a.p16 != nullptr;
+  const size_t row16 = (size_t)f * 2;
+  const double inv16 = pre16 ? ldexp(1.0, -*a.s16) : 0.0;
+  // prefilter bound: |p.c - fp16 dot| <= (p2 + c2) e16 + 2^-24 2^-s16 |c|_1
+  const double e16 = 0x1p-11 + (double)(f + 4) * 0x1p-24;
+  auto load_center = [&]() {  // cen (from global rows written this pass) -> fp32 copy + L1 norm
+    for (int q = t; q < f; q += CS) cen32[q] = (float)cen[q];
+    __syncthreads();
+    if (t == 0) {
+      double l1 = 0.0;
+      for (int q = 0; q < f; ++q) l1 += fabs(cen[q]);
+      s_cl1 = l1;
+    }
+    __syncthreads();
+  };
   for (int q = t; q < f; q += CS) cen[q] = __ldcg(a.centers + q);
   __syncthreads();
+  load_center();
   unsigned long long tm0 = 0, tm1 = 0;
   const bool timing = a.dbg && blockIdx.x == 0 && t == 0;
   for (int j = 0; j + 1 < a.k; ++j) {
@@ -733,18 +875,29 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     // stage the warp's 32 rows with one bulk copy when any of them is needed
     // (per-row copies of only the needed rows measured slower: TMA issue
     // rate); returns false when the rows are read from global instead
+    // passes after the first stage the fp16 rows (half the bytes; rows padded
+    // to 32 so a slice is always whole and 16-byte aligned)
+    const bool use16 = pre16 && j > 0;
     auto issue = [&](int64_t ch, unsigned mask, int bsel) -> bool {
       if (!mask) return false;
       const int64_t u0 = ch * CS + w * 32;
-      const int64_t u1 = (u0 + 32) < n ? (u0 + 32) : n;
-      const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
-      const size_t sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
-      if (a0 + sz > total_bytes) return false;  // buffer tail: read from global
+      const unsigned char* src;
+      size_t sz;
+      if (use16) {
+        src = reinterpret_cast<const unsigned char*>(a.p16) + (size_t)u0 * row16;
+        sz = 32 * row16;
+      } else {
+        const int64_t u1 = (u0 + 32) < n ? (u0 + 32) : n;
+        const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
+        sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
+        if (a0 + sz > total_bytes) return false;  // buffer tail: read from global
+        src = gbase + a0;
+      }
       __syncwarp();
       if (lane == 0) {
         sm100::fence_proxy_async_smem();
         sm100::mbar_arrive_expect_tx(bars + 2 * w + bsel, (uint32_t)sz);
-        sm100::bulk_load_1d(sm_raw + L.buf_off + (size_t)(2 * w + bsel) * L.buf, gbase + a0, (uint32_t)sz,
+        sm100::bulk_load_1d(sm_raw + L.buf_off + (size_t)(2 * w + bsel) * L.buf, src, (uint32_t)sz,
                             bars + 2 * w + bsel);
       }
       return true;
@@ -776,7 +929,76 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
           sm100::mbar_wait(bars + 2 * w + bA, (phbits >> bA) & 1u);
           phbits ^= 1u << bA;
         }
-        if (needA) {
+        bool exact = needA;
+        if (needA && use16) {
+          // certified fp16 prefilter: skip when even the smallest distance the
+          // fp16 dot allows cannot go below d2 (the float64 result would keep d2)
+          const __half* x16 = reinterpret_cast<const __half*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf +
+                                                              (size_t)lane * row16);
+          float acc = 0.f;
+#pragma unroll 5
+          for (int q = 0; q < f; ++q) acc = fmaf(__half2float(x16[q]), cen32[q], acc);
+          const double ps = mp2A + cc;
+          const double eb = ps * e16 + 0x1p-24 * inv16 * s_cl1 * 1.01;
+          const double dlo = ps - 2.0 * ((double)acc * inv16 + eb) - 0x1p-40 * ps;
+          exact = !(dlo >= oldA);
+        }
+        if (a.dbg) {
+          const unsigned nn = __popc(__ballot_sync(0xffffffffu, needA)), ne = __popc(__ballot_sync(0xffffffffu, exact));
+          if (lane == 0) {
+            atomicAdd(a.dbg + 4, (unsigned long long)nn);
+            atomicAdd(a.dbg + 5, (unsigned long long)ne);
+          }
+        }
+        if (use16) {
+          // the few points the prefilter could not settle: float64 distance from
+          // the global rows, four points at a time, eight lanes per point on
+          // strided factors (coalesced segments, every load of a round in flight)
+          unsigned em = __ballot_sync(0xffffffffu, exact);
+          const int sl = lane & 7, grp = lane >> 3;
+          while (em) {
+            int mine = -1;
+            for (int g = 0; g < 4 && em; ++g) {
+              const int b = __ffs(em) - 1;
+              em &= em - 1;
+              if (g == grp) mine = b;
+            }
+            double dot = 0.0;
+            if (mine >= 0) {
+              const P* x = points + (chA * CS + w * 32 + mine) * f;
+              for (int k0 = 0; k0 < f; k0 += 64) {
+                P xv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int k = k0 + sl + 8 * i;
+                  xv[i] = k < f ? x[k] : P(0);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int k = k0 + sl + 8 * i;
+                  if (k < f) dot = fma((double)xv[i], cen[k], dot);
+                }
+              }
+            }
+            dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+            // hand each group's dot to the owner lane of its point
+            for (int g = 0; g < 4; ++g) {
+              const int who = __shfl_sync(0xffffffffu, mine, g * 8);
+              const double dg = __shfl_sync(0xffffffffu, dot, g * 8);
+              if (who == lane) {
+                double d = (mp2A + cc) - 2.0 * dg;
+                d = d > 0.0 ? d : 0.0;
+                if (d < oldA) {
+                  a.d2[meA] = d;
+                  a.near[meA] = j;
+                  fin = d;
+                }
+              }
+            }
+          }
+        } else if (exact) {
           const size_t s0 = (size_t)(chA * CS + w * 32) * row_bytes;  // slice start
           const P* x = sA ? reinterpret_cast<const P*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + (s0 & 15) +
                                                        (size_t)lane * row_bytes)
@@ -879,6 +1101,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       a.seed_c2[j + 1] = a.p2[p];
     }
     __syncthreads();
+    load_center();
     // squared distances new seed -> seeds 0..j, one warp per seed across the grid
     for (int64_t q = (int64_t)blockIdx.x * wpb + w; q <= j; q += G * wpb) {
       const double* cq = a.centers + q * f;
@@ -898,6 +1121,29 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     grid_barrier(a.barrier, gen);
     if (timing) a.dbg[3] += gtimer() - tm0;
   }
+}
+
+// compact fp16 copy of the points scaled by 2^s (max |x| 2^s in [1, 2)),
+// rows padded with zeros to a multiple of 32; s from the device max
+template <class P>
+__global__ void pack16_compact_kernel(const P* __restrict__ x, int64_t n, int f, int64_t n_pad,
+                                      const unsigned long long* __restrict__ maxbits, __half* __restrict__ out,
+                                      int* __restrict__ s_out) {
+  const double m = __longlong_as_double((long long)*maxbits);
+  const int sc = m > 0.0 ? -ilogb(m) : 0;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *s_out = sc;
+  if (i >= n_pad * f) return;
+  out[i] = __double2half(i < n * f ? ldexp((double)x[i], sc) : 0.0);
+}
+
+template <class P>
+__global__ void max_abs_pts_kernel(const P* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs((double)x[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
 template <class P>
@@ -1036,13 +1282,31 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
       a.chunk_sums = csum.p;
       a.range_sums = rsum.p;
       a.nchunks = nch;
+      // fp16 prefilter copy (experimental switch SIMDEX_SEED_F16)
+      Scratch<__half> p16;
+      Scratch<unsigned long long> mxb;
+      Scratch<int> s16;
+      if (std::getenv("SIMDEX_SEED_F16")) {  // experimental: measured slower than the fp32 slices
+        const int64_t n_pad = ceil_div(n, 32) * 32;
+        SIMDEX_CUDA(p16.alloc((size_t)n_pad * f, s));
+        SIMDEX_CUDA(mxb.alloc(1, s));
+        SIMDEX_CUDA(s16.alloc(1, s));
+        SIMDEX_CUDA(cudaMemsetAsync(mxb.p, 0, sizeof(unsigned long long), s));
+        max_abs_pts_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(n * f, 256), 4 * 148), 256, 0, s>>>(
+            points, n * f, mxb.p);
+        pack16_compact_kernel<P><<<(unsigned)ceil_div(n_pad * f, 256), 256, 0, s>>>(points, n, f, n_pad, mxb.p,
+                                                                                     p16.p, s16.p);
+        SIMDEX_LAUNCH_CHECK("pack16_compact");
+        a.p16 = p16.p;
+        a.s16 = s16.p;
+      }
       a.degenerate = out_deg;
       a.barrier = bar.p;
       Scratch<unsigned long long> dbg;
       const bool timing = std::getenv("SIMDEX_SEED_TIMING") != nullptr;
       if (timing) {
-        SIMDEX_CUDA(dbg.alloc(4, s));
-        SIMDEX_CUDA(cudaMemsetAsync(dbg.p, 0, 4 * sizeof(unsigned long long), s));
+        SIMDEX_CUDA(dbg.alloc(6, s));
+        SIMDEX_CUDA(cudaMemsetAsync(dbg.p, 0, 6 * sizeof(unsigned long long), s));
         a.dbg = dbg.p;
       }
       const P* pts = points;
@@ -1053,11 +1317,14 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
       _prof.end();
       count_launches(1);
       if (timing) {
-        unsigned long long h[4];
+        unsigned long long h[6];
         SIMDEX_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, s));
         SIMDEX_CUDA(cudaStreamSynchronize(s));
-        fprintf(stderr, "[simdex] seed grid %lld x %lld: update %.3f ms barrier %.3f ms pick %.3f ms barrier %.3f ms\n",
-                (long long)grid, (long long)cs, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6);
+        fprintf(stderr,
+                "[simdex] seed grid %lld x %lld: update %.3f ms barrier %.3f ms pick %.3f ms barrier %.3f ms; "
+                "per pass: triangle-unskipped %.0f exact %.0f of %lld\n",
+                (long long)grid, (long long)cs, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6,
+                (double)h[4] / (k - 1), (double)h[5] / (k - 1), (long long)n);
       }
       return SIMDEX_OK;
     }
@@ -1082,8 +1349,12 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
 template <class P>
 int mean_impl(const P* points, int32_t f, const int64_t* members, const int64_t* offsets, int32_t c,
               double* centers, cudaStream_t s) {
+  const int S = std::max(1, std::min(16, (4 * sm_count() + c - 1) / c));  // CTAs per cluster
+  Scratch<double> psum;
+  SIMDEX_CUDA(psum.alloc((size_t)c * S * f, s));
   ProfileScope _prof("centroid_mean", s);
-  centroid_mean_kernel<P><<<(unsigned)c, kMeanWarps * 32, 0, s>>>(points, f, members, offsets, centers);
+  centroid_mean_kernel<P><<<(unsigned)(c * S), kMeanWarps * 32, 0, s>>>(points, f, members, offsets, S, psum.p);
+  combine_mean_kernel<<<(unsigned)ceil_div((int64_t)c * f, 256), 256, 0, s>>>(psum.p, offsets, c, S, f, centers);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("centroid_mean");
   return SIMDEX_OK;
@@ -1126,20 +1397,38 @@ extern "C" int simdex_kmeans_update(const double* points, const float* points32,
                    "simdex_kmeans_update: null pointer");
   SIMDEX_CHECK_ARG(n >= 1 && f >= 1 && c >= 1 && n < INT32_MAX, "simdex_kmeans_update: bad sizes");
   cudaStream_t s = as_stream(stream);
-  Scratch<double> keys;
-  Scratch<int32_t> ids;
-  Scratch<unsigned long long> cnt;
-  SIMDEX_CUDA(keys.alloc(n, s));
-  SIMDEX_CUDA(ids.alloc(n, s));
-  SIMDEX_CUDA(cnt.alloc(c, s));
-  SIMDEX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * c, s));
-  cluster_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(assign, n, keys.p, ids.p, cnt.p);
-  SIMDEX_LAUNCH_CHECK("cluster_keys");
-  SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, n, s));
-  offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
-  SIMDEX_LAUNCH_CHECK("offsets");
-  members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(ids.p, n, out_members);
-  SIMDEX_LAUNCH_CHECK("members");
+  if (c <= 8192) {
+    // stable counting sort by cluster
+    const int64_t nb = ceil_div(n, kGroupBlock);
+    Scratch<int32_t> bcount;
+    Scratch<int64_t> totals;
+    SIMDEX_CUDA(bcount.alloc((size_t)c * nb, s));
+    SIMDEX_CUDA(totals.alloc(c, s));
+    group_hist_kernel<<<(unsigned)nb, 256, sizeof(int32_t) * c, s>>>(assign, n, c, nb, bcount.p);
+    SIMDEX_LAUNCH_CHECK("group_hist");
+    group_cluster_scan_kernel<<<(unsigned)ceil_div(c, 8), 256, 0, s>>>(bcount.p, nb, c, totals.p);
+    SIMDEX_LAUNCH_CHECK("group_cluster_scan");
+    group_offsets_kernel<<<1, 1024, 0, s>>>(totals.p, c, out_counts, out_offsets);
+    SIMDEX_LAUNCH_CHECK("group_offsets");
+    group_scatter_kernel<<<(unsigned)nb, 32, sizeof(int32_t) * c, s>>>(assign, n, c, nb, bcount.p, out_offsets,
+                                                                      out_members);
+    SIMDEX_LAUNCH_CHECK("group_scatter");
+  } else {
+    Scratch<double> keys;
+    Scratch<int32_t> ids;
+    Scratch<unsigned long long> cnt;
+    SIMDEX_CUDA(keys.alloc(n, s));
+    SIMDEX_CUDA(ids.alloc(n, s));
+    SIMDEX_CUDA(cnt.alloc(c, s));
+    SIMDEX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * c, s));
+    cluster_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(assign, n, keys.p, ids.p, cnt.p);
+    SIMDEX_LAUNCH_CHECK("cluster_keys");
+    SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, n, s));
+    offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
+    SIMDEX_LAUNCH_CHECK("offsets");
+    members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(ids.p, n, out_members);
+    SIMDEX_LAUNCH_CHECK("members");
+  }
   if (!centers) return SIMDEX_OK;  // grouping only (members/offsets/counts)
   if (points32) return mean_impl<float>(points32, f, out_members, out_offsets, c, centers, s);
   return mean_impl<double>(points, f, out_members, out_offsets, c, centers, s);
