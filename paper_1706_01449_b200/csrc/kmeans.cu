@@ -663,7 +663,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
   ++gen;
   if (threadIdx.x == 0) {
     __threadfence();
-    atomicAdd(bar, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(1u) : "memory");
     const unsigned want = gen * gridDim.x;
     while (ld_acquire_u32(bar) < want) __nanosleep(32);
     __threadfence();
@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
   for (int q = t; q < f; q += CS) cen[q] = __ldcg(a.centers + q);
   __syncthreads();
   load_center();
-  unsigned long long tm0 = 0, tm1 = 0;
+  unsigned long long tm0 = 0, tm1 = 0, wait1 = 0;
   const bool timing = a.dbg && blockIdx.x == 0 && t == 0;
   for (int j = 0; j + 1 < a.k; ++j) {
     if (timing) tm0 = gtimer();
@@ -843,15 +843,17 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       }
     __syncthreads();
     const double cc = L.kc ? scc[j] : __ldcg(a.seed_c2 + j);
-    // chunks are dealt round-robin (concurrent CTAs stream neighbouring rows);
-    // the pick's CTA ranges are contiguous and summed after the barrier
-    const int64_t r0 = blockIdx.x, r1 = a.nchunks;
+    // 32-point slices: each CTA owns a contiguous range, its warps take the
+    // slices round-robin and run their own pipelines (no CTA-wide step until
+    // the range is done); the CTA then adds its range's slice sums in order
+    const int64_t g0 = a.nchunks * blockIdx.x / G, g1 = a.nchunks * (blockIdx.x + 1) / G;
+    const int64_t GW = wpb, r0 = g0 + w, r1 = g1;  // this CTA's contiguous range, warps interleaved
     // ------------------------------------------------------------ (U) update
     // per warp, a three-stage pipeline over this CTA's chunks: the test inputs
     // of chunk C load while chunk B's rows stream into one staging buffer and
     // chunk A (other buffer) is scored
     auto load_regs = [&](int64_t ch, double& mp2, double& old, int& an) {
-      const int64_t me = ch * CS + w * 32 + lane;
+      const int64_t me = ch * 32 + lane;
       mp2 = 0.0;
       old = DBL_MAX;
       an = 0;
@@ -864,7 +866,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       }
     };
     auto test = [&](int64_t ch, double mp2, double old, int an) -> bool {
-      const int64_t me = ch * CS + w * 32 + lane;
+      const int64_t me = ch * 32 + lane;
       if (ch >= r1 || me >= n) return false;
       if (j == 0) return true;
       const double c2a = L.kc ? scc[an] : __ldcg(a.seed_c2 + an);
@@ -880,7 +882,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     const bool use16 = pre16 && j > 0;
     auto issue = [&](int64_t ch, unsigned mask, int bsel) -> bool {
       if (!mask) return false;
-      const int64_t u0 = ch * CS + w * 32;
+      const int64_t u0 = ch * 32;
       const unsigned char* src;
       size_t sz;
       if (use16) {
@@ -910,11 +912,10 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     unsigned mA = __ballot_sync(0xffffffffu, needA);
     int bA = 0;
     bool sA = issue(chA, mA, bA);
-    int64_t chB = chA + G;
+    int64_t chB = chA + GW;
     load_regs(chB, mp2B, oldB, anB);
-    int par = 0;
     while (chA < r1) {
-      const int64_t chC = chB + G;
+      const int64_t chC = chB + GW;
       const bool needB = test(chB, mp2B, oldB, anB);
       const unsigned mB = __ballot_sync(0xffffffffu, needB);
       const bool sB = issue(chB, mB, bA ^ 1);
@@ -922,7 +923,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       int anC;
       load_regs(chC, mp2C, oldC, anC);
       // score chunk A
-      const int64_t meA = chA * CS + w * 32 + lane;
+      const int64_t meA = chA * 32 + lane;
       double fin = oldA;
       if (mA) {
         if (sA) {
@@ -943,13 +944,6 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
           const double dlo = ps - 2.0 * ((double)acc * inv16 + eb) - 0x1p-40 * ps;
           exact = !(dlo >= oldA);
         }
-        if (a.dbg) {
-          const unsigned nn = __popc(__ballot_sync(0xffffffffu, needA)), ne = __popc(__ballot_sync(0xffffffffu, exact));
-          if (lane == 0) {
-            atomicAdd(a.dbg + 4, (unsigned long long)nn);
-            atomicAdd(a.dbg + 5, (unsigned long long)ne);
-          }
-        }
         if (use16) {
           // the few points the prefilter could not settle: float64 distance from
           // the global rows, four points at a time, eight lanes per point on
@@ -965,7 +959,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
             }
             double dot = 0.0;
             if (mine >= 0) {
-              const P* x = points + (chA * CS + w * 32 + mine) * f;
+              const P* x = points + (chA * 32 + mine) * f;
               for (int k0 = 0; k0 < f; k0 += 64) {
                 P xv[8];
 #pragma unroll
@@ -999,7 +993,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
             }
           }
         } else if (exact) {
-          const size_t s0 = (size_t)(chA * CS + w * 32) * row_bytes;  // slice start
+          const size_t s0 = (size_t)(chA * 32) * row_bytes;  // slice start
           const P* x = sA ? reinterpret_cast<const P*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + (s0 & 15) +
                                                        (size_t)lane * row_bytes)
                           : points + meA * f;
@@ -1017,14 +1011,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       }
       double v = meA < n ? fin : 0.0;
       v = warp_sum(v);
-      if (lane == 0) red[par][w] = v;
-      __syncthreads();
-      if (t == 0) {
-        double sum = 0.0;
-        for (int q = 0; q < wpb; ++q) sum += red[par][q];
-        a.chunk_sums[chA] = sum;
-      }
-      par ^= 1;
+      if (lane == 0) a.chunk_sums[chA] = v;
       chA = chB;
       mp2A = mp2B;
       oldA = oldB;
@@ -1042,9 +1029,8 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       a.dbg[0] += tm1 - tm0;
       tm0 = tm1;
     }
-    grid_barrier(a.barrier, gen);
-    if (t == 0) {  // this CTA's contiguous range of chunk sums, in chunk order
-      const int64_t g0 = a.nchunks * blockIdx.x / G, g1 = a.nchunks * (blockIdx.x + 1) / G;
+    __syncthreads();
+    if (t == 0) {  // this CTA's range of slice sums, in slice order
       double rs = 0.0;
       for (int64_t b = g0; b < g1; b += 8) {
         double vv[8];
@@ -1055,7 +1041,11 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       }
       a.range_sums[blockIdx.x] = rs;
     }
-    grid_barrier(a.barrier, gen);
+    {
+      unsigned long long tw0 = (a.dbg && t == 0) ? gtimer() : 0;
+      grid_barrier(a.barrier, gen);
+      if (a.dbg && t == 0) wait1 += gtimer() - tw0;
+    }
     if (timing) {
       tm1 = gtimer();
       a.dbg[1] += tm1 - tm0;
@@ -1082,10 +1072,10 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     double before;
     const int64_t rg = cta_crossing([&](int64_t q) { return __ldcg(a.range_sums + q); }, G, 0.0, target, wsum,
                                     &s_base, &s_block, &before);
-    const int64_t g0 = a.nchunks * rg / G, g1 = a.nchunks * (rg + 1) / G;
-    const int64_t chk = g0 + cta_crossing([&](int64_t q) { return __ldcg(a.chunk_sums + g0 + q); }, g1 - g0, before,
+    const int64_t x0 = a.nchunks * rg / G, x1 = a.nchunks * (rg + 1) / G;
+    const int64_t chk = x0 + cta_crossing([&](int64_t q) { return __ldcg(a.chunk_sums + x0 + q); }, x1 - x0, before,
                                           target, wsum, &s_base, &s_block, &before);
-    const int64_t pb = chk * CS, pe = (pb + CS) < n ? (pb + CS) : n;
+    const int64_t pb = chk * 32, pe = (pb + 32) < n ? (pb + 32) : n;
     const int64_t pp = pb + cta_crossing([&](int64_t q) { return __ldcg(a.d2 + pb + q); }, pe - pb, before, target,
                                          wsum, &s_base, &s_block, &before);
     if (t == 0) s_pick = (unsigned long long)pp;
@@ -1120,6 +1110,10 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     }
     grid_barrier(a.barrier, gen);
     if (timing) a.dbg[3] += gtimer() - tm0;
+  }
+  if (a.dbg && t == 0) {
+    atomicAdd(a.dbg + 4, wait1);
+    atomicMin(a.dbg + 5, wait1);
   }
 }
 
@@ -1258,7 +1252,7 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
     if (occ >= 1) {
       SIMDEX_CUDA(cudaFuncSetAttribute(seed_persistent_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)psm));
-      const int64_t cs = 32 * wpb, nch = ceil_div(n, cs);
+      const int64_t cs = 32 * wpb, nch = ceil_div(n, 32);  // 32-point slices
       Scratch<unsigned> bar;
       Scratch<double> csum, rsum;
       int64_t grid = (int64_t)occ * sm_count();
@@ -1282,11 +1276,11 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
       a.chunk_sums = csum.p;
       a.range_sums = rsum.p;
       a.nchunks = nch;
-      // fp16 prefilter copy (experimental switch SIMDEX_SEED_F16)
+      // fp16 copy for the certified prefilter of passes > 0 (SIMDEX_SEED_NO_F16 disables)
       Scratch<__half> p16;
       Scratch<unsigned long long> mxb;
       Scratch<int> s16;
-      if (std::getenv("SIMDEX_SEED_F16")) {  // experimental: measured slower than the fp32 slices
+      if (!std::getenv("SIMDEX_SEED_NO_F16")) {
         const int64_t n_pad = ceil_div(n, 32) * 32;
         SIMDEX_CUDA(p16.alloc((size_t)n_pad * f, s));
         SIMDEX_CUDA(mxb.alloc(1, s));
@@ -1306,7 +1300,8 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
       const bool timing = std::getenv("SIMDEX_SEED_TIMING") != nullptr;
       if (timing) {
         SIMDEX_CUDA(dbg.alloc(6, s));
-        SIMDEX_CUDA(cudaMemsetAsync(dbg.p, 0, 6 * sizeof(unsigned long long), s));
+        SIMDEX_CUDA(cudaMemsetAsync(dbg.p, 0, 5 * sizeof(unsigned long long), s));
+        SIMDEX_CUDA(cudaMemsetAsync(dbg.p + 5, 0xff, sizeof(unsigned long long), s));
         a.dbg = dbg.p;
       }
       const P* pts = points;
@@ -1322,9 +1317,9 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
         SIMDEX_CUDA(cudaStreamSynchronize(s));
         fprintf(stderr,
                 "[simdex] seed grid %lld x %lld: update %.3f ms barrier %.3f ms pick %.3f ms barrier %.3f ms; "
-                "per pass: triangle-unskipped %.0f exact %.0f of %lld\n",
+                "barrier-1 wait per CTA: mean %.1f us min %.1f us (%lld points)\n",
                 (long long)grid, (long long)cs, h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6,
-                (double)h[4] / (k - 1), (double)h[5] / (k - 1), (long long)n);
+                (double)h[4] / grid * 1e-3, (double)h[5] * 1e-3, (long long)n);
       }
       return SIMDEX_OK;
     }
