@@ -177,15 +177,16 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
         return torch.as_tensor(a_h, device=dev), True
 
     assign, d2, _, obj = _ops.kmeans_assign(pts, centers, points32=p32)
-    history = [float(obj.item())]
+    objs = [obj]  # read back once at the end (no per-iteration sync for the history)
     for _ in range(max_iters):
         counts, _, _ = _ops.kmeans_update(pts, assign, centers, points32=p32)
         assign, _ = repair(assign, d2, counts)
         new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
-        history.append(float(obj.item()))
+        objs.append(obj)
         if int(changed.item()) == 0:
             break
         assign = new_assign
+    history = [float(v) for v in torch.cat(objs).cpu().numpy()]
     counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
     assign, fixed = repair(assign, d2, counts)
     if fixed:

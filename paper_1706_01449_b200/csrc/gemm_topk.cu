@@ -599,15 +599,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // operand-side prep
 // ---------------------------------------------------------------------------
 __global__ void row_cu_kernel(const double* __restrict__ norms, int64_t rows, int64_t rows_pad, double scale,
-                              float* __restrict__ cu) {
+                              float* __restrict__ cu, const double* __restrict__ scale_dev = nullptr) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows_pad) return;
+  if (scale_dev) scale = *scale_dev;
   cu[r] = r < rows ? __double2float_ru(norms[r] * scale) : 0.f;
 }
 
 // per-row scaled norms (rounded up) + 32-row chunk maxima; one warp per chunk
 __global__ void item_nrm_kernel(const double* __restrict__ norms, int64_t rows, int64_t rows_pad, double scale,
-                                float* __restrict__ nrm, float* __restrict__ nmax32) {
+                                float* __restrict__ nrm, float* __restrict__ nmax32,
+                                const double* __restrict__ scale_dev = nullptr) {
+  if (scale_dev) scale = *scale_dev;
   const int64_t chunk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t r = chunk * 32 + lane;
@@ -635,11 +638,28 @@ __global__ void max_abs_any_kernel(const P* __restrict__ x, int64_t n, double mu
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// operand scales of the augmented product from the device maxima
+// (m[0] = max|p|, m[1] = max|c|, m[2] = max |c|^2/2): exponents and the
+// factors row_cu / item_nrm need -- no host round trip
+__global__ void assign_scales_kernel(const unsigned long long* __restrict__ mx, double eps, int* __restrict__ sexp,
+                                     double* __restrict__ sfac) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double m0 = __longlong_as_double((long long)mx[0]), m1 = __longlong_as_double((long long)mx[1]),
+               m2 = __longlong_as_double((long long)mx[2]);
+  const double mu = fmax(m0, 1.0), mc = fmax(m1, m2);
+  const int su = -ilogb(mu), sc = mc > 0.0 ? -ilogb(mc) : 0;
+  sexp[0] = su;
+  sexp[1] = sc;
+  sfac[0] = eps * ldexp(1.0, su);
+  sfac[1] = ldexp(1.0, sc);
+}
+
 // eight threads per row, each writing 16-byte pieces (8 halves) of the row
 template <class P>
 __global__ void pack_aug_kernel(const P* __restrict__ x, const double* __restrict__ sq, int64_t rows, int f,
-                                int centers, int scale_exp, int64_t rows_pad, int kp, uint16_t* __restrict__ out,
-                                double* __restrict__ gnorm) {
+                                int centers, const int* __restrict__ scale_exp_dev, int64_t rows_pad, int kp,
+                                uint16_t* __restrict__ out, double* __restrict__ gnorm) {
+  const int scale_exp = *scale_exp_dev;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = g >> 3;
   const int sub = (int)(g & 7);
@@ -1635,17 +1655,12 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
       centers, (int64_t)c * f, 1.0, mx.p + 1);
   max_abs_any_kernel<double><<<1, 256, 0, s>>>(c2, c, 0.5, mx.p + 2);
   SIMDEX_LAUNCH_CHECK("max_abs_any");
-  unsigned long long hm[3];
-  SIMDEX_CUDA(cudaMemcpyAsync(hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
-  SIMDEX_CUDA(cudaStreamSynchronize(s));
-  double m[3];
-  for (int i = 0; i < 3; ++i) std::memcpy(&m[i], &hm[i], sizeof(double));
-  const double mu = std::max(m[0], 1.0), mc = std::max(m[1], m[2]);
-  if (!std::isfinite(mu) || !std::isfinite(mc)) {
-    set_error("kmeans_assign: non-finite values");
-    return SIMDEX_EINVAL;
-  }
-  const int su = -std::ilogb(mu), sc = mc > 0.0 ? -std::ilogb(mc) : 0;
+  Scratch<int> sexp;
+  Scratch<double> sfac;
+  SIMDEX_CUDA(sexp.alloc(2, s));
+  SIMDEX_CUDA(sfac.alloc(2, s));
+  assign_scales_kernel<<<1, 32, 0, s>>>(mx.p, eps_for(kp), sexp.p, sfac.p);
+  SIMDEX_LAUNCH_CHECK("assign_scales");
   const int k_eff = 1;
   RowState st;
   if ((rc = st.alloc(nu_pad, k_eff, s))) return rc;
@@ -1667,19 +1682,18 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   SIMDEX_CUDA(inrm.alloc(nc_pad, s));
   SIMDEX_CUDA(inmax.alloc(nc_pad / 32, s));
   ProfileScope _prof("assign_pack", s);
-  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, su, nu_pad, kp, ua.p,
-                                                                          un.p);
-  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad * 8, 256), 256, 0, s>>>(centers, c2, c, f, 1, sc, nc_pad, kp,
-                                                                               ca.p, cn.p);
+  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, sexp.p, nu_pad, kp,
+                                                                          ua.p, un.p);
+  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad * 8, 256), 256, 0, s>>>(centers, c2, c, f, 1, sexp.p + 1,
+                                                                               nc_pad, kp, ca.p, cn.p);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("pack_aug");
   units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units.p, n_units.p, nunits);
   SIMDEX_LAUNCH_CHECK("units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un.p, n, nu_pad, eps_for(kp) * std::ldexp(1.0, su),
-                                                               cu.p);
+  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un.p, n, nu_pad, 0.0, cu.p, sfac.p);
   SIMDEX_LAUNCH_CHECK("row_cu");
-  item_nrm_kernel<<<(unsigned)ceil_div(nc_pad / 32, 8), 256, 0, s>>>(cn.p, c, nc_pad, std::ldexp(1.0, sc), inrm.p,
-                                                                      inmax.p);
+  item_nrm_kernel<<<(unsigned)ceil_div(nc_pad / 32, 8), 256, 0, s>>>(cn.p, c, nc_pad, 0.0, inrm.p, inmax.p,
+                                                                      sfac.p + 1);
   SIMDEX_LAUNCH_CHECK("item_nrm");
   CUtensorMap ma, mb;
   if ((rc = make_map(&ma, ua.p, nu_pad, kp))) return rc;
@@ -1715,8 +1729,7 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   fp.out_d2 = out_d2;
   fp.changed = changed;
   if ((rc = launch_finalize(fp, n, s))) return rc;
-  SIMDEX_CUDA(cudaMemcpyAsync(n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  SIMDEX_CUDA(cudaStreamSynchronize(s));
+  SIMDEX_CUDA(cudaMemcpyAsync(n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   return SIMDEX_OK;
 }
 

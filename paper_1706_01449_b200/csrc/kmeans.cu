@@ -25,7 +25,7 @@ namespace simdex {
 
 int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, const double* p2,
                        const double* centers, const double* c2, int32_t c, const int64_t* prev, int64_t* out_assign,
-                       double* out_d2, unsigned long long* changed, int64_t* over_rows, int32_t* n_over,
+                       double* out_d2, unsigned long long* changed, int64_t* over_rows, int32_t* n_over_dev,
                        cudaStream_t s);
 
 namespace {
@@ -47,65 +47,61 @@ __global__ void sqnorm_kernel(const P* __restrict__ x, int64_t n, int f, double*
   out[i] = s;
 }
 
+// Exact float64 assignment (clustering.py:96-101), one thread per point.
+// With `rows` it handles the listed points only (count read on the device,
+// grid-stride over blocks so the host needs no count).
 template <class P>
 __global__ void __launch_bounds__(kAssignThreads) assign_kernel(
     const P* __restrict__ points, const double* __restrict__ p2, int64_t n, int f, const double* __restrict__ centers,
     const double* __restrict__ c2, int c, const int64_t* __restrict__ prev, int64_t* __restrict__ out_assign,
-    double* __restrict__ out_d2, unsigned long long* __restrict__ changed, double* __restrict__ block_sums,
-    const int64_t* __restrict__ rows, int64_t n_rows) {
+    double* __restrict__ out_d2, unsigned long long* __restrict__ changed, const int64_t* __restrict__ rows,
+    const int32_t* __restrict__ n_rows) {
   __shared__ double cs[kCC][kFC + 1];
-  __shared__ double red[kAssignThreads / 32];
-  const int64_t idx = (int64_t)blockIdx.x * kAssignThreads + threadIdx.x;
-  const bool live = rows ? idx < n_rows : idx < n;
-  const int64_t u = rows ? (live ? rows[idx] : 0) : idx;
-  const P* x = points + (live ? u : 0) * f;
-  const double pp = live ? p2[u] : 0.0;
-  double best = DBL_MAX;
-  int64_t arg = 0;
-  for (int c0 = 0; c0 < c; c0 += kCC) {
-    double acc[kCC];
+  const int64_t limit = rows ? (int64_t)*n_rows : n;
+  for (int64_t base = (int64_t)blockIdx.x * kAssignThreads; base < limit;
+       base += (int64_t)gridDim.x * kAssignThreads) {
+    const int64_t idx = base + threadIdx.x;
+    const bool live = idx < limit;
+    const int64_t u = rows ? (live ? rows[idx] : 0) : idx;
+    const P* x = points + (live ? u : 0) * f;
+    const double pp = live ? p2[u] : 0.0;
+    double best = DBL_MAX;
+    int64_t arg = 0;
+    for (int c0 = 0; c0 < c; c0 += kCC) {
+      double acc[kCC];
 #pragma unroll
-    for (int j = 0; j < kCC; ++j) acc[j] = 0.0;
-    for (int k0 = 0; k0 < f; k0 += kFC) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < kCC * kFC; e += kAssignThreads) {
-        int j = e / kFC, k = e % kFC;
-        cs[j][k] = (c0 + j < c && k0 + k < f) ? centers[(int64_t)(c0 + j) * f + k0 + k] : 0.0;
+      for (int j = 0; j < kCC; ++j) acc[j] = 0.0;
+      for (int k0 = 0; k0 < f; k0 += kFC) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kCC * kFC; e += kAssignThreads) {
+          int j = e / kFC, k = e % kFC;
+          cs[j][k] = (c0 + j < c && k0 + k < f) ? centers[(int64_t)(c0 + j) * f + k0 + k] : 0.0;
+        }
+        __syncthreads();
+        const int kn = (f - k0) < kFC ? (f - k0) : kFC;
+        for (int k = 0; k < kn; ++k) {
+          const double xk = live ? (double)x[k0 + k] : 0.0;
+#pragma unroll
+          for (int j = 0; j < kCC; ++j) acc[j] = fma(xk, cs[j][k], acc[j]);
+        }
       }
-      __syncthreads();
-      const int kn = (f - k0) < kFC ? (f - k0) : kFC;
-      for (int k = 0; k < kn; ++k) {
-        const double xk = live ? (double)x[k0 + k] : 0.0;
 #pragma unroll
-        for (int j = 0; j < kCC; ++j) acc[j] = fma(xk, cs[j][k], acc[j]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kCC; ++j) {
-      if (c0 + j < c) {
-        double d = (pp + c2[c0 + j]) - 2.0 * acc[j];  // clustering.py:100
-        d = d > 0.0 ? d : 0.0;                        // np.maximum(d2, 0)
-        if (d < best) {                               // strict: first minimum wins (argmin)
-          best = d;
-          arg = c0 + j;
+      for (int j = 0; j < kCC; ++j) {
+        if (c0 + j < c) {
+          double d = (pp + c2[c0 + j]) - 2.0 * acc[j];  // clustering.py:100
+          d = d > 0.0 ? d : 0.0;                        // np.maximum(d2, 0)
+          if (d < best) {                               // strict: first minimum wins (argmin)
+            best = d;
+            arg = c0 + j;
+          }
         }
       }
     }
-  }
-  double mine = 0.0;
-  if (live) {
-    out_assign[u] = arg;
-    out_d2[u] = best;
-    mine = best;
-    if (prev && prev[u] != arg) atomicAdd(changed, 1ull);
-  }
-  mine = warp_sum(mine);  // deterministic block sum of d2 (fixed tree)
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kAssignThreads / 32; ++w) s += red[w];
-    if (block_sums) block_sums[blockIdx.x] = s;
+    if (live) {
+      out_assign[u] = arg;
+      out_d2[u] = best;
+      if (prev && prev[u] != arg) atomicAdd(changed, 1ull);
+    }
   }
 }
 
@@ -1182,20 +1178,20 @@ int assign_impl(const double* points, const float* points32, const P* px, int64_
   if (f + 1 <= kAssignGemmMaxF) {
     // tensor-core candidates + exact float64 d2; overflowing bands go to the SIMT kernel
     Scratch<int64_t> over;
+    Scratch<int32_t> n_over;
     SIMDEX_CUDA(over.alloc(n, s));
-    int32_t n_over = 0;
+    SIMDEX_CUDA(n_over.alloc(1, s));
     int rc = gemm_kmeans_assign(points, points32, n, f, p2.p, centers, c2.p, c, prev, out_assign, out_d2, changed,
-                                over.p, &n_over, s);
+                                over.p, n_over.p, s);
     if (rc) return rc;
-    if (n_over > 0) {
-      assign_kernel<P><<<(unsigned)ceil_div(n_over, kAssignThreads), kAssignThreads, 0, s>>>(
-          px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, nullptr, over.p, n_over);
-      SIMDEX_LAUNCH_CHECK("assign");
-    }
+    // rows whose band overflowed (rare): exact SIMT kernel, count read on the device
+    assign_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(n, kAssignThreads), 2 * sm_count()), kAssignThreads, 0,
+                       s>>>(px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, over.p, n_over.p);
+    SIMDEX_LAUNCH_CHECK("assign");
   } else {
     ProfileScope _prof("kmeans_assign", s);
     assign_kernel<P><<<(unsigned)ceil_div(n, kAssignThreads), kAssignThreads, 0, s>>>(
-        px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, nullptr, nullptr, 0);
+        px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, nullptr, nullptr);
     _prof.end();
     SIMDEX_LAUNCH_CHECK("assign");
   }
