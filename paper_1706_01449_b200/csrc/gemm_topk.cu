@@ -1054,39 +1054,6 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
   }
 }
 
-// stage 1: an initial certified threshold per row from the exact scores of
-// its cluster's first k list items (all inside the prefix, k <= B'): their
-// minimum lower-bounds the k-th best prefix score, so the row starts filtering
-// at once instead of admitting the first chunks wholesale.  One warp per row.
-template <class Q>
-__global__ void prefix_t0_kernel(const int64_t* __restrict__ row_user, const int32_t* __restrict__ row_cluster,
-                                 int64_t rows, const double* __restrict__ users, const Q* __restrict__ items,
-                                 const int32_t* __restrict__ list_ids, int64_t n, int f, int k, double scale,
-                                 float* __restrict__ t0) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const int64_t user = row_user[r];
-  if (user < 0) {
-    if (lane == 0) t0[r] = -INFINITY;
-    return;
-  }
-  const int32_t* ids = list_ids + (int64_t)row_cluster[r] * n;
-  const double* u = users + user * f;
-  double mn = DBL_MAX;
-  for (int j = 0; j < k; ++j) {
-    const Q* x = items + (int64_t)ids[j] * f;
-    double s = 0.0;
-    for (int q = lane; q < f; q += 32) s = fma(u[q], (double)x[q], s);
-    s = warp_sum(s);
-    mn = fmin(mn, s);
-  }
-  if (lane == 0) {
-    const double v = mn * scale;
-    t0[r] = __double2float_rd(v - fabs(v) * 0x1p-40);
-  }
-}
-
 // stage 2: pack the continuing rows densely (rows past the count are zero)
 __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
                                  int64_t rows_max, const int64_t* __restrict__ row_user,
@@ -1465,19 +1432,6 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
   if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
   TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
-  Scratch<float> t0s;
-  if (k_eff <= bp) {
-    SIMDEX_CUDA(t0s.alloc(rows_max, s));
-    const double scale = std::ldexp(1.0, su + si);
-    if (items32)
-      prefix_t0_kernel<float><<<(unsigned)ceil_div(rows_max, 8), 256, 0, s>>>(
-          row_user.p, rclus.p, rows_max, users, items32, list_ids, ni, f, k_eff, scale, t0s.p);
-    else
-      prefix_t0_kernel<double><<<(unsigned)ceil_div(rows_max, 8), 256, 0, s>>>(
-          row_user.p, rclus.p, rows_max, users, items, list_ids, ni, f, k_eff, scale, t0s.p);
-    SIMDEX_LAUNCH_CHECK("prefix_t0");
-    p.row_T0 = t0s.p;
-  }
   const bool stats = getenv("SIMDEX_STATS") != nullptr;
   Scratch<int64_t> hops;
   if (stats) {
