@@ -192,6 +192,16 @@ def run_reference(args):
 # our arm
 # ---------------------------------------------------------------------------
 
+def _profiled_traffic(path, k):
+    """DRAM bytes per gemm_topk launch (read + write) from the committed ncu
+    --set full capture of the same workload (profiles/), or None."""
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_gemm_topk_traffic.json")
+    if path != "index" or k != 10 or not os.path.exists(f):
+        return None
+    with open(f) as fh:
+        return json.load(fh)["traffic_bytes_per_launch"]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -286,7 +296,7 @@ def run_ours(args):
         achieved = flops / (gemm_ms / 1000.0) / 1e12
         roof = {"kernel": "gemm_topk_kernel (tcgen05 fp16 x fp16 -> fp32 TMEM, fused certified top-K)",
                 "bound": "tensor", "achieved": achieved, "peak": bf16, "peak_kind": f"{peak_kind} dense bf16 (= fp16 dense rate on B200; burst)",
-                "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": _profiled_traffic(path, k),
                 "algorithmic_flops_per_step": flops, "launch_ms_per_step": gemm_ms,
                 "launches_per_step": kernels["gemm_topk"]["launches_per_step"], "per_unit": per_unit,
                 "share_of_step": gemm_ms / ms_per_step}
