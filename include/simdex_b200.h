@@ -93,11 +93,11 @@ SIMDEX_API int simdex_pack_f16(const double* x, int64_t rows, int32_t f, int32_t
  *   heap_ops: optional int64[nu]: per user count of tile scores above the
  *   running K-th at the time the tile is merged (brute.py:95-97; tile order
  *   differs from the reference, the count is analogous, not bit-equal).
- *   items32 (nullable): exact float32 copy of items for the rescoring reads;
+ *   users32 / items32 (nullable): exact float32 copies for the rescoring reads;
  *   item_perm (nullable): the item operand ib / i_norm is in this row order
  *   (e.g. simdex_norm_order), ib has ib_rows rows (0: 256*ceil(ni/256)).
  * Requires k_eff <= 256; larger k goes through simdex_topk_exact. */
-SIMDEX_API int simdex_topk_matmul(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu,
+SIMDEX_API int simdex_topk_matmul(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu,
                        const double* items, const float* items32, const uint16_t* ib, const double* i_norm,
                        const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                        int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k,
@@ -209,7 +209,7 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
  * list_ids, from simdex_build_index).
  * out_visited follows the reference: n if B >= n, else max(B, walk visited).
  * Requires k_eff <= 256 and f <= 256 (else use simdex_walk). */
-SIMDEX_API int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
+SIMDEX_API int simdex_query_ws(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,
                     const double* items, const float* items32, const uint16_t* ib, const double* item_norms,
                     const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, int32_t si,

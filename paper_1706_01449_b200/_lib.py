@@ -33,7 +33,7 @@ SIGNATURES = {
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
     "simdex_max_abs": [P, I64, P, P],
     "simdex_pack_f16": [P, I64, I32, I32, I64, I32, P, P, P],
-    "simdex_topk_matmul": [P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, P],
+    "simdex_topk_matmul": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, P],
     "simdex_norm_order": [P, I64, P, P],
     "simdex_to_f32": [P, I64, P, P, P],
     "simdex_kmeans_seed": [P, P, I64, I32, I32, I64, P, P, P, P, P],
@@ -43,7 +43,7 @@ SIGNATURES = {
     "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P, P],
     "simdex_list_positions": [P, I32, I64, P, P],
     "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
-    "simdex_query_ws": [P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64, P,
+    "simdex_query_ws": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64, P,
                         P, P, I64, I32, P, P, P, P],
     "simdex_ws_stats": [P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],

@@ -84,14 +84,14 @@ def topk_exact(users, items, k, rows=None):
     return ids, sc
 
 
-def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32=None):
+def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32=None, users32=None):
     nu, f = users.shape
     ni = items.shape[0]
     k_eff = min(k, ni)
     ids = torch.empty((nu, k_eff), dtype=I32, device=users.device)
     sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
-    call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(pu.op), ptr(pu.norms), nu,
+    call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu,
          ptr(_c(items, F64)), ptr(items32), ptr(pi.op), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
          pu.scale_exp,
          pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), stream_ptr())
@@ -215,7 +215,7 @@ def group_queries(q_user, assign, c):
 
 
 def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k,
-             items32=None):
+             items32=None, users32=None):
     """Work-sharing batch query; ``grouped`` = group_queries(...) output.
     Returns (ids, scores, visited) in the original query order."""
     nu, f = users.shape
@@ -228,7 +228,7 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
-    call("simdex_query_ws", ptr(_c(users, F64)), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(items32),
+    call("simdex_query_ws", ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(items32),
          ptr(pi.op),
          ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),
          ptr(_c(list_pos, I32)),

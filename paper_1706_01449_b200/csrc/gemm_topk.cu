@@ -833,12 +833,28 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     const int e = base + sg;
     double part = 0.0;
     if (act && e < cnt) {
+      // strided partials (lane sl takes q = sl, sl+8, ...), loads of a
+      // 64-factor chunk issued together before the FMAs
       if (p.items32) {
         const float* x = p.items32 + (int64_t)si[e] * p.f;
-        for (int q = sl; q < p.f; q += 8) part = fma((double)x[q], us[q], part);
+        for (int k0 = 0; k0 < p.f; k0 += 64) {
+          float xv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xv[i] = k0 + sl + 8 * i < p.f ? x[k0 + sl + 8 * i] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (k0 + sl + 8 * i < p.f) part = fma((double)xv[i], us[k0 + sl + 8 * i], part);
+        }
       } else {
         const double* x = p.items + (int64_t)si[e] * p.f;
-        for (int q = sl; q < p.f; q += 8) part = fma(x[q], us[q], part);
+        for (int k0 = 0; k0 < p.f; k0 += 64) {
+          double xv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xv[i] = k0 + sl + 8 * i < p.f ? x[k0 + sl + 8 * i] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (k0 + sl + 8 * i < p.f) part = fma(xv[i], us[k0 + sl + 8 * i], part);
+        }
       }
     }
     part += __shfl_xor_sync(0xffffffffu, part, 4);
@@ -1292,7 +1308,7 @@ void read_ws_stats(int64_t* out) {
 }
 
 // Brute-force fused path (topk_matmul).
-int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
+int gemm_topk_brute(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
                     const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
                     int64_t* heap_ops, float* debug_out, cudaStream_t s) {
@@ -1342,6 +1358,7 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
   fp.total_rows = nu;
   fp.nu = nu;
   fp.users = users;
+  fp.users32 = users32;
   fp.items = items;
   fp.items32 = items32;
   fp.f = f;
@@ -1375,7 +1392,7 @@ int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_nor
 //            whose K-th beats the ceiling at B' are done (visited = B');
 //   stage 2  the remaining users x the whole catalogue (certified top-K), and
 //            visited from the closed form of Algorithm 1's stop position.
-int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
+int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                  int32_t f, int32_t kp, int32_t su, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
@@ -1459,6 +1476,7 @@ int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, i
   fp.row_cluster = rclus.p;
   fp.nu = nu;
   fp.users = users;
+  fp.users32 = users32;
   fp.items = items;
   fp.items32 = items32;
   fp.f = f;

@@ -3,11 +3,11 @@
 #include "common.cuh"
 
 namespace simdex {
-int gemm_topk_brute(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
+int gemm_topk_brute(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
                     const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
                     int64_t* heap_ops, float* debug_out, cudaStream_t s);
-int gemm_topk_ws(const double* users, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
+int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                  int32_t f, int32_t kp, int32_t su, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
@@ -54,7 +54,7 @@ __global__ void group_offsets_kernel(const unsigned long long* counts, int c, in
 
 using namespace simdex;
 
-extern "C" int simdex_topk_matmul(const double* users, const uint16_t* ub, const double* u_norm, int64_t nu,
+extern "C" int simdex_topk_matmul(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu,
                                   const double* items, const float* items32, const uint16_t* ib, const double* i_norm,
                                   const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
                                   int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
@@ -68,7 +68,7 @@ extern "C" int simdex_topk_matmul(const double* users, const uint16_t* ub, const
     return exact_topk_rows(users, items, ni, f, nullptr, nu, k, out_ids, out_scores, as_stream(stream));
   }
   SIMDEX_CHECK_ARG(kp % 64 == 0 && kp >= f, "simdex_topk_matmul: kp must be a multiple of 64 >= f");
-  return gemm_topk_brute(users, ub, u_norm, nu, items, items32, ib, i_norm, item_perm, ib_rows, ni, f, kp, su, si, k, out_ids,
+  return gemm_topk_brute(users, users32, ub, u_norm, nu, items, items32, ib, i_norm, item_perm, ib_rows, ni, f, kp, su, si, k, out_ids,
                          out_scores, heap_ops, nullptr, as_stream(stream));
 }
 
@@ -89,7 +89,7 @@ extern "C" int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t*
   SIMDEX_CUDA(in.alloc(ni, s));
   SIMDEX_CUDA(cudaMemsetAsync(un.p, 0, sizeof(double) * nu, s));
   SIMDEX_CUDA(cudaMemsetAsync(in.p, 0, sizeof(double) * ni, s));
-  return gemm_topk_brute(nullptr, ub, un.p, nu, nullptr, nullptr, ib, in.p, nullptr, 0, ni, f, kp, 0, 0, 1, nullptr, nullptr,
+  return gemm_topk_brute(nullptr, nullptr, ub, un.p, nu, nullptr, nullptr, ib, in.p, nullptr, 0, ni, f, kp, 0, 0, 1, nullptr, nullptr,
                          nullptr, out, s);
 }
 
@@ -117,7 +117,7 @@ extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int
   return SIMDEX_OK;
 }
 
-extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const double* user_norms, int64_t nu,
+extern "C" int simdex_query_ws(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,
                                const double* items, const float* items32, const uint16_t* ib,
                                const double* item_norms,
                                const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
@@ -136,7 +136,7 @@ extern "C" int simdex_query_ws(const double* users, const uint16_t* ub, const do
   SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
                    "simdex_query_ws: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);
   if (nq == 0) return SIMDEX_OK;
-  return gemm_topk_ws(users, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, si,
+  return gemm_topk_ws(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, si,
                       list_ids, list_pos,
                       bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
                       out_scores, out_visited, as_stream(stream));

@@ -285,7 +285,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
             if q_users is index._dev.get("all_users"):
                 index._dev[key] = grouped
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, index.block_size,
-                             index.device_prefix(model), grouped, k, items32=_device.f32_exact(model.items))
+                             index.device_prefix(model), grouped, k, items32=_device.f32_exact(model.items),
+                             users32=_device.f32_exact(model.users))
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
     out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
     if work_sharing:  # k beyond the tensor-core envelope: WS visited = n if B >= n else max(B, walk visited)
