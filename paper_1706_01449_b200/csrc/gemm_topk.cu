@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(t_full + buf, use & 1);
         tc_fence_after();
         bool released = false;
-        if (h < ntile_a) {
+        if (h < ntile_a && p.skip_epi != 5) {
           const int tile_valid = min(kTileN, un.n_items - t * kTileN);
           // two chunks of 32 columns per TMEM wait; once the whole tile is in
           // registers the accumulator buffer goes back to the MMA warp
@@ -447,48 +447,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                     p.debug_out[grow * p.debug_ld + un.b_row0 + c0 + i] = __uint_as_float(raw[c][i]);
                 continue;
               }
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[c][i]);
+              if (nvalid < 32) {  // the last, partial tile only (warp-uniform)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? v[i] : -INFINITY;
+              }
+              // chunk max as a tree of 3-input FMNMX3 (17 instructions for 32 values)
+              float m[11];
+#pragma unroll
+              for (int i = 0; i < 10; ++i) m[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+              m[10] = fmaxf(v[30], v[31]);
+              const float m0 = fmax3(m[0], m[1], m[2]), m1 = fmax3(m[3], m[4], m[5]);
+              const float m2 = fmax3(m[6], m[7], m[8]), m3 = fmaxf(m[9], m[10]);
+              const float mx = fmaxf(fmax3(m0, m1, m2), m3);
+              const float nmax = ch == 0 ? nm4.x : ch == 1 ? nm4.y : ch == 2 ? nm4.z : nm4.w;
+              const float em = fmaf(cu, nmax, p.e_abs);  // the chunk's widest band
+              // rows that cannot take candidates (padding, overflowed) never pass
+              const bool pass = p.skip_epi != 2 && mx + em >= ((live && !flags) ? T : INFINITY);
+              // fast path: one vote per chunk; everything below is the rare, warp-uniform slow path
+              if (!__any_sync(0xffffffffu, pass)) continue;
               const bool act = live && !flags;
               unsigned mask = 0;  // items of this chunk whose upper bound reaches T
               const float* nrm = p.item_nrm + un.b_row0 + c0;
-              float vloc[32];  // the chunk, spilled for the (rare) appends: indexed dynamically
-              if (act) {
-                float v[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[c][i]);
-                if (nvalid < 32) {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? v[i] : -INFINITY;
+              float vloc[32];  // the chunk, spilled for the appends: indexed dynamically
+              if (pass) {
+                if constexpr (KT == 1) {
+                  // k = 1: the chunk max less the widest band lower-bounds its best item
+                  top[0] = fmaxf(top[0], mx - em);
+                  T = fmaxf(T, top[0]);
                 }
-                // chunk max as a tree of 3-input FMNMX3 (17 instructions for 32 values)
-                float m[11];
+                // coarse mask against the chunk-uniform band (a superset of the
+                // per-item test, which the append loop applies): bit i set iff
+                // v[i] - Tc >= 0, sign bits packed by funnel shifts
+                const float Tc = (T - em) - fabsf(T) * 0x1p-22f - 0x1p-126f;
+                unsigned neg = 0;
 #pragma unroll
-                for (int i = 0; i < 10; ++i) m[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
-                m[10] = fmaxf(v[30], v[31]);
-                const float m0 = fmax3(m[0], m[1], m[2]), m1 = fmax3(m[3], m[4], m[5]);
-                const float m2 = fmax3(m[6], m[7], m[8]), m3 = fmaxf(m[9], m[10]);
-                const float mx = fmaxf(fmax3(m0, m1, m2), m3);
-                const float nmax = ch == 0 ? nm4.x : ch == 1 ? nm4.y : ch == 2 ? nm4.z : nm4.w;
-                const float em = fmaf(cu, nmax, p.e_abs);  // the chunk's widest band
-                if (p.skip_epi != 2 && mx + em >= T) {  // else nothing in this chunk can qualify
-                  if constexpr (KT == 1) {
-                    // k = 1: the chunk max less the widest band lower-bounds its best item
-                    top[0] = fmaxf(top[0], mx - em);
-                    T = fmaxf(T, top[0]);
-                  }
-                  // coarse mask against the chunk-uniform band (a superset of the
-                  // per-item test, which the append loop applies): bit i set iff
-                  // v[i] - Tc >= 0, sign bits packed by funnel shifts
-                  const float Tc = (T - em) - fabsf(T) * 0x1p-22f - 0x1p-126f;
-                  unsigned neg = 0;
+                for (int i = 31; i >= 0; --i) neg = __funnelshift_l(__float_as_uint(v[i] - Tc), neg, 1);
+                mask = ~neg;
+                if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
+                if (p.skip_epi == 3) mask = 0;
+                if (mask) {
 #pragma unroll
-                  for (int i = 31; i >= 0; --i) neg = __funnelshift_l(__float_as_uint(v[i] - Tc), neg, 1);
-                  mask = ~neg;
-                  if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
-                  if (p.skip_epi == 3) mask = 0;
-                  if (mask) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) vloc[i] = v[i];
-                  }
+                  for (int i = 0; i < 32; ++i) vloc[i] = v[i];
                 }
               }
               // converged append loop: every lane with pending items takes one per round
