@@ -350,6 +350,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       uint32_t acc = 0;
       int iter = 0;
+      // descriptors are built once: the start-address field (bits 0-13, in
+      // 16-byte units) of a base descriptor is advanced by plain adds
+      const uint64_t a_desc0 = umma_desc_sw128(smem_u32(a_sm));
+      const uint64_t b_desc0 = umma_desc_sw128(smem_u32(b_sm));
+      const int ksteps = p.k_steps;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++iter) {
         const Unit un = p.units[u];
         const int ntile_a = un.rows > kTileM ? 2 : 1;
@@ -361,13 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(t_empty + buf, (use & 1) ^ 1);
           mbar_wait(full + stage, phase);
           tc_fence_after();
+          const uint64_t bd0 = b_desc0 + (uint64_t)((stage * KB * kSlab) >> 4);
           for (int h = 0; h < ntile_a; ++h) {
             const uint32_t d = tbase + (buf * 2 + h) * kTileN;
-            for (int ks = 0; ks < p.k_steps; ++ks) {
-              const int kb = ks >> 2, kk = ks & 3;
-              const uint64_t ad = umma_desc_sw128(smem_u32(a_sm + (h * KB + kb) * kSlab) + kk * 32);
-              const uint64_t bd = umma_desc_sw128(smem_u32(b_sm + (stage * KB + kb) * kSlab) + kk * 32);
-              mma_f16(d, ad, bd, kIdesc, ks > 0 ? 1u : 0u);
+            const uint64_t ad0 = a_desc0 + (uint64_t)((h * KB * kSlab) >> 4);
+#pragma unroll 4
+            for (int ks = 0; ks < ksteps; ++ks) {
+              const uint32_t off = (uint32_t)((ks >> 2) * (kSlab >> 4) + (ks & 3) * 2);
+              mma_f16(d, ad0 + off, bd0 + off, kIdesc, ks > 0 ? 1u : 0u);
             }
           }
           mma_commit(empty + stage);  // smem slot free once these MMAs retire
