@@ -834,10 +834,27 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     si[e] = INT32_MAX;
   }
   __syncwarp();
+  if (p.mode == kAssign) {
+    // k-means: one lane per candidate, factors in order -- the arithmetic of
+    // the squared norms, so a point equal to a centre gets exactly d2 = 0
+    for (int e = gl; e < cmax2; e += LPR) {
+      if (act && e < cnt) {
+        double dot = 0.0;
+        if (p.items32) {
+          const float* x = p.items32 + (int64_t)si[e] * p.f;
+          for (int q = 0; q < p.f; ++q) dot = fma((double)x[q], us[q], dot);
+        } else {
+          const double* x = p.items + (int64_t)si[e] * p.f;
+          for (int q = 0; q < p.f; ++q) dot = fma(x[q], us[q], dot);
+        }
+        ss[e] = dot;
+      }
+    }
+  }
   // LPR/8 candidates per round, 8 lanes each (strided partials + xor tree)
   constexpr int SG = LPR / 8;
   const int sg = gl >> 3, sl = gl & 7;
-  for (int base = 0; base < cmax2; base += SG) {
+  for (int base = 0; base < (p.mode == kAssign ? 0 : cmax2); base += SG) {
     const int e = base + sg;
     double part = 0.0;
     if (act && e < cnt) {

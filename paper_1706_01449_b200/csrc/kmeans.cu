@@ -221,6 +221,74 @@ __global__ void __launch_bounds__(kMeanWarps * 32) centroid_mean_kernel(const P*
   }
 }
 
+// centroid = sum over members in id order / count: the reference's
+// users[sel].mean(axis=0) adds the rows in order (numpy reduces a
+// non-contiguous axis sequentially), so the centroids are bit-identical to
+// the reference's for the same assignment.  One CTA per cluster: member rows
+// are staged in shared memory 64 at a time with asynchronous copies (double
+// buffered), thread k adds factor k sequentially.  Empty clusters keep their
+// centroid (clustering.py:170-172).
+constexpr int kSeqMaxF = 1024;  // 8 factors per thread
+
+template <class P>
+__global__ void __launch_bounds__(128) centroid_seq_kernel(const P* __restrict__ points, int f,
+                                                           const int64_t* __restrict__ members,
+                                                           const int64_t* __restrict__ offsets, int kSeqRows,
+                                                           double* __restrict__ centers) {
+  extern __shared__ __align__(16) unsigned char seq_raw[];
+  P* buf = reinterpret_cast<P*>(seq_raw);  // [2][kSeqRows * f]
+  __shared__ int64_t ids[128];             // member ids of the chunk being staged
+  const int cl = blockIdx.x, t = threadIdx.x;
+  const int64_t b = offsets[cl], e = offsets[cl + 1];
+  if (e == b) return;
+  const int64_t nchunk = (e - b + kSeqRows - 1) / kSeqRows;
+  auto rows_of = [&](int64_t ch) {
+    const int64_t r0 = b + ch * kSeqRows;
+    return (int)((e - r0) < kSeqRows ? (e - r0) : kSeqRows);
+  };
+  // ids of the chunk in shared memory first, then one asynchronous copy per
+  // element with no load on its address path
+  auto stage = [&](int64_t ch, int slot) {
+    const int rows = rows_of(ch);
+    if (t < rows) ids[t] = members[b + ch * kSeqRows + t];
+    __syncthreads();
+    P* dst = buf + (size_t)slot * kSeqRows * f;
+    for (int idx = t; idx < rows * f; idx += blockDim.x) {
+      const int r = idx / f, q = idx - r * f;
+      const P* src = points + ids[r] * f + q;
+      if constexpr (sizeof(P) == 8)
+        sm100::cp_async8(dst + idx, src);
+      else
+        sm100::cp_async4(dst + idx, src);
+    }
+    sm100::cp_async_commit();
+    __syncthreads();  // ids may be overwritten by the next stage
+  };
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // thread t owns factors t + 128 h
+  stage(0, 0);
+  for (int64_t ch = 0; ch < nchunk; ++ch) {
+    sm100::cp_async_wait<0>();  // chunk ch landed
+    __syncthreads();
+    if (ch + 1 < nchunk) stage(ch + 1, (int)((ch + 1) & 1));  // streams while chunk ch is summed
+    const int rows = rows_of(ch);
+    const P* src = buf + (size_t)(ch & 1) * kSeqRows * f;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const int k = t + 128 * h;
+      if (k < f) {
+#pragma unroll 8
+        for (int r = 0; r < rows; ++r) acc[h] += (double)src[r * f + k];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const int k = t + 128 * h;
+    if (k < f) centers[(int64_t)cl * f + k] = acc[h] / (double)(e - b);
+  }
+}
+
 // centroid = (sum of the S part sums, in part order) / count; empty clusters
 // keep their centroid (clustering.py:170-172)
 __global__ void combine_mean_kernel(const double* __restrict__ psum, const int64_t* __restrict__ offsets, int c,
@@ -941,52 +1009,44 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
           exact = !(dlo >= oldA);
         }
         if (use16) {
-          // the few points the prefilter could not settle: float64 distance from
-          // the global rows, four points at a time, eight lanes per point on
-          // strided factors (coalesced segments, every load of a round in flight)
+          // the few points the prefilter could not settle: float64 distance in
+          // factor order (the arithmetic of pass 0, so a duplicate of a seed
+          // gets exactly 0).  Four rows per round are staged into the free
+          // upper part of the slice buffer by 8-lane groups (coalesced), then
+          // each owner lane adds its row sequentially.
           unsigned em = __ballot_sync(0xffffffffu, exact);
+          unsigned char* scratch = sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + 32 * row16;
           const int sl = lane & 7, grp = lane >> 3;
           while (em) {
             int mine = -1;
             for (int g = 0; g < 4 && em; ++g) {
-              const int b = __ffs(em) - 1;
+              const int bsel = __ffs(em) - 1;
               em &= em - 1;
-              if (g == grp) mine = b;
+              if (g == grp) mine = bsel;
             }
-            double dot = 0.0;
+            P* slot = reinterpret_cast<P*>(scratch) + grp * f;
             if (mine >= 0) {
               const P* x = points + (chA * 32 + mine) * f;
-              for (int k0 = 0; k0 < f; k0 += 64) {
-                P xv[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const int k = k0 + sl + 8 * i;
-                  xv[i] = k < f ? x[k] : P(0);
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const int k = k0 + sl + 8 * i;
-                  if (k < f) dot = fma((double)xv[i], cen[k], dot);
-                }
+              for (int q = sl; q < f; q += 8) slot[q] = x[q];
+            }
+            __syncwarp();
+            int myslot = -1;  // which group staged this lane's point
+            for (int g = 0; g < 4; ++g)
+              if (__shfl_sync(0xffffffffu, mine, g * 8) == lane) myslot = g;
+            if (myslot >= 0) {
+              const P* x = reinterpret_cast<const P*>(scratch) + myslot * f;
+              double dot = 0.0;
+#pragma unroll 5
+              for (int q = 0; q < f; ++q) dot = fma((double)x[q], cen[q], dot);
+              double d = (mp2A + cc) - 2.0 * dot;
+              d = d > 0.0 ? d : 0.0;
+              if (d < oldA) {
+                a.d2[meA] = d;
+                a.near[meA] = j;
+                fin = d;
               }
             }
-            dot += __shfl_xor_sync(0xffffffffu, dot, 4);
-            dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-            dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-            // hand each group's dot to the owner lane of its point
-            for (int g = 0; g < 4; ++g) {
-              const int who = __shfl_sync(0xffffffffu, mine, g * 8);
-              const double dg = __shfl_sync(0xffffffffu, dot, g * 8);
-              if (who == lane) {
-                double d = (mp2A + cc) - 2.0 * dg;
-                d = d > 0.0 ? d : 0.0;
-                if (d < oldA) {
-                  a.d2[meA] = d;
-                  a.near[meA] = j;
-                  fin = d;
-                }
-              }
-            }
+            __syncwarp();
           }
         } else if (exact) {
           const size_t s0 = (size_t)(chA * 32) * row_bytes;  // slice start
@@ -1272,11 +1332,11 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
       a.chunk_sums = csum.p;
       a.range_sums = rsum.p;
       a.nchunks = nch;
-      // fp16 copy for the certified prefilter of passes > 0 (SIMDEX_SEED_NO_F16 disables)
+      // optional fp16 copy for a certified prefilter of passes > 0 (SIMDEX_SEED_F16)
       Scratch<__half> p16;
       Scratch<unsigned long long> mxb;
       Scratch<int> s16;
-      if (!std::getenv("SIMDEX_SEED_NO_F16")) {
+      if (std::getenv("SIMDEX_SEED_F16")) {  // measured slower than the fp32 slices once exact zeros are kept
         const int64_t n_pad = ceil_div(n, 32) * 32;
         SIMDEX_CUDA(p16.alloc((size_t)n_pad * f, s));
         SIMDEX_CUDA(mxb.alloc(1, s));
@@ -1340,12 +1400,17 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
 template <class P>
 int mean_impl(const P* points, int32_t f, const int64_t* members, const int64_t* offsets, int32_t c,
               double* centers, cudaStream_t s) {
-  const int S = std::max(1, std::min(16, (4 * sm_count() + c - 1) / c));  // CTAs per cluster
-  Scratch<double> psum;
-  SIMDEX_CUDA(psum.alloc((size_t)c * S * f, s));
+  if (f > kSeqMaxF) {
+    set_error("kmeans_update: f > %d unsupported", kSeqMaxF);
+    return SIMDEX_EUNSUPPORTED;
+  }
+  // rows staged per chunk: up to 64, two buffers within 96 KB
+  int rows = (int)((96 * 1024) / (2 * (size_t)f * sizeof(P)));
+  rows = rows > 64 ? 64 : (rows < 1 ? 1 : rows);
+  const size_t smem = 2 * (size_t)rows * f * sizeof(P);
+  SIMDEX_CUDA(cudaFuncSetAttribute(centroid_seq_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileScope _prof("centroid_mean", s);
-  centroid_mean_kernel<P><<<(unsigned)(c * S), kMeanWarps * 32, 0, s>>>(points, f, members, offsets, S, psum.p);
-  combine_mean_kernel<<<(unsigned)ceil_div((int64_t)c * f, 256), 256, 0, s>>>(psum.p, offsets, c, S, f, centers);
+  centroid_seq_kernel<P><<<(unsigned)c, 128, smem, s>>>(points, f, members, offsets, rows, centers);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("centroid_mean");
   return SIMDEX_OK;
