@@ -299,7 +299,11 @@ def run_ours(args):
                 "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": _profiled_traffic(path, k),
                 "algorithmic_flops_per_step": flops, "launch_ms_per_step": gemm_ms,
                 "launches_per_step": kernels["gemm_topk"]["launches_per_step"], "per_unit": per_unit,
-                "share_of_step": gemm_ms / ms_per_step}
+                "share_of_step": gemm_ms / ms_per_step,
+                # BASELINE's north star states its GEMM target against a split-fp32
+                # peak (3xTF32 = dense bf16 / 6 with TF32 = bf16 / 2); the certified
+                # single-pass fp16 product needs one pass, so it can exceed that
+                "split_fp32_peak": bf16 / 6.0, "frac_vs_split_fp32_peak": achieved / (bf16 / 6.0)}
 
     # ---- e2e: public API from host buffers (run_pipeline), per step
     e2e = None
