@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const bool act = live && !flags;
               unsigned mask = 0;  // items of this chunk whose upper bound reaches T
               const float* nrm = p.item_nrm + un.b_row0 + c0;
+              const float nrm_l = __ldg(nrm + lane);  // lane i holds item i's norm (coalesced)
               float vloc[32];  // the chunk, spilled for the appends: indexed dynamically
               if (pass) {
                 if constexpr (KT == 1) {
@@ -501,11 +502,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               // converged append loop: every lane with pending items takes one per round
               while (__any_sync(0xffffffffu, mask != 0u)) {
+                const int i = mask ? __ffs(mask) - 1 : 0;
+                const float ni = __shfl_sync(0xffffffffu, nrm_l, i);  // item i's norm from lane i
                 if (mask) {
-                  const int i = __ffs(mask) - 1;
                   mask &= mask - 1;
                   const float vi = vloc[i];
-                  const float e = fmaf(cu, __ldg(nrm + i), p.e_abs);
+                  const float e = fmaf(cu, ni, p.e_abs);
                   const float hi = vi + e;
                   if (hi >= T && !flags) {  // T may have risen within this chunk
                     my_hi[cnt] = hi;
@@ -520,19 +522,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                   }
                 }
-                if constexpr (KT > 0) {
-                  // a full buffer is filtered against the current T by the whole warp
-                  unsigned full = __ballot_sync(0xffffffffu, cnt == p.cap);
-                  while (full) {
-                    const int who = __ffs(full) - 1;
-                    full &= full - 1;
-                    const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
-                    const float t_w = __shfl_sync(0xffffffffu, T, who);
-                    const int nc = warp_filter(p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, p.cap, t_w, lane);
-                    if (lane == who) {
-                      cnt = nc;
-                      if (cnt > p.cap - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
-                    }
+              }
+              if constexpr (KT > 0) {
+                // keep >= 32 free slots (a chunk appends at most 32): a nearly full
+                // buffer is filtered against the current T by the whole warp
+                unsigned full = __ballot_sync(0xffffffffu, cnt > p.cap - 32);
+                while (full) {
+                  const int who = __ffs(full) - 1;
+                  full &= full - 1;
+                  const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+                  const int c_w = __shfl_sync(0xffffffffu, cnt, who);
+                  const float t_w = __shfl_sync(0xffffffffu, T, who);
+                  const int nc = warp_filter(p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, c_w, t_w, lane);
+                  if (lane == who) {
+                    cnt = nc;
+                    if (cnt > p.cap - 32 - max(8, p.cap / 8)) flags = 1;  // band wider than the buffer
                   }
                 }
               }
@@ -755,6 +759,19 @@ __device__ int64_t ceiling_count(const double* b, int64_t n, double unorm, doubl
   return lo;
 }
 
+// a row whose candidates do not fit: prefix rows redo the full list (stage
+// 2 from T0 = -inf), other rows go to the exact float64 path
+__device__ __forceinline__ void overflow_row(const FinalizeParams& p, int64_t r, int64_t user, int64_t out) {
+  if (p.mode == kPrefix) {
+    p.row_T0_out[r] = -INFINITY;
+    p.cont_list[atomicAdd(p.cont_n, 1)] = r;
+  } else {
+    const int sl = atomicAdd(p.over_n, 1);
+    p.over_list[sl] = (p.mode == kBrute || p.mode == kAssign) ? user : r;
+    p.over_out[sl] = out;
+  }
+}
+
 // 4 rows per warp, 8 lanes per row: exact float64 rescoring of the row's
 // certified candidates, (score desc, id asc) bitonic sort, output; plus the
 // work-sharing bookkeeping of the mode.
@@ -783,16 +800,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
       out = p.row_out ? p.row_out[r] : r;
       c = (p.mode == kPrefix || p.mode == kFullList) ? p.row_cluster[r] : 0;
       if (p.row_flags[r]) {
-        if (gl == 0) {
-          if (p.mode == kPrefix) {  // band overflow on the prefix: redo it on the full list
-            p.row_T0_out[r] = -INFINITY;
-            p.cont_list[atomicAdd(p.cont_n, 1)] = r;
-          } else {
-            const int sl = atomicAdd(p.over_n, 1);
-            p.over_list[sl] = (p.mode == kBrute || p.mode == kAssign) ? user : r;
-            p.over_out[sl] = out;
-          }
-        }
+        if (gl == 0) overflow_row(p, r, user, out);
       } else {
         act = true;
         cnt = p.row_count[r];
@@ -819,10 +827,17 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     const unsigned mine = (bal & gmask) >> (grp * LPR);
     if (keep) {
       const int dst = kept + __popc(mine & ((1u << gl) - 1u));
-      const int32_t pos = cid[e];
-      si[dst] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
+      if (dst < p.pow2) {
+        const int32_t pos = cid[e];
+        si[dst] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
+      }
     }
     kept += __popc(mine);
+  }
+  if (act && kept > p.pow2) {  // more survivors than the row's shared-memory slots
+    if (gl == 0) overflow_row(p, r, user, out);
+    act = false;
+    kept = 0;
   }
   cnt = kept;
   const int cmax2 = __reduce_max_sync(0xffffffffu, cnt);
@@ -1189,7 +1204,7 @@ int kt_for(int k_eff) {
 
 int cap_for(int k_eff) {
   const int kt = kt_for(k_eff);
-  if (kt > 0) return kt <= 16 ? 64 : (kt <= 32 ? 128 : 256);  // T is exact-current: the buffer holds the band
+  if (kt > 0) return kt <= 32 ? 128 : 256;  // T exact-current: the band + 32 free slots
   int c = 4 * k_eff + 64;
   int p = 64;
   while (p < c) p <<= 1;
@@ -1401,7 +1416,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
   fp.item_perm = item_perm;
-  fp.pow2 = pow2_at_least(st.cap);
+  fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   if ((rc = launch_finalize(fp, nu, s))) return rc;
   int32_t n_over = 0;
   SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -1528,7 +1543,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.over_list = over_list.p;
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
-  fp.pow2 = pow2_at_least(st.cap);
+  fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   if ((rc = launch_finalize(fp, rows_max, s))) return rc;
   if (bp >= ni) {  // the prefix was the whole list
     record_ws_stats(nq, 0, bp, ni, f);
@@ -1718,7 +1733,7 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   fp.over_list = over_rows;
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
-  fp.pow2 = pow2_at_least(st.cap);
+  fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   fp.p2 = p2;
   fp.c2 = c2;
   fp.prev = prev;
