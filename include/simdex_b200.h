@@ -208,6 +208,9 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
  * then follows in closed form from the exact top-K (list_pos = inverse of
  * list_ids, from simdex_build_index).
  * out_visited follows the reference: n if B >= n, else max(B, walk visited).
+ * block == 0: no work sharing (query_batch(work_sharing=False)): every query
+ * takes the full-list pass and out_visited is Algorithm 1's stop position
+ * from position 0, exactly simdex_walk's; prefix_b / prefix_norm may be NULL.
  * Requires k_eff <= 256 and f <= 256 (else use simdex_walk). */
 SIMDEX_API int simdex_query_ws(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,
                     const double* items, const float* items32, const uint16_t* ib, const double* item_norms,

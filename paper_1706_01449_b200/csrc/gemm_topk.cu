@@ -1110,6 +1110,22 @@ __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t
   }
 }
 
+// no work sharing (block = 0): every live row goes straight to the full-list
+// pass with T0 = -inf (its visited is Algorithm 1's stop position from 0)
+__global__ void all_rows_continue_kernel(const int64_t* __restrict__ row_user, int64_t rows, int64_t* __restrict__ cont,
+                                         int32_t* __restrict__ cont_n, float* __restrict__ t0) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  t0[r] = -INFINITY;
+  const bool live = row_user[r] >= 0;
+  const unsigned m = __ballot_sync(__activemask(), live);
+  int base = 0;
+  const int lane = threadIdx.x & 31, leader = __ffs(__activemask()) - 1;
+  if (lane == leader && m) base = atomicAdd(cont_n, __popc(m));
+  base = __shfl_sync(__activemask(), base, leader);
+  if (live) cont[base + __popc(m & ((1u << lane) - 1u))] = r;
+}
+
 // stage 2: pack the continuing rows densely (rows past the count are zero)
 __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
                                  int64_t rows_max, const int64_t* __restrict__ row_user,
@@ -1440,7 +1456,9 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
                  double* out_scores, int64_t* out_visited, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
+  const bool no_ws = block == 0;  // every query walks the whole list (query_batch(work_sharing=False))
   const int64_t bp = block < ni ? block : ni;
+  if (no_ws) b_pad = 0;
   GemmGeometry g;
   int rc = geometry(kp, &g);
   if (rc) return rc;
@@ -1464,8 +1482,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   SIMDEX_CUDA(row_user.alloc(rows_max, s));
   SIMDEX_CUDA(row_out.alloc(rows_max, s));
   SIMDEX_CUDA(rclus.alloc(rows_max, s));
-  SIMDEX_CUDA(pnrm.alloc((size_t)c * b_pad, s));
-  SIMDEX_CUDA(pnmax.alloc((size_t)c * b_pad / 32, s));
+  SIMDEX_CUDA(pnrm.alloc((size_t)c * b_pad + 1, s));
+  SIMDEX_CUDA(pnmax.alloc((size_t)c * b_pad / 32 + 1, s));
   SIMDEX_CUDA(cont.alloc(rows_max, s));
   SIMDEX_CUDA(t0.alloc(rows_max, s));
   SIMDEX_CUDA(cont_n.alloc(1, s));
@@ -1482,6 +1500,9 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
                                                                    ucu.p, a_pk.p, cu.p, row_user.p, row_out.p,
                                                                    rclus.p);
   SIMDEX_LAUNCH_CHECK("ws_rows");
+  int grid = 0;
+  const bool stats = getenv("SIMDEX_STATS") != nullptr;
+  if (!no_ws) {
   item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
       prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm.p, pnmax.p);
   SIMDEX_LAUNCH_CHECK("item_nrm");
@@ -1489,14 +1510,13 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
   if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
   TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
-  const bool stats = getenv("SIMDEX_STATS") != nullptr;
   Scratch<int64_t> hops;
   if (stats) {
     SIMDEX_CUDA(hops.alloc(rows_max, s));
     SIMDEX_CUDA(cudaMemsetAsync(hops.p, 0, sizeof(int64_t) * rows_max, s));
     p.heap_ops = hops.p;
   }
-  int grid = (int)(units_max < sm_count() ? units_max : sm_count());
+  grid = (int)(units_max < sm_count() ? units_max : sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
   if (stats) {
     std::vector<int64_t> hh(rows_max);
@@ -1505,6 +1525,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     for (auto v : hh) tot += v;
     fprintf(stderr, "[simdex] stage1 appends per query %.2f\n", (double)tot / (double)nq);
   }
+  }  // !no_ws
 
   SIMDEX_CUDA(cudaMemsetAsync(cont_n.p, 0, sizeof(int32_t), s));
   SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
@@ -1544,8 +1565,15 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.over_out = over_out.p;
   fp.over_n = over_n.p;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
-  if ((rc = launch_finalize(fp, rows_max, s))) return rc;
-  if (bp >= ni) {  // the prefix was the whole list
+  if (no_ws) {
+    fp.prefix = 0;  // no floor: visited is the stop position from 0
+    all_rows_continue_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(row_user.p, rows_max, cont.p,
+                                                                              cont_n.p, t0.p);
+    SIMDEX_LAUNCH_CHECK("all_rows_continue");
+  } else if ((rc = launch_finalize(fp, rows_max, s))) {
+    return rc;
+  }
+  if (!no_ws && bp >= ni) {  // the prefix was the whole list
     record_ws_stats(nq, 0, bp, ni, f);
     return SIMDEX_OK;
   }

@@ -127,11 +127,13 @@ extern "C" int simdex_query_ws(const double* users, const float* users32, const 
                                const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
                                int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
   SIMDEX_CHECK_ARG(users && ub && user_norms && items && ib && item_norms && list_ids && list_pos && bounds &&
-                       prefix_b && prefix_norm && q_user && q_off && out_ids && out_scores && out_visited,
+                       (block == 0 || (prefix_b && prefix_norm)) && q_user && q_off && out_ids && out_scores &&
+                       out_visited,
                    "simdex_query_ws: null pointer");
-  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 1 && c >= 1 && kp % 64 == 0 && kp >= f,
+  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 0 && c >= 1 && kp % 64 == 0 && kp >= f,
                    "simdex_query_ws: bad sizes");
-  SIMDEX_CHECK_ARG(b_pad % 128 == 0 && b_pad >= (block < ni ? block : ni), "simdex_query_ws: bad prefix padding");
+  SIMDEX_CHECK_ARG(block == 0 || (b_pad % 128 == 0 && b_pad >= (block < ni ? block : ni)),
+                   "simdex_query_ws: bad prefix padding");
   const int64_t k_eff = k < ni ? k : ni;
   SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
                    "simdex_query_ws: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);

@@ -277,16 +277,19 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
         if q_users is None:
             q_users = index._dev["all_users"] = torch.arange(model.num_users, dtype=torch.int64, device=users.device)
     pu, pi = _device.packed(model.users), _device.packed_sorted(model.items)
-    if work_sharing and min(k, n) <= 256 and pu.kp <= 256:
+    if min(k, n) <= 256 and pu.kp <= 256:
+        # tensor-core path; without work sharing every query takes the full-list
+        # pass (block 0) and visited is Algorithm 1's stop position, exactly the walk's
         key = ("grouped", q_users.data_ptr(), q_users.shape[0])
         grouped = index._dev.get(key) if q_users is index._dev.get("all_users") else None
         if grouped is None:
             grouped = _ops.group_queries(q_users, index.device_assignment(), index.num_clusters)
             if q_users is index._dev.get("all_users"):
                 index._dev[key] = grouped
-        return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, index.block_size,
-                             index.device_prefix(model), grouped, k, items32=_device.f32_exact(model.items),
-                             users32=_device.f32_exact(model.users))
+        block = index.block_size if work_sharing else 0
+        prefix = index.device_prefix(model) if work_sharing else (None, None, 0)
+        return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
+                             items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users))
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
     out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
     if work_sharing:  # k beyond the tensor-core envelope: WS visited = n if B >= n else max(B, walk visited)
