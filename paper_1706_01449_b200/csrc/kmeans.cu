@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128) centroid_seq_kernel(const P* __restrict__
                                                            double* __restrict__ centers) {
   extern __shared__ __align__(16) unsigned char seq_raw[];
   P* buf = reinterpret_cast<P*>(seq_raw);  // [2][kSeqRows * f]
-  __shared__ int64_t ids[128];             // member ids of the chunk being staged
+  __shared__ int64_t ids[256];             // member ids of the chunk being staged
   const int cl = blockIdx.x, t = threadIdx.x;
   const int64_t b = offsets[cl], e = offsets[cl + 1];
   if (e == b) return;
@@ -250,16 +250,24 @@ __global__ void __launch_bounds__(128) centroid_seq_kernel(const P* __restrict__
   // element with no load on its address path
   auto stage = [&](int64_t ch, int slot) {
     const int rows = rows_of(ch);
-    if (t < rows) ids[t] = members[b + ch * kSeqRows + t];
+    for (int i = t; i < rows; i += blockDim.x) ids[i] = members[b + ch * kSeqRows + i];
     __syncthreads();
     P* dst = buf + (size_t)slot * kSeqRows * f;
-    for (int idx = t; idx < rows * f; idx += blockDim.x) {
-      const int r = idx / f, q = idx - r * f;
-      const P* src = points + ids[r] * f + q;
-      if constexpr (sizeof(P) == 8)
-        sm100::cp_async8(dst + idx, src);
-      else
-        sm100::cp_async4(dst + idx, src);
+    // warp per row, lanes across 8-byte pieces (two floats when f is even)
+    const int lane = t & 31, nw = blockDim.x >> 5;
+    const bool pairs = sizeof(P) == 4 && (f & 1) == 0;
+    const int pieces = pairs ? f >> 1 : f;
+    for (int r = t >> 5; r < rows; r += nw) {
+      const P* src = points + ids[r] * f;
+      P* d = dst + (size_t)r * f;
+      for (int q = lane; q < pieces; q += 32) {
+        if (pairs)
+          sm100::cp_async8(d + 2 * q, src + 2 * q);
+        else if constexpr (sizeof(P) == 8)
+          sm100::cp_async8(d + q, src + q);
+        else
+          sm100::cp_async4(d + q, src + q);
+      }
     }
     sm100::cp_async_commit();
     __syncthreads();  // ids may be overwritten by the next stage
@@ -1404,9 +1412,9 @@ int mean_impl(const P* points, int32_t f, const int64_t* members, const int64_t*
     set_error("kmeans_update: f > %d unsupported", kSeqMaxF);
     return SIMDEX_EUNSUPPORTED;
   }
-  // rows staged per chunk: up to 64, two buffers within 96 KB
-  int rows = (int)((96 * 1024) / (2 * (size_t)f * sizeof(P)));
-  rows = rows > 64 ? 64 : (rows < 1 ? 1 : rows);
+  // rows staged per chunk: up to 256, two buffers within 110 KB (two CTAs per SM)
+  int rows = (int)((110 * 1024) / (2 * (size_t)f * sizeof(P)));
+  rows = rows > 256 ? 256 : (rows < 1 ? 1 : rows);
   const size_t smem = 2 * (size_t)rows * f * sizeof(P);
   SIMDEX_CUDA(cudaFuncSetAttribute(centroid_seq_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileScope _prof("centroid_mean", s);
