@@ -92,7 +92,6 @@ struct TopkParams {
   int64_t* heap_ops;
   float* debug_out;
   int64_t debug_ld;
-  int skip_epi;  // timing experiments only: drain TMEM without filtering
 };
 
 // three-input max (sm_100 FMNMX3)
@@ -100,60 +99,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
-}
-
-__device__ __forceinline__ void swapf(float& a, float& b) {
-  float t = a;
-  a = b;
-  b = t;
-}
-
-// k-th largest (1-based) of a[0..n): three-way quickselect, a is permuted.
-__device__ __noinline__ float kth_largest(float* a, int n, int k) {
-  int lo = 0, hi = n - 1;
-  const int want = k - 1;
-  while (lo < hi) {
-    const float pv = a[(lo + hi) >> 1];
-    int lt = lo, i = lo, gt = hi;
-    while (i <= gt) {
-      if (a[i] > pv) {
-        swapf(a[lt], a[i]);
-        ++lt;
-        ++i;
-      } else if (a[i] < pv) {
-        swapf(a[i], a[gt]);
-        --gt;
-      } else {
-        ++i;
-      }
-    }
-    if (want < lt)
-      hi = lt - 1;
-    else if (want > gt)
-      lo = gt + 1;
-    else
-      return pv;
-  }
-  return a[lo];
-}
-
-// k > 32: raise T to the k-th largest lower bound in the buffer, drop entries
-// whose upper bound falls below it.
-__device__ __noinline__ void compact_select(float* lo, float* hi, int32_t* id, int& cnt, float& T, int k_eff) {
-  float tmp[kMaxCap];
-  for (int e = 0; e < cnt; ++e) tmp[e] = lo[e];
-  const float kth = kth_largest(tmp, cnt, k_eff);
-  if (kth > T) T = kth;
-  int w = 0;
-  for (int e = 0; e < cnt; ++e) {
-    if (hi[e] >= T) {
-      lo[w] = lo[e];
-      hi[w] = hi[e];
-      id[w] = id[e];
-      ++w;
-    }
-  }
-  cnt = w;
 }
 
 // k > 32, warp-cooperative: the 32 lanes jointly re-select lane `who`'s
@@ -214,19 +159,6 @@ __device__ __noinline__ void warp_compact(float* lo, float* hi, int32_t* id, int
   }
   *cnt_out = w;
   *T_out = T;
-}
-
-// k <= 32: drop entries whose upper bound is below the (current) T.
-__device__ __noinline__ void compact_filter(float* hi, int32_t* id, int& cnt, float T) {
-  int w = 0;
-  for (int e = 0; e < cnt; ++e) {
-    if (hi[e] >= T) {
-      hi[w] = hi[e];
-      id[w] = id[e];
-      ++w;
-    }
-  }
-  cnt = w;
 }
 
 // k <= 64, warp-cooperative: drop lane `who`'s buffer entries whose upper
@@ -421,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(t_full + buf, use & 1);
         tc_fence_after();
         bool released = false;
-        if (h < ntile_a && p.skip_epi != 5) {
+        if (h < ntile_a) {
           const int tile_valid = min(kTileN, un.n_items - t * kTileN);
           // two chunks of 32 columns per TMEM wait; once the whole tile is in
           // registers the accumulator buffer goes back to the MMA warp
@@ -440,7 +372,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == 0) mbar_arrive(t_empty + buf);
               released = true;
             }
-            if (p.skip_epi == 1) continue;
 #pragma unroll
             for (int c = 0; c < LDC; ++c) {
               const int ch = cg + c;
@@ -471,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float nmax = ch == 0 ? nm4.x : ch == 1 ? nm4.y : ch == 2 ? nm4.z : nm4.w;
               const float em = fmaf(cu, nmax, p.e_abs);  // the chunk's widest band
               // rows that cannot take candidates (padding, overflowed) never pass
-              const bool pass = p.skip_epi != 2 && mx + em >= ((live && !flags) ? T : INFINITY);
+              const bool pass = mx + em >= ((live && !flags) ? T : INFINITY);
               // fast path: one vote per chunk; everything below is the rare, warp-uniform slow path
               if (!__any_sync(0xffffffffu, pass)) continue;
               const bool act = live && !flags;
@@ -494,7 +425,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 31; i >= 0; --i) neg = __funnelshift_l(__float_as_uint(v[i] - Tc), neg, 1);
                 mask = ~neg;
                 if (nvalid < 32) mask &= (1u << nvalid) - 1u;  // -inf padding must not pass a -inf T
-                if (p.skip_epi == 3) mask = 0;
                 if (mask) {
 #pragma unroll
                   for (int i = 0; i < 32; ++i) vloc[i] = v[i];
@@ -1330,7 +1260,6 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   p.stages = g.stages;
   p.cap = st.cap;
   p.k_eff = k_eff;
-  p.skip_epi = std::getenv("SIMDEX_SKIP_EPI") ? std::atoi(std::getenv("SIMDEX_SKIP_EPI")) : 0;
   p.cand_id = st.cid.p;
   p.cand_lo = st.lo.p;
   p.cand_hi = st.hi.p;

@@ -16,8 +16,6 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include <cuda_fp16.h>
-
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -713,8 +711,6 @@ struct SeedArgs {
   int32_t* degenerate;
   unsigned* barrier;
   unsigned long long* dbg;  // optional phase timers (ns): update, barrier 1, pick, barrier 2
-  const __half* p16;        // compact fp16 copy of the points x 2^s16, rows padded to 32 (null: off)
-  const int* s16;           // its scale exponent (device scalar)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -769,7 +765,7 @@ __device__ __forceinline__ double cta_scan(double x, double* wsum, double* total
 // seed-seed distances and seed norms, per-warp double-buffered row staging
 struct PSeedSmem {
   int kc;  // cached seeds (0: read cd2 / seed_c2 from global)
-  size_t buf, cen_off, cen32_off, cdc_off, scc_off, bar_off, buf_off, total;
+  size_t buf, cen_off, cdc_off, scc_off, bar_off, buf_off, total;
 };
 
 __host__ __device__ inline PSeedSmem pseed_smem(int f, size_t esize, int k, int wpb) {
@@ -778,8 +774,7 @@ __host__ __device__ inline PSeedSmem pseed_smem(int f, size_t esize, int k, int 
   m.buf = ((32 * row + 32) + 127) & ~size_t(127);
   m.kc = k <= 2048 ? k : 0;
   m.cen_off = 0;
-  m.cen32_off = ((size_t)f * 8 + 15) & ~size_t(15);
-  m.cdc_off = m.cen32_off + (((size_t)f * 4 + 15) & ~size_t(15));
+  m.cdc_off = ((size_t)f * 8 + 15) & ~size_t(15);
   m.scc_off = m.cdc_off + (size_t)m.kc * 8;
   m.bar_off = (m.scc_off + (size_t)m.kc * 8 + 15) & ~size_t(15);
   m.buf_off = (m.bar_off + (size_t)wpb * 2 * 8 + 127) & ~size_t(127);
@@ -869,11 +864,9 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
   const int CS = blockDim.x, wpb = CS >> 5;  // chunk = one point per thread
   const PSeedSmem L = pseed_smem(f, sizeof(P), a.k, wpb);
   double* cen = reinterpret_cast<double*>(sm_raw + L.cen_off);
-  float* cen32 = reinterpret_cast<float*>(sm_raw + L.cen32_off);
   double* cdc = reinterpret_cast<double*>(sm_raw + L.cdc_off);
   double* scc = reinterpret_cast<double*>(sm_raw + L.scc_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + L.bar_off);
-  __shared__ double s_cl1;  // L1 norm of the pass's center (fp16 prefilter bound)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (lane == 0) {
     sm100::mbar_init(bars + 2 * w, 1);
@@ -886,24 +879,8 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
   const int64_t G = gridDim.x;
   uint32_t phbits = 0;  // mbarrier phase per staging buffer
   unsigned gen = 0;
-  const bool pre16 = a.p16 != nullptr;
-  const size_t row16 = (size_t)f * 2;
-  const double inv16 = pre16 ? ldexp(1.0, -*a.s16) : 0.0;
-  // prefilter bound: |p.c - fp16 dot| <= (p2 + c2) e16 + 2^-24 2^-s16 |c|_1
-  const double e16 = 0x1p-11 + (double)(f + 4) * 0x1p-24;
-  auto load_center = [&]() {  // cen (from global rows written this pass) -> fp32 copy + L1 norm
-    for (int q = t; q < f; q += CS) cen32[q] = (float)cen[q];
-    __syncthreads();
-    if (t == 0) {
-      double l1 = 0.0;
-      for (int q = 0; q < f; ++q) l1 += fabs(cen[q]);
-      s_cl1 = l1;
-    }
-    __syncthreads();
-  };
   for (int q = t; q < f; q += CS) cen[q] = __ldcg(a.centers + q);
   __syncthreads();
-  load_center();
   unsigned long long tm0 = 0, tm1 = 0, wait1 = 0;
   const bool timing = a.dbg && blockIdx.x == 0 && t == 0;
   for (int j = 0; j + 1 < a.k; ++j) {
@@ -947,26 +924,16 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       return !(cda >= 4.0 * (old + eta) * (1.0 + 0x1p-30));
     };
     // stage the warp's 32 rows with one bulk copy when any of them is needed
-    // (per-row copies of only the needed rows measured slower: TMA issue
-    // rate); returns false when the rows are read from global instead
-    // passes after the first stage the fp16 rows (half the bytes; rows padded
-    // to 32 so a slice is always whole and 16-byte aligned)
-    const bool use16 = pre16 && j > 0;
+    // (per-row copies of only the needed rows, by TMA or cp.async, measured
+    // slower: issue rate); returns false when the rows are read from global
     auto issue = [&](int64_t ch, unsigned mask, int bsel) -> bool {
       if (!mask) return false;
       const int64_t u0 = ch * 32;
-      const unsigned char* src;
-      size_t sz;
-      if (use16) {
-        src = reinterpret_cast<const unsigned char*>(a.p16) + (size_t)u0 * row16;
-        sz = 32 * row16;
-      } else {
-        const int64_t u1 = (u0 + 32) < n ? (u0 + 32) : n;
-        const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
-        sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
-        if (a0 + sz > total_bytes) return false;  // buffer tail: read from global
-        src = gbase + a0;
-      }
+      const int64_t u1 = (u0 + 32) < n ? (u0 + 32) : n;
+      const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
+      const size_t sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
+      if (a0 + sz > total_bytes) return false;  // buffer tail: read from global
+      const unsigned char* src = gbase + a0;
       __syncwarp();
       if (lane == 0) {
         sm100::fence_proxy_async_smem();
@@ -1002,61 +969,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
           sm100::mbar_wait(bars + 2 * w + bA, (phbits >> bA) & 1u);
           phbits ^= 1u << bA;
         }
-        bool exact = needA;
-        if (needA && use16) {
-          // certified fp16 prefilter: skip when even the smallest distance the
-          // fp16 dot allows cannot go below d2 (the float64 result would keep d2)
-          const __half* x16 = reinterpret_cast<const __half*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf +
-                                                              (size_t)lane * row16);
-          float acc = 0.f;
-#pragma unroll 5
-          for (int q = 0; q < f; ++q) acc = fmaf(__half2float(x16[q]), cen32[q], acc);
-          const double ps = mp2A + cc;
-          const double eb = ps * e16 + 0x1p-24 * inv16 * s_cl1 * 1.01;
-          const double dlo = ps - 2.0 * ((double)acc * inv16 + eb) - 0x1p-40 * ps;
-          exact = !(dlo >= oldA);
-        }
-        if (use16) {
-          // the few points the prefilter could not settle: float64 distance in
-          // factor order (the arithmetic of pass 0, so a duplicate of a seed
-          // gets exactly 0).  Four rows per round are staged into the free
-          // upper part of the slice buffer by 8-lane groups (coalesced), then
-          // each owner lane adds its row sequentially.
-          unsigned em = __ballot_sync(0xffffffffu, exact);
-          unsigned char* scratch = sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + 32 * row16;
-          const int sl = lane & 7, grp = lane >> 3;
-          while (em) {
-            int mine = -1;
-            for (int g = 0; g < 4 && em; ++g) {
-              const int bsel = __ffs(em) - 1;
-              em &= em - 1;
-              if (g == grp) mine = bsel;
-            }
-            P* slot = reinterpret_cast<P*>(scratch) + grp * f;
-            if (mine >= 0) {
-              const P* x = points + (chA * 32 + mine) * f;
-              for (int q = sl; q < f; q += 8) slot[q] = x[q];
-            }
-            __syncwarp();
-            int myslot = -1;  // which group staged this lane's point
-            for (int g = 0; g < 4; ++g)
-              if (__shfl_sync(0xffffffffu, mine, g * 8) == lane) myslot = g;
-            if (myslot >= 0) {
-              const P* x = reinterpret_cast<const P*>(scratch) + myslot * f;
-              double dot = 0.0;
-#pragma unroll 5
-              for (int q = 0; q < f; ++q) dot = fma((double)x[q], cen[q], dot);
-              double d = (mp2A + cc) - 2.0 * dot;
-              d = d > 0.0 ? d : 0.0;
-              if (d < oldA) {
-                a.d2[meA] = d;
-                a.near[meA] = j;
-                fin = d;
-              }
-            }
-            __syncwarp();
-          }
-        } else if (exact) {
+        if (needA) {  // scored in factor order: a duplicate of a seed gets exactly D^2 = 0
           const size_t s0 = (size_t)(chA * 32) * row_bytes;  // slice start
           const P* x = sA ? reinterpret_cast<const P*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + (s0 & 15) +
                                                        (size_t)lane * row_bytes)
@@ -1155,7 +1068,6 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       a.seed_c2[j + 1] = a.p2[p];
     }
     __syncthreads();
-    load_center();
     // squared distances new seed -> seeds 0..j, one warp per seed across the grid
     for (int64_t q = (int64_t)blockIdx.x * wpb + w; q <= j; q += G * wpb) {
       const double* cq = a.centers + q * f;
@@ -1179,29 +1091,6 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     atomicAdd(a.dbg + 4, wait1);
     atomicMin(a.dbg + 5, wait1);
   }
-}
-
-// compact fp16 copy of the points scaled by 2^s (max |x| 2^s in [1, 2)),
-// rows padded with zeros to a multiple of 32; s from the device max
-template <class P>
-__global__ void pack16_compact_kernel(const P* __restrict__ x, int64_t n, int f, int64_t n_pad,
-                                      const unsigned long long* __restrict__ maxbits, __half* __restrict__ out,
-                                      int* __restrict__ s_out) {
-  const double m = __longlong_as_double((long long)*maxbits);
-  const int sc = m > 0.0 ? -ilogb(m) : 0;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) *s_out = sc;
-  if (i >= n_pad * f) return;
-  out[i] = __double2half(i < n * f ? ldexp((double)x[i], sc) : 0.0);
-}
-
-template <class P>
-__global__ void max_abs_pts_kernel(const P* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
-  double m = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = fmax(m, fabs((double)x[i]));
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
 template <class P>
@@ -1340,24 +1229,6 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
       a.chunk_sums = csum.p;
       a.range_sums = rsum.p;
       a.nchunks = nch;
-      // optional fp16 copy for a certified prefilter of passes > 0 (SIMDEX_SEED_F16)
-      Scratch<__half> p16;
-      Scratch<unsigned long long> mxb;
-      Scratch<int> s16;
-      if (std::getenv("SIMDEX_SEED_F16")) {  // measured slower than the fp32 slices once exact zeros are kept
-        const int64_t n_pad = ceil_div(n, 32) * 32;
-        SIMDEX_CUDA(p16.alloc((size_t)n_pad * f, s));
-        SIMDEX_CUDA(mxb.alloc(1, s));
-        SIMDEX_CUDA(s16.alloc(1, s));
-        SIMDEX_CUDA(cudaMemsetAsync(mxb.p, 0, sizeof(unsigned long long), s));
-        max_abs_pts_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(n * f, 256), 4 * 148), 256, 0, s>>>(
-            points, n * f, mxb.p);
-        pack16_compact_kernel<P><<<(unsigned)ceil_div(n_pad * f, 256), 256, 0, s>>>(points, n, f, n_pad, mxb.p,
-                                                                                     p16.p, s16.p);
-        SIMDEX_LAUNCH_CHECK("pack16_compact");
-        a.p16 = p16.p;
-        a.s16 = s16.p;
-      }
       a.degenerate = out_deg;
       a.barrier = bar.p;
       Scratch<unsigned long long> dbg;
