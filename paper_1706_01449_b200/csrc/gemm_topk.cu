@@ -1507,12 +1507,16 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     return SIMDEX_OK;
   }
 
-  // ---- stage 2: continuing users x the whole catalogue
-  int32_t n_cont = 0;
-  SIMDEX_CUDA(cudaMemcpyAsync(&n_cont, cont_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  SIMDEX_CUDA(cudaStreamSynchronize(s));
-  record_ws_stats(nq, n_cont, bp, ni, f);
-  if (getenv("SIMDEX_STATS")) {
+  // ---- stage 2: continuing users x the whole catalogue.  No host round
+  // trip: buffers are sized for every row, the row and unit counts are read
+  // on the device; the count reaches the host with the final synchronisation.
+  static thread_local int32_t* n_cont_host = nullptr;
+  if (!n_cont_host) SIMDEX_CUDA(cudaMallocHost(&n_cont_host, sizeof(int32_t)));
+  SIMDEX_CUDA(cudaMemcpyAsync(n_cont_host, cont_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  int32_t n_cont = -1;
+  if (stats) {
+    SIMDEX_CUDA(cudaStreamSynchronize(s));
+    n_cont = *n_cont_host;
     std::vector<int32_t> hc(rows_max);
     SIMDEX_CUDA(cudaMemcpy(hc.data(), st.cnt.p, sizeof(int32_t) * rows_max, cudaMemcpyDeviceToHost));
     std::vector<int64_t> hu(rows_max);
@@ -1531,8 +1535,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
             (long long)nq, n_cont, live ? (double)tot / live : 0.0, (long long)mx, (long long)hist[0],
             (long long)hist[1], (long long)hist[2], (long long)hist[3]);
   }
-  if (n_cont == 0) return SIMDEX_OK;
-  const int64_t rows2 = ceil_div(n_cont, kUnitRows) * kUnitRows;
+  const int64_t rows2 = ceil_div(nq, kUnitRows) * kUnitRows;  // bound on the continuing rows
   const int64_t units2 = rows2 / kUnitRows;
   SIMDEX_CUDA(a2.alloc((size_t)rows2 * kp, s));
   SIMDEX_CUDA(cu2.alloc(rows2, s));
@@ -1570,12 +1573,12 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     SIMDEX_CUDA(cudaMemcpy(hh.data(), hops2.p, sizeof(int64_t) * rows2, cudaMemcpyDeviceToHost));
     int64_t tot = 0;
     for (auto v : hh) tot += v;
-    fprintf(stderr, "[simdex] stage2 appends per continuing query %.2f\n", (double)tot / (double)n_cont);
+    fprintf(stderr, "[simdex] stage2 appends per continuing query %.2f\n", (double)tot / (double)(n_cont > 0 ? n_cont : 1));
   }
   FinalizeParams f2 = fp;
   f2.mode = kFullList;
   f2.total_rows = rows2;
-  f2.n_rows_dev = nullptr;
+  f2.n_rows_dev = cont_n.p;
   f2.row_user = user2.p;
   f2.row_out = out2.p;
   f2.row_cluster = clus2.p;
@@ -1586,6 +1589,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   int32_t n_over = 0;
   SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   SIMDEX_CUDA(cudaStreamSynchronize(s));
+  record_ws_stats(nq, *n_cont_host, bp, ni, f);
   if (n_over == 0) return SIMDEX_OK;
   // band overflow on the full list: exact float64 scan for those users, same visited closed form
   SIMDEX_CUDA(fb_users.alloc(n_over, s));
