@@ -887,23 +887,36 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     p.out_ids[out * p.k_eff + i] = i < held ? si[i] : -1;
     p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
   }
-  if (p.mode == kPrefix && gl == 0) {
+  if (p.mode == kPrefix) {
     // index.py:372-387: the prefix covers the list -> n; the K-th beats the
     // ceiling at B -> B; otherwise the user continues past B.
-    if (p.prefix >= p.n) {
-      p.out_visited[out] = p.n;
-    } else if (held == p.k_eff && ss[p.k_eff - 1] > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
-      p.out_visited[out] = p.prefix;
-    } else {
-      // the prefix's exact K-th score lower-bounds the catalogue's: start the
-      // full-list pass from it (rounded down, with a 2^-40 relative guard)
-      float t0 = -INFINITY;
-      if (held == p.k_eff) {
-        const double sk = ss[p.k_eff - 1] * p.t0_scale;
-        t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
+    bool cont = false;
+    if (gl == 0) {
+      if (p.prefix >= p.n) {
+        p.out_visited[out] = p.n;
+      } else if (held == p.k_eff && ss[p.k_eff - 1] > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
+        p.out_visited[out] = p.prefix;
+      } else {
+        // the prefix's exact K-th score lower-bounds the catalogue's: start the
+        // full-list pass from it (rounded down, with a 2^-40 relative guard)
+        float t0 = -INFINITY;
+        if (held == p.k_eff) {
+          const double sk = ss[p.k_eff - 1] * p.t0_scale;
+          t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
+        }
+        p.row_T0_out[r] = t0;
+        cont = true;
       }
-      p.row_T0_out[r] = t0;
-      p.cont_list[atomicAdd(p.cont_n, 1)] = r;
+    }
+    // one atomic per warp for the continuation list (not one per row)
+    const unsigned am = __activemask();
+    const unsigned cm = __ballot_sync(am, cont);
+    if (cm) {
+      const int leader = __ffs(cm) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(p.cont_n, __popc(cm));
+      base = __shfl_sync(am, base, leader);
+      if (cont) p.cont_list[base + __popc(cm & ((1u << lane) - 1u))] = r;
     }
   }
   if (p.mode == kFullList) {
