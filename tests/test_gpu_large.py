@@ -1,0 +1,82 @@
+"""BASELINE configurations at full size on the GPU, checked against an exact
+float64 top-K of a uniform user subsample (the reference's own
+_subsample_oracle_matches pattern, tests/test_acceptance.py:258-264): cfg3
+(brute force, the optimizer's low-similarity case), cfg4 (index + work
+sharing at the R2 shape, C=1024) and cfg5 (1M x 1M, f=128, K=100)."""
+
+import numpy as np
+import pytest
+
+from conftest import near_tie_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1706_01449_b200 as pkg
+    return pkg
+
+
+def _exact_topk(users, items, k, extra=1):
+    """Exact top-(k+extra) under (score desc, id asc), float64 GEMM in chunks;
+    the extra column exposes near ties at the k-th position."""
+    kk = min(k + extra, items.shape[0])
+    ids = np.empty((users.shape[0], kk), dtype=np.int64)
+    sc = np.empty((users.shape[0], kk))
+    for a in range(0, users.shape[0], 64):
+        s = users[a:a + 64] @ items.T
+        part = np.argpartition(-s, kk - 1, axis=1)[:, :kk]
+        kth = np.take_along_axis(s, part, axis=1).min(axis=1)
+        for r in range(s.shape[0]):
+            cand = np.flatnonzero(s[r] >= kth[r])          # everything tied with the k-th too
+            order = np.lexsort((cand, -s[r, cand]))[:kk]   # score desc, id asc
+            ids[a + r] = cand[order]
+            sc[a + r] = s[r, cand[order]]
+    return ids, sc
+
+
+def _check(res_ids, res_scores, users, items, k, sample, ctx):
+    want_ids, want_sc = _exact_topk(users[sample], items, k)
+    got_ids = np.asarray(res_ids)[sample]
+    got_sc = np.asarray(res_scores)[sample]
+    k_eff = got_ids.shape[1]
+    np.testing.assert_allclose(got_sc, want_sc[:, :k_eff], rtol=1e-9, atol=1e-9, err_msg=ctx)
+    ties = near_tie_rows(want_sc, k_eff)
+    bad = np.flatnonzero((got_ids != want_ids[:, :k_eff]).any(axis=1) & ~ties)
+    assert bad.size == 0, f"{ctx}: {bad.size} rows differ, first {sample[bad[0]]}"
+
+
+def test_cfg3_brute_force_full_size(sx):
+    from paper_1706_01449_b200 import workloads as W
+    w = W.cfg3()
+    m = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
+    res = sx.topk_matmul(m, 10)
+    sample = np.sort(np.random.default_rng(0).choice(m.num_users, 2000, replace=False))
+    _check(res.item_ids, res.scores, m.users.values, m.items.values, 10, sample, "cfg3 K=10")
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_cfg4_index_work_sharing_full_size(sx, k):
+    from paper_1706_01449_b200 import workloads as W
+    w = W.cfg4()
+    m = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
+    cl = sx.kmeans(m.users, 1024, max_iters=3, seed=3)
+    idx = sx.build_index(m, cl, 4096)
+    res = sx.query_batch(idx, m, None, k, work_sharing=True)
+    sample = np.sort(np.random.default_rng(1).choice(m.num_users, 2000, replace=False))
+    _check(res.item_ids, res.scores, m.users.values, m.items.values, k, sample, f"cfg4 K={k}")
+    vis = np.asarray(res.visited)
+    assert (vis >= 4096).all() and (vis <= m.num_items).all()
+
+
+def test_cfg5_catalogue_scale_full_size(sx):
+    from paper_1706_01449_b200 import workloads as W
+    w = W.cfg5()
+    m = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
+    res = sx.topk_matmul(m, 100)
+    sample = np.sort(np.random.default_rng(2).choice(m.num_users, 256, replace=False))
+    _check(res.item_ids, res.scores, m.users.values, m.items.values, 100, sample, "cfg5 K=100")
