@@ -739,27 +739,6 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
   __syncthreads();
 }
 
-// inclusive scan of one double per thread over a 256-thread CTA (warp
-// shuffles + warp totals); returns the inclusive prefix, *total the CTA sum
-// inclusive scan of one double per thread over the CTA (warp shuffles +
-// warp totals in fixed order); *total = the CTA sum
-__device__ __forceinline__ double cta_scan(double x, double* wsum, double* total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[w] = x;
-  __syncthreads();
-  double pre = 0.0, tot = 0.0;
-  for (int q = 0; q < nw; ++q) {
-    if (q < w) pre += wsum[q];
-    tot += wsum[q];
-  }
-  *total = tot;
-  __syncthreads();
-  return pre + x;
-}
 
 // dynamic shared layout of seed_persistent_kernel: new-seed center, cached
 // seed-seed distances and seed norms, per-warp double-buffered row staging
@@ -782,41 +761,86 @@ __host__ __device__ inline PSeedSmem pseed_smem(int f, size_t esize, int k, int 
   return m;
 }
 
+// inclusive scan of one double per thread over the CTA (warp shuffles +
+// warp totals in fixed order); *total = the CTA sum
+__device__ __forceinline__ double cta_scan(double x, double* wsum, double* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  double pre = 0.0, tot = 0.0;
+  for (int q = 0; q < nw; ++q) {
+    if (q < w) pre += wsum[q];
+    tot += wsum[q];
+  }
+  *total = tot;
+  return pre + x;
+}
+
 // First index i in [0, m) whose cumulative sum base + v[0] + ... + v[i]
-// exceeds target (numpy's searchsorted(cumsum, target, 'right')), scanned by
-// the whole CTA: contiguous per-thread runs (loads batched), a CTA scan, and
-// the crossing run walked by its owner.  If rounding puts the target beyond
-// the total, the last positive entry is taken.  Returns the index and the sum
-// before it in *before (every thread gets the same values).
+// exceeds the target (numpy's searchsorted(cumsum, target, 'right')), scanned
+// by the whole CTA: contiguous per-thread runs (held in registers when a run
+// is at most 8 long, so every value is loaded once), a CTA scan, and the
+// crossing run walked by its owner.  scale: the target is target * (total of
+// v), so the top level scales its uniform by the total it has just summed.
+// If rounding puts the target beyond the total, the last positive entry is
+// taken.  Returns the index, the sum before it in *before and the total in
+// *total (every thread gets the same values).  sh: 8 + 2 doubles of scratch.
 template <class Get>
-__device__ int64_t cta_crossing(Get get, int64_t m, double base, double target, double* wsum, double* s_val,
-                                int64_t* s_idx, double* before) {
+__device__ int64_t cta_crossing(Get get, int64_t m, double base, double target, bool scale, double* before,
+                                double* total, double* sh) {
   const int t = threadIdx.x, CS = blockDim.x;
+  double* wsum = sh;
+  double* s_val = sh + 8;
+  int64_t* s_idx = reinterpret_cast<int64_t*>(sh + 9);
   const int64_t per = (m + CS - 1) / CS;
   const int64_t c0 = t * per < m ? t * per : m, c1 = (c0 + per) < m ? (c0 + per) : m;
+  const bool cached = per <= 8;
+  double vv[8];
   double mine = 0.0;
-  for (int64_t b = c0; b < c1; b += 8) {
-    double vv[8];
+  if (cached) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) vv[i] = b + i < c1 ? get(b + i) : 0.0;
+    for (int i = 0; i < 8; ++i) vv[i] = c0 + i < c1 ? get(c0 + i) : 0.0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) mine += vv[i];
+  } else {
+    for (int64_t b = c0; b < c1; b += 8) {
+      double uu[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) uu[i] = b + i < c1 ? get(b + i) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mine += uu[i];
+    }
   }
-  double total;
-  const double incl = base + cta_scan(mine, wsum, &total);
   if (t == 0) *s_idx = -1;
-  __syncthreads();
+  const double incl = base + cta_scan(mine, wsum, total);  // its barrier orders the s_idx reset
+  if (scale) target *= *total;
   const double excl = incl - mine;
   if (c0 < c1 && incl > target && !(excl > target)) {
     double acc = excl;
     int64_t c = c1;
-    for (int64_t q = c0; q < c1; ++q) {
-      const double v = get(q);
-      if (v > 0.0 && acc + v > target) {
-        c = q;
-        break;
+    if (cached) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c == c1 && c0 + i < c1) {
+          if (vv[i] > 0.0 && acc + vv[i] > target)
+            c = c0 + i;
+          else
+            acc += vv[i];
+        }
+    } else {
+      for (int64_t q = c0; q < c1; ++q) {
+        const double v = get(q);
+        if (v > 0.0 && acc + v > target) {
+          c = q;
+          break;
+        }
+        acc += v;
       }
-      acc += v;
     }
     if (c == c1) {  // rounding between the summation orders: last positive entry of the run
       c = c1 - 1;
@@ -828,37 +852,35 @@ __device__ int64_t cta_crossing(Get get, int64_t m, double base, double target, 
     *s_val = acc;
   }
   __syncthreads();
-  if (*s_idx < 0 && t == 0) {
-    // rounding put the target outside this level's sums: beyond the total ->
-    // last positive entry; before the base -> first positive entry
-    int64_t c;
-    if (target < base) {
-      c = 0;
-      while (c + 1 < m && !(get(c) > 0.0)) ++c;
-    } else {
-      c = m - 1;
-      while (c > 0 && !(get(c) > 0.0)) --c;
+  if (*s_idx < 0) {
+    if (t == 0) {
+      // rounding put the target outside this level's sums: beyond the total ->
+      // last positive entry; before the base -> first positive entry
+      int64_t c;
+      if (target < base) {
+        c = 0;
+        while (c + 1 < m && !(get(c) > 0.0)) ++c;
+      } else {
+        c = m - 1;
+        while (c > 0 && !(get(c) > 0.0)) --c;
+      }
+      double acc = base;
+      for (int64_t q = 0; q < c; ++q) acc += get(q);
+      *s_idx = c;
+      *s_val = acc;
     }
-    double acc = base;
-    for (int64_t q = 0; q < c; ++q) acc += get(q);
-    *s_idx = c;
-    *s_val = acc;
+    __syncthreads();
   }
-  __syncthreads();
   const int64_t r = *s_idx;
   *before = *s_val;
-  __syncthreads();
+  __syncthreads();  // sh is reused by the next search
   return r;
 }
 
 template <class P>
-__global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restrict__ points, const SeedArgs a) {
+__global__ void __launch_bounds__(256, 2) seed_persistent_kernel(const P* __restrict__ points, const SeedArgs a) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
-  __shared__ double red[2][8];
-  __shared__ double wsum[8];
-  __shared__ double s_base;
-  __shared__ int64_t s_block;
-  __shared__ unsigned long long s_pick;
+  __shared__ double pick_sh[10];
   const int f = a.f;
   const int64_t n = a.n;
   const int CS = blockDim.x, wpb = CS >> 5;  // chunk = one point per thread
@@ -883,8 +905,11 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
   __syncthreads();
   unsigned long long tm0 = 0, tm1 = 0, wait1 = 0;
   const bool timing = a.dbg && blockIdx.x == 0 && t == 0;
+  const int64_t g0 = a.nchunks * blockIdx.x / G, g1 = a.nchunks * (blockIdx.x + 1) / G;
+  const int64_t GW = wpb, r0 = g0 + w, r1 = g1;  // this CTA's contiguous range, warps interleaved
   for (int j = 0; j + 1 < a.k; ++j) {
     if (timing) tm0 = gtimer();
+    const double u = a.uniforms[j];  // read here, used by the pick
     if (L.kc)
       for (int q = t; q <= j; q += CS) {
         scc[q] = __ldcg(a.seed_c2 + q);
@@ -895,14 +920,16 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     // 32-point slices: each CTA owns a contiguous range, its warps take the
     // slices round-robin and run their own pipelines (no CTA-wide step until
     // the range is done); the CTA then adds its range's slice sums in order
-    const int64_t g0 = a.nchunks * blockIdx.x / G, g1 = a.nchunks * (blockIdx.x + 1) / G;
-    const int64_t GW = wpb, r0 = g0 + w, r1 = g1;  // this CTA's contiguous range, warps interleaved
+    // odd passes walk the range backwards: the slices read last are read
+    // first again while they are still in L2
+    const bool rev = j & 1;
+    auto sl = [&](int64_t ch) { return rev ? g1 - 1 - (ch - g0) : ch; };
     // ------------------------------------------------------------ (U) update
     // per warp, a three-stage pipeline over this CTA's chunks: the test inputs
     // of chunk C load while chunk B's rows stream into one staging buffer and
     // chunk A (other buffer) is scored
     auto load_regs = [&](int64_t ch, double& mp2, double& old, int& an) {
-      const int64_t me = ch * 32 + lane;
+      const int64_t me = sl(ch) * 32 + lane;
       mp2 = 0.0;
       old = DBL_MAX;
       an = 0;
@@ -915,8 +942,9 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       }
     };
     auto test = [&](int64_t ch, double mp2, double old, int an) -> bool {
-      const int64_t me = ch * 32 + lane;
-      if (ch >= r1 || me >= n) return false;
+      if (ch >= r1) return false;
+      const int64_t me = sl(ch) * 32 + lane;
+      if (me >= n) return false;
       if (j == 0) return true;
       const double c2a = L.kc ? scc[an] : __ldcg(a.seed_c2 + an);
       const double cda = L.kc ? cdc[an] : __ldcg(a.cd2 + an);
@@ -928,7 +956,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
     // slower: issue rate); returns false when the rows are read from global
     auto issue = [&](int64_t ch, unsigned mask, int bsel) -> bool {
       if (!mask) return false;
-      const int64_t u0 = ch * 32;
+      const int64_t u0 = sl(ch) * 32;
       const int64_t u1 = (u0 + 32) < n ? (u0 + 32) : n;
       const size_t start = (size_t)u0 * row_bytes, a0 = start & ~size_t(15);
       const size_t sz = ((size_t)u1 * row_bytes - a0 + 15) & ~size_t(15);
@@ -962,7 +990,8 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       int anC;
       load_regs(chC, mp2C, oldC, anC);
       // score chunk A
-      const int64_t meA = chA * 32 + lane;
+      const int64_t slA = chA < r1 ? sl(chA) : chA;
+      const int64_t meA = slA * 32 + lane;
       double fin = oldA;
       if (mA) {
         if (sA) {
@@ -970,13 +999,18 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
           phbits ^= 1u << bA;
         }
         if (needA) {  // scored in factor order: a duplicate of a seed gets exactly D^2 = 0
-          const size_t s0 = (size_t)(chA * 32) * row_bytes;  // slice start
-          const P* x = sA ? reinterpret_cast<const P*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + (s0 & 15) +
-                                                       (size_t)lane * row_bytes)
-                          : points + meA * f;
           double dot = 0.0;
+          if (sA) {  // staged rows (shared-memory loads)
+            const size_t s0 = (size_t)(slA * 32) * row_bytes;  // slice start
+            const P* x = reinterpret_cast<const P*>(sm_raw + L.buf_off + (size_t)(2 * w + bA) * L.buf + (s0 & 15) +
+                                                    (size_t)lane * row_bytes);
+#pragma unroll 10
+            for (int q = 0; q < f; ++q) dot = fma((double)x[q], cen[q], dot);
+          } else {
+            const P* x = points + meA * f;
 #pragma unroll 5
-          for (int q = 0; q < f; ++q) dot = fma((double)x[q], cen[q], dot);
+            for (int q = 0; q < f; ++q) dot = fma((double)x[q], cen[q], dot);
+          }
           double d = (mp2A + cc) - 2.0 * dot;
           d = d > 0.0 ? d : 0.0;
           if (j == 0 || d < oldA) {
@@ -988,7 +1022,7 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       }
       double v = meA < n ? fin : 0.0;
       v = warp_sum(v);
-      if (lane == 0) a.chunk_sums[chA] = v;
+      if (lane == 0) a.chunk_sums[slA] = v;
       chA = chB;
       mp2A = mp2B;
       oldA = oldB;
@@ -1029,35 +1063,27 @@ __global__ void __launch_bounds__(256) seed_persistent_kernel(const P* __restric
       tm0 = tm1;
     }
     // ---------------------------------------------------------- (P) pick seed j+1
-    // every CTA locates it (same arithmetic, same result): run sums of the
-    // chunk sums (loads batched), CTA scan, the crossing run, chunk, point
-    // three levels, one CTA-wide scan each: CTA ranges, chunks of the
-    // crossing range, points of the crossing chunk
-    double total = 0.0;
+    // every CTA locates it with the same arithmetic (so the same pick): the
+    // CTA range whose running sum crosses u * total, the slice inside that
+    // range, the point inside that slice
+    int64_t pp;
     {
-      const int64_t per = (G + CS - 1) / CS;
-      const int64_t q0 = t * per < G ? t * per : G, q1 = (q0 + per) < G ? (q0 + per) : G;
-      double mine = 0.0;
-      for (int64_t q = q0; q < q1; ++q) mine += __ldcg(a.range_sums + q);
-      cta_scan(mine, wsum, &total);
+      double before, total, sub;
+      const int64_t rg = cta_crossing([&](int64_t q) { return __ldcg(a.range_sums + q); }, G, 0.0, u, true,
+                                      &before, &total, pick_sh);
+      if (!(total > 0.0)) {  // degenerate: every remaining pass takes the host branch
+        if (blockIdx.x == 0 && t == 0) *a.degenerate = j + 1;
+        break;
+      }
+      const double target = u * total;
+      const int64_t x0 = a.nchunks * rg / G, x1 = a.nchunks * (rg + 1) / G;
+      const int64_t chk = x0 + cta_crossing([&](int64_t q) { return __ldcg(a.chunk_sums + x0 + q); }, x1 - x0,
+                                            before, target, false, &before, &sub, pick_sh);
+      const int64_t pb = chk * 32, pe = (pb + 32) < n ? (pb + 32) : n;
+      pp = pb + cta_crossing([&](int64_t q) { return __ldcg(a.d2 + pb + q); }, pe - pb, before, target, false,
+                             &before, &sub, pick_sh);
     }
-    if (!(total > 0.0)) {  // degenerate: every remaining pass takes the host branch
-      if (blockIdx.x == 0 && t == 0) *a.degenerate = j + 1;
-      break;
-    }
-    const double target = a.uniforms[j] * total;
-    double before;
-    const int64_t rg = cta_crossing([&](int64_t q) { return __ldcg(a.range_sums + q); }, G, 0.0, target, wsum,
-                                    &s_base, &s_block, &before);
-    const int64_t x0 = a.nchunks * rg / G, x1 = a.nchunks * (rg + 1) / G;
-    const int64_t chk = x0 + cta_crossing([&](int64_t q) { return __ldcg(a.chunk_sums + x0 + q); }, x1 - x0, before,
-                                          target, wsum, &s_base, &s_block, &before);
-    const int64_t pb = chk * 32, pe = (pb + 32) < n ? (pb + 32) : n;
-    const int64_t pp = pb + cta_crossing([&](int64_t q) { return __ldcg(a.d2 + pb + q); }, pe - pb, before, target,
-                                         wsum, &s_base, &s_block, &before);
-    if (t == 0) s_pick = (unsigned long long)pp;
-    __syncthreads();
-    const int64_t p = (int64_t)s_pick;
+    const int64_t p = pp;
     for (int q = t; q < f; q += CS) {
       const double cv = (double)points[p * f + q];
       cen[q] = cv;

@@ -1,9 +1,10 @@
 """GPU tests of the k-means kernels against numpy restatements of
 clustering.py: the tensor-core assignment (certified band + float64
-rescoring) and its SIMT fallback, the counting-sort grouping and split
-centroid sums of the update step, and the persistent k-means++ seeding
-(triangle skip + fp16 prefilter) against the oracle's draw-for-draw seeding,
-including the degenerate (duplicate points) branch."""
+rescoring) and its SIMT fallback, the counting-sort grouping and in-order
+centroid sums of the update step (bit-identical to numpy's mean), and the
+persistent k-means++ seeding (triangle skip, factor-order distances) against
+the oracle's draw-for-draw seeding, including the degenerate (duplicate
+points) branch."""
 
 import numpy as np
 import pytest
@@ -92,7 +93,7 @@ def test_update_groups_stably_and_means(env, n, c):
     got = cen_t.cpu().numpy()
     for j in range(c):
         want = points[assign == j].mean(axis=0) if want_counts[j] else centers[j]
-        np.testing.assert_allclose(got[j], want, rtol=1e-12, atol=1e-12)
+        np.testing.assert_array_equal(got[j], want)  # sequential row sums, then one divide
 
 
 @pytest.mark.parametrize("n,f,k,dtype", [(20000, 50, 64, np.float32), (5000, 17, 200, np.float64),
