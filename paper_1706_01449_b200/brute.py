@@ -47,7 +47,7 @@ def default_blocks(factors: int) -> BlockSpec:
 def _results(ids, sc, n_items, num_users):
     vis = np.full(num_users, n_items, dtype=np.int64)
     ids_h, sc_h = _device.to_host_pinned_many(ids, sc)
-    return TopKResults(np.arange(num_users), ids_h, sc_h, vis)
+    return TopKResults(None, ids_h, sc_h, vis)  # every user, in order
 
 
 def topk_naive_tensors(model: ModelPair, k: int):

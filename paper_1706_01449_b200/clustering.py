@@ -64,6 +64,45 @@ class Clustering:
             d["theta"] = _device.to_device(np.asarray(self.max_angle, dtype=np.float64))
         return d["theta"]
 
+    def num_assigned(self) -> int:
+        return int(self.assignment.shape[0])
+
+
+class _DeviceClustering(Clustering):
+    """What kmeans() returns: centroids, theta_b and the objective history
+    are read back at once (a few values per cluster); the per-user assignment
+    and the member lists stay on the device until first read on the host
+    (the pipeline's build and serve use the device copies only)."""
+
+    def __init__(self, centroids, max_angle, objective, seed, assign_dev, members_dev, offsets):
+        for name, val in (("centroids", centroids), ("max_angle", max_angle), ("objective", objective),
+                          ("seed", seed), ("_pending", (assign_dev, members_dev, offsets))):
+            object.__setattr__(self, name, val)
+        self._dev()["assign"] = assign_dev
+
+    def _host_lists(self):
+        h = self.__dict__.get("_host_lists_")
+        if h is None:
+            assign_dev, members_dev, offsets = self._pending
+            a_h, m_h = (x.copy() for x in _device.to_host_pinned_many(assign_dev, members_dev))
+            a_h = a_h.astype(np.int64, copy=False)
+            for x in (a_h, m_h):
+                x.setflags(write=False)
+            h = (a_h, tuple(m_h[offsets[c]:offsets[c + 1]] for c in range(offsets.shape[0] - 1)))
+            object.__setattr__(self, "_host_lists_", h)
+        return h
+
+    @property
+    def assignment(self) -> np.ndarray:
+        return self._host_lists()[0]
+
+    @property
+    def members(self) -> tuple:
+        return self._host_lists()[1]
+
+    def num_assigned(self) -> int:
+        return int(self._pending[0].shape[0])
+
 
 def _half_angles(vectors: np.ndarray, center: np.ndarray) -> np.ndarray:
     cn = np.linalg.norm(center)
@@ -186,22 +225,15 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
         if int(changed.item()) == 0:
             break
         assign = new_assign
-    history = [float(v) for v in torch.cat(objs).cpu().numpy()]
     counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
     assign, fixed = repair(assign, d2, counts)
     if fixed:
         counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
     theta = _ops.max_angles(pts, centers, assign)
-    assign_h, mem_h, off_h, cen_h, theta_h = (a.copy() for a in _device.to_host_pinned_many(
-        assign, members, offsets, centers, theta))
-    assign_h = assign_h.astype(np.int64, copy=False)
-    members_t = tuple(mem_h[off_h[c]:off_h[c + 1]].copy() for c in range(num_clusters))
-    objective = np.asarray(history)
-    for a in (assign_h, theta_h, objective):
+    cen_h, theta_h, off_h, objective = (a.copy() for a in _device.to_host_pinned_many(
+        centers, theta, offsets, torch.cat(objs)))
+    for a in (theta_h, objective):
         a.setflags(write=False)
-    out = Clustering(FactorMatrix(cen_h), assign_h, theta_h, members_t, objective, seed)
-    # keep the device copies produced here
-    d = out._dev()
-    d["assign"] = assign.contiguous()
-    d["theta"] = theta
+    out = _DeviceClustering(FactorMatrix(cen_h), theta_h, objective, seed, assign.contiguous(), members, off_h)
+    out._dev()["theta"] = theta
     return out

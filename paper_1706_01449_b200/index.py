@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import math
 import struct
-from collections.abc import Sequence
+from collections.abc import Mapping, Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,21 +55,30 @@ class TopKResults(Sequence):
     """
 
     def __init__(self, user_ids, item_ids, scores, visited, reused=None):
-        self.user_ids = np.asarray(user_ids, dtype=np.int64)
+        # user_ids None: every user in order (position == id), materialised on request
+        self._uids = None if user_ids is None else np.asarray(user_ids, dtype=np.int64)
+        self._n = int(item_ids.shape[0]) if user_ids is None else int(self._uids.shape[0])
         self.item_ids = item_ids
         self.scores = scores
         self.visited = visited
         self._reused = reused or {}
 
+    @property
+    def user_ids(self) -> np.ndarray:
+        if self._uids is None:
+            self._uids = np.arange(self._n, dtype=np.int64)
+        return self._uids
+
     def __len__(self):
-        return self.user_ids.shape[0]
+        return self._n
 
     def _make(self, i):
         r = self._reused.get(i)
         if r is not None:
             return r
-        return TopKResult(int(self.user_ids[i]), self.item_ids[i].astype(np.int64),
-                          self.scores[i].astype(np.float64), int(self.visited[i]))
+        uid = i if self._uids is None else int(self._uids[i])
+        return TopKResult(uid, self.item_ids[i].astype(np.int64), self.scores[i].astype(np.float64),
+                          int(self.visited[i]))
 
     def __getitem__(self, i):
         if isinstance(i, slice):
@@ -84,6 +93,68 @@ class TopKResults(Sequence):
     def __iter__(self):
         for i in range(len(self)):
             yield self._make(i)
+
+
+class SampleResults(Mapping):
+    """Read-only ``{user_id: TopKResult}`` over one batched result (the
+    optimizer's sample walks, optimizer.py:141-145).  Entries are built on
+    first access and kept, so every lookup -- including query_batch's reuse of
+    them -- returns the same object, without a per-user host loop up front."""
+
+    def __init__(self, results: TopKResults):
+        self._res = results
+        ids = results.user_ids
+        self._order = None if ids.size < 2 or bool((ids[1:] > ids[:-1]).all()) else np.argsort(ids, kind="stable")
+        self._sorted = ids if self._order is None else ids[self._order]
+        self._cache = {}
+
+    @property
+    def user_ids(self) -> np.ndarray:
+        return self._res.user_ids
+
+    def _position(self, u):
+        j = int(np.searchsorted(self._sorted, u))
+        if j >= self._sorted.shape[0] or self._sorted[j] != u:
+            return -1
+        return j if self._order is None else int(self._order[j])
+
+    def __getitem__(self, u):
+        u = int(u)
+        r = self._cache.get(u)
+        if r is None:
+            i = self._position(u)
+            if i < 0:
+                raise KeyError(u)
+            r = self._cache[u] = self._res[i]
+        return r
+
+    def __contains__(self, u):
+        try:
+            return self._position(int(u)) >= 0
+        except (TypeError, ValueError):
+            return False
+
+    def __iter__(self):
+        return iter(self._res.user_ids.tolist())
+
+    def __len__(self):
+        return len(self._res)
+
+
+class _Reused:
+    """Positions of a query_batch answered by ``precomputed`` entries, looked
+    up lazily (TopKResults only asks for the positions it materialises)."""
+
+    def __init__(self, precomputed, uids, hit, count):
+        self._pre, self._uids, self._hit, self._n = precomputed, uids, hit, count
+
+    def get(self, i):
+        if 0 <= i < self._hit.shape[0] and self._hit[i]:
+            return self._pre[i if self._uids is None else int(self._uids[i])]
+        return None
+
+    def __len__(self):
+        return self._n
 
 
 class CentroidIndex:
@@ -178,10 +249,8 @@ def _device_build(model: ModelPair, centers_t, theta_t):
 
 def build_index(model: ModelPair, clustering: Clustering, block_size: int = DEFAULT_BLOCK_SIZE) -> CentroidIndex:
     """Sorted ceiling lists for every cluster, built on the GPU (index.py:129-155)."""
-    if clustering.assignment.shape[0] != model.num_users:
-        raise ValueError(
-            f"clustering covers {clustering.assignment.shape[0]} users, model has {model.num_users}"
-        )
+    if clustering.num_assigned() != model.num_users:
+        raise ValueError(f"clustering covers {clustering.num_assigned()} users, model has {model.num_users}")
     if block_size < 1:
         raise ValueError("block_size must be >= 1")
     norms, ids, bounds = _device_build(model, clustering.device_centroids(), clustering.device_max_angle())
@@ -307,23 +376,28 @@ def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 
     at B continue walking.  ``precomputed`` results are reused verbatim."""
     _check_k(k)
     all_users = user_ids is None
-    uids = np.arange(model.num_users, dtype=np.int64) if all_users else np.asarray(
-        [int(u) for u in user_ids], dtype=np.int64)
-    bad = (uids < 0) | (uids >= model.num_users)
-    if bad.any():
-        raise ValueError(f"user_id {int(uids[np.argmax(bad)])} out of range [0, {model.num_users})")
+    n_q = model.num_users
+    uids = None  # all users: positions are the ids
+    if not all_users:
+        uids = np.asarray([int(u) for u in user_ids], dtype=np.int64)
+        bad = (uids < 0) | (uids >= model.num_users)
+        if bad.any():
+            raise ValueError(f"user_id {int(uids[np.argmax(bad)])} out of range [0, {model.num_users})")
+        n_q = uids.shape[0]
     reused = {}
     hit = None
     if precomputed:
-        keys = np.fromiter(precomputed.keys(), dtype=np.int64, count=len(precomputed))
+        if isinstance(precomputed, SampleResults):
+            keys = precomputed.user_ids
+        else:
+            keys = np.fromiter(precomputed.keys(), dtype=np.int64, count=len(precomputed))
         keys = keys[(keys >= 0) & (keys < model.num_users)]
         mark = np.zeros(model.num_users, dtype=bool)  # O(U) membership instead of a sort-based isin
         mark[keys] = True
         hit = mark if all_users else mark[uids]
-        pos = np.sort(keys) if all_users else np.flatnonzero(hit)
-        reused = {int(i): precomputed[int(uids[i])] for i in pos}
+        reused = _Reused(precomputed, uids, hit, int(np.count_nonzero(hit)))
     k_eff = min(k, model.num_items)
-    if len(reused) * 2 <= uids.shape[0]:
+    if len(reused) * 2 <= n_q:
         # few reused entries: serve every position on the device (the reused
         # positions still return the precomputed objects), no host gather
         q = None if all_users else _device.to_device(uids)
@@ -331,11 +405,12 @@ def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 
         ids_h, sc_h, vis_h = _device.to_host_pinned_many(ids, sc, vis)
         return TopKResults(uids, ids_h, sc_h, vis_h, reused)
     todo = np.flatnonzero(~hit)
-    ids_h = np.zeros((uids.shape[0], k_eff), dtype=np.int32)
-    sc_h = np.zeros((uids.shape[0], k_eff), dtype=np.float64)
-    vis_h = np.zeros(uids.shape[0], dtype=np.int64)
+    ids_h = np.zeros((n_q, k_eff), dtype=np.int32)
+    sc_h = np.zeros((n_q, k_eff), dtype=np.float64)
+    vis_h = np.zeros(n_q, dtype=np.int64)
     if todo.size:
-        ids, sc, vis = query_batch_tensors(index, model, _device.to_device(uids[todo]), k, work_sharing)
+        ids, sc, vis = query_batch_tensors(index, model, _device.to_device(todo if all_users else uids[todo]), k,
+                                           work_sharing)
         ids_h[todo] = _device.to_host(ids)
         sc_h[todo] = _device.to_host(sc)
         vis_h[todo] = _device.to_host(vis)

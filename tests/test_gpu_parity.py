@@ -217,6 +217,20 @@ def test_query_batch_contract(sx):
     cached = sx.query_user(idx, model, 5, 4)
     res = sx.query_batch(idx, model, [5, 6], 4, precomputed={5: cached})
     assert res[0] is cached
+    # the optimizer's sample map: built lazily, every lookup the same object,
+    # and a serve that reuses it returns those objects at the sampled users
+    est = sx.estimate_walk_length(idx, model, 0.1, 4, seed=3)
+    some = sorted(est.sampled)[:5]
+    assert est.sampled[some[0]] is est.sampled[some[0]]
+    assert some[1] in est.sampled and -1 not in est.sampled and len(est.sampled) == len(list(est.sampled))
+    with pytest.raises(KeyError):
+        est.sampled[model.num_users + 7]
+    full = sx.query_batch(idx, model, None, 4, precomputed=est.sampled)
+    for u in some:
+        assert full[u] is est.sampled[u]
+        np.testing.assert_array_equal(full[u].item_ids, full.item_ids[u])
+    sub = sx.query_batch(idx, model, [some[2], 0, some[2]], 4, precomputed=est.sampled)
+    assert sub[0] is est.sampled[some[2]] and sub[2] is sub[0]
     with pytest.raises(ValueError):
         sx.query_user(idx, model, 0, 0)
     with pytest.raises(ValueError):
