@@ -29,6 +29,13 @@ int cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::simdex::cuda_fail(_e, #call); \
   } while (0)
 
+// same, inside internal helpers that return cudaError_t
+#define SIMDEX_TRY(call)                 \
+  do {                                   \
+    cudaError_t _e = (call);             \
+    if (_e != cudaSuccess) return _e;    \
+  } while (0)
+
 // Every kernel launch site ends with SIMDEX_LAUNCH_CHECK (or count_launches
 // for loops), which also feeds simdex_launch_count().
 void count_launches(int64_t n);
@@ -108,6 +115,11 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { ret
 // Batched (score desc, id asc) sort of `segs` equal-length segments of
 // (key, id) pairs; keys are float64 values sorted descending.
 cudaError_t segmented_sort_desc(double* keys, int32_t* ids, int64_t segs, int64_t len, cudaStream_t s);
+
+// Positions 0..n-1 grouped by label assign[i] in [0, c), stable ((label,
+// position) order), with counts [c] and offsets [c + 1] (kmeans.cu).
+cudaError_t group_stable(const int64_t* assign, int64_t n, int c, int64_t* out_counts, int64_t* out_members,
+                         int64_t* out_offsets, cudaStream_t s);
 
 // Exact fp64 top-K of rows x a column set.  cols == nullptr means all ni
 // items; otherwise cols[r] is a per-row... (not used).  Internal form used by

@@ -2,8 +2,9 @@
 //   * per-(cluster, item) half-angle theta_ic and Eq. 2 ceiling in float64,
 //   * per-cluster theta_b (max member angle) via an order-free atomic max,
 //   * a batched merge sort of every cluster's list by (ceiling desc, id asc):
-//     2048-element tiles bitonic-sorted in shared memory, then merge-path
-//     passes over HBM/L2 (keys are unique because ids are).
+//     2048-element tiles sorted in shared memory (8 per thread in registers,
+//     then merge-path merges), then merge passes whose CTAs stage their two
+//     input ranges in shared memory (keys are unique because ids are).
 #include <cfloat>
 #include <cmath>
 
@@ -13,110 +14,208 @@ namespace simdex {
 namespace {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortTile = 2048;  // elements per shared-memory tile
-constexpr int kMergeItems = 8;   // outputs per thread per merge pass
-
-struct KV {
-  double k;
-  int32_t id;
-};
+constexpr int kSortItems = 8;                           // elements per thread
+constexpr int kSortTile = kSortThreads * kSortItems;  // elements per CTA tile
 
 __device__ __forceinline__ bool kv_before(double ka, int32_t ia, double kb, int32_t ib) {
   // (key desc, id asc); -0.0 == +0.0 like numpy's comparisons
   return ka > kb || (ka == kb && ia < ib);
 }
 
-__global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(double* keys, int32_t* ids, int64_t len,
-                                                                 int64_t tiles_per_seg) {
-  __shared__ double sk[kSortTile];
-  __shared__ int32_t si[kSortTile];
-  const int64_t seg = blockIdx.x / tiles_per_seg, t = blockIdx.x % tiles_per_seg;
-  const int64_t base = seg * len + t * kSortTile;
-  const int64_t n = (len - t * kSortTile) < kSortTile ? (len - t * kSortTile) : kSortTile;
-  for (int i = threadIdx.x; i < kSortTile; i += kSortThreads) {
-    if (i < n) {
-      sk[i] = keys[base + i];
-      si[i] = ids[base + i];
-    } else {
-      sk[i] = -DBL_MAX;
-      si[i] = INT32_MAX;
-    }
-  }
-  for (int size = 2; size <= kSortTile; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < kSortTile / 2; i += kSortThreads) {
-        int lo = 2 * i - (i & (stride - 1));
-        int hi = lo + stride;
-        bool up = ((lo & size) == 0);
-        double ka = sk[lo], kb = sk[hi];
-        int32_t ia = si[lo], ib = si[hi];
-        bool swap = up ? kv_before(kb, ib, ka, ia) : kv_before(ka, ia, kb, ib);
-        if (swap) {
-          sk[lo] = kb;
-          sk[hi] = ka;
-          si[lo] = ib;
-          si[hi] = ia;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += kSortThreads) {
-    keys[base + i] = sk[i];
-    ids[base + i] = si[i];
-  }
-}
+// Shared-memory slot of tile element e: one pad slot per 8 elements, so a
+// thread's 8 consecutive elements (stride 8 across the warp) hit distinct banks.
+__device__ __forceinline__ int pad8(int e) { return e + (e >> 3); }
+constexpr int kSortSlots = kSortTile + kSortTile / 8;
 
-// Merge adjacent runs of width w inside every segment: src -> dst.
-__global__ void __launch_bounds__(kSortThreads) merge_pass_kernel(const double* __restrict__ sk,
-                                                                  const int32_t* __restrict__ si, double* dk,
-                                                                  int32_t* di, int64_t len, int64_t w,
-                                                                  int64_t chunks_per_seg, int64_t segs) {
-  const int64_t gt = (int64_t)blockIdx.x * kSortThreads + threadIdx.x;
-  const int64_t seg = gt / chunks_per_seg;
-  if (seg >= segs) return;
-  const int64_t o0 = (gt % chunks_per_seg) * kMergeItems;  // output position within segment
-  if (o0 >= len) return;
-  const int64_t a0 = (o0 / (2 * w)) * (2 * w);
-  const int64_t la = (len - a0) < w ? (len - a0) : w;
-  const int64_t b0 = a0 + la;
-  const int64_t lb = (len - b0) < w ? ((len - b0) > 0 ? (len - b0) : 0) : w;
-  const double* A = sk + seg * len + a0;
-  const int32_t* Ai = si + seg * len + a0;
-  const double* B = sk + seg * len + b0;
-  const int32_t* Bi = si + seg * len + b0;
-  const int64_t o = o0 - a0;  // position within the merged pair
-  int64_t lo = o - lb > 0 ? o - lb : 0, hi = o < la ? o : la;
+// Number of A elements among the first d outputs of merge(A, B) (merge path);
+// A(i) / B(j) return (key, id) of the i-th / j-th element.
+template <class FA, class FB>
+__device__ __forceinline__ int merge_split(FA A, int la, FB B, int lb, int d) {
+  int lo = d - lb > 0 ? d - lb : 0, hi = d < la ? d : la;
   while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    int64_t j = o - mid - 1;
-    if (kv_before(A[mid], Ai[mid], B[j], Bi[j]))
+    const int mid = (lo + hi) >> 1;
+    double ka, kb;
+    int32_t ia, ib;
+    A(mid, ka, ia);
+    B(d - mid - 1, kb, ib);
+    if (kv_before(ka, ia, kb, ib))
       lo = mid + 1;
     else
       hi = mid;
   }
-  int64_t i = lo, j = o - lo;
+  return lo;
+}
+
+// kSortItems outputs of merge(A, B) starting at (i, j), into registers
+// (padding (-inf, INT32_MAX) once both inputs are exhausted)
+template <class FA, class FB>
+__device__ __forceinline__ void merge_run(FA A, int la, FB B, int lb, int i, int j, double* rk, int32_t* ri) {
+  double ka = -DBL_MAX, kb = -DBL_MAX;
+  int32_t ia = INT32_MAX, ib = INT32_MAX;
+  if (i < la) A(i, ka, ia);
+  if (j < lb) B(j, kb, ib);
+#pragma unroll
+  for (int t = 0; t < kSortItems; ++t) {
+    const bool takeA = i < la && (j >= lb || kv_before(ka, ia, kb, ib));
+    if (takeA) {
+      rk[t] = ka;
+      ri[t] = ia;
+      if (++i < la) A(i, ka, ia);
+    } else {
+      rk[t] = j < lb ? kb : -DBL_MAX;
+      ri[t] = j < lb ? ib : INT32_MAX;
+      if (++j < lb) B(j, kb, ib);
+    }
+  }
+}
+
+// Sort every kSortTile-element tile of every segment: 8 elements per thread
+// sorted in registers, then merge-path merges of doubling runs in shared memory.
+__global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(double* keys, int32_t* ids, int64_t len,
+                                                                 int64_t tiles_per_seg) {
+  __shared__ double sk[kSortSlots];
+  __shared__ int32_t si[kSortSlots];
+  const int64_t seg = blockIdx.x / tiles_per_seg, tile = blockIdx.x % tiles_per_seg;
+  const int64_t base = seg * len + tile * kSortTile;
+  const int n = (int)((len - tile * kSortTile) < kSortTile ? (len - tile * kSortTile) : kSortTile);
+  const int t = threadIdx.x;
+  for (int e = t; e < kSortTile; e += kSortThreads) {  // coalesced; padding sorts last
+    sk[pad8(e)] = e < n ? keys[base + e] : -DBL_MAX;
+    si[pad8(e)] = e < n ? ids[base + e] : INT32_MAX;
+  }
+  __syncthreads();
+  double rk[kSortItems];
+  int32_t ri[kSortItems];
+#pragma unroll
+  for (int q = 0; q < kSortItems; ++q) {
+    rk[q] = sk[pad8(t * kSortItems + q)];
+    ri[q] = si[pad8(t * kSortItems + q)];
+  }
+  // odd-even transposition network over the thread's 8 elements
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+#pragma unroll
+    for (int q = r & 1; q + 1 < kSortItems; q += 2) {
+      if (kv_before(rk[q + 1], ri[q + 1], rk[q], ri[q])) {
+        const double tk = rk[q];
+        rk[q] = rk[q + 1];
+        rk[q + 1] = tk;
+        const int32_t ti = ri[q];
+        ri[q] = ri[q + 1];
+        ri[q + 1] = ti;
+      }
+    }
+  }
+  for (int w = kSortItems; w < kSortTile; w <<= 1) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSortItems; ++q) {
+      sk[pad8(t * kSortItems + q)] = rk[q];
+      si[pad8(t * kSortItems + q)] = ri[q];
+    }
+    __syncthreads();
+    const int o = t * kSortItems, a0 = (o / (2 * w)) * (2 * w), d = o - a0;
+    auto A = [&](int i, double& k, int32_t& id) {
+      k = sk[pad8(a0 + i)];
+      id = si[pad8(a0 + i)];
+    };
+    auto B = [&](int j, double& k, int32_t& id) {
+      k = sk[pad8(a0 + w + j)];
+      id = si[pad8(a0 + w + j)];
+    };
+    const int i = merge_split(A, w, B, w, d);
+    merge_run(A, w, B, w, i, d - i, rk, ri);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kSortItems; ++q) {
+    sk[pad8(t * kSortItems + q)] = rk[q];
+    si[pad8(t * kSortItems + q)] = ri[q];
+  }
+  __syncthreads();
+  for (int e = t; e < n; e += kSortThreads) {
+    keys[base + e] = sk[pad8(e)];
+    ids[base + e] = si[pad8(e)];
+  }
+}
+
+// Merge adjacent sorted runs of width w inside every segment, src -> dst; each
+// CTA writes one kSortTile-element output tile (tiles never straddle a pair:
+// 2w is a multiple of the tile).  Its A and B ranges are found by a merge-path
+// search over global memory, staged in shared memory, and merged there.
+__global__ void __launch_bounds__(kSortThreads) merge_pass_kernel(const double* __restrict__ sk,
+                                                                  const int32_t* __restrict__ si, double* dk,
+                                                                  int32_t* di, int64_t len, int64_t w,
+                                                                  int64_t tiles_per_seg) {
+  __shared__ double tk[kSortSlots];
+  __shared__ int32_t ti[kSortSlots];
+  __shared__ int s_split[2];
+  const int64_t seg = blockIdx.x / tiles_per_seg, tile = blockIdx.x % tiles_per_seg;
+  const int64_t o0 = tile * kSortTile;  // output offset within the segment
+  const int n = (int)((len - o0) < kSortTile ? (len - o0) : kSortTile);
+  const int64_t a0 = (o0 / (2 * w)) * (2 * w);
+  const int64_t la64 = (len - a0) < w ? (len - a0) : w;
+  const int64_t b0 = a0 + la64;
+  const int64_t lb64 = (len - b0) < w ? ((len - b0) > 0 ? (len - b0) : 0) : w;
+  const int la = (int)la64, lb = (int)lb64;
+  const double* Ak = sk + seg * len + a0;
+  const int32_t* Ai = si + seg * len + a0;
+  const double* Bk = Ak + la;
+  const int32_t* Bi = Ai + la;
+  const int t = threadIdx.x;
+  const int d0 = (int)(o0 - a0), d1 = d0 + n;
+  auto GA = [&](int i, double& k, int32_t& id) {
+    k = __ldg(Ak + i);
+    id = __ldg(Ai + i);
+  };
+  auto GB = [&](int j, double& k, int32_t& id) {
+    k = __ldg(Bk + j);
+    id = __ldg(Bi + j);
+  };
+  if (t == 0) s_split[0] = merge_split(GA, la, GB, lb, d0);
+  if (t == 32) s_split[1] = merge_split(GA, la, GB, lb, d1);
+  __syncthreads();
+  const int i0 = s_split[0], i1 = s_split[1];
+  const int na = i1 - i0, j0 = d0 - i0, nb = n - na;
+  for (int e = t; e < n; e += kSortThreads) {  // A part then B part, coalesced
+    if (e < na) {
+      tk[pad8(e)] = __ldg(Ak + i0 + e);
+      ti[pad8(e)] = __ldg(Ai + i0 + e);
+    } else {
+      tk[pad8(e)] = __ldg(Bk + j0 + e - na);
+      ti[pad8(e)] = __ldg(Bi + j0 + e - na);
+    }
+  }
+  __syncthreads();
+  double rk[kSortItems];
+  int32_t ri[kSortItems];
+  const int d = t * kSortItems;
+  if (d < n) {
+    auto A = [&](int i, double& k, int32_t& id) {
+      k = tk[pad8(i)];
+      id = ti[pad8(i)];
+    };
+    auto B = [&](int j, double& k, int32_t& id) {
+      k = tk[pad8(na + j)];
+      id = ti[pad8(na + j)];
+    };
+    const int i = merge_split(A, na, B, nb, d);
+    merge_run(A, na, B, nb, i, d - i, rk, ri);
+  }
+  __syncthreads();
+  if (d < n) {
+#pragma unroll
+    for (int q = 0; q < kSortItems; ++q) {
+      tk[pad8(d + q)] = rk[q];  // positions past n hold padding and are not written out
+      ti[pad8(d + q)] = ri[q];
+    }
+  }
+  __syncthreads();
   double* D = dk + seg * len + o0;
   int32_t* Di = di + seg * len + o0;
-  const int64_t cnt = (len - o0) < kMergeItems ? (len - o0) : kMergeItems;
-  for (int64_t t = 0; t < cnt; ++t) {
-    bool takeA;
-    if (i >= la)
-      takeA = false;
-    else if (j >= lb)
-      takeA = true;
-    else
-      takeA = kv_before(A[i], Ai[i], B[j], Bi[j]);
-    if (takeA) {
-      D[t] = A[i];
-      Di[t] = Ai[i];
-      ++i;
-    } else {
-      D[t] = B[j];
-      Di[t] = Bi[j];
-      ++j;
-    }
+  for (int e = t; e < n; e += kSortThreads) {
+    D[e] = tk[pad8(e)];
+    Di[e] = ti[pad8(e)];
   }
 }
 
@@ -132,47 +231,77 @@ __global__ void item_norms_kernel(const double* __restrict__ items, int64_t ni, 
   norms[i] = sqrt(s);
 }
 
-// grid: (ceil(ni/256), c).  Writes keys = ceiling, ids = item id for the sort.
-__global__ void __launch_bounds__(256) bounds_kernel(const double* __restrict__ items,
-                                                     const double* __restrict__ norms, int64_t ni, int f,
+// unit item directions x / |x| (the division index.py's angle takes per
+// (cluster, item) pair, done once per item here), stored factor-major
+// ([f][ni]) so a warp's 32 items read one coalesced line per factor; zero
+// rows stay zero
+__global__ void unit_cols_kernel(const double* __restrict__ items, const double* __restrict__ norms, int64_t ni, int f,
+                                 double* __restrict__ unit) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ni * f) return;
+  const int64_t i = e / f;
+  const int k = (int)(e - i * f);
+  const double nrm = norms[i];
+  unit[(int64_t)k * ni + i] = nrm == 0.0 ? 0.0 : items[e] / nrm;
+}
+
+constexpr int kBoundGroup = 16;  // clusters per CTA: each item direction is read once per group
+
+// grid: (ceil(ni/128), ceil(c/16)).  Thread = item; it accumulates the
+// half-angle sums for 16 clusters at once (unit centroids in shared memory),
+// then writes keys = ceiling, ids = item id for the sort.
+__global__ void __launch_bounds__(128) bounds_kernel(const double* __restrict__ unit,
+                                                     const double* __restrict__ norms, int64_t ni, int f, int c,
                                                      const double* __restrict__ centers,
                                                      const double* __restrict__ theta, double* __restrict__ keys,
                                                      int32_t* __restrict__ ids) {
-  extern __shared__ double y[];  // unit centroid
-  __shared__ double s_cn;
-  const int c = blockIdx.y;
-  const double* cen = centers + (int64_t)c * f;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int k = 0; k < f; ++k) s = fma(cen[k], cen[k], s);
-    s_cn = sqrt(s);
-  }
-  __syncthreads();
-  const double cn = s_cn;
-  for (int k = threadIdx.x; k < f; k += blockDim.x) y[k] = cn > 0.0 ? cen[k] / cn : 0.0;
-  __syncthreads();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ni) return;
-  const double nrm = norms[i];
-  double ang;
-  if (cn == 0.0 || nrm == 0.0) {
-    ang = M_PI / 2.0;
-  } else {
-    const double* x = items + i * f;
-    double dm = 0.0, dp = 0.0;
-    for (int k = 0; k < f; ++k) {
-      double xk = x[k] / nrm;
-      double a = xk - y[k], b = xk + y[k];
-      dm = fma(a, a, dm);
-      dp = fma(b, b, dp);
+  extern __shared__ double y[];  // [kBoundGroup][f] unit centroids
+  __shared__ double s_cn[kBoundGroup];
+  const int c0 = blockIdx.y * kBoundGroup;
+  const int ng = (c - c0) < kBoundGroup ? (c - c0) : kBoundGroup;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int g = w; g < ng; g += blockDim.x >> 5) {  // centroid norms, one warp each
+    const double* cen = centers + (int64_t)(c0 + g) * f;
+    if (lane == 0) {
+      double s = 0.0;
+      for (int k = 0; k < f; ++k) s = fma(cen[k], cen[k], s);
+      s_cn[g] = sqrt(s);
     }
-    ang = 2.0 * atan2(sqrt(dm), sqrt(dp));
   }
-  const double slack = theta[c];
-  double bound = (slack < ang) ? nrm * cos(ang - slack) : nrm;
-  if (bound == 0.0) bound = 0.0;  // fold -0.0
-  keys[(int64_t)c * ni + i] = bound;
-  ids[(int64_t)c * ni + i] = (int32_t)i;
+  __syncthreads();
+  for (int e = threadIdx.x; e < ng * f; e += blockDim.x) {
+    const int g = e / f;
+    const double cn = s_cn[g];
+    y[e] = cn > 0.0 ? centers[(int64_t)c0 * f + e] / cn : 0.0;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ni) return;
+  double dm[kBoundGroup], dp[kBoundGroup];
+#pragma unroll
+  for (int g = 0; g < kBoundGroup; ++g) dm[g] = dp[g] = 0.0;
+  for (int k = 0; k < f; ++k) {
+    const double xk = __ldg(unit + (int64_t)k * ni + i);
+#pragma unroll
+    for (int g = 0; g < kBoundGroup; ++g) {
+      const double yk = y[g * f + k];
+      const double a = xk - yk, b = xk + yk;
+      dm[g] = fma(a, a, dm[g]);
+      dp[g] = fma(b, b, dp[g]);
+    }
+  }
+  const double nrm = norms[i];
+#pragma unroll
+  for (int g = 0; g < kBoundGroup; ++g) {
+    if (g < ng) {
+      const double ang = (s_cn[g] == 0.0 || nrm == 0.0) ? M_PI / 2.0 : 2.0 * atan2(sqrt(dm[g]), sqrt(dp[g]));
+      const double slack = theta[c0 + g];
+      double bound = (slack < ang) ? nrm * cos(ang - slack) : nrm;
+      if (bound == 0.0) bound = 0.0;  // fold -0.0
+      keys[(int64_t)(c0 + g) * ni + i] = bound;
+      ids[(int64_t)(c0 + g) * ni + i] = (int32_t)i;
+    }
+  }
 }
 
 // theta_b: per-user angle to its centroid, atomic max on the (non-negative) bits.
@@ -237,11 +366,8 @@ cudaError_t segmented_sort_desc(double* keys, int32_t* ids, int64_t segs, int64_
     return e;
   double *srck = keys, *dstk = k2;
   int32_t *srci = ids, *dsti = i2;
-  const int64_t chunks = ceil_div(len, kMergeItems);
   for (int64_t w = kSortTile; w < len; w <<= 1) {
-    const int64_t threads = segs * chunks;
-    merge_pass_kernel<<<(unsigned)ceil_div(threads, kSortThreads), kSortThreads, 0, s>>>(srck, srci, dstk, dsti,
-                                                                                          len, w, chunks, segs);
+    merge_pass_kernel<<<(unsigned)(segs * tiles), kSortThreads, 0, s>>>(srck, srci, dstk, dsti, len, w, tiles);
     count_launches(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     double* tk = srck;
@@ -273,11 +399,17 @@ extern "C" int simdex_build_index(const double* items, int64_t ni, int32_t f, co
   cudaStream_t s = as_stream(stream);
   item_norms_kernel<<<(unsigned)ceil_div(ni, 256), 256, 0, s>>>(items, ni, f, out_item_norms);
   SIMDEX_LAUNCH_CHECK("item_norms");
-  dim3 grid((unsigned)ceil_div(ni, 256), (unsigned)c);
-  const size_t smem = (size_t)f * sizeof(double);
-  if (smem > 48 * 1024) SIMDEX_CUDA(cudaFuncSetAttribute(bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Scratch<double> unit;
+  SIMDEX_CUDA(unit.alloc(ni * f, s));
+  unit_cols_kernel<<<(unsigned)ceil_div(ni * f, 256), 256, 0, s>>>(items, out_item_norms, ni, f, unit.p);
+  SIMDEX_LAUNCH_CHECK("unit_cols");
+  dim3 grid((unsigned)ceil_div(ni, 128), (unsigned)ceil_div(c, kBoundGroup));
+  const size_t smem = (size_t)kBoundGroup * f * sizeof(double);
+  if (smem > 48 * 1024)
+    SIMDEX_CUDA(cudaFuncSetAttribute(bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileScope _prof("bounds", s);
-  bounds_kernel<<<grid, 256, smem, s>>>(items, out_item_norms, ni, f, centers, theta_b, out_bounds, out_list_ids);
+  bounds_kernel<<<grid, 128, smem, s>>>(unit.p, out_item_norms, ni, f, c, centers, theta_b, out_bounds,
+                                        out_list_ids);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("bounds");
   SIMDEX_CUDA(segmented_sort_desc(out_bounds, out_list_ids, c, ni, s));

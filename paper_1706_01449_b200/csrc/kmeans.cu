@@ -1351,6 +1351,44 @@ extern "C" int simdex_kmeans_assign(const double* points, const float* points32,
                              out_objective, s);
 }
 
+namespace simdex {
+// counting sort for c <= 8192, the merge sort otherwise
+cudaError_t group_stable(const int64_t* assign, int64_t n, int c, int64_t* out_counts, int64_t* out_members,
+                         int64_t* out_offsets, cudaStream_t s) {
+  if (c <= 8192) {
+    const int64_t nb = ceil_div(n, kGroupBlock) > 0 ? ceil_div(n, kGroupBlock) : 1;
+    Scratch<int32_t> bcount;
+    Scratch<int64_t> totals;
+    SIMDEX_TRY(bcount.alloc((size_t)c * nb, s));
+    SIMDEX_TRY(totals.alloc(c, s));
+    group_hist_kernel<<<(unsigned)nb, 256, sizeof(int32_t) * c, s>>>(assign, n, c, nb, bcount.p);
+    group_cluster_scan_kernel<<<(unsigned)ceil_div(c, 8), 256, 0, s>>>(bcount.p, nb, c, totals.p);
+    group_offsets_kernel<<<1, 1024, 0, s>>>(totals.p, c, out_counts, out_offsets);
+    if (n > 0)
+      group_scatter_kernel<<<(unsigned)nb, 32, sizeof(int32_t) * c, s>>>(assign, n, c, nb, bcount.p, out_offsets,
+                                                                        out_members);
+    count_launches(n > 0 ? 4 : 3);
+    return cudaGetLastError();
+  }
+  Scratch<double> keys;
+  Scratch<int32_t> ids;
+  Scratch<unsigned long long> cnt;
+  SIMDEX_TRY(keys.alloc(n, s));
+  SIMDEX_TRY(ids.alloc(n, s));
+  SIMDEX_TRY(cnt.alloc(c, s));
+  cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * c, s);
+  if (n > 0) {
+    cluster_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(assign, n, keys.p, ids.p, cnt.p);
+    cudaError_t e = segmented_sort_desc(keys.p, ids.p, 1, n, s);
+    if (e != cudaSuccess) return e;
+  }
+  offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
+  if (n > 0) members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(ids.p, n, out_members);
+  count_launches(n > 0 ? 3 : 1);
+  return cudaGetLastError();
+}
+}  // namespace simdex
+
 extern "C" int simdex_kmeans_update(const double* points, const float* points32, int64_t n, int32_t f,
                                     const int64_t* assign, int32_t c, double* centers, int64_t* out_counts,
                                     int64_t* out_members, int64_t* out_offsets, void* stream) {
@@ -1358,38 +1396,7 @@ extern "C" int simdex_kmeans_update(const double* points, const float* points32,
                    "simdex_kmeans_update: null pointer");
   SIMDEX_CHECK_ARG(n >= 1 && f >= 1 && c >= 1 && n < INT32_MAX, "simdex_kmeans_update: bad sizes");
   cudaStream_t s = as_stream(stream);
-  if (c <= 8192) {
-    // stable counting sort by cluster
-    const int64_t nb = ceil_div(n, kGroupBlock);
-    Scratch<int32_t> bcount;
-    Scratch<int64_t> totals;
-    SIMDEX_CUDA(bcount.alloc((size_t)c * nb, s));
-    SIMDEX_CUDA(totals.alloc(c, s));
-    group_hist_kernel<<<(unsigned)nb, 256, sizeof(int32_t) * c, s>>>(assign, n, c, nb, bcount.p);
-    SIMDEX_LAUNCH_CHECK("group_hist");
-    group_cluster_scan_kernel<<<(unsigned)ceil_div(c, 8), 256, 0, s>>>(bcount.p, nb, c, totals.p);
-    SIMDEX_LAUNCH_CHECK("group_cluster_scan");
-    group_offsets_kernel<<<1, 1024, 0, s>>>(totals.p, c, out_counts, out_offsets);
-    SIMDEX_LAUNCH_CHECK("group_offsets");
-    group_scatter_kernel<<<(unsigned)nb, 32, sizeof(int32_t) * c, s>>>(assign, n, c, nb, bcount.p, out_offsets,
-                                                                      out_members);
-    SIMDEX_LAUNCH_CHECK("group_scatter");
-  } else {
-    Scratch<double> keys;
-    Scratch<int32_t> ids;
-    Scratch<unsigned long long> cnt;
-    SIMDEX_CUDA(keys.alloc(n, s));
-    SIMDEX_CUDA(ids.alloc(n, s));
-    SIMDEX_CUDA(cnt.alloc(c, s));
-    SIMDEX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * c, s));
-    cluster_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(assign, n, keys.p, ids.p, cnt.p);
-    SIMDEX_LAUNCH_CHECK("cluster_keys");
-    SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, n, s));
-    offsets_kernel<<<1, 32, 0, s>>>(cnt.p, c, out_counts, out_offsets);
-    SIMDEX_LAUNCH_CHECK("offsets");
-    members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(ids.p, n, out_members);
-    SIMDEX_LAUNCH_CHECK("members");
-  }
+  SIMDEX_CUDA(group_stable(assign, n, c, out_counts, out_members, out_offsets, s));
   if (!centers) return SIMDEX_OK;  // grouping only (members/offsets/counts)
   if (points32) return mean_impl<float>(points32, f, out_members, out_offsets, c, centers, s);
   return mean_impl<double>(points, f, out_members, out_offsets, c, centers, s);

@@ -21,33 +21,17 @@ namespace {
 constexpr int kMaxMatmulK = 256;
 constexpr int kMaxKp = 256;
 
-__global__ void group_keys_kernel(const int64_t* __restrict__ q_user, int64_t nq, const int64_t* __restrict__ assign,
-                                  double* keys, int32_t* ids, unsigned long long* counts) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nq) return;
-  const int64_t c = assign[q_user[i]];
-  keys[i] = -(double)c;  // (key desc, id asc) == (cluster asc, query position asc)
-  ids[i] = (int32_t)i;
-  atomicAdd(counts + c, 1ull);
+// label of each query position: its user's cluster
+__global__ void query_labels_kernel(const int64_t* __restrict__ q_user, int64_t nq, const int64_t* __restrict__ assign,
+                                    int64_t* __restrict__ labels) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) labels[i] = assign[q_user[i]];
 }
 
-__global__ void group_scatter_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ q_user, int64_t nq,
-                                     int64_t* __restrict__ out_q, int64_t* __restrict__ out_perm) {
-  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nq) return;
-  const int32_t i = ids[j];
-  out_q[j] = q_user[i];
-  out_perm[j] = i;
-}
-
-__global__ void group_offsets_kernel(const unsigned long long* counts, int c, int64_t* off) {
-  if (threadIdx.x != 0) return;
-  int64_t acc = 0;
-  for (int j = 0; j < c; ++j) {
-    off[j] = acc;
-    acc += (int64_t)counts[j];
-  }
-  off[c] = acc;
+__global__ void gather_users_kernel(const int64_t* __restrict__ perm, const int64_t* __restrict__ q_user, int64_t nq,
+                                    int64_t* __restrict__ out_q) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nq) out_q[j] = q_user[perm[j]];
 }
 }  // namespace
 }  // namespace simdex
@@ -98,22 +82,19 @@ extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int
   SIMDEX_CHECK_ARG(q_user && assign && out_q_user && out_perm && out_off, "simdex_group_queries: null pointer");
   SIMDEX_CHECK_ARG(nq >= 0 && nq < INT32_MAX && c >= 1, "simdex_group_queries: bad sizes");
   cudaStream_t s = as_stream(stream);
-  Scratch<double> keys;
-  Scratch<int32_t> ids;
-  Scratch<unsigned long long> counts;
-  SIMDEX_CUDA(keys.alloc(nq, s));
-  SIMDEX_CUDA(ids.alloc(nq, s));
+  // (cluster, query position) order by a stable counting sort
+  Scratch<int64_t> labels, counts;
+  SIMDEX_CUDA(labels.alloc(nq > 0 ? nq : 1, s));
   SIMDEX_CUDA(counts.alloc(c, s));
-  SIMDEX_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * c, s));
   if (nq > 0) {
-    group_keys_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(q_user, nq, assign, keys.p, ids.p, counts.p);
-    SIMDEX_LAUNCH_CHECK("group_keys");
-    SIMDEX_CUDA(segmented_sort_desc(keys.p, ids.p, 1, nq, s));
-    group_scatter_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(ids.p, q_user, nq, out_q_user, out_perm);
-    SIMDEX_LAUNCH_CHECK("group_scatter");
+    query_labels_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(q_user, nq, assign, labels.p);
+    SIMDEX_LAUNCH_CHECK("query_labels");
   }
-  group_offsets_kernel<<<1, 32, 0, s>>>(counts.p, c, out_off);
-  SIMDEX_LAUNCH_CHECK("group_offsets");
+  SIMDEX_CUDA(group_stable(labels.p, nq, c, counts.p, out_perm, out_off, s));
+  if (nq > 0) {
+    gather_users_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, s>>>(out_perm, q_user, nq, out_q_user);
+    SIMDEX_LAUNCH_CHECK("gather_users");
+  }
   return SIMDEX_OK;
 }
 

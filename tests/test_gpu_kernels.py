@@ -129,3 +129,57 @@ def test_cfg2_full_size_against_reference(sx):
         est = sx.estimate_walk_length(idx, m, 0.001, k, seed=1)
         np.testing.assert_allclose([est.mean_visited, est.ci_low, est.ci_high, est.sample_size], g[f"est_k{k}"],
                                    rtol=1e-12)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 2047, 2048, 2049, 4097, 17770, 100003])
+def test_norm_order_sort_matches_lexsort(n):
+    """simdex_norm_order (the merge sort every list build uses): (value desc,
+    id asc) with many exact ties and signed zeros, against numpy's lexsort."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1706_01449_b200 import _lib
+    from paper_1706_01449_b200._lib import stream_ptr
+    rng = np.random.default_rng(n)
+    v = rng.integers(0, max(2, n // 5), n).astype(np.float64) * 0.25
+    v[rng.random(n) < 0.1] = -0.0
+    v[rng.random(n) < 0.1] = 0.0
+    d = torch.as_tensor(v, device="cuda")
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    _lib.call("simdex_norm_order", d.data_ptr(), n, perm.data_ptr(), stream_ptr())
+    want = np.lexsort((np.arange(n), -v))
+    np.testing.assert_array_equal(perm.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("ni,c,f", [(5000, 7, 13), (4096, 3, 50), (9000, 20, 8)])
+def test_build_index_lists_match_oracle(ni, c, f):
+    """Eq. 2 ceilings and the (ceiling desc, id asc) lists at sizes that take
+    the merge passes, against the oracle's build_index (its numpy norms sum
+    pairwise, so ceilings agree to ~1e-12; the order is checked exactly)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import simdex_oracle as O
+    from paper_1706_01449_b200 import _ops
+    rng = np.random.default_rng(ni + c)
+    items = rng.normal(size=(ni, f)) * rng.lognormal(0, 0.5, ni)[:, None]
+    items[3] = 0.0  # zero item: angle pi/2, ceiling 0
+    items[ni // 2] = items[ni // 3]  # duplicate rows: equal ceilings, id order
+    centers = rng.normal(size=(c, f))
+    theta = rng.uniform(0.0, 1.2, c)
+    norms, ids, bounds = _ops.build_index(torch.as_tensor(items, device="cuda"), torch.as_tensor(centers, device="cuda"),
+                                          torch.as_tensor(theta, device="cuda"))
+    want_ids, want_b, want_norms = O.build_index(items, centers, theta)
+    got_ids, got_b = ids.cpu().numpy().astype(np.int64), bounds.cpu().numpy()
+    np.testing.assert_allclose(norms.cpu().numpy(), want_norms, rtol=1e-14)
+    for r in range(c):
+        # a permutation in (ceiling desc, id asc) order of its own ceilings ...
+        assert np.array_equal(np.sort(got_ids[r]), np.arange(ni))
+        order = np.lexsort((got_ids[r], -got_b[r]))
+        np.testing.assert_array_equal(order, np.arange(ni))
+        # ... whose ceilings are the oracle's, item by item
+        by_item = np.empty(ni)
+        by_item[got_ids[r]] = got_b[r]
+        want_item = np.empty(ni)
+        want_item[want_ids[r]] = want_b[r]
+        np.testing.assert_allclose(by_item, want_item, rtol=1e-12, atol=1e-13)  # cos near 0: absolute
