@@ -295,6 +295,92 @@ __global__ void __launch_bounds__(128) centroid_seq_kernel(const P* __restrict__
   }
 }
 
+// rows in member order: sorted[j] = points[members[j]] (a warp per 8 rows,
+// lanes across the row), so every cluster's rows are one contiguous range
+template <class P>
+__global__ void gather_rows_kernel(const P* __restrict__ points, int f, const int64_t* __restrict__ members,
+                                   int64_t n, P* __restrict__ sorted) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t j = w * 8; j < n && j < w * 8 + 8; ++j) {
+    const P* src = points + members[j] * f;
+    P* dst = sorted + j * f;
+    for (int k = lane; k < f; k += 32) dst[k] = src[k];
+  }
+}
+
+constexpr int kMeanStages = 4;
+constexpr int kMeanStageBytes = 24 * 1024;
+
+// Centroid sums in member order from the member-ordered rows: one CTA per
+// cluster streams its contiguous row range through a 4-stage ring of 1-D bulk
+// copies; thread t owns factors t + 128 h and adds the rows strictly in order
+// (numpy's mean(axis=0) adds rows one after another), then one divide.
+template <class P>
+__global__ void __launch_bounds__(128) centroid_stream_kernel(const P* __restrict__ sorted, int f,
+                                                              const int64_t* __restrict__ offsets, int rows_per_stage,
+                                                              int stage_bytes, double* __restrict__ centers) {
+  extern __shared__ __align__(128) unsigned char mraw[];
+  __shared__ __align__(8) uint64_t bars[kMeanStages];
+  const int cl = blockIdx.x, t = threadIdx.x;
+  const int64_t b = offsets[cl], e = offsets[cl + 1];
+  if (e == b) return;
+  const size_t rb = (size_t)f * sizeof(P);
+  const int64_t nst = (e - b + rows_per_stage - 1) / rows_per_stage;
+  const unsigned char* g = reinterpret_cast<const unsigned char*>(sorted);
+  auto stage_range = [&](int64_t i, size_t& a0, uint32_t& sz, int& rows) {
+    const int64_t r0 = b + i * rows_per_stage;
+    const int64_t r1 = (r0 + rows_per_stage) < e ? (r0 + rows_per_stage) : e;
+    rows = (int)(r1 - r0);
+    a0 = ((size_t)r0 * rb) & ~size_t(15);
+    sz = (uint32_t)((((size_t)r1 * rb) - a0 + 15) & ~size_t(15));
+  };
+  if (t == 0) {
+    for (int q = 0; q < kMeanStages; ++q) sm100::mbar_init(bars + q, 1);
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t i) {
+    size_t a0;
+    uint32_t sz;
+    int rows;
+    stage_range(i, a0, sz, rows);
+    const int q = (int)(i % kMeanStages);
+    sm100::mbar_arrive_expect_tx(bars + q, sz);
+    sm100::bulk_load_1d(mraw + (size_t)q * stage_bytes, g + a0, sz, bars + q);
+  };
+  if (t == 0)
+    for (int64_t i = 0; i < nst && i < kMeanStages; ++i) issue(i);
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = 0; i < nst; ++i) {
+    const int q = (int)(i % kMeanStages);
+    sm100::mbar_wait(bars + q, (uint32_t)((i / kMeanStages) & 1));
+    size_t a0;
+    uint32_t sz;
+    int rows;
+    stage_range(i, a0, sz, rows);
+    const P* x = reinterpret_cast<const P*>(mraw + (size_t)q * stage_bytes + (((size_t)(b + i * rows_per_stage) * rb) - a0));
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const int k = t + 128 * h;
+      if (k < f) {
+#pragma unroll 8
+        for (int r = 0; r < rows; ++r) acc[h] += (double)x[(size_t)r * f + k];
+      }
+    }
+    __syncthreads();  // stage q consumed by every thread
+    if (t == 0 && i + kMeanStages < nst) {
+      sm100::fence_proxy_async_smem();
+      issue(i + kMeanStages);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const int k = t + 128 * h;
+    if (k < f) centers[(int64_t)cl * f + k] = acc[h] / (double)(e - b);
+  }
+}
+
 // centroid = (sum of the S part sums, in part order) / count; empty clusters
 // keep their centroid (clustering.py:170-172)
 __global__ void combine_mean_kernel(const double* __restrict__ psum, const int64_t* __restrict__ offsets, int c,
@@ -1303,16 +1389,33 @@ int seed_impl(const P* points, int64_t n, int32_t f, int32_t k, int64_t first, c
 }
 
 template <class P>
-int mean_impl(const P* points, int32_t f, const int64_t* members, const int64_t* offsets, int32_t c,
+int mean_impl(const P* points, int64_t n, int32_t f, const int64_t* members, const int64_t* offsets, int32_t c,
               double* centers, cudaStream_t s) {
   if (f > kSeqMaxF) {
     set_error("kmeans_update: f > %d unsupported", kSeqMaxF);
     return SIMDEX_EUNSUPPORTED;
   }
-  // rows staged per chunk: up to 256, two buffers within 110 KB (two CTAs per SM)
-  int rows = (int)((110 * 1024) / (2 * (size_t)f * sizeof(P)));
+  const size_t rb = (size_t)f * sizeof(P);
+  if (rb + 32 <= (size_t)kMeanStageBytes) {
+    // member-ordered copy, then contiguous streamed sums
+    Scratch<P> sorted;
+    SIMDEX_CUDA(sorted.alloc((size_t)n * f + 64 / sizeof(P), s));  // + slack for 16-byte rounded copies
+    gather_rows_kernel<P><<<(unsigned)ceil_div(n, 64), 256, 0, s>>>(points, f, members, n, sorted.p);
+    SIMDEX_LAUNCH_CHECK("gather_rows");
+    const int rows = (int)((kMeanStageBytes - 32) / rb);
+    const size_t smem = (size_t)kMeanStages * kMeanStageBytes;
+    SIMDEX_CUDA(cudaFuncSetAttribute(centroid_stream_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    ProfileScope _prof("centroid_mean", s);
+    centroid_stream_kernel<P><<<(unsigned)c, 128, smem, s>>>(sorted.p, f, offsets, rows, kMeanStageBytes, centers);
+    _prof.end();
+    SIMDEX_LAUNCH_CHECK("centroid_mean");
+    return SIMDEX_OK;
+  }
+  // wide rows: gather-staged kernel
+  int rows = (int)((110 * 1024) / (2 * rb));
   rows = rows > 256 ? 256 : (rows < 1 ? 1 : rows);
-  const size_t smem = 2 * (size_t)rows * f * sizeof(P);
+  const size_t smem = 2 * (size_t)rows * rb;
   SIMDEX_CUDA(cudaFuncSetAttribute(centroid_seq_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfileScope _prof("centroid_mean", s);
   centroid_seq_kernel<P><<<(unsigned)c, 128, smem, s>>>(points, f, members, offsets, rows, centers);
@@ -1398,8 +1501,8 @@ extern "C" int simdex_kmeans_update(const double* points, const float* points32,
   cudaStream_t s = as_stream(stream);
   SIMDEX_CUDA(group_stable(assign, n, c, out_counts, out_members, out_offsets, s));
   if (!centers) return SIMDEX_OK;  // grouping only (members/offsets/counts)
-  if (points32) return mean_impl<float>(points32, f, out_members, out_offsets, c, centers, s);
-  return mean_impl<double>(points, f, out_members, out_offsets, c, centers, s);
+  if (points32) return mean_impl<float>(points32, n, f, out_members, out_offsets, c, centers, s);
+  return mean_impl<double>(points, n, f, out_members, out_offsets, c, centers, s);
 }
 
 extern "C" int simdex_kmeans_seed(const double* points, const float* points32, int64_t n, int32_t f, int32_t k,
