@@ -1617,6 +1617,57 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   return SIMDEX_OK;
 }
 
+// k-means finalize, a thread per point: the certified candidates' exact
+// float64 d2 = (p2 + c2) - 2 p.c (factors in order -- the arithmetic of the
+// squared norms, so a point equal to a centre gets exactly 0), first minimum
+// (clustering.py:100 + argmin).  Rows whose band overflowed (or, defensively,
+// kept no candidate) go to the float64 SIMT pass.
+template <class P>
+__global__ void __launch_bounds__(256) assign_finalize_kernel(const FinalizeParams p, const P* __restrict__ pts) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool changed = false;
+  if (r < p.total_rows) {
+    bool over = p.row_flags[r] != 0;
+    double bd = DBL_MAX;
+    int32_t bj = INT32_MAX;
+    if (!over) {
+      const int cnt = p.row_count[r];
+      const float Tr = p.row_T[r];
+      const int32_t* cid = p.cand_id + r * p.cap;
+      const float* chi = p.cand_hi + r * p.cap;
+      const double pp = p.p2[r];
+      const P* u = pts + r * p.f;
+      for (int e = 0; e < cnt; ++e) {
+        if (!(chi[e] >= Tr)) continue;
+        const int32_t j = cid[e];
+        const double* x = p.items + (int64_t)j * p.f;
+        double dot = 0.0;
+#pragma unroll 10
+        for (int q = 0; q < p.f; ++q) dot = fma(x[q], (double)u[q], dot);
+        double d = (pp + p.c2[j]) - 2.0 * dot;
+        d = d > 0.0 ? d : 0.0;
+        if (d < bd || (d == bd && j < bj)) {
+          bd = d;
+          bj = j;
+        }
+      }
+      over = bj == INT32_MAX;
+    }
+    if (over) {
+      const int sl = atomicAdd(p.over_n, 1);
+      p.over_list[sl] = r;
+      p.over_out[sl] = r;
+    } else {
+      p.out_assign[r] = bj;
+      p.out_d2[r] = bd;
+      changed = p.prev && p.prev[r] != bj;
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, changed);
+  if (m && lane == __ffs(m) - 1) atomicAdd(p.changed, (unsigned long long)__popc(m));
+}
+
 // k-means assignment on the tensor cores (clustering.py:96-101, 175-177):
 // augmented product + certified top-1 band, exact float64 d2 over the band's
 // candidates.  Rows whose band overflows are returned in over_rows (count in
@@ -1714,7 +1765,10 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   fp.out_assign = out_assign;
   fp.out_d2 = out_d2;
   fp.changed = changed;
-  if ((rc = launch_finalize(fp, n, s))) return rc;
+  ProfileScope _pf("finalize_assign", s);
+  assign_finalize_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(fp, px);
+  _pf.end();
+  SIMDEX_LAUNCH_CHECK("finalize_assign");
   SIMDEX_CUDA(cudaMemcpyAsync(n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   return SIMDEX_OK;
 }
