@@ -796,42 +796,6 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
       }
     }
   }
-  // LPR/8 candidates per round, 8 lanes each (strided partials + xor tree)
-  constexpr int SG = LPR / 8;
-  const int sg = gl >> 3, sl = gl & 7;
-  for (int base = 0; base < (p.mode == kAssign ? 0 : cmax2); base += SG) {
-    const int e = base + sg;
-    double part = 0.0;
-    if (act && e < cnt) {
-      // strided partials (lane sl takes q = sl, sl+8, ...), loads of a
-      // 64-factor chunk issued together before the FMAs
-      if (p.items32) {
-        const float* x = p.items32 + (int64_t)si[e] * p.f;
-        for (int k0 = 0; k0 < p.f; k0 += 64) {
-          float xv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) xv[i] = k0 + sl + 8 * i < p.f ? x[k0 + sl + 8 * i] : 0.f;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (k0 + sl + 8 * i < p.f) part = fma((double)xv[i], us[k0 + sl + 8 * i], part);
-        }
-      } else {
-        const double* x = p.items + (int64_t)si[e] * p.f;
-        for (int k0 = 0; k0 < p.f; k0 += 64) {
-          double xv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) xv[i] = k0 + sl + 8 * i < p.f ? x[k0 + sl + 8 * i] : 0.0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (k0 + sl + 8 * i < p.f) part = fma(xv[i], us[k0 + sl + 8 * i], part);
-        }
-      }
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 4);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    if (act && sl == 0 && e < cnt) ss[e] = part;
-  }
   if (p.mode == kAssign) {  // clustering.py:100 + argmin (first minimum) over the candidates
     __syncwarp();
     double bd = DBL_MAX;
@@ -862,31 +826,128 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     }
     return;
   }
-  // bitonic sort by (score desc, id asc), 8 lanes per row
-  for (int size = 2; size <= np2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      __syncwarp();
-      for (int i = gl; i < np2 / 2; i += LPR) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const double a = ss[lo], b = ss[hi];
-        const int32_t ia = si[lo], ib = si[hi];
-        if (up ? ranks_before(b, ib, a, ia) : ranks_before(a, ia, b, ib)) {
-          ss[lo] = b;
-          ss[hi] = a;
-          si[lo] = ib;
-          si[hi] = ia;
+  // exact float64 rescoring.  Narrow rows with several survivors per lane
+  // group: one lane per candidate (two partial sums over the even / odd
+  // factors, so identical rows still score identically); otherwise LPR/8
+  // candidates per round, 8 lanes each (strided partials + xor tree)
+  const bool lane_per_cand = p.f <= 64 && cmax2 > LPR / 2;
+  constexpr int SG = LPR / 8;
+  const int sg = gl >> 3, sl = gl & 7;
+  for (int base = 0; base < (lane_per_cand ? 0 : cmax2); base += SG) {
+    const int e = base + sg;
+    double part = 0.0;
+    if (act && e < cnt) {
+      if (p.items32) {
+        const float* x = p.items32 + (int64_t)si[e] * p.f;
+        for (int k0 = 0; k0 < p.f; k0 += 64) {
+          float xv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xv[i] = k0 + sl + 8 * i < p.f ? x[k0 + sl + 8 * i] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (k0 + sl + 8 * i < p.f) part = fma((double)xv[i], us[k0 + sl + 8 * i], part);
+        }
+      } else {
+        const double* x = p.items + (int64_t)si[e] * p.f;
+        for (int k0 = 0; k0 < p.f; k0 += 64) {
+          double xv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xv[i] = k0 + sl + 8 * i < p.f ? x[k0 + sl + 8 * i] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (k0 + sl + 8 * i < p.f) part = fma(xv[i], us[k0 + sl + 8 * i], part);
         }
       }
     }
+    part += __shfl_xor_sync(0xffffffffu, part, 4);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    if (act && sl == 0 && e < cnt) ss[e] = part;
+  }
+  for (int e = gl; e < (lane_per_cand ? cmax2 : 0); e += LPR) {
+    if (act && e < cnt) {
+      double d0 = 0.0, d1 = 0.0;
+      const int64_t id = si[e];
+      if (p.items32) {
+        const float* x = p.items32 + id * p.f;
+        if ((p.f & 1) == 0) {
+          const float2* x2 = reinterpret_cast<const float2*>(x);
+#pragma unroll 5
+          for (int q = 0; q < p.f / 2; ++q) {
+            const float2 v = x2[q];
+            d0 = fma((double)v.x, us[2 * q], d0);
+            d1 = fma((double)v.y, us[2 * q + 1], d1);
+          }
+        } else {
+          for (int q = 0; q < p.f; ++q) d0 = fma((double)x[q], us[q], d0);
+        }
+      } else {
+        const double* x = p.items + id * p.f;
+        for (int q = 0; q < p.f; ++q) d0 = fma(x[q], us[q], d0);
+      }
+      ss[e] = d0 + d1;
+    }
   }
   __syncwarp();
-  if (!act) return;
-  const int held = cnt < p.k_eff ? cnt : p.k_eff;
-  for (int i = gl; i < p.k_eff; i += LPR) {
-    p.out_ids[out * p.k_eff + i] = i < held ? si[i] : -1;
-    p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
+  const int held = act ? (cnt < p.k_eff ? cnt : p.k_eff) : 0;
+  double kth = -DBL_MAX;
+  int64_t mp = -1;
+  if (cmax2 <= 32) {
+    // few survivors: each candidate's rank under (score desc, id asc) is its output slot
+    for (int e = gl; e < cmax2; e += LPR) {
+      if (act && e < cnt) {
+        const double se = ss[e];
+        const int32_t ie = si[e];
+        int rank = 0;
+        for (int o = 0; o < cnt; ++o) rank += ranks_before(ss[o], si[o], se, ie) ? 1 : 0;
+        if (rank < p.k_eff) {
+          p.out_ids[out * p.k_eff + rank] = ie;
+          p.out_scores[out * p.k_eff + rank] = se;
+          if (rank == p.k_eff - 1) kth = se;
+          if (p.mode == kFullList) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + ie]);
+        }
+      }
+    }
+    if (act)
+      for (int i = held + gl; i < p.k_eff; i += LPR) {
+        p.out_ids[out * p.k_eff + i] = -1;
+        p.out_scores[out * p.k_eff + i] = -DBL_MAX;
+      }
+  } else {
+    // bitonic sort by (score desc, id asc)
+    for (int size = 2; size <= np2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        __syncwarp();
+        for (int i = gl; i < np2 / 2; i += LPR) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const double a = ss[lo], b = ss[hi];
+          const int32_t ia = si[lo], ib = si[hi];
+          if (up ? ranks_before(b, ib, a, ia) : ranks_before(a, ia, b, ib)) {
+            ss[lo] = b;
+            ss[hi] = a;
+            si[lo] = ib;
+            si[hi] = ia;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (act) {
+      for (int i = gl; i < p.k_eff; i += LPR) {
+        p.out_ids[out * p.k_eff + i] = i < held ? si[i] : -1;
+        p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
+        if (p.mode == kFullList && i < held) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
+      }
+      if (held == p.k_eff) kth = ss[p.k_eff - 1];
+    }
   }
+  if (p.mode == kBrute) return;
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    kth = fmax(kth, __shfl_xor_sync(0xffffffffu, kth, o));
+    mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+  }
+  if (!act) return;
   if (p.mode == kPrefix) {
     // index.py:372-387: the prefix covers the list -> n; the K-th beats the
     // ceiling at B -> B; otherwise the user continues past B.
@@ -894,14 +955,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     if (gl == 0) {
       if (p.prefix >= p.n) {
         p.out_visited[out] = p.n;
-      } else if (held == p.k_eff && ss[p.k_eff - 1] > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
+      } else if (held == p.k_eff && kth > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
         p.out_visited[out] = p.prefix;
       } else {
         // the prefix's exact K-th score lower-bounds the catalogue's: start the
         // full-list pass from it (rounded down, with a 2^-40 relative guard)
         float t0 = -INFINITY;
         if (held == p.k_eff) {
-          const double sk = ss[p.k_eff - 1] * p.t0_scale;
+          const double sk = kth * p.t0_scale;
           t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
         }
         p.row_T0_out[r] = t0;
@@ -925,11 +986,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     // 1 + the largest list position of a top-K item and s_K the K-th score,
     //   visited = min(n, max(P, k_eff, #{j : bounds[j]*||u|| >= s_K})),
     // floored at B for work sharing (index.py:372-387).
-    int64_t mp = -1;
-    for (int i = gl; i < held; i += LPR) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + si[i]]);
-    for (int o = LPR / 2; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(gmask, mp, o));
     if (gl == 0) {
-      const int64_t q = ceiling_count(p.bounds + (int64_t)c * p.n, p.n, p.unorm[user], ss[p.k_eff - 1]);
+      const int64_t q = ceiling_count(p.bounds + (int64_t)c * p.n, p.n, p.unorm[user], kth);
       int64_t v = max(max(mp + 1, (int64_t)p.k_eff), q);
       if (v > p.n) v = p.n;
       if (v < p.prefix) v = p.prefix;

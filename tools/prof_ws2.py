@@ -17,5 +17,5 @@ torch.cuda.synchronize()
 _lib.profile(True)
 t = time.perf_counter(); out = I.query_batch_tensors(idx, m, None, k, True); torch.cuda.synchronize()
 dt = time.perf_counter() - t
-ks = {n: _lib.profile_read(n) for n in ("gemm_topk", "finalize", "walk", "select_rows")}
+ks = {n: _lib.profile_read(n) for n in ("gemm_topk", "finalize", "walk", "select_rows", "seed_pick", "seed_t0")}
 print("k", k, "ms", 1000 * dt, " ".join(f"{n}={v[0]:.3f}ms/{v[1]}" for n, v in ks.items() if v[1]), "stats", _lib.ws_stats(), flush=True)
