@@ -401,6 +401,31 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float mx = fmaxf(fmax3(m0, m1, m2), m3);
               const float nmax = ch == 0 ? nm4.x : ch == 1 ? nm4.y : ch == 2 ? nm4.z : nm4.w;
               const float em = fmaf(cu, nmax, p.e_abs);  // the chunk's widest band
+              if constexpr (KT > 1) {
+                // a unit's first chunk with no threshold yet (T = -inf in every
+                // row): all 32 items go in with the chunk-wide band (hi = v + em
+                // >= v + e_i, lo = v - em <= v - e_i: still certified bounds),
+                // stored as vectors; the top-K of the lower bounds is built in
+                // registers instead of 32 dependent append rounds
+                if (t == 0 && ch == 0 && nvalid >= 32 &&
+                    __all_sync(0xffffffffu, !(live && !flags) || (T == -INFINITY && cnt == 0))) {
+                  if (live && !flags) {
+                    float4* dh = reinterpret_cast<float4*>(my_hi);
+                    int4* di = reinterpret_cast<int4*>(my_id);
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                      dh[q4] = make_float4(v[4 * q4] + em, v[4 * q4 + 1] + em, v[4 * q4 + 2] + em, v[4 * q4 + 3] + em);
+                      di[q4] = make_int4(c0 + 4 * q4, c0 + 4 * q4 + 1, c0 + 4 * q4 + 2, c0 + 4 * q4 + 3);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) push_top<KTT>(top, v[i] - em);
+                    cnt = 32;
+                    hops += 32;
+                    T = fmaxf(T, KTT == kk + 1 ? top[KTT - 1] : top_at<KTT>(top, kk));
+                  }
+                  continue;
+                }
+              }
               // rows that cannot take candidates (padding, overflowed) never pass
               const bool pass = mx + em >= ((live && !flags) ? T : INFINITY);
               // fast path: one vote per chunk; everything below is the rare, warp-uniform slow path
