@@ -14,7 +14,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsimdex_b200.so")
+LIB_PATH = os.environ.get("SIMDEX_LIB_PATH") or os.path.join(_HERE, "lib", "libsimdex_b200.so")  # override: A/B timing only
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "simdex_b200.h")
 
 P = C.c_void_p

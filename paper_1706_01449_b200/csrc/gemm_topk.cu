@@ -92,6 +92,10 @@ struct TopkParams {
   int64_t* heap_ops;
   float* debug_out;
   int64_t debug_ld;
+  // item operand in descending-norm order: a unit stops streaming once no row
+  // can take another candidate (Cauchy-Schwarz against the remaining norms)
+  int norm_sorted;
+  float g_mul;  // (1/eps + 2)(1 + 2^-20): ||u|| + 2 eps ||u|| from eps ||u|| (scaled, rounded up)
 };
 
 // three-input max (sm_100 FMNMX3)
@@ -204,7 +208,7 @@ __device__ __forceinline__ float top_at(const float (&t)[KT], int k) {
   return r;
 }
 
-template <int KT>
+template <int KT, bool EX>  // EX: early exit on a norm-sorted item operand
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_topk_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const TopkParams p) {
@@ -223,6 +227,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* t_full = a_full + 2;   // [2]
   uint64_t* t_empty = a_full + 4;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+  // early-exit bookkeeping (norm-sorted operands), tagged so stale entries never match
+  volatile int32_t* stage_end = reinterpret_cast<volatile int32_t*>(bars) + 64;   // [8] stage sequence no. of an end marker
+  volatile int32_t* buf_end = stage_end + 8;                                      // [2] accumulator use no. of an end marker
+  volatile long long* wdone = reinterpret_cast<volatile long long*>(bars) + 40;  // [8] (unit << 32) | tile after which a warp is done
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -234,6 +242,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(a_full, 1);
     mbar_init(a_empty, 1);
+    for (int i = 0; i < 8; ++i) {
+      stage_end[i] = -1;
+      wdone[i] = -1;
+    }
+    buf_end[0] = buf_end[1] = -1;
     for (int b = 0; b < 2; ++b) {
       mbar_init(t_full + b, 1);
       mbar_init(t_empty + b, kEpiWarps);
@@ -253,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
+      int32_t seq = 0;  // stages issued so far
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++iter) {
         const Unit un = p.units[u];
         const int ntile_a = un.rows > kTileM ? 2 : 1;
@@ -263,15 +277,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(a_sm + (h * KB + kb) * kSlab, &map_a, a_full, kb * 64, (int)(un.a_row0 + h * kTileM));
         const int n_tiles = (un.n_items + kTileN - 1) / kTileN;
         for (int t = 0; t < n_tiles; ++t) {
+          bool stop = EX && t > 0 && (t & 3) == 0;
+          for (int w = 0; stop && w < kEpiWarps; ++w) {
+            const long long e = wdone[w];
+            stop = (int)(e >> 32) == u && (int)(e & 0xffffffffll) < t;
+          }
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(full + stage, KB * kSlab);
-          for (int kb = 0; kb < KB; ++kb)
-            tma_load_2d(b_sm + (stage * KB + kb) * kSlab, &map_b, full + stage, kb * 64,
-                        (int)(un.b_row0 + t * kTileN));
+          if (stop) {  // every epilogue warp is done with this unit: end marker instead of tile t
+            stage_end[stage] = seq;
+            mbar_arrive(full + stage);
+          } else {
+            mbar_arrive_expect_tx(full + stage, KB * kSlab);
+            for (int kb = 0; kb < KB; ++kb)
+              tma_load_2d(b_sm + (stage * KB + kb) * kSlab, &map_b, full + stage, kb * 64,
+                          (int)(un.b_row0 + t * kTileN));
+          }
+          ++seq;
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
+          if (stop) break;
         }
       }
     }
@@ -287,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t a_desc0 = umma_desc_sw128(smem_u32(a_sm));
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(b_sm));
       const int ksteps = p.k_steps;
+      int32_t seq = 0;  // stages consumed so far
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++iter) {
         const Unit un = p.units[u];
         const int ntile_a = un.rows > kTileM ? 2 : 1;
@@ -298,6 +325,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(t_empty + buf, (use & 1) ^ 1);
           mbar_wait(full + stage, phase);
           tc_fence_after();
+          if (EX && (t & 3) == 0 && t > 0 && stage_end[stage] == seq) {  // markers only replace tiles t = 4j  // end marker: pass it on to the epilogue
+            mbar_arrive(empty + stage);
+            buf_end[buf] = (int32_t)use;
+            mbar_arrive(t_full + buf);
+            ++seq;
+            ++acc;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            break;
+          }
+          ++seq;
           const uint64_t bd0 = b_desc0 + (uint64_t)((stage * KB * kSlab) >> 4);
           for (int h = 0; h < ntile_a; ++h) {
             const uint32_t d = tbase + (buf * 2 + h) * kTileN;
@@ -346,12 +386,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the tile's four 32-item norm maxima, loaded one tile ahead (off the critical path)
       const float4* nm4p = reinterpret_cast<const float4*>(p.item_nmax32 + (un.b_row0 >> 5));
       float4 nm4_next = __ldg(nm4p);
+      const float gu = cu * p.g_mul;  // ||u|| + 2 eps ||u||, scaled, rounded up
+      bool done = false;              // no row of this warp can take another candidate
       for (int t = 0; t < n_tiles; ++t, ++acc) {
         const uint32_t buf = acc & 1, use = acc >> 1;
         const float4 nm4 = nm4_next;
         if (t + 1 < n_tiles) nm4_next = __ldg(nm4p + t + 1);
         mbar_wait(t_full + buf, use & 1);
         tc_fence_after();
+        if (EX && (t & 3) == 0 && t > 0 && buf_end[buf] == (int32_t)use) {  // the unit ended early
+          __syncwarp();
+          if (lane == 0) mbar_arrive(t_empty + buf);
+          ++acc;
+          break;
+        }
         bool released = false;
         if (h < ntile_a) {
           const int tile_valid = min(kTileN, un.n_items - t * kTileN);
@@ -522,6 +570,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(t_empty + buf);
+        }
+        if (EX && !done && (t & 3) == 3 && t + 1 < n_tiles) {
+          // every later item has ||i|| <= the next tile's first norm, so its
+          // upper bound is at most ||u|| n + 2 (eps ||u|| n + e_abs)
+          const float bound = fmaf(gu, nm4_next.x, 2.f * p.e_abs) * (1.f + 0x1p-20f);
+          if (__all_sync(0xffffffffu, !(live && !flags) || bound < T)) {
+            done = true;
+            if (lane == 0) wdone[ew] = ((long long)u << 32) | (long long)t;
+          }
         }
       }
       if constexpr (KT == 0) {
@@ -1276,9 +1333,10 @@ int geometry(int kp, GemmGeometry* g) {
 template <int KT>
 int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
                    cudaStream_t s) {
-  SIMDEX_CUDA(cudaFuncSetAttribute(gemm_topk_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  auto kern = p.norm_sorted ? gemm_topk_kernel<KT, true> : gemm_topk_kernel<KT, false>;
+  SIMDEX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   ProfileScope _prof("gemm_topk", s);
-  gemm_topk_kernel<KT><<<grid, kThreads, g.smem, s>>>(ma, mb, p);
+  kern<<<grid, kThreads, g.smem, s>>>(ma, mb, p);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("gemm_topk");
   return SIMDEX_OK;
@@ -1362,6 +1420,7 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   p.row_count = st.cnt.p;
   p.row_flags = st.flags.p;
   p.row_T_out = st.rowT.p;
+  p.g_mul = (float)((1.0 / eps_for(((f + 63) / 64) * 64) + 2.0) * (1.0 + 0x1p-20));
   return p;
 }
 
@@ -1430,6 +1489,17 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   p.heap_ops = heap_ops;
   p.debug_out = debug_out;
   p.debug_ld = ni;
+  // early exit pays when the catalogue's norms are skewed (the streaming
+  // kernel with exit checks is slower when no tile can be skipped): decided
+  // from the norm-sorted operand's largest and median norms
+  p.norm_sorted = 0;
+  if (item_perm != nullptr && !debug_out && ni >= 2 * kTileN && !getenv("SIMDEX_NO_EARLY_EXIT")) {
+    double nn[2];
+    SIMDEX_CUDA(cudaMemcpyAsync(&nn[0], i_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SIMDEX_CUDA(cudaMemcpyAsync(&nn[1], i_norm + ni / 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    SIMDEX_CUDA(cudaStreamSynchronize(s));
+    p.norm_sorted = nn[1] < 0.6 * nn[0];
+  }
   const int grid = (int)(nunits < sm_count() ? nunits : sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
   if (debug_out) return SIMDEX_OK;
@@ -1656,6 +1726,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
   TopkParams p2 = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu2.p, g, f, k_eff);
   p2.row_T0 = t02.p;
+  p2.norm_sorted = item_perm != nullptr && !getenv("SIMDEX_NO_EARLY_EXIT");
   Scratch<int64_t> hops2;
   if (stats) {
     SIMDEX_CUDA(hops2.alloc(rows2, s));
