@@ -54,11 +54,20 @@ int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni,
 namespace {
 using namespace sm100;
 
-constexpr int kUnitRows = 256;
+#ifndef SIMDEX_M_TILES
+#define SIMDEX_M_TILES 1
+#endif
+// 128-row M tiles per unit and CTAs per SM: one M tile per CTA with two CTAs
+// per SM (each CTA: 2 accumulator buffers x 128 columns of TMEM, 4 epilogue
+// warps), so one CTA's slow epilogue warp never gates the other's hand-off
+constexpr int kMTiles = SIMDEX_M_TILES;
+constexpr int kCtasPerSm = kMTiles == 1 ? 2 : 1;
+constexpr int kUnitRows = 128 * kMTiles;
+constexpr int kTmemCols = kMTiles * 2 * 128;
 constexpr int kTileM = 128;
 constexpr int kTileN = 128;
 constexpr int kSlab = kTileM * 128;  // one [128 rows x 64 fp16] swizzled slab: 16 KB
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 4 * kMTiles;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kMaxCap = 512;
 constexpr uint32_t kIdesc = idesc_f16_f32(kTileM, kTileN);
@@ -209,7 +218,7 @@ __device__ __forceinline__ float top_at(const float (&t)[KT], int k) {
 }
 
 template <int KT, bool EX>  // EX: early exit on a norm-sorted item operand
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     gemm_topk_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const TopkParams p) {
   constexpr bool kDebug = KT < 0;         // raw accumulators to p.debug_out, no selection
@@ -218,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int KB = p.kb, S = p.stages;
   uint8_t* a_sm = base;
-  uint8_t* b_sm = base + 2 * KB * kSlab;
+  uint8_t* b_sm = base + kMTiles * KB * kSlab;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_sm + S * KB * kSlab);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++seq;
           const uint64_t bd0 = b_desc0 + (uint64_t)((stage * KB * kSlab) >> 4);
           for (int h = 0; h < ntile_a; ++h) {
-            const uint32_t d = tbase + (buf * 2 + h) * kTileN;
+            const uint32_t d = tbase + (buf * kMTiles + h) * kTileN;
             const uint64_t ad0 = a_desc0 + (uint64_t)((h * KB * kSlab) >> 4);
 #pragma unroll 4
             for (int ks = 0; ks < ksteps; ++ks) {
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t raw[LDC][32];
 #pragma unroll
             for (int c = 0; c < LDC; ++c)
-              tmem_ld32_nowait(tbase + lane_off + (buf * 2 + h) * kTileN + (cg + c) * 32, raw[c]);
+              tmem_ld32_nowait(tbase + lane_off + (buf * kMTiles + h) * kTileN + (cg + c) * 32, raw[c]);
             tmem_wait_ld();
             if (cg + LDC >= kTileN / 32) {
               tc_fence_before();
@@ -615,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    tmem_dealloc(tbase, kTmemCols);
   }
 }
 
@@ -1313,12 +1322,18 @@ int cap_for(int k_eff) {
 struct GemmGeometry {
   int kb, stages;
   size_t smem;
+  int ctas_per_sm;  // kCtasPerSm, or 1 when a CTA's operands need more than half the SM's shared memory
 };
 
 int geometry(int kp, GemmGeometry* g) {
   g->kb = kp / 64;
-  const size_t budget = 225 * 1024;
-  const size_t fixed = 1024 + 2 * (size_t)g->kb * kSlab + 512;
+  const size_t fixed = 1024 + kMTiles * (size_t)g->kb * kSlab + 512;
+  g->ctas_per_sm = kCtasPerSm;
+  size_t budget = kCtasPerSm == 1 ? 225 * 1024 : 112 * 1024;
+  if (fixed + 2 * (size_t)g->kb * kSlab > budget) {  // fewer than 2 stages would fit: one CTA per SM
+    g->ctas_per_sm = 1;
+    budget = 225 * 1024;
+  }
   int s = 6;
   while (s > 1 && fixed + (size_t)s * g->kb * kSlab > budget) --s;
   g->stages = s;
@@ -1500,7 +1515,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
     SIMDEX_CUDA(cudaStreamSynchronize(s));
     p.norm_sorted = nn[1] < 0.6 * nn[0];
   }
-  const int grid = (int)(nunits < sm_count() ? nunits : sm_count());
+  const int grid = (int)(nunits < g.ctas_per_sm * sm_count() ? nunits : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
   if (debug_out) return SIMDEX_OK;
   SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
@@ -1611,7 +1626,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     SIMDEX_CUDA(cudaMemsetAsync(hops.p, 0, sizeof(int64_t) * rows_max, s));
     p.heap_ops = hops.p;
   }
-  grid = (int)(units_max < sm_count() ? units_max : sm_count());
+  grid = (int)(units_max < g.ctas_per_sm * sm_count() ? units_max : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
   if (stats) {
     std::vector<int64_t> hh(rows_max);
@@ -1733,7 +1748,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     SIMDEX_CUDA(cudaMemsetAsync(hops2.p, 0, sizeof(int64_t) * rows2, s));
     p2.heap_ops = hops2.p;
   }
-  grid = (int)(units2 < sm_count() ? units2 : sm_count());
+  grid = (int)(units2 < g.ctas_per_sm * sm_count() ? units2 : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma2, mb2, p2, g, grid, s))) return rc;
   if (stats) {
     std::vector<int64_t> hh(rows2);
@@ -1890,7 +1905,7 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   if ((rc = make_map(&ma, ua.p, nu_pad, kp))) return rc;
   if ((rc = make_map(&mb, ca.p, nc_pad, kp))) return rc;
   TopkParams tp = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu.p, g, f + 1, k_eff);
-  const int grid = (int)(nunits < sm_count() ? nunits : sm_count());
+  const int grid = (int)(nunits < g.ctas_per_sm * sm_count() ? nunits : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma, mb, tp, g, grid, s))) return rc;
   SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
