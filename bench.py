@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
@@ -70,17 +70,35 @@ class Clocks:
                  "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        self.skip = 0
+
+    def _rows(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7 and parts[0].isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        return rows
+
+    def start_region(self):
+        """Wait (<= 5 s) until the sampler is producing, then mark the start of
+        the timed region: only samples taken after this point are reported."""
+        if self.proc is None:
+            return
+        t0 = time.time()
+        while not self._rows() and time.time() - t0 < 5.0:
+            time.sleep(0.02)
+        self.skip = len(self._rows())
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         self.proc.wait()
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7 and parts[0].isdigit():
-                rows.append(parts)
+        rows = self._rows()[self.skip:]
         os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
@@ -251,6 +269,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clocks = Clocks(local)
+    clocks.start_region()
     _lib.profile(True)
     launches0 = _lib.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
