@@ -1167,38 +1167,46 @@ __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restric
   }
 }
 
-// packed row r of cluster j: user q_user[q_off[j] + (r - a_off[j])] or padding;
-// one thread per 16-byte vector of the packed row
+// packed row r of cluster j: user q_user[q_off[j] + (r - a_off[j])] or padding.
+// A warp per 32 packed rows: lane l locates row r0 + l's cluster (binary
+// search over a_off) once, then the warp copies the 32 rows' 16-byte vectors
 __global__ void ws_rows_kernel(const int64_t* __restrict__ q_user, const int64_t* __restrict__ q_perm,
                                const int64_t* __restrict__ q_off, const int64_t* __restrict__ a_off, int c,
                                int64_t rows_max, const uint16_t* __restrict__ ub, int kp,
                                const float* __restrict__ u_cu, uint16_t* __restrict__ a_pk, float* __restrict__ cu,
                                int64_t* __restrict__ row_user, int64_t* __restrict__ row_out,
                                int32_t* __restrict__ row_cluster) {
-  const int vpr = kp / 8;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t r = g / vpr;
-  const int v = (int)(g - r * vpr);
-  if (r >= rows_max || r >= a_off[c]) return;
-  int lo = 0, hi = c - 1;  // last j with a_off[j] <= r
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a_off[mid] <= r)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  const int j = lo;
-  const int64_t i = r - a_off[j];
-  const bool live = i < q_off[j + 1] - q_off[j];
-  const int64_t user = live ? q_user[q_off[j] + i] : -1;
-  reinterpret_cast<uint4*>(a_pk + r * kp)[v] =
-      live ? reinterpret_cast<const uint4*>(ub + user * kp)[v] : make_uint4(0, 0, 0, 0);
-  if (v == 0) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  const int64_t lim = rows_max < a_off[c] ? rows_max : a_off[c];
+  if (r0 >= lim) return;
+  const int64_t r = r0 + lane;
+  int64_t user = -1;
+  if (r < lim) {
+    int lo = 0, hi = c - 1;  // last j with a_off[j] <= r
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a_off[mid] <= r)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int j = lo;
+    const int64_t i = r - a_off[j];
+    const bool live = i < q_off[j + 1] - q_off[j];
+    user = live ? q_user[q_off[j] + i] : -1;
     cu[r] = live ? u_cu[user] : 0.f;
     row_user[r] = user;
     row_out[r] = live ? (q_perm ? q_perm[q_off[j] + i] : q_off[j] + i) : -1;
     row_cluster[r] = j;
+  }
+  const int vpr = kp / 8;
+  for (int e = lane; e < 32 * vpr; e += 32) {
+    const int i = e / vpr, v = e - i * vpr;
+    const int64_t ui = __shfl_sync(0xffffffffu, user, i);
+    if (r0 + i < lim)
+      reinterpret_cast<uint4*>(a_pk + (r0 + i) * kp)[v] =
+          ui >= 0 ? reinterpret_cast<const uint4*>(ub + ui * kp)[v] : make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -1226,10 +1234,11 @@ __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t
                                  const uint16_t* __restrict__ a_in, int kp, uint16_t* __restrict__ a2,
                                  float* __restrict__ cu2, float* __restrict__ t02, int64_t* __restrict__ user2,
                                  int64_t* __restrict__ out2, int32_t* __restrict__ clus2) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t nc = *n_cont;
-  if (r >= rows_max || r >= ((nc + kUnitRows - 1) / kUnitRows) * kUnitRows) return;
+  const int64_t lim = min(rows_max, ((nc + kUnitRows - 1) / kUnitRows) * kUnitRows);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < lim;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
   const bool live = r < nc;
   const int64_t src_row = live ? cont[r] : 0;
   const uint4* s = reinterpret_cast<const uint4*>(a_in + src_row * kp);
@@ -1241,6 +1250,7 @@ __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t
     user2[r] = live ? row_user[src_row] : -1;
     out2[r] = live ? row_out[src_row] : -1;
     clus2[r] = live ? row_cluster[src_row] : 0;
+  }
   }
 }
 
@@ -1606,7 +1616,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   SIMDEX_LAUNCH_CHECK("row_cu");
   // rows past a_off[c] stay "padding" (row_user = -1) and are skipped by finalize
   SIMDEX_CUDA(cudaMemsetAsync(row_user.p, 0xff, sizeof(int64_t) * rows_max, s));
-  ws_rows_kernel<<<(unsigned)ceil_div(rows_max * (kp / 8), 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off.p, c, rows_max, ub, kp,
+  ws_rows_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off.p, c, rows_max, ub, kp,
                                                                    ucu.p, a_pk.p, cu.p, row_user.p, row_out.p,
                                                                    rclus.p);
   SIMDEX_LAUNCH_CHECK("ws_rows");
@@ -1726,7 +1736,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   SIMDEX_CUDA(clus2.alloc(rows2, s));
   SIMDEX_CUDA(inrm.alloc(ni_pad, s));
   SIMDEX_CUDA(inmax.alloc(ni_pad / 32, s));
-  cont_rows_kernel<<<(unsigned)ceil_div(rows2, 8), 256, 0, s>>>(cont.p, cont_n.p, rows2, row_user.p, row_out.p, rclus.p,
+  cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 8), 8 * sm_count()), 256, 0, s>>>(cont.p, cont_n.p, rows2, row_user.p, row_out.p, rclus.p,
                                                                  cu.p, t0.p, a_pk.p, kp, a2.p, cu2.p, t02.p, user2.p,
                                                                  out2.p, clus2.p);
   SIMDEX_LAUNCH_CHECK("cont_rows");
