@@ -40,15 +40,22 @@ def item_shard(model: ModelPair, rank: int, world: int) -> tuple[ModelPair, int]
     return ModelPair(model.users, FactorMatrix(model.items.values[lo:hi])), lo
 
 
-def exchange_partials(ids: torch.Tensor, scores: torch.Tensor, id_offset: int, k: int, group=None):
-    """All-gather every rank's partial top-K (ids made global, padded to k
-    with id -1 / -inf) -> tensors [world, U, k] on the same device."""
-    world = dist.get_world_size(group)
+def pad_partial(ids: torch.Tensor, scores: torch.Tensor, id_offset: int, k: int):
+    """A shard's partial top-K with global ids, padded to k columns with
+    id -1 / score -inf (a shard may hold fewer than k items)."""
     u, kk = ids.shape
     pi = torch.full((u, k), -1, dtype=torch.int32, device=ids.device)
     ps = torch.full((u, k), float("-inf"), dtype=torch.float64, device=ids.device)
     pi[:, :kk] = torch.where(ids >= 0, ids + id_offset, ids)
     ps[:, :kk] = scores
+    return pi, ps
+
+
+def exchange_partials(ids: torch.Tensor, scores: torch.Tensor, id_offset: int, k: int, group=None):
+    """All-gather every rank's partial top-K (ids made global, padded to k
+    with id -1 / -inf) -> tensors [world, U, k] on the same device."""
+    world = dist.get_world_size(group)
+    pi, ps = pad_partial(ids, scores, id_offset, k)
     gi = [torch.empty_like(pi) for _ in range(world)]
     gs = [torch.empty_like(ps) for _ in range(world)]
     dist.all_gather(gi, pi, group=group)

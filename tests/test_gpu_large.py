@@ -96,3 +96,52 @@ def test_brute_force_early_exit_skewed_norms(sx, k, ln_sigma):
     res = sx.topk_matmul(m, k)
     sample = np.sort(np.random.default_rng(1).choice(m.num_users, 1500, replace=False))
     _check(res.item_ids, res.scores, m.users.values, m.items.values, k, sample, f"skewed K={k}")
+
+
+def test_catalog_sharded_shards_and_device_merge(sx):
+    """cfg5's data path on one GPU: the catalogue split into 4 contiguous
+    shards, each shard's exact top-100 by the tensor-core pass (early exit on
+    its norm-sorted operand), global ids, padded, merged on the device
+    (simdex_merge_topk) -- equal to the unsharded exact top-K."""
+    import torch
+    from paper_1706_01449_b200 import _ops, brute, sharding
+    rng = np.random.default_rng(4)
+    users = rng.normal(0.0, 1.0, (6_000, 128)).astype(np.float32)
+    items = rng.normal(0.0, 1.0, (30_001, 128))
+    items = (items * rng.lognormal(0.0, 0.7, items.shape[0])[:, None]).astype(np.float32)
+    m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    k, world = 100, 4
+    parts = []
+    for r in range(world):
+        part, off = sharding.item_shard(m, r, world)
+        ids, sc, _ = brute.topk_matmul_tensors(part, k)
+        parts.append(sharding.pad_partial(ids, sc, off, k))
+    gi = torch.stack([p[0] for p in parts]).contiguous()
+    gs = torch.stack([p[1] for p in parts]).contiguous()
+    got_i, got_s = _ops.merge_topk(gi, gs, k)
+    sample = np.sort(np.random.default_rng(0).choice(m.num_users, 400, replace=False))
+    _check(got_i.cpu().numpy(), got_s.cpu().numpy(), m.users.values, m.items.values, k, sample, "sharded K=100")
+
+
+def test_catalog_sharded_topk_nccl_single_rank(sx):
+    """catalog_sharded_topk itself over a one-rank NCCL group (the all-gather
+    and merge run for real; more ranks need more GPUs)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1706_01449_b200 import sharding
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29571")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(6)
+        users = rng.normal(0.0, 1.0, (3_000, 64)).astype(np.float32)
+        items = rng.normal(0.0, 1.0, (9_000, 64)).astype(np.float32)
+        m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+        ids, sc = sharding.catalog_sharded_topk(m, 20)
+        sample = np.sort(np.random.default_rng(1).choice(m.num_users, 300, replace=False))
+        _check(ids.cpu().numpy(), sc.cpu().numpy(), m.users.values, m.items.values, 20, sample, "nccl world 1")
+    finally:
+        dist.destroy_process_group()
