@@ -221,6 +221,23 @@ SIMDEX_API int simdex_query_ws(const double* users, const float* users32, const 
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
 
+/* simdex_query_ws with option bits (simdex_query_ws == options 0):
+ *   SIMDEX_WS_PREFIX_EXIT  the prefix pass ends a 128-query unit once every
+ *     query's certified K-th lower bound exceeds ||u|| x the list ceiling at
+ *     the next 128-item tile (Algorithm 1's own stop bound, index.py:225-227);
+ *     results are identical.  It pays when walks are short against B (the
+ *     optimizer's estimate, optimizer.py:117-145, well below B) and costs a
+ *     few percent otherwise. */
+#define SIMDEX_WS_PREFIX_EXIT 1
+SIMDEX_API int simdex_query_ws_opts(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,
+                    const double* items, const float* items32, const uint16_t* ib, const double* item_norms,
+                    const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                    int32_t f, int32_t kp, int32_t su, int32_t si,
+                    const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
+                    const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                    const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
+                    int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options, void* stream);
+
 /* Host-side statistics of this thread's last simdex_query_ws call (host
  * int64[5]): queries, queries that went on past B (second pass over the
  * catalogue), B' = min(B, n), n, f.  Lets a caller count the algorithmic

@@ -45,6 +45,8 @@ SIGNATURES = {
     "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
     "simdex_query_ws": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64, P,
                         P, P, I64, I32, P, P, P, P],
+    "simdex_query_ws_opts": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64,
+                             P, P, P, I64, I32, P, P, P, I32, P],
     "simdex_ws_stats": [P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],

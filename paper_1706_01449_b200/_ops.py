@@ -214,10 +214,14 @@ def group_queries(q_user, assign, c):
     return gq, perm, off
 
 
+WS_PREFIX_EXIT = 1  # SIMDEX_WS_PREFIX_EXIT
+
+
 def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k,
-             items32=None, users32=None):
+             items32=None, users32=None, options=0):
     """Work-sharing batch query; ``grouped`` = group_queries(...) output.
-    Returns (ids, scores, visited) in the original query order."""
+    Returns (ids, scores, visited) in the original query order.  ``options``:
+    WS_PREFIX_EXIT ends prefix units early on the list ceilings."""
     nu, f = users.shape
     ni = items.shape[0]
     c = list_ids.shape[0]
@@ -228,12 +232,14 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
-    call("simdex_query_ws", ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)), ptr(items32),
+    call("simdex_query_ws_opts", ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
+         ptr(items32),
          ptr(pi.op),
          ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),
          ptr(_c(list_pos, I32)),
          ptr(_c(bounds, F64)), c, int(block),
-         ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), stream_ptr())
+         ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), int(options),
+         stream_ptr())
     return ids, sc, vis
 
 

@@ -105,6 +105,13 @@ struct TopkParams {
   // can take another candidate (Cauchy-Schwarz against the remaining norms)
   int norm_sorted;
   float g_mul;  // (1/eps + 2)(1 + 2^-20): ||u|| + 2 eps ||u|| from eps ||u|| (scaled, rounded up)
+  float u_mul;  // (1/eps)(1 + 2^-20): ||u|| from eps ||u|| (scaled, rounded up)
+  // per operand tile (global tile id = b_row0 / 128 + t), when given: every
+  // item of tiles >= t of the unit's segment has score <= ||u|| exit_c and
+  // norm <= exit_m (scaled); otherwise (norm-sorted operand) both are the
+  // norm of the tile's first item
+  const float* exit_c;
+  const float* exit_m;
 };
 
 // three-input max (sm_100 FMNMX3)
@@ -217,10 +224,16 @@ __device__ __forceinline__ float top_at(const float (&t)[KT], int k) {
   return r;
 }
 
-template <int KT, bool EX>  // EX: early exit on a norm-sorted item operand
+// EXM: early exit mode -- 0 none; 1 norm-sorted operand (the next tile's
+// first norm bounds everything after it, checked every 4 tiles); 2 per-tile
+// bound arrays exit_c / exit_m (the work-sharing prefix's list ceilings,
+// checked after every tile)
+template <int KT, int EXM>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     gemm_topk_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const TopkParams p) {
+  constexpr bool EX = EXM != 0;
+  constexpr int XM = EXM == 2 ? 0 : 3;  // exit checks / end markers at tiles t with (t & XM) == 0
   constexpr bool kDebug = KT < 0;         // raw accumulators to p.debug_out, no selection
   constexpr int KTT = KT > 0 ? KT : 1;    // register top-K size (KT = 0: buffer re-selection)
   extern __shared__ uint8_t smem_raw[];
@@ -286,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             tma_load_2d(a_sm + (h * KB + kb) * kSlab, &map_a, a_full, kb * 64, (int)(un.a_row0 + h * kTileM));
         const int n_tiles = (un.n_items + kTileN - 1) / kTileN;
         for (int t = 0; t < n_tiles; ++t) {
-          bool stop = EX && t > 0 && (t & 3) == 0;
+          bool stop = EX && t > 0 && (t & XM) == 0;
           for (int w = 0; stop && w < kEpiWarps; ++w) {
             const long long e = wdone[w];
             stop = (int)(e >> 32) == u && (int)(e & 0xffffffffll) < t;
@@ -334,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           mbar_wait(t_empty + buf, (use & 1) ^ 1);
           mbar_wait(full + stage, phase);
           tc_fence_after();
-          if (EX && (t & 3) == 0 && t > 0 && stage_end[stage] == seq) {  // markers only replace tiles t = 4j  // end marker: pass it on to the epilogue
+          if (EX && (t & XM) == 0 && t > 0 && stage_end[stage] == seq) {  // end marker: pass it on to the epilogue
             mbar_arrive(empty + stage);
             buf_end[buf] = (int32_t)use;
             mbar_arrive(t_full + buf);
@@ -396,21 +409,33 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const float4* nm4p = reinterpret_cast<const float4*>(p.item_nmax32 + (un.b_row0 >> 5));
       float4 nm4_next = __ldg(nm4p);
       const float gu = cu * p.g_mul;  // ||u|| + 2 eps ||u||, scaled, rounded up
+      const float uu = cu * p.u_mul;  // ||u||, scaled, rounded up
+      const int64_t tile0 = un.b_row0 >> 7;
+      float ec_next = 0.f, em_next = 0.f;
+      if (EXM == 2 && n_tiles > 1) {
+        ec_next = __ldg(p.exit_c + tile0 + 1);
+        em_next = __ldg(p.exit_m + tile0 + 1);
+      }
       bool done = false;              // no row of this warp can take another candidate
       for (int t = 0; t < n_tiles; ++t, ++acc) {
         const uint32_t buf = acc & 1, use = acc >> 1;
         const float4 nm4 = nm4_next;
         if (t + 1 < n_tiles) nm4_next = __ldg(nm4p + t + 1);
+        const float ec = ec_next, em_ = em_next;  // bounds for the tiles after this one
+        if (EXM == 2 && t + 2 < n_tiles) {
+          ec_next = __ldg(p.exit_c + tile0 + t + 2);
+          em_next = __ldg(p.exit_m + tile0 + t + 2);
+        }
         mbar_wait(t_full + buf, use & 1);
         tc_fence_after();
-        if (EX && (t & 3) == 0 && t > 0 && buf_end[buf] == (int32_t)use) {  // the unit ended early
+        if (EX && (t & XM) == 0 && t > 0 && buf_end[buf] == (int32_t)use) {  // the unit ended early
           __syncwarp();
           if (lane == 0) mbar_arrive(t_empty + buf);
           ++acc;
           break;
         }
         bool released = false;
-        if (h < ntile_a) {
+        if (h < ntile_a && !(EX && done)) {
           const int tile_valid = min(kTileN, un.n_items - t * kTileN);
           // two chunks of 32 columns per TMEM wait; once the whole tile is in
           // registers the accumulator buffer goes back to the MMA warp
@@ -580,10 +605,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           __syncwarp();
           if (lane == 0) mbar_arrive(t_empty + buf);
         }
-        if (EX && !done && (t & 3) == 3 && t + 1 < n_tiles) {
+        if (EX && !done && ((t + 1) & XM) == 0 && t + 1 < n_tiles) {
           // every later item has ||i|| <= the next tile's first norm, so its
           // upper bound is at most ||u|| n + 2 (eps ||u|| n + e_abs)
-          const float bound = fmaf(gu, nm4_next.x, 2.f * p.e_abs) * (1.f + 0x1p-20f);
+          const float bound = (EXM == 2 ? fmaf(uu, ec, 2.f * fmaf(cu, em_, p.e_abs))
+                                        : fmaf(gu, nm4_next.x, 2.f * p.e_abs)) * (1.f + 0x1p-20f);
           if (__all_sync(0xffffffffu, !(live && !flags) || bound < T)) {
             done = true;
             if (lane == 0) wdone[ew] = ((long long)u << 32) | (long long)t;
@@ -1167,6 +1193,23 @@ __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restric
   }
 }
 
+// Stage-1 early-exit bounds per prefix tile (cluster j, tile t): the list's
+// ceiling at the tile's first position, scaled and rounded up, clamped at 0
+// (ceilings are non-increasing along the list and bound every member's score
+// / ||u||, index.py:90-100), and the largest item norm from the tile on.
+__global__ void prefix_exit_kernel(const double* __restrict__ bounds, int64_t n, int c, int64_t b_pad, int64_t bp,
+                                   double si_scale, const float* __restrict__ pnmax, float* __restrict__ exit_c,
+                                   float* __restrict__ exit_m) {
+  const int64_t per = b_pad / kTileN;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)c * per) return;
+  const int64_t j = g / per, pos = (g - j * per) * kTileN;
+  exit_c[g] = pos < bp ? fmaxf(0.f, __double2float_ru(bounds[j * n + pos] * si_scale)) : 0.f;
+  float m = 0.f;
+  for (int64_t ch = (j * b_pad + pos) >> 5; ch < ((j + 1) * b_pad) >> 5; ++ch) m = fmaxf(m, pnmax[ch]);
+  exit_m[g] = m;
+}
+
 // packed row r of cluster j: user q_user[q_off[j] + (r - a_off[j])] or padding.
 // A warp per 32 packed rows: lane l locates row r0 + l's cluster (binary
 // search over a_off) once, then the warp copies the 32 rows' 16-byte vectors
@@ -1358,7 +1401,7 @@ int geometry(int kp, GemmGeometry* g) {
 template <int KT>
 int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
                    cudaStream_t s) {
-  auto kern = p.norm_sorted ? gemm_topk_kernel<KT, true> : gemm_topk_kernel<KT, false>;
+  auto kern = p.exit_c ? gemm_topk_kernel<KT, 2> : p.norm_sorted ? gemm_topk_kernel<KT, 1> : gemm_topk_kernel<KT, 0>;
   SIMDEX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   ProfileScope _prof("gemm_topk", s);
   kern<<<grid, kThreads, g.smem, s>>>(ma, mb, p);
@@ -1446,6 +1489,8 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   p.row_flags = st.flags.p;
   p.row_T_out = st.rowT.p;
   p.g_mul = (float)((1.0 / eps_for(((f + 63) / 64) * 64) + 2.0) * (1.0 + 0x1p-20));
+  p.u_mul = (float)((1.0 / eps_for(((f + 63) / 64) * 64)) * (1.0 + 0x1p-20));
+
   return p;
 }
 
@@ -1574,7 +1619,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
-                 double* out_scores, int64_t* out_visited, cudaStream_t s) {
+                 double* out_scores, int64_t* out_visited, int32_t options, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   const bool no_ws = block == 0;  // every query walks the whole list (query_batch(work_sharing=False))
   const int64_t bp = block < ni ? block : ni;
@@ -1630,6 +1675,22 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
   if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
   TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
+  // early exit on the cluster ceilings (Algorithm 1's own stop bound): a
+  // unit stops once every row's threshold exceeds ||u|| x the next tile's
+  // ceiling; the prefix top-K is unchanged (later items cannot reach it)
+  Scratch<float> exit_c, exit_m;
+  if ((options & SIMDEX_WS_PREFIX_EXIT) && !getenv("SIMDEX_NO_EARLY_EXIT")) {
+    const int64_t nt = (int64_t)c * (b_pad / kTileN);
+    SIMDEX_CUDA(exit_c.alloc(nt, s));
+    SIMDEX_CUDA(exit_m.alloc(nt, s));
+    prefix_exit_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, s>>>(bounds, ni, c, b_pad, bp, std::ldexp(1.0, si),
+                                                                   pnmax.p, exit_c.p, exit_m.p);
+    SIMDEX_LAUNCH_CHECK("prefix_exit");
+    p.norm_sorted = 1;
+    p.exit_c = exit_c.p;
+    p.exit_m = exit_m.p;
+
+  }
   Scratch<int64_t> hops;
   if (stats) {
     SIMDEX_CUDA(hops.alloc(rows_max, s));

@@ -13,7 +13,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
-                 double* out_scores, int64_t* out_visited, cudaStream_t s);
+                 double* out_scores, int64_t* out_visited, int32_t options, cudaStream_t s);
 
 void read_ws_stats(int64_t* out);
 
@@ -98,6 +98,34 @@ extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int
   return SIMDEX_OK;
 }
 
+extern "C" int simdex_query_ws_opts(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,
+                               const double* items, const float* items32, const uint16_t* ib,
+                               const double* item_norms,
+                               const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
+                               int32_t su, int32_t si, const int32_t* list_ids,
+                               const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
+                               const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                               const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
+                               int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options,
+                                    void* stream) {
+  SIMDEX_CHECK_ARG(users && ub && user_norms && items && ib && item_norms && list_ids && list_pos && bounds &&
+                       (block == 0 || (prefix_b && prefix_norm)) && q_user && q_off && out_ids && out_scores &&
+                       out_visited,
+                   "simdex_query_ws_opts: null pointer");
+  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 0 && c >= 1 && kp % 64 == 0 && kp >= f,
+                   "simdex_query_ws_opts: bad sizes");
+  SIMDEX_CHECK_ARG(block == 0 || (b_pad % 128 == 0 && b_pad >= (block < ni ? block : ni)),
+                   "simdex_query_ws_opts: bad prefix padding");
+  const int64_t k_eff = k < ni ? k : ni;
+  SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
+                   "simdex_query_ws_opts: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);
+  if (nq == 0) return SIMDEX_OK;
+  return gemm_topk_ws(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, si,
+                      list_ids, list_pos,
+                      bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
+                      out_scores, out_visited, options, as_stream(stream));
+}
+
 extern "C" int simdex_query_ws(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,
                                const double* items, const float* items32, const uint16_t* ib,
                                const double* item_norms,
@@ -107,20 +135,7 @@ extern "C" int simdex_query_ws(const double* users, const float* users32, const 
                                const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
                                const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
                                int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
-  SIMDEX_CHECK_ARG(users && ub && user_norms && items && ib && item_norms && list_ids && list_pos && bounds &&
-                       (block == 0 || (prefix_b && prefix_norm)) && q_user && q_off && out_ids && out_scores &&
-                       out_visited,
-                   "simdex_query_ws: null pointer");
-  SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && block >= 0 && c >= 1 && kp % 64 == 0 && kp >= f,
-                   "simdex_query_ws: bad sizes");
-  SIMDEX_CHECK_ARG(block == 0 || (b_pad % 128 == 0 && b_pad >= (block < ni ? block : ni)),
-                   "simdex_query_ws: bad prefix padding");
-  const int64_t k_eff = k < ni ? k : ni;
-  SIMDEX_CHECK_ARG(k_eff <= kMaxMatmulK && kp <= kMaxKp,
-                   "simdex_query_ws: k_eff <= %d and f <= %d required (use simdex_walk)", kMaxMatmulK, kMaxKp);
-  if (nq == 0) return SIMDEX_OK;
-  return gemm_topk_ws(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, si,
-                      list_ids, list_pos,
-                      bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
-                      out_scores, out_visited, as_stream(stream));
+  return simdex_query_ws_opts(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows,
+                              ni, f, kp, su, si, list_ids, list_pos, bounds, c, block, prefix_b, prefix_norm, b_pad,
+                              q_user, q_perm, q_off, nq, k, out_ids, out_scores, out_visited, 0, stream);
 }

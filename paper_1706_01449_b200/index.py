@@ -333,6 +333,26 @@ def query_vector(index: CentroidIndex, model: ModelPair, vector, k: int) -> TopK
     return TopKResult(-1, _device.to_host(oi[0]).astype(np.int64), _device.to_host(os_[0]), int(ov[0].item()))
 
 
+# The prefix pass of work sharing ends a 128-query unit early (every query's
+# certified K-th above ||u|| x the list ceiling of the next tile) when the
+# optimizer's walk estimate for this index and K says walks are short against
+# B: below this fraction of B' the exit saves more tensor work than its
+# bookkeeping costs (measured: cfg4 K=10, mean walk 60 of 4,096, prefix pass
+# 1.32 -> 0.65 ms; cfg2 K=10, mean walk 1,677, +7 %).
+PREFIX_EXIT_FRACTION = 0.3
+
+
+def note_walk_estimate(index: CentroidIndex, k: int, mean_visited: float) -> None:
+    index._dev[("walk_estimate", int(k))] = float(mean_visited)
+
+
+def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int:
+    mv = index._dev.get(("walk_estimate", int(k)))
+    if not work_sharing or mv is None:
+        return 0
+    return _ops.WS_PREFIX_EXIT if mv < PREFIX_EXIT_FRACTION * min(index.block_size, n) else 0
+
+
 def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.Tensor, k: int,
                         work_sharing: bool = True):
     """Device form of query_batch: int64 user rows in, (ids int32 [n, k_eff],
@@ -358,7 +378,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
         block = index.block_size if work_sharing else 0
         prefix = index.device_prefix(model) if work_sharing else (None, None, 0)
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
-                             items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users))
+                             items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
+                             options=_ws_options(index, k, n, work_sharing))
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
     out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
     if work_sharing:  # k beyond the tensor-core envelope: WS visited = n if B >= n else max(B, walk visited)

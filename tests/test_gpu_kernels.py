@@ -126,6 +126,16 @@ def test_cfg2_full_size_against_reference(sx):
         np.testing.assert_array_equal(res.visited, g[f"ws_k{k}_visited"])
         nows = sx.query_batch(idx, m, sample[:500], k, work_sharing=False)
         np.testing.assert_array_equal(nows.visited, g[f"nows_k{k}_visited"])
+    # the same answers with the prefix pass's ceiling exit forced on (it is
+    # normally enabled only when the walk estimate is short against B)
+    from paper_1706_01449_b200 import index as I
+    for k in (1, 10, 50):
+        I.note_walk_estimate(idx, k, 0.0)
+        res = sx.query_batch(idx, m, sample, k, work_sharing=True)
+        assert_same_topk(res.item_ids, res.scores, g[f"ws_k{k}_ids"].astype(np.int64), g[f"ws_k{k}_scores"],
+                         ctx=f"cfg2 k={k} prefix exit")
+        np.testing.assert_array_equal(res.visited, g[f"ws_k{k}_visited"])
+        idx._dev.pop(("walk_estimate", k))
         est = sx.estimate_walk_length(idx, m, 0.001, k, seed=1)
         np.testing.assert_allclose([est.mean_visited, est.ci_low, est.ci_high, est.sample_size], g[f"est_k{k}"],
                                    rtol=1e-12)

@@ -71,6 +71,14 @@ def test_cfg4_index_work_sharing_full_size(sx, k):
     _check(res.item_ids, res.scores, m.users.values, m.items.values, k, sample, f"cfg4 K={k}")
     vis = np.asarray(res.visited)
     assert (vis >= 4096).all() and (vis <= m.num_items).all()
+    # with the walk estimate in place (short walks) the prefix pass exits on
+    # the list ceilings: identical ids, scores and visited for every user
+    est = sx.estimate_walk_length(idx, m, 0.001, k, seed=3)
+    assert est.mean_visited < 0.3 * 4096
+    res2 = sx.query_batch(idx, m, None, k, work_sharing=True)
+    np.testing.assert_array_equal(np.asarray(res2.item_ids), np.asarray(res.item_ids))
+    np.testing.assert_array_equal(np.asarray(res2.scores), np.asarray(res.scores))
+    np.testing.assert_array_equal(np.asarray(res2.visited), vis)
 
 
 def test_cfg5_catalogue_scale_full_size(sx):

@@ -9,6 +9,8 @@ w = W.CONFIGS[cfg]()
 m = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
 cl = sx.kmeans(m.users, w.clusters, max_iters=w.max_iters, seed=w.seed)
 idx = sx.build_index(m, cl, 4096)
+if os.environ.get("PROF_EST"):  # the optimizer's walk estimate (enables the prefix exit for short walks)
+    print("estimate", sx.estimate_walk_length(idx, m, 0.001, k, seed=w.seed).mean_visited)
 if len(sys.argv) > 3:  # timing experiment: SIMDEX_SKIP_EPI mode for the query only
     os.environ["SIMDEX_SKIP_EPI"] = sys.argv[3]
 for _ in range(3):
