@@ -213,7 +213,7 @@ def run_reference(args):
 def _profiled_traffic(path, k):
     """DRAM bytes per gemm_topk launch (read + write) from the committed ncu
     --set full capture of the same workload (profiles/), or None."""
-    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01g_gemm_topk_traffic.json")
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01h_gemm_topk_traffic.json")
     if path != "index" or k != 10 or not os.path.exists(f):
         return None
     with open(f) as fh:
