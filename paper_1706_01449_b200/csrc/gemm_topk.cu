@@ -495,15 +495,28 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) push_top<KTT>(top, v[i] - em);
                     T = fmaxf(T, KTT == kk + 1 ? top[KTT - 1] : top_at<KTT>(top, kk));
-                    // only the items that reach the new threshold are stored
-                    // (compile-time register indices, a running store slot)
+                    if constexpr (EXM == 2) {
+                      // prefix units that end within a few tiles: plain vector
+                      // stores of all 32 (finalize drops those below T)
+                      float4* dh = reinterpret_cast<float4*>(my_hi);
+                      int4* di = reinterpret_cast<int4*>(my_id);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                      const float hi = v[i] + em;
-                      if (hi >= T) {
-                        my_hi[cnt] = hi;
-                        my_id[cnt] = c0 + i;
-                        ++cnt;
+                      for (int q4 = 0; q4 < 8; ++q4) {
+                        dh[q4] = make_float4(v[4 * q4] + em, v[4 * q4 + 1] + em, v[4 * q4 + 2] + em, v[4 * q4 + 3] + em);
+                        di[q4] = make_int4(c0 + 4 * q4, c0 + 4 * q4 + 1, c0 + 4 * q4 + 2, c0 + 4 * q4 + 3);
+                      }
+                      cnt = 32;
+                    } else {
+                      // only the items that reach the new threshold are stored
+                      // (compile-time register indices, a running store slot)
+#pragma unroll
+                      for (int i = 0; i < 32; ++i) {
+                        const float hi = v[i] + em;
+                        if (hi >= T) {
+                          my_hi[cnt] = hi;
+                          my_id[cnt] = c0 + i;
+                          ++cnt;
+                        }
                       }
                     }
                     hops += cnt;
