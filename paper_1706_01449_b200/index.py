@@ -337,9 +337,10 @@ def query_vector(index: CentroidIndex, model: ModelPair, vector, k: int) -> TopK
 # certified K-th above ||u|| x the list ceiling of the next tile) when the
 # optimizer's walk estimate for this index and K says walks are short against
 # B: below this fraction of B' the exit saves more tensor work than its
-# bookkeeping costs (measured: cfg4 K=10, mean walk 60 of 4,096, prefix pass
-# 1.32 -> 0.65 ms; cfg2 K=10, mean walk 1,677, +7 %).
-PREFIX_EXIT_FRACTION = 0.3
+# bookkeeping costs (tools/exit_ab.py, all-user serve: cfg4 K=10, mean walk
+# 47 of 4,096, 2.95 -> 2.10 ms; cfg2 K=5, walk 0.30 B', 0.97 -> 0.95 ms;
+# cfg2 K=10, walk 0.44 B', break-even; cfg2 K=50, walk B', +2 %).
+PREFIX_EXIT_FRACTION = 0.4
 
 
 def note_walk_estimate(index: CentroidIndex, k: int, mean_visited: float) -> None:
