@@ -283,6 +283,10 @@ def run_ours(args):
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_sorted = sorted(step_ms)
+    step_stats = {"median": statistics.median(step_ms), "p90": step_sorted[min(len(step_sorted) - 1,
+                                                                              int(0.9 * len(step_sorted)))],
+                  "min": step_sorted[0], "max": step_sorted[-1]}
     total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.barrier()
@@ -396,7 +400,7 @@ def run_ours(args):
                        "per_rank_users": nu, "parallelism": f"users-dp{world} (each rank serves the full batch)",
                        "l2": "flushed (256 MB write) before every timed step",
                        "setup_seconds": {"cluster": t_cluster, "build": t_build}},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "e2e_serve": e2e_serve, "clocks": clk,
+            "step_ms": step_stats, "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "e2e_serve": e2e_serve, "clocks": clk,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)

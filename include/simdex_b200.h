@@ -11,7 +11,14 @@
  *     comment says "host";  matrices are row-major and dense;
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
  *     all work is enqueued on it, nothing synchronises the host unless the
- *     comment says so;
+ *     comment says so.  The serving calls (simdex_topk_matmul_ctx,
+ *     simdex_query_ws*) allocate nothing per call (their scratch lives in an
+ *     execution context, see simdex_ctx_create) and keep every count on the
+ *     device, so they can run ahead of the GPU and be captured in a CUDA
+ *     graph.  Host-synchronising entry points: simdex_topk_matmul (legacy
+ *     form: reads two item norms to pick the early exit), simdex_topk_exact
+ *     with k_eff > 4096, simdex_kmeans_seed's degenerate branch (host RNG),
+ *     simdex_profile_read;
  *   - factor matrices are float64 [rows, f] like the reference's FactorMatrix
  *     (model_io.py:37-48);  item ids / list positions are int32 (|I| < 2^31);
  *     user ids are int64;
@@ -59,6 +66,19 @@ SIMDEX_API int64_t simdex_launch_count(void);
 SIMDEX_API int simdex_profile_enable(int on);
 SIMDEX_API int simdex_profile_read(const char* name, double* total_ms, int64_t* launches);
 SIMDEX_API int simdex_profile_reset(void);
+/* Execution contexts.  A context owns a device workspace arena (grown on
+ * demand, stream-ordered, reused by every later call) and pinned host
+ * statistic slots; calls that take `ctx` carve their scratch from it instead
+ * of allocating.  ctx == NULL selects the calling thread's default context
+ * for the current device (what the legacy entry points use).  A context
+ * serves one call at a time; successive calls on different streams are
+ * ordered through an event.  Replaces the per-call numpy temporaries of the
+ * reference (brute.py:86-107, index.py:351-389) with one resident arena. */
+SIMDEX_API int simdex_ctx_create(int device, void** out_ctx);
+SIMDEX_API int simdex_ctx_destroy(void* ctx);
+/* current arena size of `ctx` in bytes (host output) */
+SIMDEX_API int simdex_ctx_workspace_bytes(void* ctx, int64_t* out_bytes);
+
 /* sm count / compute capability of `device` (host outputs). */
 SIMDEX_API int simdex_device_info(int device, int* sm_count, int* cc_major, int* cc_minor);
 
@@ -102,6 +122,21 @@ SIMDEX_API int simdex_topk_matmul(const double* users, const float* users32, con
                        const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                        int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k,
                        int32_t* out_ids, double* out_scores, int64_t* heap_ops, void* stream);
+
+/* simdex_topk_matmul in an execution context with option bits:
+ *   SIMDEX_MM_NORM_EXIT  item_perm is a descending-norm order and the pass
+ *     stops streaming a unit once no later item can enter any row's
+ *     certified band (Cauchy-Schwarz); pays on skewed norms;
+ *   SIMDEX_MM_NORM_AUTO  decide NORM_EXIT from the operand (reads the largest
+ *     and the median norm: one host synchronisation).
+ * Without NORM_AUTO the call never synchronises the host. */
+#define SIMDEX_MM_NORM_EXIT 2
+#define SIMDEX_MM_NORM_AUTO 4
+SIMDEX_API int simdex_topk_matmul_ctx(void* ctx, const double* users, const float* users32, const uint16_t* ub,
+                       const double* u_norm, int64_t nu, const double* items, const float* items32,
+                       const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows,
+                       int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k,
+                       int32_t* out_ids, double* out_scores, int64_t* heap_ops, int32_t options, void* stream);
 
 /* ------------------------------------------------------------------------
  * Clustering (clustering.py)
@@ -238,10 +273,23 @@ SIMDEX_API int simdex_query_ws_opts(const double* users, const float* users32, c
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options, void* stream);
 
+/* simdex_query_ws_opts in an execution context (NULL: the thread default). */
+SIMDEX_API int simdex_query_ws_ctx(void* ctx, const double* users, const float* users32, const uint16_t* ub,
+                    const double* user_norms, int64_t nu,
+                    const double* items, const float* items32, const uint16_t* ib, const double* item_norms,
+                    const int32_t* item_perm, int64_t ib_rows, int64_t ni,
+                    int32_t f, int32_t kp, int32_t su, int32_t si,
+                    const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
+                    const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                    const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
+                    int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options, void* stream);
+
 /* Host-side statistics of this thread's last simdex_query_ws call (host
  * int64[5]): queries, queries that went on past B (second pass over the
  * catalogue), B' = min(B, n), n, f.  Lets a caller count the algorithmic
- * tensor work 2*f*(nq*B' + n_cont*n) of the call. */
+ * tensor work 2*f*(nq*B' + n_cont*n) of the call.  The continuing count is
+ * copied to the host asynchronously: read it after the call's stream has
+ * synchronised. */
 SIMDEX_API int simdex_ws_stats(int64_t* out5);
 
 /* Group queries by their cluster (index.py:346-348), stable in query order:

@@ -30,10 +30,15 @@ SIGNATURES = {
     "simdex_profile_read": [C.c_char_p, P, P],
     "simdex_profile_reset": [],
     "simdex_device_info": [C.c_int, P, P, P],
+    "simdex_ctx_create": [C.c_int, P],
+    "simdex_ctx_destroy": [P],
+    "simdex_ctx_workspace_bytes": [P, P],
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
     "simdex_max_abs": [P, I64, P, P],
     "simdex_pack_f16": [P, I64, I32, I32, I64, I32, P, P, P],
     "simdex_topk_matmul": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, P],
+    "simdex_topk_matmul_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, I32,
+                               P],
     "simdex_norm_order": [P, I64, P, P],
     "simdex_to_f32": [P, I64, P, P, P],
     "simdex_kmeans_seed": [P, P, I64, I32, I32, I64, P, P, P, P, P],
@@ -47,6 +52,8 @@ SIGNATURES = {
                         P, P, I64, I32, P, P, P, P],
     "simdex_query_ws_opts": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64,
                              P, P, P, I64, I32, P, P, P, I32, P],
+    "simdex_query_ws_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P,
+                            I64, P, P, P, I64, I32, P, P, P, I32, P],
     "simdex_ws_stats": [P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
@@ -126,6 +133,13 @@ def ws_stats():
     buf = (C.c_int64 * 5)()
     call("simdex_ws_stats", C.cast(buf, C.c_void_p))
     return tuple(int(x) for x in buf)
+
+
+def workspace_bytes() -> int:
+    """Arena size of this thread's default execution context on the current device."""
+    out = C.c_int64(0)
+    call("simdex_ctx_workspace_bytes", None, C.byref(out))
+    return out.value
 
 
 def ptr(t):

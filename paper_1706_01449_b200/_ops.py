@@ -41,6 +41,7 @@ class Packed:
     rows: int
     perm: torch.Tensor | None = None   # operand row -> item id (norm-sorted operand), else None
     rows_pad: int = 0                  # rows of the fp16 operand
+    norm_exit: bool = False            # norm-sorted and skewed enough for the brute-force early exit
 
 
 ROW_PAD = 256
@@ -57,7 +58,11 @@ def norm_sorted(p: Packed) -> Packed:
     onorm = torch.empty((1, rows_pad), dtype=F64, device=p.op.device)
     call("simdex_build_prefix", ptr(p.op), ptr(p.norms), p.rows, p.kp, ptr(perm), 1, p.rows, rows_pad, ptr(out),
          ptr(onorm), stream_ptr())
-    return Packed(out.view(rows_pad, p.kp), onorm.view(rows_pad), p.scale_exp, p.kp, p.rows, perm, rows_pad)
+    # the exit's extra control flow costs ~14 % where nothing can be skipped
+    # (i.i.d. norms); decided once per operand from the largest and median norm
+    top, mid = (float(v) for v in onorm.view(-1)[torch.tensor([0, p.rows // 2], device=onorm.device)].tolist())
+    skewed = p.rows >= 256 and mid < 0.6 * top
+    return Packed(out.view(rows_pad, p.kp), onorm.view(rows_pad), p.scale_exp, p.kp, p.rows, perm, rows_pad, skewed)
 
 
 def pack(x: torch.Tensor, max_abs: float) -> Packed:
@@ -91,10 +96,10 @@ def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32
     ids = torch.empty((nu, k_eff), dtype=I32, device=users.device)
     sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
-    call("simdex_topk_matmul", ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu,
+    call("simdex_topk_matmul_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu,
          ptr(_c(items, F64)), ptr(items32), ptr(pi.op), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
-         pu.scale_exp,
-         pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), stream_ptr())
+         pu.scale_exp, pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), MM_NORM_EXIT if pi.norm_exit else 0,
+         stream_ptr())
     return ids, sc, hops
 
 
@@ -215,6 +220,7 @@ def group_queries(q_user, assign, c):
 
 
 WS_PREFIX_EXIT = 1  # SIMDEX_WS_PREFIX_EXIT
+MM_NORM_EXIT = 2    # SIMDEX_MM_NORM_EXIT
 
 
 def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k,
@@ -232,7 +238,7 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix
-    call("simdex_query_ws_opts", ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
+    call("simdex_query_ws_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
          ptr(items32),
          ptr(pi.op),
          ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),

@@ -29,14 +29,31 @@ struct Pending {
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_event_pool;  // recycled events: no cudaEventCreate in a timed loop
 std::map<std::string, std::pair<double, int64_t>> g_prof_acc;
+
+cudaEvent_t pooled_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
 }  // namespace
 
 ProfileScope::ProfileScope(const char* name, cudaStream_t s) : s_(s) {
   if (!g_prof_on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
   name_ = name;
-  cudaEventCreate(&a_);
-  cudaEventCreate(&b_);
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    a_ = pooled_event();
+    b_ = pooled_event();
+  }
   cudaEventRecord(a_, s);
   on_ = true;
 }
@@ -47,6 +64,91 @@ void ProfileScope::end() {
   cudaEventRecord(b_, s_);
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_pending.push_back(Pending{name_, a_, b_});
+}
+
+// ---------------------------------------------------------------------------
+// execution context
+// ---------------------------------------------------------------------------
+struct Ctx {
+  int device = 0;
+  char* arena = nullptr;
+  size_t cap = 0;
+  cudaStream_t last = nullptr;  // stream of the previous call
+  cudaEvent_t done = nullptr;   // end of the previous call on `last`
+  bool have_done = false;
+  bool busy = false;
+  int64_t* host = nullptr;  // pinned statistics slots
+};
+
+namespace {
+constexpr int kHostSlots = 16;
+
+int ctx_init(Ctx* c, int device) {
+  c->device = device;
+  SIMDEX_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+  SIMDEX_CUDA(cudaMallocHost(&c->host, kHostSlots * sizeof(int64_t)));
+  memset(c->host, 0, kHostSlots * sizeof(int64_t));
+  return SIMDEX_OK;
+}
+}  // namespace
+
+Ctx* ctx_or_default(void* ctx) {
+  if (ctx) return reinterpret_cast<Ctx*>(ctx);
+  static thread_local std::map<int, Ctx*> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = per_device.find(dev);
+  if (it != per_device.end()) return it->second;
+  Ctx* c = new Ctx();
+  if (ctx_init(c, dev) != SIMDEX_OK) {
+    delete c;
+    return nullptr;
+  }
+  per_device[dev] = c;
+  return c;
+}
+
+int64_t* ctx_host_slots(Ctx* c) { return c->host; }
+
+Workspace::Workspace(Ctx* c, cudaStream_t s) : c_(c), s_(s) {}
+
+int Workspace::commit() {
+  if (!c_) {
+    set_error("no execution context");
+    return SIMDEX_ECUDA;
+  }
+  if (c_->busy) {
+    set_error("execution context already in use by an enclosing call");
+    return SIMDEX_EINVAL;
+  }
+  // order this call after the context's previous call when the stream changed
+  if (c_->have_done && c_->last != s_) SIMDEX_CUDA(cudaStreamWaitEvent(s_, c_->done, 0));
+  size_t need = 0;
+  for (auto& r : reqs_) need += (r.bytes + 255) & ~size_t(255);
+  if (need > c_->cap) {
+    size_t grow = (need + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    if (c_->arena) SIMDEX_CUDA(cudaFreeAsync(c_->arena, s_));
+    c_->arena = nullptr;
+    c_->cap = 0;
+    keep_pool_warm();
+    SIMDEX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c_->arena), grow, s_));
+    c_->cap = grow;
+  }
+  size_t off = 0;
+  for (auto& r : reqs_) {
+    *r.p = c_->arena + off;
+    off += (r.bytes + 255) & ~size_t(255);
+  }
+  c_->busy = true;
+  committed_ = true;
+  return SIMDEX_OK;
+}
+
+Workspace::~Workspace() {
+  if (!committed_) return;
+  c_->busy = false;
+  c_->last = s_;
+  c_->have_done = cudaEventRecord(c_->done, s_) == cudaSuccess;
 }
 
 void set_error(const char* fmt, ...) {
@@ -96,6 +198,46 @@ extern "C" const char* simdex_last_error(void) { return g_err; }
 
 extern "C" int64_t simdex_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+extern "C" int simdex_ctx_create(int device, void** out_ctx) {
+  SIMDEX_CHECK_ARG(out_ctx, "simdex_ctx_create: null pointer");
+  int prev = 0;
+  SIMDEX_CUDA(cudaGetDevice(&prev));
+  SIMDEX_CUDA(cudaSetDevice(device));
+  Ctx* c = new Ctx();
+  int rc = ctx_init(c, device);
+  cudaSetDevice(prev);
+  if (rc != SIMDEX_OK) {
+    delete c;
+    return rc;
+  }
+  *out_ctx = c;
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_ctx_destroy(void* ctx) {
+  if (!ctx) return SIMDEX_OK;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  SIMDEX_CHECK_ARG(!c->busy, "simdex_ctx_destroy: context in use");
+  int prev = 0;
+  SIMDEX_CUDA(cudaGetDevice(&prev));
+  SIMDEX_CUDA(cudaSetDevice(c->device));
+  if (c->have_done) cudaEventSynchronize(c->done);
+  if (c->arena) cudaFree(c->arena);
+  if (c->done) cudaEventDestroy(c->done);
+  if (c->host) cudaFreeHost(c->host);
+  cudaSetDevice(prev);
+  delete c;
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_ctx_workspace_bytes(void* ctx, int64_t* out_bytes) {
+  SIMDEX_CHECK_ARG(out_bytes, "simdex_ctx_workspace_bytes: null pointer");
+  Ctx* c = ctx_or_default(ctx);
+  SIMDEX_CHECK_ARG(c, "simdex_ctx_workspace_bytes: no context");
+  *out_bytes = (int64_t)c->cap;
+  return SIMDEX_OK;
+}
+
 extern "C" int simdex_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof_on = on != 0;
@@ -112,8 +254,8 @@ extern "C" int simdex_profile_read(const char* name, double* total_ms, int64_t* 
     auto& acc = g_prof_acc[p.name];
     acc.first += ms;
     acc.second += 1;
-    cudaEventDestroy(p.a);
-    cudaEventDestroy(p.b);
+    g_event_pool.push_back(p.a);
+    g_event_pool.push_back(p.b);
   }
   g_pending.clear();
   auto it = g_prof_acc.find(name);
@@ -126,8 +268,8 @@ extern "C" int simdex_profile_reset(void) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   for (auto& p : g_pending) {
     cudaEventSynchronize(p.b);
-    cudaEventDestroy(p.a);
-    cudaEventDestroy(p.b);
+    g_event_pool.push_back(p.a);
+    g_event_pool.push_back(p.b);
   }
   g_pending.clear();
   g_prof_acc.clear();

@@ -7,6 +7,7 @@
 
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/simdex_b200.h"
 
@@ -85,6 +86,43 @@ struct Scratch {
 int sm_count();
 
 // ---------------------------------------------------------------------------
+// Execution context (simdex_ctx_*): a device workspace arena reused across
+// calls, so the serving entry points allocate nothing and never synchronise
+// the host; a pinned host word per statistic; cross-stream ordering.  NULL
+// in the C-ABI selects the calling thread's default context for the current
+// device.  One call at a time per context (the default one is per thread).
+// ---------------------------------------------------------------------------
+struct Ctx;
+Ctx* ctx_or_default(void* ctx);
+// pinned host int64 slots of the context (valid after the stream synchronises)
+int64_t* ctx_host_slots(Ctx* c);
+
+// Typed buffers carved out of the context arena for ONE call: add() every
+// buffer first, then commit() (grows the arena stream-ordered when needed,
+// orders this stream after the context's previous stream, assigns pointers).
+// The destructor records the end of the call for the next one's ordering.
+class Workspace {
+ public:
+  Workspace(Ctx* c, cudaStream_t s);
+  ~Workspace();
+  template <class T>
+  void add(T** p, size_t count) {
+    reqs_.push_back(Req{reinterpret_cast<void**>(p), (count == 0 ? 1 : count) * sizeof(T)});
+  }
+  int commit();
+
+ private:
+  struct Req {
+    void** p;
+    size_t bytes;
+  };
+  Ctx* c_;
+  cudaStream_t s_;
+  std::vector<Req> reqs_;
+  bool committed_ = false;
+};
+
+// ---------------------------------------------------------------------------
 // Result ordering: (score desc, id asc)  -- index.py:158-163
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ bool ranks_before(double sa, int32_t ia, double sb, int32_t ib) {
@@ -131,6 +169,16 @@ int exact_topk_rows(const double* users, const double* items, int64_t ni, int32_
 int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni, int32_t f, const int64_t* rows,
                            int64_t n_rows, int32_t k, const int64_t* out_map, int32_t* out_ids, double* out_scores,
                            cudaStream_t s);
+
+// Exact float64 top-K of a DEVICE-counted row list (the band-overflow
+// fallback of the tensor-core passes; no host round trip): for r < *n_rows,
+// user row = user_of ? user_of[rows[r]] : rows[r], written to output row
+// out_map[r].  `slab` is float64 [exact_slab_ctas(ni), ni] scratch.  k_eff <= 1024.
+int exact_slab_ctas(int64_t ni);
+int exact_topk_devcount(const double* users, const float* users32, const double* items, const float* items32,
+                        int64_t ni, int32_t f, const int64_t* rows, const int64_t* user_of, const int32_t* n_rows,
+                        int32_t k, const int64_t* out_map, int32_t* out_ids, double* out_scores, double* slab,
+                        cudaStream_t s);
 
 // Merge `parts` sorted lists per row.
 int merge_lists(const int32_t* in_ids, const double* in_scores, int32_t parts, int64_t nu, int32_t kk,

@@ -99,19 +99,15 @@ __device__ void block_bitonic(Entry* e, int n) {
   __syncthreads();
 }
 
-// One CTA per row: exact top-k_eff of S[row, :ni].
-__global__ void __launch_bounds__(256) select_rows_kernel(const double* __restrict__ S, int64_t ni, int k_eff,
-                                                          int pow2, int32_t* __restrict__ out_ids,
-                                                          double* __restrict__ out_scores, int64_t out_row0,
-                                                          const int64_t* __restrict__ out_map) {
-  extern __shared__ unsigned char smem_raw[];
-  Entry* buf = reinterpret_cast<Entry*>(smem_raw);
+// The calling CTA's exact top-k_eff of row[0, ni) into out_ids / out_scores
+// [k_eff] (buf: pow2 entries of shared memory).
+__device__ void select_row_block(const double* __restrict__ row, int64_t ni, int k_eff, int pow2, Entry* buf,
+                                 int32_t* __restrict__ o_ids, double* __restrict__ o_scores) {
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix;
   __shared__ int s_need;
   __shared__ int s_nlt, s_neq_base;
   __shared__ int warp_cnt[8];
-  const double* row = S + (int64_t)blockIdx.x * ni;
 
   uint64_t prefix = 0, mask = 0;
   int need = k_eff;  // rank (1-based) of the wanted key among keys matching prefix
@@ -176,11 +172,55 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
   }
   for (int i = k_eff + threadIdx.x; i < pow2; i += blockDim.x) buf[i] = Entry{-DBL_MAX, INT32_MAX};
   block_bitonic(buf, pow2);
+  for (int i = threadIdx.x; i < k_eff; i += blockDim.x) {
+    o_ids[i] = buf[i].id;
+    o_scores[i] = buf[i].s;
+  }
+  __syncthreads();
+}
+
+// One CTA per row: exact top-k_eff of S[row, :ni].
+__global__ void __launch_bounds__(256) select_rows_kernel(const double* __restrict__ S, int64_t ni, int k_eff,
+                                                          int pow2, int32_t* __restrict__ out_ids,
+                                                          double* __restrict__ out_scores, int64_t out_row0,
+                                                          const int64_t* __restrict__ out_map) {
+  extern __shared__ unsigned char smem_raw[];
+  Entry* buf = reinterpret_cast<Entry*>(smem_raw);
   const int64_t orow = out_map ? out_map[out_row0 + blockIdx.x] : out_row0 + blockIdx.x;
   const int64_t o = orow * (int64_t)k_eff;
-  for (int i = threadIdx.x; i < k_eff; i += blockDim.x) {
-    out_ids[o + i] = buf[i].id;
-    out_scores[o + i] = buf[i].s;
+  select_row_block(S + (int64_t)blockIdx.x * ni, ni, k_eff, pow2, buf, out_ids + o, out_scores + o);
+}
+
+// Device-counted rows (the tensor-core passes' band-overflow fallback): a
+// persistent CTA per slab row scores its user against every item in float64
+// (factor order, like score_f64_kernel) into the slab, then selects.
+template <class U, class I>
+__global__ void __launch_bounds__(256) exact_rows_dev_kernel(const U* __restrict__ users, const I* __restrict__ items,
+                                                             int64_t ni, int f, const int64_t* __restrict__ rows,
+                                                             const int64_t* __restrict__ user_of,
+                                                             const int32_t* __restrict__ n_rows, int k_eff, int pow2,
+                                                             const int64_t* __restrict__ out_map,
+                                                             int32_t* __restrict__ out_ids,
+                                                             double* __restrict__ out_scores, double* __restrict__ slab) {
+  extern __shared__ unsigned char smem_raw[];
+  Entry* buf = reinterpret_cast<Entry*>(smem_raw);
+  double* urow = reinterpret_cast<double*>(smem_raw + (size_t)pow2 * sizeof(Entry));
+  const int n = *n_rows;
+  double* row = slab + (int64_t)blockIdx.x * ni;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    int64_t u = rows[r];
+    if (user_of) u = user_of[u];
+    for (int q = threadIdx.x; q < f; q += blockDim.x) urow[q] = (double)users[u * f + q];
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < ni; j += blockDim.x) {
+      const I* x = items + j * f;
+      double acc = 0.0;
+      for (int q = 0; q < f; ++q) acc = fma(urow[q], (double)x[q], acc);
+      row[j] = acc;
+    }
+    __syncthreads();
+    const int64_t o = out_map[r] * (int64_t)k_eff;
+    select_row_block(row, ni, k_eff, pow2, buf, out_ids + o, out_scores + o);
   }
 }
 
@@ -287,6 +327,46 @@ int exact_topk_rows_mapped(const double* users, const double* items, int64_t ni,
       SIMDEX_LAUNCH_CHECK("take_prefix");
     }
   }
+  return SIMDEX_OK;
+}
+
+int exact_slab_ctas(int64_t ni) {
+  int64_t g = (int64_t(32) << 20) / (ni > 0 ? ni : 1);  // 256 MB of float64 rows
+  const int64_t mx = 2 * (int64_t)sm_count();
+  return (int)(g < 1 ? 1 : g > mx ? mx : g);
+}
+
+int exact_topk_devcount(const double* users, const float* users32, const double* items, const float* items32,
+                        int64_t ni, int32_t f, const int64_t* rows, const int64_t* user_of, const int32_t* n_rows,
+                        int32_t k, const int64_t* out_map, int32_t* out_ids, double* out_scores, double* slab,
+                        cudaStream_t s) {
+  const int k_eff = (int)(k < ni ? k : ni);
+  int pow2 = 1;
+  while (pow2 < k_eff) pow2 <<= 1;
+  const size_t smem = (size_t)pow2 * sizeof(Entry) + (size_t)f * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_error("exact fallback: k_eff %d / f %d too large", k_eff, f);
+    return SIMDEX_EUNSUPPORTED;
+  }
+  const int grid = exact_slab_ctas(ni);
+#define SIMDEX_EXACT_DEV(U, I, uu, ii)                                                                       \
+  do {                                                                                                     \
+    if (smem > 48 * 1024)                                                                                  \
+      SIMDEX_CUDA(cudaFuncSetAttribute(exact_rows_dev_kernel<U, I>,                                        \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));           \
+    exact_rows_dev_kernel<U, I><<<grid, 256, smem, s>>>(uu, ii, ni, f, rows, user_of, n_rows, k_eff, pow2,  \
+                                                        out_map, out_ids, out_scores, slab);               \
+  } while (0)
+  if (users32 && items32)
+    SIMDEX_EXACT_DEV(float, float, users32, items32);
+  else if (users32)
+    SIMDEX_EXACT_DEV(float, double, users32, items);
+  else if (items32)
+    SIMDEX_EXACT_DEV(double, float, users, items32);
+  else
+    SIMDEX_EXACT_DEV(double, double, users, items);
+#undef SIMDEX_EXACT_DEV
+  SIMDEX_LAUNCH_CHECK("exact_rows_dev");
   return SIMDEX_OK;
 }
 

@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include <cuda_fp16.h>
@@ -1136,24 +1137,19 @@ __global__ void fallback_visited_kernel(const int64_t* __restrict__ rows, const 
                                         const double* __restrict__ bounds, const double* __restrict__ unorm, int64_t n,
                                         int64_t prefix, int k_eff, const int32_t* __restrict__ out_ids,
                                         const double* __restrict__ out_scores, int64_t* __restrict__ out_visited) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= *n_rows) return;
-  const int64_t r = rows[i];
-  const int64_t user = row_user[r], out = row_out[r];
-  const int c = row_cluster[r];
-  int64_t mp = -1;
-  for (int t = 0; t < k_eff; ++t) mp = max(mp, (int64_t)list_pos[(int64_t)c * n + out_ids[out * k_eff + t]]);
-  const int64_t q = ceiling_count(bounds + (int64_t)c * n, n, unorm[user], out_scores[out * k_eff + k_eff - 1]);
-  int64_t v = max(max(mp + 1, (int64_t)k_eff), q);
-  if (v > n) v = n;
-  if (v < prefix) v = prefix;
-  out_visited[out] = v;
-}
-
-__global__ void fallback_users_kernel(const int64_t* __restrict__ rows, const int32_t* n_rows,
-                                      const int64_t* __restrict__ row_user, int64_t* __restrict__ users_out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < *n_rows) users_out[i] = row_user[rows[i]];
+  const int64_t cnt = *n_rows;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rows[i];
+    const int64_t user = row_user[r], out = row_out[r];
+    const int c = row_cluster[r];
+    int64_t mp = -1;
+    for (int t = 0; t < k_eff; ++t) mp = max(mp, (int64_t)list_pos[(int64_t)c * n + out_ids[out * k_eff + t]]);
+    const int64_t q = ceiling_count(bounds + (int64_t)c * n, n, unorm[user], out_scores[out * k_eff + k_eff - 1]);
+    int64_t v = max(max(mp + 1, (int64_t)k_eff), q);
+    if (v > n) v = n;
+    if (v < prefix) v = prefix;
+    out_visited[out] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1335,7 +1331,35 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// A tensor map is a pure function of (address, rows, kp): cached per thread,
+// so a serving call encodes nothing after its first run.
+struct MapKey {
+  const void* ptr;
+  int64_t rows;
+  int kp;
+  bool operator<(const MapKey& o) const {
+    return ptr != o.ptr ? ptr < o.ptr : rows != o.rows ? rows < o.rows : kp < o.kp;
+  }
+};
+
+int encode_map(CUtensorMap* m, const void* ptr, int64_t rows, int kp);
+
 int make_map(CUtensorMap* m, const void* ptr, int64_t rows, int kp) {
+  static thread_local std::map<MapKey, CUtensorMap> cache;
+  const MapKey key{ptr, rows, kp};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *m = it->second;
+    return SIMDEX_OK;
+  }
+  const int rc = encode_map(m, ptr, rows, kp);
+  if (rc) return rc;
+  if (cache.size() >= 512) cache.clear();
+  cache[key] = *m;
+  return SIMDEX_OK;
+}
+
+int encode_map(CUtensorMap* m, const void* ptr, int64_t rows, int kp) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -1418,7 +1442,15 @@ template <int KT>
 int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
                    cudaStream_t s) {
   auto kern = p.exit_c ? gemm_topk_kernel<KT, 2> : p.norm_sorted ? gemm_topk_kernel<KT, 1> : gemm_topk_kernel<KT, 0>;
-  SIMDEX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  static size_t set_for[16][3] = {};  // per device and exit mode: largest shared-memory size already allowed
+  const int em = p.exit_c ? 2 : p.norm_sorted ? 1 : 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  size_t& done = set_for[dev & 15][em];
+  if (g.smem > done) {
+    SIMDEX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    done = g.smem;
+  }
   ProfileScope _prof("gemm_topk", s);
   kern<<<grid, kThreads, g.smem, s>>>(ma, mb, p);
   _prof.end();
@@ -1455,7 +1487,13 @@ int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, cudaStream_t s) 
     set_error("finalize: candidate buffer too large");
     return SIMDEX_EUNSUPPORTED;
   }
-  SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static size_t set_for[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > set_for[dev & 15]) {
+    SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set_for[dev & 15] = smem;
+  }
   ProfileScope _prof("finalize", s);
   finalize_kernel<LPR><<<(unsigned)ceil_div(rows, RPW * warps), 32 * warps, smem, s>>>(fp);
   _prof.end();
@@ -1467,20 +1505,20 @@ int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
   return fp.k_eff > 32 ? launch_finalize_lpr<32>(fp, rows, s) : launch_finalize_lpr<8>(fp, rows, s);
 }
 
-// Candidate buffers + per-row state for up to `rows` packed rows.
+// Candidate buffers + per-row state for up to `rows` packed rows (carved
+// out of the context workspace).
 struct RowState {
-  Scratch<int32_t> cid, cnt, flags;
-  Scratch<float> lo, hi, rowT;
-  int cap;
-  int alloc(int64_t rows, int k_eff, cudaStream_t s) {
+  int32_t *cid = nullptr, *cnt = nullptr, *flags = nullptr;
+  float *lo = nullptr, *hi = nullptr, *rowT = nullptr;
+  int cap = 0;
+  void add(Workspace& ws, int64_t rows, int k_eff) {
     cap = cap_for(k_eff);
-    SIMDEX_CUDA(cid.alloc((size_t)rows * cap, s));
-    SIMDEX_CUDA(hi.alloc((size_t)rows * cap, s));
-    SIMDEX_CUDA(lo.alloc(kt_for(k_eff) > 0 ? 1 : (size_t)rows * cap, s));
-    SIMDEX_CUDA(cnt.alloc(rows, s));
-    SIMDEX_CUDA(flags.alloc(rows, s));
-    SIMDEX_CUDA(rowT.alloc(rows, s));
-    return SIMDEX_OK;
+    ws.add(&cid, (size_t)rows * cap);
+    ws.add(&hi, (size_t)rows * cap);
+    ws.add(&lo, kt_for(k_eff) > 0 ? 1 : (size_t)rows * cap);
+    ws.add(&cnt, rows);
+    ws.add(&flags, rows);
+    ws.add(&rowT, rows);
   }
 };
 
@@ -1498,12 +1536,12 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   p.stages = g.stages;
   p.cap = st.cap;
   p.k_eff = k_eff;
-  p.cand_id = st.cid.p;
-  p.cand_lo = st.lo.p;
-  p.cand_hi = st.hi.p;
-  p.row_count = st.cnt.p;
-  p.row_flags = st.flags.p;
-  p.row_T_out = st.rowT.p;
+  p.cand_id = st.cid;
+  p.cand_lo = st.lo;
+  p.cand_hi = st.hi;
+  p.row_count = st.cnt;
+  p.row_flags = st.flags;
+  p.row_T_out = st.rowT;
   p.g_mul = (float)((1.0 / eps_for(((f + 63) / 64) * 64) + 2.0) * (1.0 + 0x1p-20));
   p.u_mul = (float)((1.0 / eps_for(((f + 63) / 64) * 64)) * (1.0 + 0x1p-20));
 
@@ -1516,28 +1554,39 @@ int pow2_at_least(int x) {
   return p;
 }
 
+// fallback_visited launches grid-stride: the overflow count lives on the
+// device, a fixed grid covers any count
+constexpr int kFallbackGrid = 64;
+
 }  // namespace
 
 // Work-sharing call statistics (simdex_ws_stats): queries, rows that went on
 // past B, prefix length, list length, factors -- enough for the caller to
-// count the algorithmic tensor work of the last call.
+// count the algorithmic tensor work of the last call.  The continuing-row
+// count reaches a pinned host slot of the context asynchronously; it is
+// valid once the stream has synchronised.
 static thread_local int64_t g_ws_stats[5] = {0, 0, 0, 0, 0};
-void record_ws_stats(int64_t nq, int64_t n_cont, int64_t bp, int64_t n, int64_t f) {
+static thread_local const int64_t* g_ws_cont_slot = nullptr;
+void record_ws_stats(int64_t nq, const int64_t* n_cont_slot, int64_t n_cont, int64_t bp, int64_t n, int64_t f) {
   g_ws_stats[0] = nq;
   g_ws_stats[1] = n_cont;
   g_ws_stats[2] = bp;
   g_ws_stats[3] = n;
   g_ws_stats[4] = f;
+  g_ws_cont_slot = n_cont_slot;
 }
 void read_ws_stats(int64_t* out) {
   for (int i = 0; i < 5; ++i) out[i] = g_ws_stats[i];
+  if (g_ws_cont_slot) out[1] = *g_ws_cont_slot;
 }
 
-// Brute-force fused path (topk_matmul).
+// Brute-force fused path (topk_matmul).  No allocation, no host round trip
+// (options & SIMDEX_MM_NORM_AUTO excepted: it reads two norms to decide the
+// early exit).
 int gemm_topk_brute(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
                     const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
-                    int64_t* heap_ops, float* debug_out, cudaStream_t s) {
+                    int64_t* heap_ops, float* debug_out, int32_t options, Ctx* ctx, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   GemmGeometry g;
   int rc = geometry(kp, &g);
@@ -1545,51 +1594,61 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   const int64_t nu_pad = ceil_div(nu, 256) * 256;
   const int64_t ni_pad = ib_rows > 0 ? ib_rows : ceil_div(ni, 256) * 256;  // rows of the item operand
   const int64_t nunits = ceil_div(nu, kUnitRows);
+  const bool fallback = debug_out == nullptr;
+  Workspace ws(ctx, s);
   RowState st;
-  if ((rc = st.alloc(nu_pad, k_eff, s))) return rc;
-  Scratch<Unit> units;
-  Scratch<int32_t> n_units, over_n;
-  Scratch<float> cu, inrm, inmax;
-  Scratch<int64_t> over_list, over_out;
-  SIMDEX_CUDA(units.alloc(nunits, s));
-  SIMDEX_CUDA(n_units.alloc(1, s));
-  SIMDEX_CUDA(cu.alloc(nu_pad, s));
-  SIMDEX_CUDA(inrm.alloc(ni_pad, s));
-  SIMDEX_CUDA(inmax.alloc(ni_pad / 32, s));
-  SIMDEX_CUDA(over_n.alloc(1, s));
-  SIMDEX_CUDA(over_list.alloc(nu, s));
-  SIMDEX_CUDA(over_out.alloc(nu, s));
+  st.add(ws, nu_pad, k_eff);
+  Unit* units;
+  int32_t *n_units, *over_n;
+  float *cu, *inrm, *inmax;
+  int64_t *over_list, *over_out;
+  double* slab = nullptr;
+  ws.add(&units, nunits);
+  ws.add(&n_units, 1);
+  ws.add(&cu, nu_pad);
+  ws.add(&inrm, ni_pad);
+  ws.add(&inmax, ni_pad / 32);
+  ws.add(&over_n, 1);
+  ws.add(&over_list, nu);
+  ws.add(&over_out, nu);
+  if (fallback) ws.add(&slab, (size_t)exact_slab_ctas(ni) * ni);
+  if ((rc = ws.commit())) return rc;
   const double eps = eps_for(kp);
-  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, nu, ni, units.p, n_units.p,
+  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, nu, ni, units, n_units,
                                                                           nunits);
   SIMDEX_LAUNCH_CHECK("units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(u_norm, nu, nu_pad, eps * std::ldexp(1.0, su), cu.p);
+  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(u_norm, nu, nu_pad, eps * std::ldexp(1.0, su), cu);
   SIMDEX_LAUNCH_CHECK("row_cu");
-  item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm.p,
-                                                                      inmax.p);
+  item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm,
+                                                                      inmax);
   SIMDEX_LAUNCH_CHECK("item_nrm");
   CUtensorMap ma, mb;
   if ((rc = make_map(&ma, ub, nu_pad, kp))) return rc;
   if ((rc = make_map(&mb, ib, ni_pad, kp))) return rc;
-  TopkParams p = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu.p, g, f, k_eff);
+  TopkParams p = make_params(st, units, n_units, inrm, inmax, cu, g, f, k_eff);
   p.heap_ops = heap_ops;
   p.debug_out = debug_out;
   p.debug_ld = ni;
   // early exit pays when the catalogue's norms are skewed (the streaming
-  // kernel with exit checks is slower when no tile can be skipped): decided
-  // from the norm-sorted operand's largest and median norms
+  // kernel with exit checks is slower when no tile can be skipped): the
+  // caller decides once per operand (SIMDEX_MM_NORM_EXIT); NORM_AUTO reads
+  // the norm-sorted operand's largest and median norms here
   p.norm_sorted = 0;
   if (item_perm != nullptr && !debug_out && ni >= 2 * kTileN && !getenv("SIMDEX_NO_EARLY_EXIT")) {
-    double nn[2];
-    SIMDEX_CUDA(cudaMemcpyAsync(&nn[0], i_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
-    SIMDEX_CUDA(cudaMemcpyAsync(&nn[1], i_norm + ni / 2, sizeof(double), cudaMemcpyDeviceToHost, s));
-    SIMDEX_CUDA(cudaStreamSynchronize(s));
-    p.norm_sorted = nn[1] < 0.6 * nn[0];
+    if (options & SIMDEX_MM_NORM_EXIT) {
+      p.norm_sorted = 1;
+    } else if (options & SIMDEX_MM_NORM_AUTO) {
+      double nn[2];
+      SIMDEX_CUDA(cudaMemcpyAsync(&nn[0], i_norm, sizeof(double), cudaMemcpyDeviceToHost, s));
+      SIMDEX_CUDA(cudaMemcpyAsync(&nn[1], i_norm + ni / 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+      SIMDEX_CUDA(cudaStreamSynchronize(s));
+      p.norm_sorted = nn[1] < 0.6 * nn[0];
+    }
   }
   const int grid = (int)(nunits < g.ctas_per_sm * sm_count() ? nunits : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
   if (debug_out) return SIMDEX_OK;
-  SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
+  SIMDEX_CUDA(cudaMemsetAsync(over_n, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
   fp.mode = kBrute;
   fp.total_rows = nu;
@@ -1602,25 +1661,22 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   fp.n = ni;
   fp.k_eff = k_eff;
   fp.cap = st.cap;
-  fp.cand_id = st.cid.p;
-  fp.cand_hi = st.hi.p;
-  fp.row_T = st.rowT.p;
-  fp.row_count = st.cnt.p;
-  fp.row_flags = st.flags.p;
+  fp.cand_id = st.cid;
+  fp.cand_hi = st.hi;
+  fp.row_T = st.rowT;
+  fp.row_count = st.cnt;
+  fp.row_flags = st.flags;
   fp.out_ids = out_ids;
   fp.out_scores = out_scores;
-  fp.over_list = over_list.p;
-  fp.over_out = over_out.p;
-  fp.over_n = over_n.p;
+  fp.over_list = over_list;
+  fp.over_out = over_out;
+  fp.over_n = over_n;
   fp.item_perm = item_perm;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   if ((rc = launch_finalize(fp, nu, s))) return rc;
-  int32_t n_over = 0;
-  SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  SIMDEX_CUDA(cudaStreamSynchronize(s));
-  if (n_over > 0)
-    return exact_topk_rows_mapped(users, items, ni, f, over_list.p, n_over, k, over_out.p, out_ids, out_scores, s);
-  return SIMDEX_OK;
+  // band overflow (rare): exact float64 rows, the count read on the device
+  return exact_topk_devcount(users, users32, items, items32, ni, f, over_list, nullptr, over_n, k, over_out,
+                             out_ids, out_scores, slab, s);
 }
 
 // Work-sharing path (query_batch, work_sharing=True):
@@ -1629,13 +1685,15 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
 //            whose K-th beats the ceiling at B' are done (visited = B');
 //   stage 2  the remaining users x the whole catalogue (certified top-K), and
 //            visited from the closed form of Algorithm 1's stop position.
+// Every buffer comes from the context workspace and every count stays on the
+// device: the call enqueues its kernels and returns (CUDA-graph capturable).
 int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                  int32_t f, int32_t kp, int32_t su, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
-                 double* out_scores, int64_t* out_visited, int32_t options, cudaStream_t s) {
+                 double* out_scores, int64_t* out_visited, int32_t options, Ctx* ctx, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   const bool no_ws = block == 0;  // every query walks the whole list (query_batch(work_sharing=False))
   const int64_t bp = block < ni ? block : ni;
@@ -1647,91 +1705,114 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   const int64_t units_max = ceil_div(nq, kUnitRows) + c;
   const int64_t ni_pad = ib_rows > 0 ? ib_rows : ceil_div(ni, 256) * 256;
   const double eps = eps_for(kp);
+  const bool stats = getenv("SIMDEX_STATS") != nullptr;
+  const bool prefix_exit = !no_ws && (options & SIMDEX_WS_PREFIX_EXIT) && !getenv("SIMDEX_NO_EARLY_EXIT");
+  const bool stage2 = no_ws || bp < ni;
+  const int64_t rows2 = ceil_div(nq, kUnitRows) * kUnitRows;  // bound on the continuing rows
+  const int64_t units2 = rows2 / kUnitRows;
+  const int64_t nt = (int64_t)c * (b_pad / kTileN);
+
+  Workspace ws(ctx, s);
   RowState st;
-  if ((rc = st.alloc(rows_max, k_eff, s))) return rc;
-  Scratch<Unit> units;
-  Scratch<int32_t> n_units, cont_n, over_n, rclus, clus2;
-  Scratch<float> cu, ucu, pnrm, pnmax, inrm, inmax, cu2, t0, t02;
-  Scratch<int64_t> a_off, row_user, row_out, cont, over_list, over_out, user2, out2, fb_users;
-  Scratch<uint16_t> a_pk, a2;
-  SIMDEX_CUDA(units.alloc(units_max, s));
-  SIMDEX_CUDA(n_units.alloc(1, s));
-  SIMDEX_CUDA(a_off.alloc(c + 1, s));
-  SIMDEX_CUDA(a_pk.alloc((size_t)rows_max * kp, s));
-  SIMDEX_CUDA(cu.alloc(rows_max, s));
-  SIMDEX_CUDA(ucu.alloc(nu, s));
-  SIMDEX_CUDA(row_user.alloc(rows_max, s));
-  SIMDEX_CUDA(row_out.alloc(rows_max, s));
-  SIMDEX_CUDA(rclus.alloc(rows_max, s));
-  SIMDEX_CUDA(pnrm.alloc((size_t)c * b_pad + 1, s));
-  SIMDEX_CUDA(pnmax.alloc((size_t)c * b_pad / 32 + 1, s));
-  SIMDEX_CUDA(cont.alloc(rows_max, s));
-  SIMDEX_CUDA(t0.alloc(rows_max, s));
-  SIMDEX_CUDA(cont_n.alloc(1, s));
-  SIMDEX_CUDA(over_n.alloc(1, s));
-  SIMDEX_CUDA(over_list.alloc(rows_max, s));
-  SIMDEX_CUDA(over_out.alloc(rows_max, s));
-  ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off.p, units.p, n_units.p);
+  st.add(ws, rows_max, k_eff);
+  Unit* units;
+  int32_t *n_units, *cont_n, *over_n, *rclus, *clus2 = nullptr;
+  float *cu, *ucu, *pnrm = nullptr, *pnmax = nullptr, *inrm = nullptr, *inmax = nullptr, *cu2 = nullptr, *t0,
+        *t02 = nullptr, *exit_c = nullptr, *exit_m = nullptr;
+  int64_t *a_off, *row_user, *row_out, *cont, *over_list, *over_out, *user2 = nullptr, *out2 = nullptr;
+  uint16_t *a_pk, *a2 = nullptr;
+  double* slab = nullptr;
+  ws.add(&units, units_max > units2 ? units_max : units2);
+  ws.add(&n_units, 1);
+  ws.add(&a_off, c + 1);
+  ws.add(&a_pk, (size_t)rows_max * kp);
+  ws.add(&cu, rows_max);
+  ws.add(&ucu, nu);
+  ws.add(&row_user, rows_max);
+  ws.add(&row_out, rows_max);
+  ws.add(&rclus, rows_max);
+  ws.add(&cont, rows_max);
+  ws.add(&t0, rows_max);
+  ws.add(&cont_n, 1);
+  ws.add(&over_n, 1);
+  ws.add(&over_list, rows_max);
+  ws.add(&over_out, rows_max);
+  if (!no_ws) {
+    ws.add(&pnrm, (size_t)c * b_pad + 1);
+    ws.add(&pnmax, (size_t)c * b_pad / 32 + 1);
+  }
+  if (prefix_exit) {
+    ws.add(&exit_c, nt);
+    ws.add(&exit_m, nt);
+  }
+  if (stage2) {
+    ws.add(&a2, (size_t)rows2 * kp);
+    ws.add(&cu2, rows2);
+    ws.add(&t02, rows2);
+    ws.add(&user2, rows2);
+    ws.add(&out2, rows2);
+    ws.add(&clus2, rows2);
+    ws.add(&inrm, ni_pad);
+    ws.add(&inmax, ni_pad / 32);
+    ws.add(&slab, (size_t)exact_slab_ctas(ni) * ni);
+  }
+  if ((rc = ws.commit())) return rc;
+  int64_t* host = ctx_host_slots(ctx);
+
+  ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off, units, n_units);
   SIMDEX_LAUNCH_CHECK("ws_units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu.p);
+  row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu);
   SIMDEX_LAUNCH_CHECK("row_cu");
   // rows past a_off[c] stay "padding" (row_user = -1) and are skipped by finalize
-  SIMDEX_CUDA(cudaMemsetAsync(row_user.p, 0xff, sizeof(int64_t) * rows_max, s));
-  ws_rows_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off.p, c, rows_max, ub, kp,
-                                                                   ucu.p, a_pk.p, cu.p, row_user.p, row_out.p,
-                                                                   rclus.p);
+  SIMDEX_CUDA(cudaMemsetAsync(row_user, 0xff, sizeof(int64_t) * rows_max, s));
+  ws_rows_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off, c, rows_max, ub, kp,
+                                                                   ucu, a_pk, cu, row_user, row_out, rclus);
   SIMDEX_LAUNCH_CHECK("ws_rows");
   int grid = 0;
-  const bool stats = getenv("SIMDEX_STATS") != nullptr;
   if (!no_ws) {
-  item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
-      prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm.p, pnmax.p);
-  SIMDEX_LAUNCH_CHECK("item_nrm");
-  CUtensorMap ma, mb;
-  if ((rc = make_map(&ma, a_pk.p, rows_max, kp))) return rc;
-  if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
-  TopkParams p = make_params(st, units.p, n_units.p, pnrm.p, pnmax.p, cu.p, g, f, k_eff);
-  // early exit on the cluster ceilings (Algorithm 1's own stop bound): a
-  // unit stops once every row's threshold exceeds ||u|| x the next tile's
-  // ceiling; the prefix top-K is unchanged (later items cannot reach it)
-  Scratch<float> exit_c, exit_m;
-  if ((options & SIMDEX_WS_PREFIX_EXIT) && !getenv("SIMDEX_NO_EARLY_EXIT")) {
-    const int64_t nt = (int64_t)c * (b_pad / kTileN);
-    SIMDEX_CUDA(exit_c.alloc(nt, s));
-    SIMDEX_CUDA(exit_m.alloc(nt, s));
-    prefix_exit_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, s>>>(bounds, ni, c, b_pad, bp, std::ldexp(1.0, si),
-                                                                   pnmax.p, exit_c.p, exit_m.p);
-    SIMDEX_LAUNCH_CHECK("prefix_exit");
-    p.norm_sorted = 1;
-    p.exit_c = exit_c.p;
-    p.exit_m = exit_m.p;
+    item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
+        prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm, pnmax);
+    SIMDEX_LAUNCH_CHECK("item_nrm");
+    CUtensorMap ma, mb;
+    if ((rc = make_map(&ma, a_pk, rows_max, kp))) return rc;
+    if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
+    TopkParams p = make_params(st, units, n_units, pnrm, pnmax, cu, g, f, k_eff);
+    // early exit on the cluster ceilings (Algorithm 1's own stop bound): a
+    // unit stops once every row's threshold exceeds ||u|| x the next tile's
+    // ceiling; the prefix top-K is unchanged (later items cannot reach it)
+    if (prefix_exit) {
+      prefix_exit_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, s>>>(bounds, ni, c, b_pad, bp, std::ldexp(1.0, si),
+                                                                     pnmax, exit_c, exit_m);
+      SIMDEX_LAUNCH_CHECK("prefix_exit");
+      p.norm_sorted = 1;
+      p.exit_c = exit_c;
+      p.exit_m = exit_m;
+    }
+    Scratch<int64_t> hops;
+    if (stats) {
+      SIMDEX_CUDA(hops.alloc(rows_max, s));
+      SIMDEX_CUDA(cudaMemsetAsync(hops.p, 0, sizeof(int64_t) * rows_max, s));
+      p.heap_ops = hops.p;
+    }
+    grid = (int)(units_max < g.ctas_per_sm * sm_count() ? units_max : g.ctas_per_sm * sm_count());
+    if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
+    if (stats) {
+      std::vector<int64_t> hh(rows_max);
+      SIMDEX_CUDA(cudaMemcpy(hh.data(), hops.p, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
+      int64_t tot = 0;
+      for (auto v : hh) tot += v;
+      fprintf(stderr, "[simdex] stage1 appends per query %.2f\n", (double)tot / (double)nq);
+    }
+  }
 
-  }
-  Scratch<int64_t> hops;
-  if (stats) {
-    SIMDEX_CUDA(hops.alloc(rows_max, s));
-    SIMDEX_CUDA(cudaMemsetAsync(hops.p, 0, sizeof(int64_t) * rows_max, s));
-    p.heap_ops = hops.p;
-  }
-  grid = (int)(units_max < g.ctas_per_sm * sm_count() ? units_max : g.ctas_per_sm * sm_count());
-  if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
-  if (stats) {
-    std::vector<int64_t> hh(rows_max);
-    SIMDEX_CUDA(cudaMemcpy(hh.data(), hops.p, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
-    int64_t tot = 0;
-    for (auto v : hh) tot += v;
-    fprintf(stderr, "[simdex] stage1 appends per query %.2f\n", (double)tot / (double)nq);
-  }
-  }  // !no_ws
-
-  SIMDEX_CUDA(cudaMemsetAsync(cont_n.p, 0, sizeof(int32_t), s));
-  SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
+  SIMDEX_CUDA(cudaMemsetAsync(cont_n, 0, sizeof(int32_t), s));
+  SIMDEX_CUDA(cudaMemsetAsync(over_n, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
   fp.mode = kPrefix;
   fp.total_rows = rows_max;
-  fp.row_user = row_user.p;
-  fp.row_out = row_out.p;
-  fp.row_cluster = rclus.p;
+  fp.row_user = row_user;
+  fp.row_out = row_out;
+  fp.row_cluster = rclus;
   fp.nu = nu;
   fp.users = users;
   fp.users32 = users32;
@@ -1746,49 +1827,45 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.prefix = bp;
   fp.k_eff = k_eff;
   fp.cap = st.cap;
-  fp.cand_id = st.cid.p;
-  fp.cand_hi = st.hi.p;
-  fp.row_T = st.rowT.p;
-  fp.row_count = st.cnt.p;
-  fp.row_flags = st.flags.p;
+  fp.cand_id = st.cid;
+  fp.cand_hi = st.hi;
+  fp.row_T = st.rowT;
+  fp.row_count = st.cnt;
+  fp.row_flags = st.flags;
   fp.out_ids = out_ids;
   fp.out_scores = out_scores;
   fp.out_visited = out_visited;
-  fp.row_T0_out = t0.p;
+  fp.row_T0_out = t0;
   fp.t0_scale = std::ldexp(1.0, su + si);
-  fp.cont_list = cont.p;
-  fp.cont_n = cont_n.p;
-  fp.over_list = over_list.p;
-  fp.over_out = over_out.p;
-  fp.over_n = over_n.p;
+  fp.cont_list = cont;
+  fp.cont_n = cont_n;
+  fp.over_list = over_list;
+  fp.over_out = over_out;
+  fp.over_n = over_n;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   if (no_ws) {
     fp.prefix = 0;  // no floor: visited is the stop position from 0
-    all_rows_continue_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(row_user.p, rows_max, cont.p,
-                                                                              cont_n.p, t0.p);
+    all_rows_continue_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(row_user, rows_max, cont, cont_n, t0);
     SIMDEX_LAUNCH_CHECK("all_rows_continue");
   } else if ((rc = launch_finalize(fp, rows_max, s))) {
     return rc;
   }
-  if (!no_ws && bp >= ni) {  // the prefix was the whole list
-    record_ws_stats(nq, 0, bp, ni, f);
+  if (!stage2) {  // the prefix was the whole list
+    record_ws_stats(nq, nullptr, 0, bp, ni, f);
     return SIMDEX_OK;
   }
 
-  // ---- stage 2: continuing users x the whole catalogue.  No host round
-  // trip: buffers are sized for every row, the row and unit counts are read
-  // on the device; the count reaches the host with the final synchronisation.
-  static thread_local int32_t* n_cont_host = nullptr;
-  if (!n_cont_host) SIMDEX_CUDA(cudaMallocHost(&n_cont_host, sizeof(int32_t)));
-  SIMDEX_CUDA(cudaMemcpyAsync(n_cont_host, cont_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  int32_t n_cont = -1;
+  // ---- stage 2: continuing users x the whole catalogue.  Buffers are sized
+  // for every row; the row and unit counts are read on the device; the count
+  // reaches the host statistics slot asynchronously.
+  // (slot 0 holds the int32 count in its low half; the high half stays 0)
+  SIMDEX_CUDA(cudaMemcpyAsync(&host[0], cont_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   if (stats) {
     SIMDEX_CUDA(cudaStreamSynchronize(s));
-    n_cont = *n_cont_host;
     std::vector<int32_t> hc(rows_max);
-    SIMDEX_CUDA(cudaMemcpy(hc.data(), st.cnt.p, sizeof(int32_t) * rows_max, cudaMemcpyDeviceToHost));
+    SIMDEX_CUDA(cudaMemcpy(hc.data(), st.cnt, sizeof(int32_t) * rows_max, cudaMemcpyDeviceToHost));
     std::vector<int64_t> hu(rows_max);
-    SIMDEX_CUDA(cudaMemcpy(hu.data(), row_user.p, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
+    SIMDEX_CUDA(cudaMemcpy(hu.data(), row_user, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
     int64_t tot = 0, live = 0, mx = 0, hist[8] = {0};
     for (int64_t r = 0; r < rows_max; ++r)
       if (hu[r] >= 0) {
@@ -1798,36 +1875,24 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
         hist[hc[r] < 16 ? 0 : hc[r] < 32 ? 1 : hc[r] < 64 ? 2 : 3]++;
       }
     fprintf(stderr,
-            "[simdex] query_ws nq=%lld continue_past_B=%d stage1 candidates mean=%.2f max=%lld "
+            "[simdex] query_ws nq=%lld continue_past_B=%lld stage1 candidates mean=%.2f max=%lld "
             "<16:%lld <32:%lld <64:%lld >=64:%lld\n",
-            (long long)nq, n_cont, live ? (double)tot / live : 0.0, (long long)mx, (long long)hist[0],
+            (long long)nq, (long long)host[0], live ? (double)tot / live : 0.0, (long long)mx, (long long)hist[0],
             (long long)hist[1], (long long)hist[2], (long long)hist[3]);
   }
-  const int64_t rows2 = ceil_div(nq, kUnitRows) * kUnitRows;  // bound on the continuing rows
-  const int64_t units2 = rows2 / kUnitRows;
-  SIMDEX_CUDA(a2.alloc((size_t)rows2 * kp, s));
-  SIMDEX_CUDA(cu2.alloc(rows2, s));
-  SIMDEX_CUDA(t02.alloc(rows2, s));
-  SIMDEX_CUDA(user2.alloc(rows2, s));
-  SIMDEX_CUDA(out2.alloc(rows2, s));
-  SIMDEX_CUDA(clus2.alloc(rows2, s));
-  SIMDEX_CUDA(inrm.alloc(ni_pad, s));
-  SIMDEX_CUDA(inmax.alloc(ni_pad / 32, s));
-  cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 8), 8 * sm_count()), 256, 0, s>>>(cont.p, cont_n.p, rows2, row_user.p, row_out.p, rclus.p,
-                                                                 cu.p, t0.p, a_pk.p, kp, a2.p, cu2.p, t02.p, user2.p,
-                                                                 out2.p, clus2.p);
+  cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 8), 8 * sm_count()), 256, 0, s>>>(
+      cont, cont_n, rows2, row_user, row_out, rclus, cu, t0, a_pk, kp, a2, cu2, t02, user2, out2, clus2);
   SIMDEX_LAUNCH_CHECK("cont_rows");
-  units_from_count_kernel<<<(unsigned)ceil_div(units2, 256), 256, 0, s>>>(cont_n.p, 0, ni, units.p, n_units.p,
-                                                                          units2);
+  units_from_count_kernel<<<(unsigned)ceil_div(units2, 256), 256, 0, s>>>(cont_n, 0, ni, units, n_units, units2);
   SIMDEX_LAUNCH_CHECK("units");
-  item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm.p,
-                                                                      inmax.p);
+  item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm,
+                                                                      inmax);
   SIMDEX_LAUNCH_CHECK("item_nrm");
   CUtensorMap ma2, mb2;
-  if ((rc = make_map(&ma2, a2.p, rows2, kp))) return rc;
+  if ((rc = make_map(&ma2, a2, rows2, kp))) return rc;
   if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
-  TopkParams p2 = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu2.p, g, f, k_eff);
-  p2.row_T0 = t02.p;
+  TopkParams p2 = make_params(st, units, n_units, inrm, inmax, cu2, g, f, k_eff);
+  p2.row_T0 = t02;
   p2.norm_sorted = item_perm != nullptr && !getenv("SIMDEX_NO_EARLY_EXIT");
   Scratch<int64_t> hops2;
   if (stats) {
@@ -1842,33 +1907,28 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     SIMDEX_CUDA(cudaMemcpy(hh.data(), hops2.p, sizeof(int64_t) * rows2, cudaMemcpyDeviceToHost));
     int64_t tot = 0;
     for (auto v : hh) tot += v;
-    fprintf(stderr, "[simdex] stage2 appends per continuing query %.2f\n", (double)tot / (double)(n_cont > 0 ? n_cont : 1));
+    fprintf(stderr, "[simdex] stage2 appends per continuing query %.2f\n",
+            (double)tot / (double)(host[0] > 0 ? host[0] : 1));
   }
   FinalizeParams f2 = fp;
   f2.mode = kFullList;
   f2.total_rows = rows2;
-  f2.n_rows_dev = cont_n.p;
-  f2.row_user = user2.p;
-  f2.row_out = out2.p;
-  f2.row_cluster = clus2.p;
+  f2.n_rows_dev = cont_n;
+  f2.row_user = user2;
+  f2.row_out = out2;
+  f2.row_cluster = clus2;
   f2.cont_list = nullptr;
   f2.cont_n = nullptr;
   f2.item_perm = item_perm;
   if ((rc = launch_finalize(f2, rows2, s))) return rc;
-  int32_t n_over = 0;
-  SIMDEX_CUDA(cudaMemcpyAsync(&n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  SIMDEX_CUDA(cudaStreamSynchronize(s));
-  record_ws_stats(nq, *n_cont_host, bp, ni, f);
-  if (n_over == 0) return SIMDEX_OK;
-  // band overflow on the full list: exact float64 scan for those users, same visited closed form
-  SIMDEX_CUDA(fb_users.alloc(n_over, s));
-  fallback_users_kernel<<<(unsigned)ceil_div(n_over, 256), 256, 0, s>>>(over_list.p, over_n.p, user2.p, fb_users.p);
-  SIMDEX_LAUNCH_CHECK("fallback_users");
-  if ((rc = exact_topk_rows_mapped(users, items, ni, f, fb_users.p, n_over, k, over_out.p, out_ids, out_scores, s)))
+  record_ws_stats(nq, &host[0], -1, bp, ni, f);
+  // band overflow on the full list (rare): exact float64 scan for those users
+  // and the same visited closed form; counts read on the device
+  if ((rc = exact_topk_devcount(users, users32, items, items32, ni, f, over_list, user2, over_n, k, over_out, out_ids,
+                                out_scores, slab, s)))
     return rc;
-  fallback_visited_kernel<<<(unsigned)ceil_div(n_over, 256), 256, 0, s>>>(
-      over_list.p, over_n.p, user2.p, out2.p, clus2.p, list_pos, bounds, unorm, ni, bp, k_eff, out_ids, out_scores,
-      out_visited);
+  fallback_visited_kernel<<<kFallbackGrid, 256, 0, s>>>(over_list, over_n, user2, out2, clus2, list_pos, bounds, unorm,
+                                                        ni, bp, k_eff, out_ids, out_scores, out_visited);
   SIMDEX_LAUNCH_CHECK("fallback_visited");
   return SIMDEX_OK;
 }
@@ -1939,62 +1999,64 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   if (rc) return rc;
   const int64_t nu_pad = ceil_div(n, 256) * 256, nc_pad = ceil_div(c, 256) * 256;
   const int64_t nunits = nu_pad / kUnitRows;
-  Scratch<unsigned long long> mx;
-  SIMDEX_CUDA(mx.alloc(3, s));
-  SIMDEX_CUDA(cudaMemsetAsync(mx.p, 0, 3 * sizeof(unsigned long long), s));
-  const int64_t nf = n * (int64_t)f;
-  max_abs_any_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(nf, 256), 4 * 148), 256, 0, s>>>(px, nf, 1.0, mx.p);
-  max_abs_any_kernel<double><<<(unsigned)std::min<int64_t>(ceil_div((int64_t)c * f, 256), 64), 256, 0, s>>>(
-      centers, (int64_t)c * f, 1.0, mx.p + 1);
-  max_abs_any_kernel<double><<<1, 256, 0, s>>>(c2, c, 0.5, mx.p + 2);
-  SIMDEX_LAUNCH_CHECK("max_abs_any");
-  Scratch<int> sexp;
-  Scratch<double> sfac;
-  SIMDEX_CUDA(sexp.alloc(2, s));
-  SIMDEX_CUDA(sfac.alloc(2, s));
-  assign_scales_kernel<<<1, 32, 0, s>>>(mx.p, eps_for(kp), sexp.p, sfac.p);
-  SIMDEX_LAUNCH_CHECK("assign_scales");
   const int k_eff = 1;
+  Workspace ws(ctx_or_default(nullptr), s);
+  unsigned long long* mx;
+  int* sexp;
+  double* sfac;
   RowState st;
-  if ((rc = st.alloc(nu_pad, k_eff, s))) return rc;
-  Scratch<uint16_t> ua, ca;
-  Scratch<double> un, cn;
-  Scratch<Unit> units;
-  Scratch<int32_t> n_units, over_n;
-  Scratch<float> cu, inrm, inmax;
-  Scratch<int64_t> over_out;
-  SIMDEX_CUDA(ua.alloc((size_t)nu_pad * kp, s));
-  SIMDEX_CUDA(ca.alloc((size_t)nc_pad * kp, s));
-  SIMDEX_CUDA(un.alloc(nu_pad, s));
-  SIMDEX_CUDA(cn.alloc(nc_pad, s));
-  SIMDEX_CUDA(units.alloc(nunits, s));
-  SIMDEX_CUDA(n_units.alloc(1, s));
-  SIMDEX_CUDA(over_n.alloc(1, s));
-  SIMDEX_CUDA(over_out.alloc(n, s));
-  SIMDEX_CUDA(cu.alloc(nu_pad, s));
-  SIMDEX_CUDA(inrm.alloc(nc_pad, s));
-  SIMDEX_CUDA(inmax.alloc(nc_pad / 32, s));
+  uint16_t *ua, *ca;
+  double *un, *cn;
+  Unit* units;
+  int32_t *n_units, *over_n;
+  float *cu, *inrm, *inmax;
+  int64_t* over_out;
+  ws.add(&mx, 3);
+  ws.add(&sexp, 2);
+  ws.add(&sfac, 2);
+  st.add(ws, nu_pad, k_eff);
+  ws.add(&ua, (size_t)nu_pad * kp);
+  ws.add(&ca, (size_t)nc_pad * kp);
+  ws.add(&un, nu_pad);
+  ws.add(&cn, nc_pad);
+  ws.add(&units, nunits);
+  ws.add(&n_units, 1);
+  ws.add(&over_n, 1);
+  ws.add(&over_out, n);
+  ws.add(&cu, nu_pad);
+  ws.add(&inrm, nc_pad);
+  ws.add(&inmax, nc_pad / 32);
+  if ((rc = ws.commit())) return rc;
+  SIMDEX_CUDA(cudaMemsetAsync(mx, 0, 3 * sizeof(unsigned long long), s));
+  const int64_t nf = n * (int64_t)f;
+  max_abs_any_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(nf, 256), 4 * 148), 256, 0, s>>>(px, nf, 1.0, mx);
+  max_abs_any_kernel<double><<<(unsigned)std::min<int64_t>(ceil_div((int64_t)c * f, 256), 64), 256, 0, s>>>(
+      centers, (int64_t)c * f, 1.0, mx + 1);
+  max_abs_any_kernel<double><<<1, 256, 0, s>>>(c2, c, 0.5, mx + 2);
+  SIMDEX_LAUNCH_CHECK("max_abs_any");
+  assign_scales_kernel<<<1, 32, 0, s>>>(mx, eps_for(kp), sexp, sfac);
+  SIMDEX_LAUNCH_CHECK("assign_scales");
   ProfileScope _prof("assign_pack", s);
-  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, sexp.p, nu_pad, kp,
-                                                                          ua.p, un.p);
-  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad * 8, 256), 256, 0, s>>>(centers, c2, c, f, 1, sexp.p + 1,
-                                                                               nc_pad, kp, ca.p, cn.p);
+  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, sexp, nu_pad, kp,
+                                                                          ua, un);
+  pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad * 8, 256), 256, 0, s>>>(centers, c2, c, f, 1, sexp + 1,
+                                                                               nc_pad, kp, ca, cn);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("pack_aug");
-  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units.p, n_units.p, nunits);
+  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units, n_units, nunits);
   SIMDEX_LAUNCH_CHECK("units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un.p, n, nu_pad, 0.0, cu.p, sfac.p);
+  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un, n, nu_pad, 0.0, cu, sfac);
   SIMDEX_LAUNCH_CHECK("row_cu");
-  item_nrm_kernel<<<(unsigned)ceil_div(nc_pad / 32, 8), 256, 0, s>>>(cn.p, c, nc_pad, 0.0, inrm.p, inmax.p,
-                                                                      sfac.p + 1);
+  item_nrm_kernel<<<(unsigned)ceil_div(nc_pad / 32, 8), 256, 0, s>>>(cn, c, nc_pad, 0.0, inrm, inmax,
+                                                                      sfac + 1);
   SIMDEX_LAUNCH_CHECK("item_nrm");
   CUtensorMap ma, mb;
-  if ((rc = make_map(&ma, ua.p, nu_pad, kp))) return rc;
-  if ((rc = make_map(&mb, ca.p, nc_pad, kp))) return rc;
-  TopkParams tp = make_params(st, units.p, n_units.p, inrm.p, inmax.p, cu.p, g, f + 1, k_eff);
+  if ((rc = make_map(&ma, ua, nu_pad, kp))) return rc;
+  if ((rc = make_map(&mb, ca, nc_pad, kp))) return rc;
+  TopkParams tp = make_params(st, units, n_units, inrm, inmax, cu, g, f + 1, k_eff);
   const int grid = (int)(nunits < g.ctas_per_sm * sm_count() ? nunits : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma, mb, tp, g, grid, s))) return rc;
-  SIMDEX_CUDA(cudaMemsetAsync(over_n.p, 0, sizeof(int32_t), s));
+  SIMDEX_CUDA(cudaMemsetAsync(over_n, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
   fp.mode = kAssign;
   fp.total_rows = n;
@@ -2006,14 +2068,14 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   fp.n = c;
   fp.k_eff = k_eff;
   fp.cap = st.cap;
-  fp.cand_id = st.cid.p;
-  fp.cand_hi = st.hi.p;
-  fp.row_T = st.rowT.p;
-  fp.row_count = st.cnt.p;
-  fp.row_flags = st.flags.p;
+  fp.cand_id = st.cid;
+  fp.cand_hi = st.hi;
+  fp.row_T = st.rowT;
+  fp.row_count = st.cnt;
+  fp.row_flags = st.flags;
   fp.over_list = over_rows;
-  fp.over_out = over_out.p;
-  fp.over_n = over_n.p;
+  fp.over_out = over_out;
+  fp.over_n = over_n;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   fp.p2 = p2;
   fp.c2 = c2;
@@ -2025,7 +2087,7 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   assign_finalize_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(fp, px);
   _pf.end();
   SIMDEX_LAUNCH_CHECK("finalize_assign");
-  SIMDEX_CUDA(cudaMemcpyAsync(n_over, over_n.p, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  SIMDEX_CUDA(cudaMemcpyAsync(n_over, over_n, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   return SIMDEX_OK;
 }
 

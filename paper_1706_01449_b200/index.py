@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import math
 import struct
-from collections.abc import Mapping, Sequence
+from collections.abc import Mapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,17 +44,23 @@ class TopKResult:
         return list(zip(self.item_ids.tolist(), self.scores.tolist()))
 
 
-class TopKResults(Sequence):
-    """Lazy ``list[TopKResult]`` over batched [n, K] result arrays.
+class TopKResults(list):
+    """``list[TopKResult]`` over batched [n, K] result arrays, built lazily.
 
-    Indexing/iteration build TopKResult objects on demand (fresh int64 /
-    float64 arrays per element, like the reference's list); ``reused`` maps
-    positions to existing TopKResult objects that must be returned as-is
+    The reference returns a plain list (index.py:305-389, brute.py:59-113).
+    This is a list subclass whose elements are created on demand: indexing,
+    iteration, ``len``, ``==``, ``+`` and ``in`` work without building all n
+    objects, and the first mutating call (append, sort, item assignment, ...)
+    materialises every element into the list proper, after which it is an
+    ordinary list.  Elements are fresh TopKResult objects with int64 / float64
+    arrays, except ``reused`` positions, which return the given objects as-is
     (``precomputed`` in query_batch, index.py:330-332).  The whole-batch
-    arrays are available as ``.item_ids`` / ``.scores`` / ``.visited``.
+    arrays are ``.item_ids`` / ``.scores`` / ``.visited`` (as computed; not
+    updated by later list mutation).
     """
 
     def __init__(self, user_ids, item_ids, scores, visited, reused=None):
+        list.__init__(self)
         # user_ids None: every user in order (position == id), materialised on request
         self._uids = None if user_ids is None else np.asarray(user_ids, dtype=np.int64)
         self._n = int(item_ids.shape[0]) if user_ids is None else int(self._uids.shape[0])
@@ -62,15 +68,13 @@ class TopKResults(Sequence):
         self.scores = scores
         self.visited = visited
         self._reused = reused or {}
+        self._lazy = True
 
     @property
     def user_ids(self) -> np.ndarray:
         if self._uids is None:
             self._uids = np.arange(self._n, dtype=np.int64)
         return self._uids
-
-    def __len__(self):
-        return self._n
 
     def _make(self, i):
         r = self._reused.get(i)
@@ -80,19 +84,101 @@ class TopKResults(Sequence):
         return TopKResult(uid, self.item_ids[i].astype(np.int64), self.scores[i].astype(np.float64),
                           int(self.visited[i]))
 
+    def _materialize(self):
+        if self._lazy:
+            elems = [self._make(i) for i in range(self._n)]
+            self._lazy = False
+            list.extend(self, elems)
+
+    # -- read access (lazy) --------------------------------------------------
+    def __len__(self):
+        return self._n if self._lazy else list.__len__(self)
+
     def __getitem__(self, i):
+        if not self._lazy:
+            return list.__getitem__(self, i)
         if isinstance(i, slice):
-            return [self._make(j) for j in range(*i.indices(len(self)))]
-        n = len(self)
+            return [self._make(j) for j in range(*i.indices(self._n))]
+        i = int(i)
         if i < 0:
-            i += n
-        if not 0 <= i < n:
-            raise IndexError("TopKResults index out of range")
+            i += self._n
+        if not 0 <= i < self._n:
+            raise IndexError("list index out of range")
         return self._make(i)
 
     def __iter__(self):
-        for i in range(len(self)):
-            yield self._make(i)
+        if not self._lazy:
+            return list.__iter__(self)
+        return (self._make(i) for i in range(self._n))
+
+    def __reversed__(self):
+        if not self._lazy:
+            return list.__reversed__(self)
+        return (self._make(i) for i in range(self._n - 1, -1, -1))
+
+    def __contains__(self, x):
+        return any(x is e or x == e for e in self)
+
+    def __eq__(self, other):
+        if not isinstance(other, list):
+            return NotImplemented
+        return len(self) == len(other) and all(a is b or a == b for a, b in zip(self, other))
+
+    def __ne__(self, other):
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    __hash__ = None
+
+    def __add__(self, other):
+        if not isinstance(other, list):
+            return NotImplemented
+        return list(self) + list(other)
+
+    def __radd__(self, other):
+        if not isinstance(other, list):
+            return NotImplemented
+        return list(other) + list(self)
+
+    def __mul__(self, n):
+        return list(self) * n
+
+    __rmul__ = __mul__
+
+    def __repr__(self):
+        if self._lazy and self._n > 6:
+            head = ", ".join(repr(self._make(i)) for i in range(3))
+            return f"[{head}, ... ({self._n} results)]"
+        return repr(list(self))
+
+    def __reduce__(self):
+        return (list, (list(self),))
+
+    def copy(self):
+        return list(self)
+
+    def index(self, x, *args):
+        self._materialize()
+        return list.index(self, x, *args)
+
+    def count(self, x):
+        return sum(1 for e in self if e is x or e == x)
+
+    # -- mutation: materialise, then behave as a plain list -------------------
+    def _mutator(name):  # noqa: N805 -- class-body helper
+        base = getattr(list, name)
+
+        def method(self, *args, **kwargs):
+            self._materialize()
+            return base(self, *args, **kwargs)
+
+        method.__name__ = name
+        return method
+
+    for _name in ("append", "extend", "insert", "pop", "remove", "clear", "sort", "reverse", "__setitem__",
+                  "__delitem__", "__iadd__", "__imul__"):
+        locals()[_name] = _mutator(_name)
+    del _name, _mutator
 
 
 class SampleResults(Mapping):
@@ -224,11 +310,24 @@ class CentroidIndex:
         return self.clustering.device_assignment()
 
     def device_prefix(self, model: ModelPair):
-        key = ("prefix", id(model.items))
-        if key not in self._dev:
+        """Per-cluster prefix operand of ``model.items`` (cached with a strong
+        reference to that matrix, so a recycled id() can never alias it)."""
+        ent = self._dev.get("prefix")
+        if ent is None or ent[0] is not model.items:
             ids, _ = self.device_lists()
-            self._dev[key] = _ops.build_prefix(_device.packed(model.items), ids, self.block_size)
-        return self._dev[key]
+            ent = self._dev["prefix"] = (model.items, _ops.build_prefix(_device.packed(model.items), ids,
+                                                                        self.block_size))
+        return ent[1]
+
+    def device_all_users(self, num_users: int, dev):
+        """(arange(num_users) on the device, its cluster grouping), cached per
+        user count (a model grown by add_user gets a fresh entry)."""
+        key = ("all_users", int(num_users))
+        ent = self._dev.get(key)
+        if ent is None:
+            q = torch.arange(num_users, dtype=torch.int64, device=dev)
+            ent = self._dev[key] = (q, _ops.group_queries(q, self.device_assignment(), self.num_clusters))
+        return ent
 
 
 def item_bound(item_norm: float, item_angle: float, cluster_angle: float) -> float:
@@ -362,20 +461,15 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
     items = _device.f64(model.items)
     ids, bounds = index.device_lists()
     n = model.num_items
+    grouped = None
     if q_users is None:
-        q_users = index._dev.get("all_users")
-        if q_users is None:
-            q_users = index._dev["all_users"] = torch.arange(model.num_users, dtype=torch.int64, device=users.device)
+        q_users, grouped = index.device_all_users(model.num_users, users.device)
     pu, pi = _device.packed(model.users), _device.packed_sorted(model.items)
     if min(k, n) <= 256 and pu.kp <= 256:
         # tensor-core path; without work sharing every query takes the full-list
         # pass (block 0) and visited is Algorithm 1's stop position, exactly the walk's
-        key = ("grouped", q_users.data_ptr(), q_users.shape[0])
-        grouped = index._dev.get(key) if q_users is index._dev.get("all_users") else None
         if grouped is None:
             grouped = _ops.group_queries(q_users, index.device_assignment(), index.num_clusters)
-            if q_users is index._dev.get("all_users"):
-                index._dev[key] = grouped
         block = index.block_size if work_sharing else 0
         prefix = index.device_prefix(model) if work_sharing else (None, None, 0)
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
@@ -488,12 +582,17 @@ def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> Centroi
     out.clustering = clustering
     out._shape = index._shape
     out._host = dict(index._host)
-    out._dev = {key: val for key, val in index._dev.items() if not (isinstance(key, tuple) and lists is not None)}
+    # the user grouping depends on the clustering (always new here); the
+    # prefix operand and list positions on the lists; walk estimates stay
+    # (they only pick an option, the results are identical either way)
+    out._dev = {key: val for key, val in index._dev.items()
+                if not (isinstance(key, tuple) and key[0] == "all_users")}
     if lists is not None:
         out._host.pop("item_ids", None)
         out._host.pop("bounds", None)
         out._dev["ids"], out._dev["bounds"] = lists
         out._dev.pop("pos", None)
+        out._dev.pop("prefix", None)
     return out
 
 

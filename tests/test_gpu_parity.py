@@ -290,6 +290,52 @@ def test_mutations_stay_exact(sx):
     np.testing.assert_array_equal(r.item_ids, want[-1])
 
 
+def test_add_user_after_cached_serve(sx):
+    """a query_batch(None) before add_user must not leave a
+    cached all-users grouping that hides the new user afterwards."""
+    import simdex_oracle as oracle
+    g = load_golden("syn1")
+    model = _model(sx, g)
+    idx = sx.build_index(model, _ref_clustering(sx, g, 4), 64)
+    before = sx.query_batch(idx, model, None, 5)
+    assert len(before) == model.num_users
+    for vec in (model.users.values[3].copy(), np.full(model.factors, -3.0)):  # fits / drifts
+        idx2, model2, _ = sx.add_user(idx, model, vec)
+        after = sx.query_batch(idx2, model2, None, 5)
+        assert len(after) == model2.num_users == model.num_users + 1
+        want, _ = oracle.topk_naive(model2.users.values, model2.items.values, 5)
+        np.testing.assert_array_equal(after[-1].item_ids, want[-1])
+        np.testing.assert_array_equal(after.item_ids[:, :], want)
+        again = sx.query_batch(idx, model, None, 5)  # the original index still serves its own users
+        assert len(again) == model.num_users
+
+
+def test_band_overflow_falls_back_exactly(sx):
+    """Hundreds of exactly tied items overflow every row's candidate buffer:
+    the device-counted exact fallback must produce the reference ordering
+    (score desc, id asc) on both the brute-force and the work-sharing path."""
+    import simdex_oracle as oracle
+    rng = np.random.default_rng(5)
+    f = 24
+    items = rng.normal(size=(900, f))
+    items[100:700] = items[50]  # 601 copies of one vector
+    users = rng.normal(size=(300, f))
+    users[:150] = items[50] * rng.uniform(0.5, 2.0, size=(150, 1))  # these users rank the copies first
+    model = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    want, want_sc = oracle.topk_naive(users, items, 20)
+    res = sx.topk_matmul(model, 20)
+    np.testing.assert_array_equal(res.item_ids, want)
+    np.testing.assert_allclose(res.scores, want_sc, rtol=1e-9, atol=1e-9)
+    cl = sx.kmeans(model.users, 3, max_iters=5, seed=2)
+    idx = sx.build_index(model, cl, 256)
+    for ws in (True, False):
+        out = sx.query_batch(idx, model, None, 20, work_sharing=ws)
+        np.testing.assert_array_equal(out.item_ids, want)
+        walked = [sx.query_user(idx, model, u, 20).visited for u in (0, 1, 200, 299)]
+        if not ws:
+            assert [int(out.visited[u]) for u in (0, 1, 200, 299)] == walked
+
+
 def test_sidecar_round_trip(sx, tmp_path):
     g = load_golden("syn1")
     model = _model(sx, g)
