@@ -2,27 +2,33 @@
 index path of BASELINE.json configs[1] (Netflix shape, 480,189 x 17,770,
 C=256 k-means with 3 iterations, B=4096 work sharing).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2] [--k K]
 
-One step = serve every user of the workload (exact top-K, the path the
-cost optimizer picks) with the model, clustering and index already resident
-in HBM.  Each rank of an N-GPU run serves its own full copy of the workload
-(weak scaling, no data-path collective).  ``e2e`` is the same metric through
-the public API from HOST buffers: upload (pinned), cluster, build, estimate,
-decide, serve, download the [U, K] results -- i.e. run_pipeline.
+One step = exact top-K of every user of the workload through the path the
+cost optimizer picks, with the model, clustering and index resident in HBM.
+With N ranks (one process per GPU, torchrun) the fixed user set is split
+(strong scaling, no data-path collective): the index path routes users by
+cluster (sharding.IndexShard), the blocked product cuts contiguous user
+blocks (sharding.UserShard), and the catalogue-sharded config (cfg5) splits
+the items and exchanges per-user-slice partial lists with an NCCL
+all-to-all before the device merge (sharding.CatalogShard).  The time is the
+max over ranks.  ``e2e`` is the same metric through the public API from
+HOST buffers: upload, cluster, build, estimate, decide, serve, download --
+run_pipeline (N = 1) or sharding.run_pipeline_shard (N > 1).
 
---impl reference times the reference algorithm's CPU implementation (the
-oracle port in oracle/, the reference being pure Python) on the host cores,
-P worker processes over disjoint user slices, each step a bounded sample.
+--impl reference times the UNMODIFIED reference package (mipserve, installed
+offline into baseline/_ref) on the host cores: P worker processes over
+disjoint user samples, one BLAS thread each (the reference protocol,
+PAPER.md:1080-1085), each step a bounded sample.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -30,13 +36,17 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "gemm_topk_traffic.json")
+KERNEL_SOURCES = ("paper_1706_01449_b200/csrc/gemm_topk.cu", "paper_1706_01449_b200/csrc/sm100.cuh",
+                  "paper_1706_01449_b200/csrc/common.cuh")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--k", type=int, default=None)
@@ -49,67 +59,88 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def kernel_source_hash():
+    h = hashlib.sha256()
+    for rel in KERNEL_SOURCES:
+        with open(os.path.join(ROOT, rel), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
 
 
 class Clocks:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    """SM clock and throttle-reason sampling DURING the timed region: an NVML
+    thread polling every 2 ms (the timed region of a default run is tens of
+    milliseconds, below nvidia-smi's 100 ms loop)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, device_index):
-        self.path = f"/tmp/simdex_clocks_{os.getpid()}.csv"
-        self.proc = None
+        import threading
+        self.samples = []
+        self.err = None
+        self._stop = threading.Event()
+        self._on = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(device_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
-        self.skip = 0
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[device_index]) if vis and vis.split(",")[0].isdigit() else device_index
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(phys)
+            self.max_mhz = int(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self._reasons = (getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None)
+                             or N.nvmlDeviceGetCurrentClocksThrottleReasons)
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception as e:  # noqa: BLE001 -- report, do not fail the bench
+            self.N, self.err = None, f"nvml unavailable: {e}"
 
-    def _rows(self):
-        rows = []
-        try:
-            for line in open(self.path):
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 7 and parts[0].isdigit():
-                    rows.append(parts)
-        except OSError:
-            pass
-        return rows
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            if self._on.is_set():
+                try:
+                    self.samples.append((int(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)),
+                                         int(self._reasons(self.h))))
+                except Exception:  # noqa: BLE001
+                    pass
+            time.sleep(0.002)
 
     def start_region(self):
-        """Wait (<= 5 s) until the sampler is producing, then mark the start of
-        the timed region: only samples taken after this point are reported."""
-        if self.proc is None:
-            return
-        t0 = time.time()
-        while not self._rows() and time.time() - t0 < 5.0:
-            time.sleep(0.02)
-        self.skip = len(self._rows())
+        self._on.set()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        rows = self._rows()[self.skip:]
-        os.unlink(self.path)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [int(r[0]) for r in rows]
+        if self.N is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no sampler"]}
+        self._on.clear()
+        self._stop.set()
+        self.thread.join()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
         reasons = set()
-        for r in rows:
-            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[3:7]):
-                if val.lower() == "active":
+        for _, bits in self.samples:
+            for name, attr in self.REASONS:
+                if bits & int(getattr(self.N, attr, 0)):
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": sorted(reasons),
-                "samples": len(rows)}
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples), "sampler": "nvml 2 ms"}
 
 
 def dist_env():
@@ -119,65 +150,78 @@ def dist_env():
     return world, rank, local
 
 
+def workload_path(w):
+    return "catalog" if w.name == "cfg5" else w.expected_path
+
+
 # ---------------------------------------------------------------------------
-# reference arm: the oracle port on host cores
+# the reference package (mipserve, unmodified) on host cores
 # ---------------------------------------------------------------------------
 
-_CPU_STATE = {}
+_REF = {}
 
 
-def _cpu_worker(args):
-    """One worker's share of a step (state inherited through fork)."""
-    sample, k, block = args
-    import simdex_oracle as O
-    st = _CPU_STATE
-    t0 = time.perf_counter()
-    O.query_batch(st["index"], st["items"], st["users"], list(sample), k, block)
+def _import_reference():
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import mipserve
+    if not os.path.abspath(mipserve.__file__).startswith(os.path.abspath(REF_PATH)):
+        raise ImportError(f"mipserve resolved to {mipserve.__file__}, not baseline/_ref")
+    return mipserve
+
+
+def _ref_worker(args):
+    """One worker's share of a step (reference state inherited through fork)."""
+    sample, k = args
+    from threadpoolctl import threadpool_limits
+    M = _REF["M"]
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        if _REF["index"] is not None:
+            M.query_batch(_REF["index"], _REF["model"], sample.tolist(), k)
+        else:
+            sub = M.ModelPair(M.FactorMatrix(_REF["model"].users.values[sample]), _REF["model"].items)
+            M.topk_matmul(sub, k)
     return len(sample), time.perf_counter() - t0
 
 
-def cpu_reference(workload, k, steps, warmup, cores, per_worker, block=4096, matmul=False):
-    """Time the reference algorithm (oracle port) on `cores` processes; returns
-    (users/s per step list, sample description)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+def reference_setup(w, clustering=None):
+    """mipserve model (+ index for the index path).  ``clustering`` = (centroids,
+    assignment) to build the reference index from (its own build_index); None
+    runs the reference's own kmeans."""
+    M = _import_reference()
+    model = M.ModelPair(M.FactorMatrix(w.users.astype(np.float64)), M.FactorMatrix(w.items.astype(np.float64)))
+    idx = None
+    if w.expected_path == "index":
+        if clustering is None:
+            cl = M.kmeans(model.users, w.clusters, max_iters=w.max_iters, seed=w.seed)
+        else:
+            cen, assign = clustering
+            theta = M.compute_max_angles(model.users, M.FactorMatrix(cen), assign)
+            c = cen.shape[0]
+            cl = M.Clustering(M.FactorMatrix(cen), assign, theta,
+                              tuple(np.flatnonzero(assign == j) for j in range(c)), np.empty(0), w.seed)
+        idx = M.build_index(model, cl, 4096)
+    _REF.update(M=M, model=model, index=idx)
+    return model, idx
+
+
+def reference_rates(w, k, steps, warmup, cores, per_worker, seed=12345):
+    """Per timed step: (users, wall seconds) over `cores` forked workers, each
+    on its own random sample of `per_worker` users."""
     import multiprocessing as mp
-
-    import simdex_oracle as O
-    users = workload.users.astype(np.float64)
-    items = workload.items.astype(np.float64)
-    rng = np.random.default_rng(12345)
-    if matmul:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(1)
-
-        def one(sample):
-            t0 = time.perf_counter()
-            O.topk_matmul(users[sample], items, k)
-            return len(sample), time.perf_counter() - t0
-        rates = []
-        for s in range(warmup + steps):
-            sample = np.sort(rng.choice(users.shape[0], per_worker, replace=False))
-            n, dt = one(sample)
-            if s >= warmup:
-                rates.append(n / dt)
-        return rates, f"topk_matmul on {per_worker} random users per step, 1 process"
-    from threadpoolctl import threadpool_limits
-    threadpool_limits(1)  # the reference protocol: one BLAS thread per process (PAPER.md:1080-1085)
-    cl = O.kmeans(users, workload.clusters, workload.max_iters, workload.seed)
-    ids, bounds, _ = O.build_index(items, cl["centroids"], cl["max_angle"])
-    _CPU_STATE.update(index=(ids, bounds, cl["assignment"]), items=items, users=users)
-    rates = []
+    rng = np.random.default_rng(seed)
+    out = []
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         for s in range(warmup + steps):
-            samples = [np.sort(rng.choice(users.shape[0], per_worker, replace=False)) for _ in range(cores)]
+            samples = [np.sort(rng.choice(w.users.shape[0], per_worker, replace=False)) for _ in range(cores)]
             t0 = time.perf_counter()
-            out = pool.map(_cpu_worker, [(smp, k, block) for smp in samples])
+            res = pool.map(_ref_worker, [(smp, k) for smp in samples])
             wall = time.perf_counter() - t0
             if s >= warmup:
-                rates.append(sum(n for n, _ in out) / wall)
-    return rates, (f"query_batch work-sharing (B={block}) over {per_worker} random users per process per step, "
-                   f"{cores} processes, index built by the oracle k-means/build_index")
+                out.append((sum(n for n, _ in res), wall))
+    return out
 
 
 def run_reference(args):
@@ -187,37 +231,81 @@ def run_reference(args):
     from paper_1706_01449_b200 import workloads as W
     w = W.CONFIGS[args.config]()
     k = args.k or w.k
+    try:
+        M = _import_reference()
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"mipserve not importable from baseline/_ref: {e}"}))
+        return
     cores = len(os.sched_getaffinity(0))
-    matmul = w.expected_path == "matmul"
-    per = 400 if matmul else 2000
-    rates, sample = cpu_reference(w, k, args.steps, args.warmup, cores, per, matmul=matmul)
-    v = float(np.mean(rates))
+    path = workload_path(w)
+    t0 = time.perf_counter()
+    reference_setup(w)
+    setup_s = time.perf_counter() - t0
+    per = {"index": 1500, "matmul": 120, "catalog": 2}[path]
+    steps = reference_rates(w, k, args.steps, args.warmup, cores, per)
+    users = sum(n for n, _ in steps)
+    wall = sum(t for _, t in steps)
+    v = users / wall
+    nu, ni, f = w.users.shape[0], w.items.shape[0], w.users.shape[1]
+    what = "query_batch work_sharing=True (B=4096)" if w.expected_path == "index" else "topk_matmul"
+    sample = (f"mipserve {getattr(M, '__version__', '?')} (baseline/_ref, unmodified) {what} on {per} random "
+              f"users per process per step, {cores} processes x 1 BLAS thread; setup (reference kmeans + "
+              f"build_index) {setup_s:.1f} s, untimed")
     line = {
-        "impl": "reference", "metric": f"exact top-K users/sec (f={w.users.shape[1]}, K={k})", "value": v,
-        "unit": "users/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * w.users.shape[0] / v, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": {"workload": f"{w.name}: {w.users.shape[0]}x{w.items.shape[0]}x{w.users.shape[1]} K={k}",
-                   "path": "matmul" if matmul else "index+work-sharing"},
-        "cpu_baseline": {"value": v, "unit": "users/s", "cores": 1 if matmul else cores, "kind": "port",
-                         "sample": sample},
+        "impl": "reference", "metric": f"exact top-K users/sec (f={f}, K={k})", "value": v, "unit": "users/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * wall / len(steps), "users_per_step": users / len(steps),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": f"{w.name}: {nu}x{ni}x{f}, K={k}" + (f", C={w.clusters}, B=4096"
+                                                                     if w.expected_path == "index" else ""),
+                   "path": path},
+        "cpu_baseline": {"value": v, "unit": "users/s", "cores": cores, "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_ours(w, k, cl_host):
+    """The reference (1 core) on a bounded sample; for the index path its
+    index is built by the reference's build_index from the GPU clustering
+    (identical to the reference's own k-means at cfg2:
+    tests/test_gpu_kernels.py::test_cfg2_full_size_against_reference)."""
+    try:
+        _, idx = reference_setup(w, cl_host)
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "users/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    per = min(250_000, w.users.shape[0]) if idx is not None else 300  # ~10 s of one core
+    steps = reference_rates(w, k, 1, 0, 1, per, seed=777)
+    users = sum(n for n, _ in steps)
+    wall = sum(t for _, t in steps)
+    what = "query_batch work_sharing=True (B=4096)" if idx is not None else "topk_matmul"
+    return {"value": users / wall, "unit": "users/s", "cores": 1, "kind": "reference",
+            "sample": f"mipserve {what} on {per} random users, 1 process x 1 BLAS thread, {wall:.1f} s"
+                      + ("; index by mipserve.build_index from the GPU clustering" if idx is not None else ""),
+            "cpu_model": cpu_model()}
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 
-def _profiled_traffic(path, k):
-    """DRAM bytes per gemm_topk launch (read + write) from the committed ncu
-    --set full capture of the same workload (profiles/), or None."""
-    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01h_gemm_topk_traffic.json")
-    if path != "index" or k != 10 or not os.path.exists(f):
-        return None
-    with open(f) as fh:
-        return json.load(fh)["traffic_bytes_per_launch"]
+def committed_traffic(kernel):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu --set full
+    capture (profiles/gemm_topk_traffic.json), only when it was taken on the
+    current kernel sources (hash match); else None."""
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            t = json.load(fh)
+    except (OSError, ValueError):
+        return None, "no committed capture"
+    if t.get("kernel_source_hash") != kernel_source_hash():
+        return None, "committed capture is from other kernel sources"
+    ent = t.get("launches", {}).get(kernel)
+    if not ent:
+        return None, f"no capture of {kernel}"
+    return ent["dram_bytes"], t.get("capture", "")
 
 
 def run_ours(args):
@@ -229,7 +317,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1706_01449_b200 as sx
-    from paper_1706_01449_b200 import _device, _lib, _ops, optimizer
+    from paper_1706_01449_b200 import _lib, optimizer, sharding
     from paper_1706_01449_b200 import index as index_mod
     from paper_1706_01449_b200 import workloads as W
 
@@ -239,29 +327,45 @@ def run_ours(args):
     nu, ni, f = w.users.shape[0], w.items.shape[0], w.users.shape[1]
     model = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
     dev = torch.device("cuda", local)
+    path = workload_path(w)
 
-    # ---- setup (untimed): cluster, build, estimate, decide -- run_pipeline's stages
-    t0 = time.perf_counter()
-    cl = sx.kmeans(model.users, min(w.clusters or 8, nu), max_iters=w.max_iters, seed=w.seed)
-    torch.cuda.synchronize()
-    t_cluster = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    idx = sx.build_index(model, cl, 4096)
-    torch.cuda.synchronize()
-    t_build = time.perf_counter() - t0
-    est = sx.estimate_walk_length(idx, model, 0.001, k, seed=w.seed)
-    decision = sx.decide(est.mean_visited, ni, 4096, k, optimizer.resolve_h0(None))
-    path = w.expected_path if args.config != "cfg2" else decision
-    q = torch.arange(nu, dtype=torch.int64, device=dev)
+    # ---- setup (untimed): run_pipeline's stages up to the decision
+    setup, decision, est, plan, cl_host, shard, shard_info = {}, None, None, None, None, None, {}
+    if path != "catalog":
+        plan = optimizer.plan_pipeline(model, k=k, num_clusters=min(w.clusters or 8, nu), block_size=4096,
+                                       max_iters=w.max_iters, seed=w.seed)
+        decision, est = plan.decision, plan.walk
+        setup = {"cluster": plan.cluster_seconds, "build": plan.build_seconds, "estimate": plan.estimate_seconds}
+        cl = plan.index.clustering
+        cl_host = (cl.centroids.values, np.asarray(cl.assignment))
+    served = "catalog" if path == "catalog" else decision  # follow the optimizer
+    if served == "index":
+        if world > 1:
+            shard = sharding.IndexShard(plan.index, model, rank, world, est)
+            shard_info = {"users": int(shard.user_ids.size), "work_share": shard.share}
+
+            def step():
+                return shard.topk_tensors(k)
+        else:
+            def step():
+                return index_mod.query_batch_tensors(plan.index, model, None, k, work_sharing=True)
+    elif served == "matmul":
+        if world > 1:
+            shard = sharding.UserShard(model, rank, world)
+            shard_info = {"users": int(shard.hi - shard.lo)}
+
+        def step():
+            return shard.topk_tensors(k) if shard is not None else sx.brute.topk_matmul_tensors(model, k)[:2]
+    else:  # catalogue sharded
+        if world > 1:
+            shard = sharding.CatalogShard(model, rank, world)
+            shard_info = {"items": int(shard.model.num_items if shard.model else 0),
+                          "users_merged": int(shard.user_hi - shard.user_lo)}
+
+        def step():
+            return shard.topk_tensors(k) if shard is not None else sx.brute.topk_matmul_tensors(model, k)[:2]
+
     flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)  # > 126 MB L2
-
-    if path == "index":
-        def step():
-            return index_mod.query_batch_tensors(idx, model, None, k, work_sharing=True)
-    else:
-        def step():
-            return sx.brute.topk_matmul_tensors(model, k)
-
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         step()
@@ -269,143 +373,192 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clocks = Clocks(local)
-    clocks.start_region()
     _lib.profile(True)
     launches0 = _lib.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
+    clocks.start_region()
     for s in range(args.steps):
         flush.fill_(s & 0x7F)
         ev[s][0].record(stream)
-        out = step()
+        step()
         ev[s][1].record(stream)
     torch.cuda.synchronize()
-    launches = _lib.launch_count() - launches0
     clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    step_sorted = sorted(step_ms)
-    step_stats = {"median": statistics.median(step_ms), "p90": step_sorted[min(len(step_sorted) - 1,
-                                                                              int(0.9 * len(step_sorted)))],
-                  "min": step_sorted[0], "max": step_sorted[-1]}
+    srt = sorted(step_ms)
+    step_stats = {"median": statistics.median(step_ms), "p90": srt[min(len(srt) - 1, int(0.9 * len(srt)))],
+                  "min": srt[0], "max": srt[-1]}
     total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.barrier()
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(total_ms.item()) / args.steps
-    value = world * nu / (ms_per_step / 1000.0)
+    value = nu / (ms_per_step / 1000.0)  # the fixed user set, all ranks together
 
-    # ---- dominant kernel roofline: per-kernel CUDA events recorded by the
-    # library on the launching stream during the timed steps (simdex_profile_*)
+    # ---- per-kernel times: CUDA events recorded by the library on the
+    # launching stream around each launch during the timed steps
     kernels = {}
-    for name in ("gemm_topk", "finalize", "walk", "select_rows", "score_f64"):
+    for name in ("gemm_topk", "gemm_topk_prefix", "gemm_topk_full", "finalize", "finalize_prefix", "finalize_full",
+                 "walk", "select_rows", "score_f64"):
         ms, n = _lib.profile_read(name)
         if n:
             kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": n / args.steps}
     _lib.profile(False)
-    gemm_ms = kernels.get("gemm_topk", {}).get("ms_per_step")
-    k_eff = min(k, ni)
-    if path == "index":
-        # two tensor-core passes per step: every user x its cluster's first B'
-        # list items, then the users not certified at B' x the whole catalogue
-        nq, n_cont, bp, _, _ = _lib.ws_stats()
-        flops = 2.0 * f * (nq * bp + n_cont * ni)
-        per_unit = (f"2*f*(B' + frac_continuing*|I|) flop per user: B'={bp}, continuing {n_cont}/{nq} users "
-                    f"({n_cont / max(nq, 1):.3f}) over |I|={ni}")
-    else:
-        flops = 2.0 * f * ni * nu
-        per_unit = f"2*f*|I| = {2 * f * ni} flop per user"
-    roof = None
-    if gemm_ms:
-        achieved = flops / (gemm_ms / 1000.0) / 1e12
-        roof = {"kernel": "gemm_topk_kernel (tcgen05 fp16 x fp16 -> fp32 TMEM, fused certified top-K)",
-                "bound": "tensor", "achieved": achieved, "peak": bf16, "peak_kind": f"{peak_kind} dense bf16 (= fp16 dense rate on B200; burst)",
-                "unit": "TFLOP/s", "frac": achieved / bf16, "traffic": _profiled_traffic(path, k),
-                "algorithmic_flops_per_step": flops, "launch_ms_per_step": gemm_ms,
-                "launches_per_step": kernels["gemm_topk"]["launches_per_step"], "per_unit": per_unit,
-                "share_of_step": gemm_ms / ms_per_step,
-                # BASELINE's north star states its GEMM target against a split-fp32
-                # peak (3xTF32 = dense bf16 / 6 with TF32 = bf16 / 2); the certified
-                # single-pass fp16 product needs one pass, so it can exceed that
-                "split_fp32_peak": bf16 / 6.0, "frac_vs_split_fp32_peak": achieved / (bf16 / 6.0)}
+    kern_ms = sum(v["ms_per_step"] for name, v in kernels.items() if name.startswith(("gemm", "finalize")))
+    roof = roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, _lib)
 
-    # ---- e2e: public API from host buffers (run_pipeline), per step
-    e2e = None
-    if not args.no_e2e:
-        host_u = torch.from_numpy(model.users.values).pin_memory()
-        host_i = torch.from_numpy(model.items.values).pin_memory()
-        e2e_steps = max(1, min(3, args.steps))
-        e2e_warm = 2  # first passes pay one-time costs (pinned host pools, tensor maps, allocator growth)
-        times = []
-        for s in range(e2e_steps + e2e_warm):
-            m2 = sx.ModelPair(sx.FactorMatrix(model.users.values), sx.FactorMatrix(model.items.values))
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            m2.users.__dict__["_device"][local] = {"f64": host_u.to(dev, non_blocking=True)}
-            m2.items.__dict__["_device"][local] = {"f64": host_i.to(dev, non_blocking=True)}
-            res, rep = sx.run_pipeline(m2, k=k, num_clusters=min(w.clusters or 8, nu), block_size=4096,
-                                       max_iters=w.max_iters, seed=w.seed, force=path)
-            _ = res.item_ids  # results are host arrays [U, K] once run_pipeline returns
-            torch.cuda.synchronize()
-            if s >= e2e_warm:
-                times.append(time.perf_counter() - t0)
-        t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        k_eff = min(k, ni)
-        e2e = {"value": world * nu / float(t.item()), "unit": "users/s",
-               "h2d_bytes_per_step": int(model.users.values.nbytes + model.items.values.nbytes),
-               "d2h_bytes_per_step": int(nu * k_eff * (4 + 8) + nu * 8),
-               "what": "run_pipeline from host float64 matrices: H2D, k-means, build, estimate, serve, D2H [U,K]",
-               "stage_seconds": {"cluster": rep.cluster_seconds, "build": rep.build_seconds,
-                                 "estimate": rep.estimate_seconds, "serve": rep.serve_seconds}}
+    # ---- e2e: public API from host buffers, per step
+    e2e = e2e_serve = None
+    if not args.no_e2e and served != "catalog":
+        e2e = measure_e2e(sx, sharding, model, w, k, served, rank, world, dev, torch, dist)
+        e2e_serve = measure_e2e_serve(sx, plan, model, k, served, world, shard, dev, torch, dist, nu)
 
-    # ---- serving through the public API with the model and index resident:
-    # query_batch for every user, results materialised on the host (D2H inside)
-    e2e_serve = None
-    if not args.no_e2e:
-        times = []
-        for s in range(4):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            if path == "index":
-                res = sx.query_batch(idx, model, None, k, work_sharing=True)
-            else:
-                res = sx.topk_matmul(model, k)
-            _ = res.item_ids
-            torch.cuda.synchronize()
-            if s >= 1:
-                times.append(time.perf_counter() - t0)
-        t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_serve = {"value": world * nu / float(t.item()), "unit": "users/s", "h2d_bytes_per_step": 0,
-                     "d2h_bytes_per_step": int(nu * min(k, ni) * (4 + 8) + nu * 8),
-                     "what": "query_batch (public API) for all users, model + index resident, results to host"}
-
-    # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on a bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        matmul = path == "matmul"
-        rates, sample = cpu_reference(w, k, 2, 0, 1, 300 if matmul else 8000, matmul=matmul)
-        cpu = {"value": float(np.mean(rates)), "unit": "users/s", "cores": 1, "kind": "port", "sample": sample}
+    if rank == 0 and world == 1 and not args.no_cpu and served != "catalog":
+        cpu = cpu_baseline_ours(w, k, cl_host)
 
     if rank == 0:
         line = {
             "metric": f"exact top-K users/sec (f={f}, K={k})", "value": value, "unit": "users/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (exact) / fp16 tensor-core candidates",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "step_ms": step_stats,
+            "main_kernels_ms_per_step": kern_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 (exact) / fp16 tensor-core candidates",
             "data": "synthetic (seeded, BASELINE.json shapes; trained Netflix/R2 models unavailable)",
-            "config": {"workload": f"{w.name}: {nu}x{ni}x{f}, K={k}, C={cl.num_clusters}, B=4096",
-                       "path": path, "decision": decision, "mean_visited_sample": est.mean_visited,
-                       "per_rank_users": nu, "parallelism": f"users-dp{world} (each rank serves the full batch)",
+            "config": {"workload": f"{w.name}: {nu}x{ni}x{f}, K={k}" + (f", C={w.clusters}, B=4096"
+                                                                         if served == "index" else ""),
+                       "path": served, "decision": decision,
+                       "mean_visited_sample": None if est is None else est.mean_visited,
+                       "parallelism": (f"{world} ranks: " + {"index": "users routed by cluster",
+                                                              "matmul": "contiguous user blocks",
+                                                              "catalog": "item shards + NCCL all-to-all + merge"}
+                                       [served]) if world > 1 else "1 GPU",
+                       "rank0_shard": shard_info or None,
                        "l2": "flushed (256 MB write) before every timed step",
-                       "setup_seconds": {"cluster": t_cluster, "build": t_build}},
-            "step_ms": step_stats, "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "e2e_serve": e2e_serve, "clocks": clk,
-            "gpu_launches": launches,
+                       "setup_seconds": setup},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "e2e_serve": e2e_serve,
+            "clocks": clk, "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib):
+    """Tensor-bound roofline of the dominant kernel, gemm_topk.  Algorithmic
+    work = 2 f flops per scored (user, item) pair, f unpadded.
+    Index path, three fractions: the stage-1 prefix launch alone (it
+    multiplies every tile it is credited with: the headline ``frac``), both
+    launches (stage 2 skips norm-bounded tiles it is still credited with) and
+    the whole step.  Per rank at N > 1 (rank 0's launches)."""
+    nu, ni, f = w.users.shape[0], w.items.shape[0], w.users.shape[1]
+    peak_note = f"{peak_kind} dense bf16 = fp16 dense rate, burst"
+    if served == "index":
+        nq, n_cont, bp, _, _ = lib.ws_stats()
+        s1 = kernels.get("gemm_topk_prefix")
+        s2 = kernels.get("gemm_topk_full")
+        if not s1:
+            return None
+        f1 = 2.0 * f * nq * bp
+        f2 = 2.0 * f * n_cont * ni
+        a1 = f1 / (s1["ms_per_step"] / 1e3) / 1e12
+        gemm_ms = s1["ms_per_step"] + (s2["ms_per_step"] if s2 else 0.0)
+        traffic, src = committed_traffic("gemm_topk_prefix")
+        return {"kernel": "gemm_topk_kernel stage 1 (work-sharing prefix: every cluster's first B' list items x "
+                          "its users; tcgen05 fp16 -> fp32 TMEM, fused certified top-K)",
+                "bound": "tensor", "achieved": a1, "peak": bf16, "peak_kind": peak_note, "unit": "TFLOP/s",
+                "frac": a1 / bf16, "traffic": traffic, "traffic_source": src,
+                "per_unit": f"2*f*B' = {2 * f * bp} flop per user (B'={bp}), {nq} users per launch",
+                "algorithmic_flops_per_launch": f1, "launch_ms": s1["ms_per_step"],
+                "frac_both_launches": (f1 + f2) / (gemm_ms / 1e3) / 1e12 / bf16,
+                "both_launches_note": (f"stage 2: {n_cont}/{nq} users continue past B' over |I|={ni}, credited "
+                                       f"2f|I| each though the norm-ordered pass skips tiles"),
+                "frac_whole_step": (f1 + f2) / (ms_per_step / 1e3) / 1e12 / bf16,
+                "share_of_step": s1["ms_per_step"] / ms_per_step}
+    g = kernels.get("gemm_topk")
+    if not g:
+        return None
+    n_users = nu / world if served == "matmul" else nu
+    n_items = ni if served == "matmul" else ni / world
+    flops = 2.0 * f * n_items * n_users
+    a = flops / (g["ms_per_step"] / 1e3) / 1e12
+    traffic, src = committed_traffic("gemm_topk")
+    note = "" if served == "matmul" else " (cfg5: the norm-ordered early exit skips tiles it is credited with)"
+    return {"kernel": "gemm_topk_kernel (blocked product, tcgen05 fp16 -> fp32 TMEM, fused certified top-K)",
+            "bound": "tensor", "achieved": a, "peak": bf16, "peak_kind": peak_note, "unit": "TFLOP/s",
+            "frac": a / bf16, "traffic": traffic, "traffic_source": src,
+            "per_unit": f"2*f*|I| = {2 * f * ni} flop per user{note}", "algorithmic_flops_per_launch": flops,
+            "launch_ms": g["ms_per_step"], "frac_whole_step": flops / (ms_per_step / 1e3) / 1e12 / bf16,
+            "share_of_step": g["ms_per_step"] / ms_per_step}
+
+
+def measure_e2e(sx, sharding, model, w, k, served, rank, world, dev, torch, dist):
+    """run_pipeline from host float64 matrices (pinned H2D inside the timed
+    region), results on the host; N > 1: run_pipeline_shard per rank."""
+    nu, ni = w.users.shape[0], w.items.shape[0]
+    host_u = torch.from_numpy(model.users.values).pin_memory()
+    host_i = torch.from_numpy(model.items.values).pin_memory()
+    times, rep, n_mine = [], None, nu
+    for s in range(4):
+        m2 = sx.ModelPair(sx.FactorMatrix(model.users.values), sx.FactorMatrix(model.items.values))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        m2.users.__dict__["_device"] = {dev.index: {"f64": host_u.to(dev, non_blocking=True)}}
+        m2.items.__dict__["_device"] = {dev.index: {"f64": host_i.to(dev, non_blocking=True)}}
+        kw = dict(k=k, num_clusters=min(w.clusters or 8, nu), block_size=4096, max_iters=w.max_iters, seed=w.seed,
+                  force=served)
+        if world > 1:
+            res, rep = sharding.run_pipeline_shard(m2, rank=rank, world=world, **kw)
+        else:
+            res, rep = sx.run_pipeline(m2, **kw)
+        _ = res.item_ids
+        n_mine = len(res)
+        torch.cuda.synchronize()
+        if s >= 2:  # the first passes pay one-time costs (pinned pools, tensor maps, arena growth)
+            times.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    k_eff = min(k, ni)
+    return {"value": nu / float(t.item()), "unit": "users/s",
+            "h2d_bytes_per_step": int(model.users.values.nbytes + model.items.values.nbytes),
+            "d2h_bytes_per_step": int(n_mine * (k_eff * (4 + 8) + 8)),
+            "what": ("run_pipeline" if world == 1 else "sharding.run_pipeline_shard (max over ranks)") +
+                    " from host float64 matrices: H2D, k-means, build, estimate, decide, serve, D2H [U,K]",
+            "stage_seconds": {"cluster": rep.cluster_seconds, "build": rep.build_seconds,
+                              "estimate": rep.estimate_seconds, "serve": rep.serve_seconds}}
+
+
+def measure_e2e_serve(sx, plan, model, k, served, world, shard, dev, torch, dist, nu):
+    """Serving through the public API with the model and index resident:
+    query_batch / topk_matmul for every user (this rank's share at N > 1),
+    results materialised on the host (D2H inside)."""
+    from paper_1706_01449_b200 import _device
+    times = []
+    d2h = 0
+    for s in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world > 1:
+            out = shard.topk_tensors(k)
+            hs = _device.to_host_pinned_many(*out)
+            d2h = sum(h.nbytes for h in hs)
+        else:
+            res = (sx.query_batch(plan.index, model, None, k, work_sharing=True) if served == "index"
+                   else sx.topk_matmul(model, k))
+            _ = res.item_ids
+            d2h = res.item_ids.nbytes + res.scores.nbytes + np.asarray(res.visited).nbytes
+        torch.cuda.synchronize()
+        if s >= 1:
+            times.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": nu / float(t.item()), "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h,
+            "what": "query_batch / topk_matmul (public API), model + index resident, results to host"}
 
 
 if __name__ == "__main__":

@@ -72,6 +72,19 @@ def packed_sorted(matrix) -> _ops.Packed:
     return c["packed_sorted"]
 
 
+def share_rows(parent, child, lo: int, hi: int) -> None:
+    """Seed ``child``'s device cache (child = rows [lo, hi) of parent) with
+    views of the parent's resident copies, so a shard costs no upload."""
+    src = parent.__dict__.get("_device", {}).get(torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    if not src:
+        return
+    dst = _cache(child)
+    if "f64" in src and "f64" not in dst:
+        dst["f64"] = src["f64"][lo:hi]
+    if "f32" in src and "f32" not in dst:
+        dst["f32"] = None if src["f32"] is None else src["f32"][lo:hi]
+
+
 def norms(matrix) -> torch.Tensor:
     return packed(matrix).norms
 

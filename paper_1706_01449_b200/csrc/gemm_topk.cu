@@ -1440,7 +1440,7 @@ int geometry(int kp, GemmGeometry* g) {
 
 template <int KT>
 int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
-                   cudaStream_t s) {
+                   const char* prof, cudaStream_t s) {
   auto kern = p.exit_c ? gemm_topk_kernel<KT, 2> : p.norm_sorted ? gemm_topk_kernel<KT, 1> : gemm_topk_kernel<KT, 0>;
   static size_t set_for[16][3] = {};  // per device and exit mode: largest shared-memory size already allowed
   const int em = p.exit_c ? 2 : p.norm_sorted ? 1 : 0;
@@ -1451,33 +1451,35 @@ int launch_gemm_kt(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParam
     SIMDEX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
     done = g.smem;
   }
-  ProfileScope _prof("gemm_topk", s);
+  ProfileScope _prof(prof, s);
   kern<<<grid, kThreads, g.smem, s>>>(ma, mb, p);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("gemm_topk");
   return SIMDEX_OK;
 }
 
+// prof: the simdex_profile name of this launch (gemm_topk, gemm_topk_prefix,
+// gemm_topk_full, gemm_assign)
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const TopkParams& p, const GemmGeometry& g, int grid,
-                cudaStream_t s) {
-  if (p.debug_out) return launch_gemm_kt<-1>(ma, mb, p, g, grid, s);
+                const char* prof, cudaStream_t s) {
+  if (p.debug_out) return launch_gemm_kt<-1>(ma, mb, p, g, grid, prof, s);
   switch (kt_for(p.k_eff)) {
-    case 1: return launch_gemm_kt<1>(ma, mb, p, g, grid, s);
-    case 2: return launch_gemm_kt<2>(ma, mb, p, g, grid, s);
-    case 4: return launch_gemm_kt<4>(ma, mb, p, g, grid, s);
-    case 5: return launch_gemm_kt<5>(ma, mb, p, g, grid, s);
-    case 8: return launch_gemm_kt<8>(ma, mb, p, g, grid, s);
-    case 10: return launch_gemm_kt<10>(ma, mb, p, g, grid, s);
-    case 16: return launch_gemm_kt<16>(ma, mb, p, g, grid, s);
-    case 32: return launch_gemm_kt<32>(ma, mb, p, g, grid, s);
-    case 50: return launch_gemm_kt<50>(ma, mb, p, g, grid, s);
-    case 64: return launch_gemm_kt<64>(ma, mb, p, g, grid, s);
-    default: return launch_gemm_kt<0>(ma, mb, p, g, grid, s);
+    case 1: return launch_gemm_kt<1>(ma, mb, p, g, grid, prof, s);
+    case 2: return launch_gemm_kt<2>(ma, mb, p, g, grid, prof, s);
+    case 4: return launch_gemm_kt<4>(ma, mb, p, g, grid, prof, s);
+    case 5: return launch_gemm_kt<5>(ma, mb, p, g, grid, prof, s);
+    case 8: return launch_gemm_kt<8>(ma, mb, p, g, grid, prof, s);
+    case 10: return launch_gemm_kt<10>(ma, mb, p, g, grid, prof, s);
+    case 16: return launch_gemm_kt<16>(ma, mb, p, g, grid, prof, s);
+    case 32: return launch_gemm_kt<32>(ma, mb, p, g, grid, prof, s);
+    case 50: return launch_gemm_kt<50>(ma, mb, p, g, grid, prof, s);
+    case 64: return launch_gemm_kt<64>(ma, mb, p, g, grid, prof, s);
+    default: return launch_gemm_kt<0>(ma, mb, p, g, grid, prof, s);
   }
 }
 
 template <int LPR>
-int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
+int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, const char* prof, cudaStream_t s) {
   constexpr int RPW = 32 / LPR;
   const size_t per_row = ((size_t)fp.pow2 * 12 + (size_t)fp.f * 8 + 15) & ~size_t(15);
   int warps = 8;
@@ -1494,15 +1496,15 @@ int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, cudaStream_t s) 
     SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set_for[dev & 15] = smem;
   }
-  ProfileScope _prof("finalize", s);
+  ProfileScope _prof(prof, s);
   finalize_kernel<LPR><<<(unsigned)ceil_div(rows, RPW * warps), 32 * warps, smem, s>>>(fp);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("finalize");
   return SIMDEX_OK;
 }
 
-int launch_finalize(const FinalizeParams& fp, int64_t rows, cudaStream_t s) {
-  return fp.k_eff > 32 ? launch_finalize_lpr<32>(fp, rows, s) : launch_finalize_lpr<8>(fp, rows, s);
+int launch_finalize(const FinalizeParams& fp, int64_t rows, const char* prof, cudaStream_t s) {
+  return fp.k_eff > 32 ? launch_finalize_lpr<32>(fp, rows, prof, s) : launch_finalize_lpr<8>(fp, rows, prof, s);
 }
 
 // Candidate buffers + per-row state for up to `rows` packed rows (carved
@@ -1646,7 +1648,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
     }
   }
   const int grid = (int)(nunits < g.ctas_per_sm * sm_count() ? nunits : g.ctas_per_sm * sm_count());
-  if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
+  if ((rc = launch_gemm(ma, mb, p, g, grid, "gemm_topk", s))) return rc;
   if (debug_out) return SIMDEX_OK;
   SIMDEX_CUDA(cudaMemsetAsync(over_n, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
@@ -1673,7 +1675,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   fp.over_n = over_n;
   fp.item_perm = item_perm;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
-  if ((rc = launch_finalize(fp, nu, s))) return rc;
+  if ((rc = launch_finalize(fp, nu, "finalize", s))) return rc;
   // band overflow (rare): exact float64 rows, the count read on the device
   return exact_topk_devcount(users, users32, items, items32, ni, f, over_list, nullptr, over_n, k, over_out,
                              out_ids, out_scores, slab, s);
@@ -1795,7 +1797,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
       p.heap_ops = hops.p;
     }
     grid = (int)(units_max < g.ctas_per_sm * sm_count() ? units_max : g.ctas_per_sm * sm_count());
-    if ((rc = launch_gemm(ma, mb, p, g, grid, s))) return rc;
+    if ((rc = launch_gemm(ma, mb, p, g, grid, "gemm_topk_prefix", s))) return rc;
     if (stats) {
       std::vector<int64_t> hh(rows_max);
       SIMDEX_CUDA(cudaMemcpy(hh.data(), hops.p, sizeof(int64_t) * rows_max, cudaMemcpyDeviceToHost));
@@ -1847,7 +1849,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     fp.prefix = 0;  // no floor: visited is the stop position from 0
     all_rows_continue_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(row_user, rows_max, cont, cont_n, t0);
     SIMDEX_LAUNCH_CHECK("all_rows_continue");
-  } else if ((rc = launch_finalize(fp, rows_max, s))) {
+  } else if ((rc = launch_finalize(fp, rows_max, "finalize_prefix", s))) {
     return rc;
   }
   if (!stage2) {  // the prefix was the whole list
@@ -1901,7 +1903,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     p2.heap_ops = hops2.p;
   }
   grid = (int)(units2 < g.ctas_per_sm * sm_count() ? units2 : g.ctas_per_sm * sm_count());
-  if ((rc = launch_gemm(ma2, mb2, p2, g, grid, s))) return rc;
+  if ((rc = launch_gemm(ma2, mb2, p2, g, grid, "gemm_topk_full", s))) return rc;
   if (stats) {
     std::vector<int64_t> hh(rows2);
     SIMDEX_CUDA(cudaMemcpy(hh.data(), hops2.p, sizeof(int64_t) * rows2, cudaMemcpyDeviceToHost));
@@ -1920,7 +1922,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   f2.cont_list = nullptr;
   f2.cont_n = nullptr;
   f2.item_perm = item_perm;
-  if ((rc = launch_finalize(f2, rows2, s))) return rc;
+  if ((rc = launch_finalize(f2, rows2, "finalize_full", s))) return rc;
   record_ws_stats(nq, &host[0], -1, bp, ni, f);
   // band overflow on the full list (rare): exact float64 scan for those users
   // and the same visited closed form; counts read on the device
@@ -2055,7 +2057,7 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   if ((rc = make_map(&mb, ca, nc_pad, kp))) return rc;
   TopkParams tp = make_params(st, units, n_units, inrm, inmax, cu, g, f + 1, k_eff);
   const int grid = (int)(nunits < g.ctas_per_sm * sm_count() ? nunits : g.ctas_per_sm * sm_count());
-  if ((rc = launch_gemm(ma, mb, tp, g, grid, s))) return rc;
+  if ((rc = launch_gemm(ma, mb, tp, g, grid, "gemm_assign", s))) return rc;
   SIMDEX_CUDA(cudaMemsetAsync(over_n, 0, sizeof(int32_t), s));
   FinalizeParams fp{};
   fp.mode = kAssign;

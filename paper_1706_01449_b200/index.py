@@ -453,9 +453,25 @@ def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int
     return _ops.WS_PREFIX_EXIT if mv < PREFIX_EXIT_FRACTION * min(index.block_size, n) else 0
 
 
-def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.Tensor, k: int,
-                        work_sharing: bool = True):
-    """Device form of query_batch: int64 user rows in, (ids int32 [n, k_eff],
+class QuerySet:
+    """A fixed set of user rows prepared for repeated serving on one index:
+    the device id tensor and its grouping by cluster (simdex_group_queries),
+    computed once.  Used by the multi-GPU shards, whose user sets are fixed."""
+
+    def __init__(self, index: CentroidIndex, user_ids):
+        ids = np.asarray(user_ids, dtype=np.int64)
+        self.index = index
+        self.user_ids = ids
+        self.q = _device.to_device(ids)
+        self.grouped = _ops.group_queries(self.q, index.device_assignment(), index.num_clusters)
+
+    def __len__(self):
+        return int(self.user_ids.shape[0])
+
+
+def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int, work_sharing: bool = True):
+    """Device form of query_batch: int64 user rows in (a device tensor, a
+    QuerySet of this index, or None for every user), (ids int32 [n, k_eff],
     scores float64, visited int64) out, all on the device, in query order."""
     users = _device.f64(model.users)
     items = _device.f64(model.items)
@@ -464,6 +480,10 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users: torch.T
     grouped = None
     if q_users is None:
         q_users, grouped = index.device_all_users(model.num_users, users.device)
+    elif isinstance(q_users, QuerySet):
+        if q_users.index is not index:
+            raise ValueError("QuerySet was prepared for another index")
+        q_users, grouped = q_users.q, q_users.grouped
     pu, pi = _device.packed(model.users), _device.packed_sorted(model.items)
     if min(k, n) <= 256 and pu.kp <= 256:
         # tensor-core path; without work sharing every query takes the full-list

@@ -132,8 +132,8 @@ def test_catalog_sharded_shards_and_device_merge(sx):
 
 
 def test_catalog_sharded_topk_nccl_single_rank(sx):
-    """catalog_sharded_topk itself over a one-rank NCCL group (the all-gather
-    and merge run for real; more ranks need more GPUs)."""
+    """catalog_sharded_topk itself over a one-rank NCCL group (the all-to-all /
+    all-gather and the merge run for real; two-rank runs: test_multirank.py)."""
     import os
     import torch
     import torch.distributed as dist
@@ -148,8 +148,11 @@ def test_catalog_sharded_topk_nccl_single_rank(sx):
         users = rng.normal(0.0, 1.0, (3_000, 64)).astype(np.float32)
         items = rng.normal(0.0, 1.0, (9_000, 64)).astype(np.float32)
         m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
-        ids, sc = sharding.catalog_sharded_topk(m, 20)
         sample = np.sort(np.random.default_rng(1).choice(m.num_users, 300, replace=False))
-        _check(ids.cpu().numpy(), sc.cpu().numpy(), m.users.values, m.items.values, 20, sample, "nccl world 1")
+        for exchange in ("all_to_all", "all_gather"):
+            ids, sc, lo = sharding.catalog_sharded_topk(m, 20, exchange=exchange)
+            assert lo == 0 and ids.shape[0] == m.num_users
+            _check(ids.cpu().numpy(), sc.cpu().numpy(), m.users.values, m.items.values, 20, sample,
+                   f"nccl world 1 {exchange}")
     finally:
         dist.destroy_process_group()
