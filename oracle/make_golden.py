@@ -12,7 +12,12 @@ tests); nothing at test time reads /root/reference.
 
 ``--big`` adds the BASELINE cfg1 full-size brute-force answers and the cfg2
 full-size clustering/index/walk-sample answers (slow: the reference's
-k-means at cfg2 takes ~1 minute).
+k-means at cfg2 takes ~1 minute).  ``--cfg2-k5`` adds K = 5 to the cfg2
+fixture (same clustering, which the fixture stores).  ``--cfg4 FILE``
+writes the cfg4 fixture from a GPU clustering dumped on the box
+(tools/dump_clustering.py): the reference's compute_max_angles,
+build_index, query_batch and query_user on that clustering for a 500-user
+sample.
 """
 
 from __future__ import annotations
@@ -171,7 +176,84 @@ def big():
     print(f"cfg2 golden in {time.time() - t0:.1f}s", flush=True)
 
 
+def _ref_clustering(cen, assign, seed, users):
+    c = cen.shape[0]
+    theta = M.compute_max_angles(users, M.FactorMatrix(cen), assign)
+    return M.Clustering(M.FactorMatrix(cen), assign, theta, tuple(np.flatnonzero(assign == j) for j in range(c)),
+                        np.empty(0), seed)
+
+
+def cfg2_k5():
+    """K = 5 (a BASELINE depth) on the stored cfg2 reference clustering."""
+    from paper_1706_01449_b200 import workloads as W
+    t0 = time.time()
+    path = os.path.join(OUT, "cfg2_index.npz")
+    g = dict(np.load(path))
+    w = W.cfg2()
+    model = M.ModelPair(M.FactorMatrix(w.users), M.FactorMatrix(w.items))
+    cl = _ref_clustering(g["centroids"], g["assignment"].astype(np.int64), 1, model.users)
+    np.testing.assert_array_equal(cl.max_angle, g["max_angle"])  # the stored clustering is the reference's
+    idx = M.build_index(model, cl, 4096)
+    sample = g["sample"]
+    k = 5
+    est = MO.estimate_walk_length(idx, model, 0.001, k, seed=1)
+    g[f"est_k{k}"] = np.array([est.mean_visited, est.ci_low, est.ci_high, est.sample_size])
+    ws = M.query_batch(idx, model, sample, k, work_sharing=True)
+    g[f"ws_k{k}_ids"] = arr(ws, "item_ids").astype(np.int16)
+    g[f"ws_k{k}_scores"] = arr(ws, "scores")
+    g[f"ws_k{k}_visited"] = np.array([r.visited for r in ws], dtype=np.int32)
+    nows = [M.query_user(idx, model, int(u), k) for u in sample[:500]]
+    g[f"nows_k{k}_visited"] = np.array([r.visited for r in nows], dtype=np.int32)
+    np.savez_compressed(path, **g)
+    print(f"cfg2 K=5 in {time.time() - t0:.1f}s", flush=True)
+
+
+def cfg4_fixture(dump_path):
+    """cfg4 (1,823,179 x 136,736, C=1024) answers of the reference on the GPU
+    clustering: only the sampled users' clusters are built (a cluster's list
+    depends on its centroid and theta_b alone, index.py:129-155)."""
+    from paper_1706_01449_b200 import workloads as W
+    t0 = time.time()
+    d = np.load(dump_path)
+    cen, assign = d["centroids"], d["assignment"].astype(np.int64)
+    w = W.cfg4()
+    users = M.FactorMatrix(w.users)
+    items = M.FactorMatrix(w.items)
+    theta_all = M.compute_max_angles(users, M.FactorMatrix(cen), assign)
+    rng = np.random.default_rng(404)
+    clusters = np.sort(rng.choice(np.unique(assign), 40, replace=False))
+    pool = np.flatnonzero(np.isin(assign, clusters))
+    sample = np.sort(rng.choice(pool, 500, replace=False))
+    # the reference index over the chosen clusters only (same lists, fewer of them)
+    remap = {int(c): j for j, c in enumerate(clusters)}
+    sub_assign = np.array([remap.get(int(a), 0) for a in assign[sample]], dtype=np.int64)
+    sub_users = M.FactorMatrix(w.users[sample])
+    sub_model = M.ModelPair(sub_users, items)
+    sub_cl = M.Clustering(M.FactorMatrix(cen[clusters]), sub_assign, theta_all[clusters],
+                          tuple(np.flatnonzero(sub_assign == j) for j in range(clusters.size)), np.empty(0), 3)
+    idx = M.build_index(sub_model, sub_cl, 4096)
+    out = {"centroids": cen, "assignment_sha": np.frombuffer(__import__("hashlib").sha256(
+        assign.astype("<i8").tobytes()).digest(), dtype=np.uint8), "theta": theta_all, "sample": sample,
+        "clusters": clusters}
+    for k in (1, 10):
+        ws = M.query_batch(idx, sub_model, None, k, work_sharing=True)
+        out[f"ws_k{k}_ids"] = arr(ws, "item_ids").astype(np.int32)
+        out[f"ws_k{k}_scores"] = arr(ws, "scores")
+        out[f"ws_k{k}_visited"] = np.array([r.visited for r in ws], dtype=np.int32)
+        nows = [M.query_user(idx, sub_model, i, k) for i in range(sample.size)]
+        out[f"nows_k{k}_ids"] = arr(nows, "item_ids").astype(np.int32)
+        out[f"nows_k{k}_visited"] = np.array([r.visited for r in nows], dtype=np.int32)
+    np.savez_compressed(os.path.join(OUT, "cfg4_sample.npz"), **out)
+    print(f"cfg4 fixture in {time.time() - t0:.1f}s", flush=True)
+
+
 if __name__ == "__main__":
+    if "--cfg2-k5" in sys.argv:
+        cfg2_k5()
+        sys.exit(0)
+    if "--cfg4" in sys.argv:
+        cfg4_fixture(sys.argv[sys.argv.index("--cfg4") + 1])
+        sys.exit(0)
     os.makedirs(OUT, exist_ok=True)
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     decisions()

@@ -17,7 +17,7 @@ import torch
 
 from . import _device, _ops
 from .index import TopKResults
-from .model_io import ModelPair
+from .model_io import FactorMatrix, ModelPair
 
 # tiles the reference's default_blocks picks (brute.py:21-40); accepted for
 # API compatibility, the GPU tiling is internal
@@ -116,18 +116,43 @@ class ThroughputSample:
     unblocked_rate: float
 
 
-def measure_throughput(model: ModelPair, k: int = 1, blocks: BlockSpec | None = None) -> ThroughputSample:
-    """Time both serving styles over the full user x item workload
-    (brute.py:141-150), device-synchronised wall clock."""
+# GPU throughput is a saturation figure: a model smaller than this many
+# (user, item) pairs is measured with its users tiled up to it (the rate per
+# pair of a launch-bound run would measure launch latency, not the hardware
+# factor h0 stands for, optimizer.py:69-102).
+CALIBRATION_PAIRS = 1 << 28
+
+
+def _calibration_model(model: ModelPair) -> ModelPair:
     pairs = model.num_users * model.num_items
-    _device.packed(model.users), _device.packed(model.items), _scan_list(model)
+    if pairs >= CALIBRATION_PAIRS:
+        return model
+    cache = model.users.__dict__.setdefault("_calibration", {})
+    key = id(model.items)
+    ent = cache.get(key)
+    if ent is None or ent[0] is not model.items:
+        reps = -(-CALIBRATION_PAIRS // pairs)
+        reps = max(1, min(reps, (1 << 22) // model.num_users))  # at most ~4M users
+        ent = cache[key] = (model.items, ModelPair(FactorMatrix(np.tile(model.users.values, (reps, 1))), model.items))
+    return ent[1]
+
+
+def measure_throughput(model: ModelPair, k: int = 1, blocks: BlockSpec | None = None) -> ThroughputSample:
+    """Scored pairs per second of both serving styles (brute.py:141-150): the
+    tensor-core blocked product and the per-pair scan, each timed warm
+    (operands packed, workspace grown) with device synchronisation, on the
+    model -- or, below CALIBRATION_PAIRS, its users tiled up to that size."""
+    m = _calibration_model(model)
+    pairs = m.num_users * m.num_items
+    topk_matmul_tensors(m, k)
+    _perpair_scan(m, k)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    topk_matmul_tensors(model, k)
+    topk_matmul_tensors(m, k)
     torch.cuda.synchronize()
     blocked = max(time.perf_counter() - t0, 1e-9)
     t0 = time.perf_counter()
-    _perpair_scan(model, k)
+    _perpair_scan(m, k)
     torch.cuda.synchronize()
     unblocked = max(time.perf_counter() - t0, 1e-9)
     return ThroughputSample(pairs / blocked, pairs / unblocked)

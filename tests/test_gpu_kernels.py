@@ -104,7 +104,7 @@ def test_cfg2_full_size_against_reference(sx):
     """BASELINE configs[1] at full size (480,189 x 17,770, f=50): the GPU
     k-means reproduces the reference clustering, and the work-sharing serve
     path returns the reference's ids, scores and visited counts on a 2,000
-    user sample for K in {1, 10, 50}."""
+    user sample for K in {1, 5, 10, 50} (every BASELINE depth)."""
     from paper_1706_01449_b200 import workloads as W
     g = load_golden("cfg2_index")
     w = W.cfg2()
@@ -119,7 +119,7 @@ def test_cfg2_full_size_against_reference(sx):
     np.testing.assert_array_equal(idx.item_ids[:, :64], g["ids_head"].astype(np.int64))
     np.testing.assert_allclose(idx.bounds[:, :64], g["bounds_head"], rtol=1e-12)
     sample = g["sample"]
-    for k in (1, 10, 50):
+    for k in (1, 5, 10, 50):
         res = sx.query_batch(idx, m, sample, k, work_sharing=True)
         want_ids = g[f"ws_k{k}_ids"].astype(np.int64)
         assert_same_topk(res.item_ids, res.scores, want_ids, g[f"ws_k{k}_scores"], ctx=f"cfg2 k={k}")
@@ -129,7 +129,7 @@ def test_cfg2_full_size_against_reference(sx):
     # the same answers with the prefix pass's ceiling exit forced on (it is
     # normally enabled only when the walk estimate is short against B)
     from paper_1706_01449_b200 import index as I
-    for k in (1, 10, 50):
+    for k in (1, 5, 10, 50):
         I.note_walk_estimate(idx, k, 0.0)
         res = sx.query_batch(idx, m, sample, k, work_sharing=True)
         assert_same_topk(res.item_ids, res.scores, g[f"ws_k{k}_ids"].astype(np.int64), g[f"ws_k{k}_scores"],
