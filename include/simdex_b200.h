@@ -104,6 +104,16 @@ SIMDEX_API int simdex_max_abs(const double* x, int64_t n, double* out, void* str
 SIMDEX_API int simdex_pack_f16(const double* x, int64_t rows, int32_t f, int32_t scale_exp,
                      int64_t rows_pad, int32_t kp, uint16_t* out_f16, double* out_norms, void* stream);
 
+/* simdex_pack_f16 with one exact power-of-two scale PER ROW (the user
+ * operand): out_row_exp int32[rows] receives e_r with max|x_r| 2^e_r in
+ * [1, 2) (0 for an all-zero row).  A small-norm row then keeps fp16's full
+ * relative precision, so its certified band stays as narrow as a large row's
+ * (with one matrix-wide scale its entries sink into fp16 subnormals and the
+ * band widens toward the exact fallback).  Pass out_row_exp as u_row_exp to
+ * simdex_topk_matmul_ctx / simdex_query_ws_ctx. */
+SIMDEX_API int simdex_pack_f16_rows(const double* x, int64_t rows, int32_t f, int64_t rows_pad, int32_t kp,
+                     uint16_t* out_f16, double* out_norms, int32_t* out_row_exp, void* stream);
+
 /* brute.py:59-113 topk_matmul: users x items product on tcgen05 tensor cores
  * (single-pass fp16 operands, fp32 accumulation in TMEM) fused with a
  * certified running top-K, then exact float64 rescoring of the surviving
@@ -129,13 +139,14 @@ SIMDEX_API int simdex_topk_matmul(const double* users, const float* users32, con
  *     certified band (Cauchy-Schwarz); pays on skewed norms;
  *   SIMDEX_MM_NORM_AUTO  decide NORM_EXIT from the operand (reads the largest
  *     and the median norm: one host synchronisation).
- * Without NORM_AUTO the call never synchronises the host. */
+ * u_row_exp (nullable): per-row scale exponents of ub (simdex_pack_f16_rows),
+ * overriding su.  Without NORM_AUTO the call never synchronises the host. */
 #define SIMDEX_MM_NORM_EXIT 2
 #define SIMDEX_MM_NORM_AUTO 4
 SIMDEX_API int simdex_topk_matmul_ctx(void* ctx, const double* users, const float* users32, const uint16_t* ub,
                        const double* u_norm, int64_t nu, const double* items, const float* items32,
                        const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows,
-                       int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k,
+                       int64_t ni, int32_t f, int32_t kp, int32_t su, const int32_t* u_row_exp, int32_t si, int32_t k,
                        int32_t* out_ids, double* out_scores, int64_t* heap_ops, int32_t options, void* stream);
 
 /* ------------------------------------------------------------------------
@@ -273,12 +284,13 @@ SIMDEX_API int simdex_query_ws_opts(const double* users, const float* users32, c
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options, void* stream);
 
-/* simdex_query_ws_opts in an execution context (NULL: the thread default). */
+/* simdex_query_ws_opts in an execution context (NULL: the thread default);
+ * u_row_exp (nullable): per-row scale exponents of ub (simdex_pack_f16_rows). */
 SIMDEX_API int simdex_query_ws_ctx(void* ctx, const double* users, const float* users32, const uint16_t* ub,
                     const double* user_norms, int64_t nu,
                     const double* items, const float* items32, const uint16_t* ib, const double* item_norms,
                     const int32_t* item_perm, int64_t ib_rows, int64_t ni,
-                    int32_t f, int32_t kp, int32_t su, int32_t si,
+                    int32_t f, int32_t kp, int32_t su, const int32_t* u_row_exp, int32_t si,
                     const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                     const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
@@ -291,6 +303,11 @@ SIMDEX_API int simdex_query_ws_ctx(void* ctx, const double* users, const float* 
  * copied to the host asynchronously: read it after the call's stream has
  * synchronised. */
 SIMDEX_API int simdex_ws_stats(int64_t* out5);
+
+/* Rows of this thread's last simdex_topk_matmul* / simdex_query_ws* call whose
+ * certified band outgrew the candidate buffer and were answered by the exact
+ * float64 fallback (host int64; read after the call's stream synchronised). */
+SIMDEX_API int simdex_fallback_rows(int64_t* out);
 
 /* Group queries by their cluster (index.py:346-348), stable in query order:
  * out_q_user int64[nq] grouped user rows, out_perm int64[nq] original query

@@ -64,6 +64,15 @@ def packed(matrix) -> _ops.Packed:
     return c["packed"]
 
 
+def packed_users(matrix) -> _ops.Packed:
+    """The user-side tensor-core operand: one power-of-two scale per row, so
+    small-norm users keep the band of large ones (simdex_pack_f16_rows)."""
+    c = _cache(matrix)
+    if "packed_rows" not in c:
+        c["packed_rows"] = _ops.pack_rows(f64(matrix))
+    return c["packed_rows"]
+
+
 def packed_sorted(matrix) -> _ops.Packed:
     """The packed operand re-laid out by descending row norm (catalogue passes)."""
     c = _cache(matrix)
@@ -86,6 +95,9 @@ def share_rows(parent, child, lo: int, hi: int) -> None:
 
 
 def norms(matrix) -> torch.Tensor:
+    c = _cache(matrix)
+    if "packed_rows" in c:  # same norm arithmetic in both pack kernels
+        return c["packed_rows"].norms
     return packed(matrix).norms
 
 

@@ -37,7 +37,8 @@ SIGNATURES = {
     "simdex_max_abs": [P, I64, P, P],
     "simdex_pack_f16": [P, I64, I32, I32, I64, I32, P, P, P],
     "simdex_topk_matmul": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, P],
-    "simdex_topk_matmul_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, I32, P, P, P, I32,
+    "simdex_pack_f16_rows": [P, I64, I32, I64, I32, P, P, P, P],
+    "simdex_topk_matmul_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, P, I32, I32, P, P, P, I32,
                                P],
     "simdex_norm_order": [P, I64, P, P],
     "simdex_to_f32": [P, I64, P, P, P],
@@ -52,8 +53,9 @@ SIGNATURES = {
                         P, P, I64, I32, P, P, P, P],
     "simdex_query_ws_opts": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64,
                              P, P, P, I64, I32, P, P, P, I32, P],
-    "simdex_query_ws_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P,
-                            I64, P, P, P, I64, I32, P, P, P, I32, P],
+    "simdex_query_ws_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, P, I32, P, P, P, I32, I64, P,
+                            P, I64, P, P, P, I64, I32, P, P, P, I32, P],
+    "simdex_fallback_rows": [P],
     "simdex_ws_stats": [P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
@@ -133,6 +135,14 @@ def ws_stats():
     buf = (C.c_int64 * 5)()
     call("simdex_ws_stats", C.cast(buf, C.c_void_p))
     return tuple(int(x) for x in buf)
+
+
+def fallback_rows() -> int:
+    """Rows of this thread's last serving call answered by the exact float64
+    fallback (valid after the stream synchronised)."""
+    out = C.c_int64(0)
+    call("simdex_fallback_rows", C.byref(out))
+    return out.value
 
 
 def workspace_bytes() -> int:

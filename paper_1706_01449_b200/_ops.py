@@ -42,6 +42,7 @@ class Packed:
     perm: torch.Tensor | None = None   # operand row -> item id (norm-sorted operand), else None
     rows_pad: int = 0                  # rows of the fp16 operand
     norm_exit: bool = False            # norm-sorted and skewed enough for the brute-force early exit
+    row_exp: torch.Tensor | None = None  # int32 [rows]: per-row scale exponents (pack_rows), else None
 
 
 ROW_PAD = 256
@@ -77,6 +78,20 @@ def pack(x: torch.Tensor, max_abs: float) -> Packed:
     return Packed(out, norms, e, kp, rows)
 
 
+def pack_rows(x: torch.Tensor) -> Packed:
+    """fp16 copy with one exact power-of-two scale per row (max |entry| of
+    every row in [1, 2)): the user operand (simdex_pack_f16_rows)."""
+    rows, f = x.shape
+    kp = 64 * ((f + 63) // 64)
+    rows_pad = ROW_PAD * ((rows + ROW_PAD - 1) // ROW_PAD)
+    out = torch.empty((rows_pad, kp), dtype=torch.int16, device=x.device)
+    norms = torch.empty(rows, dtype=F64, device=x.device)
+    row_exp = torch.empty(rows, dtype=I32, device=x.device)
+    call("simdex_pack_f16_rows", ptr(_c(x, F64)), rows, f, rows_pad, kp, ptr(out), ptr(norms), ptr(row_exp),
+         stream_ptr())
+    return Packed(out, norms, 0, kp, rows, row_exp=row_exp)
+
+
 def topk_exact(users, items, k, rows=None):
     nu, f = users.shape
     ni = items.shape[0]
@@ -98,8 +113,8 @@ def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
     call("simdex_topk_matmul_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu,
          ptr(_c(items, F64)), ptr(items32), ptr(pi.op), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
-         pu.scale_exp, pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops), MM_NORM_EXIT if pi.norm_exit else 0,
-         stream_ptr())
+         pu.scale_exp, ptr(pu.row_exp), pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops),
+         MM_NORM_EXIT if pi.norm_exit else 0, stream_ptr())
     return ids, sc, hops
 
 
@@ -241,7 +256,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     call("simdex_query_ws_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
          ptr(items32),
          ptr(pi.op),
-         ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, pi.scale_exp, ptr(_c(list_ids, I32)),
+         ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, ptr(pu.row_exp), pi.scale_exp,
+         ptr(_c(list_ids, I32)),
          ptr(_c(list_pos, I32)),
          ptr(_c(bounds, F64)), c, int(block),
          ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), int(options),

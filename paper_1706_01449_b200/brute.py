@@ -68,7 +68,7 @@ def topk_matmul_tensors(model: ModelPair, k: int, heap_ops: bool = False):
     if min(k, model.num_items) > MATMUL_MAX_K:
         ids, sc = _ops.topk_exact(users, items, k)
         return ids, sc, None
-    return _ops.topk_matmul(users, _device.packed(model.users), items, _device.packed_sorted(model.items), k,
+    return _ops.topk_matmul(users, _device.packed_users(model.users), items, _device.packed_sorted(model.items), k,
                             heap_ops, items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users))
 
 

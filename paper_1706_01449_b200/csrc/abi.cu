@@ -185,6 +185,8 @@ int launch_walk(const double*, const double*, const double*, int32_t, int64_t, c
                 const int64_t*, const int32_t*, int64_t, int32_t, int64_t, const int32_t*, const double*,
                 const int32_t*, int32_t, int32_t*, double*, int64_t*, cudaStream_t);
 int launch_pack_f16(const double*, int64_t, int32_t, int32_t, int64_t, int32_t, uint16_t*, double*, cudaStream_t);
+int launch_pack_f16_rows(const double*, int64_t, int32_t, int64_t, int32_t, uint16_t*, double*, int32_t*,
+                         cudaStream_t);
 int launch_gather_prefix(const uint16_t*, const double*, int64_t, int32_t, const int32_t*, int32_t, int64_t,
                          int64_t, uint16_t*, double*, cudaStream_t);
 
@@ -309,6 +311,14 @@ extern "C" int simdex_pack_f16(const double* x, int64_t rows, int32_t f, int32_t
   SIMDEX_CHECK_ARG(rows >= 1 && f >= 1 && rows_pad >= rows && kp >= f && kp % 64 == 0,
                    "simdex_pack_f16: bad sizes");
   return launch_pack_f16(x, rows, f, scale_exp, rows_pad, kp, out_f16, out_norms, as_stream(stream));
+}
+
+extern "C" int simdex_pack_f16_rows(const double* x, int64_t rows, int32_t f, int64_t rows_pad, int32_t kp,
+                                    uint16_t* out_f16, double* out_norms, int32_t* out_row_exp, void* stream) {
+  SIMDEX_CHECK_ARG(x && out_f16 && out_norms && out_row_exp, "simdex_pack_f16_rows: null pointer");
+  SIMDEX_CHECK_ARG(rows >= 1 && f >= 1 && rows_pad >= rows && kp >= f && kp % 64 == 0,
+                   "simdex_pack_f16_rows: bad sizes");
+  return launch_pack_f16_rows(x, rows, f, rows_pad, kp, out_f16, out_norms, out_row_exp, as_stream(stream));
 }
 
 extern "C" int simdex_walk(const double* users, const double* user_norms, const double* items, int32_t f,

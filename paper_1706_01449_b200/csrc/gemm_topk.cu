@@ -683,11 +683,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // ---------------------------------------------------------------------------
 // operand-side prep
 // ---------------------------------------------------------------------------
+// cu[r] = eps ||u_r|| 2^(scale exponent of row r), rounded up; row_exp (per-row
+// exponents of a simdex_pack_f16_rows operand) multiplies scale by 2^row_exp[r]
 __global__ void row_cu_kernel(const double* __restrict__ norms, int64_t rows, int64_t rows_pad, double scale,
-                              float* __restrict__ cu, const double* __restrict__ scale_dev = nullptr) {
+                              float* __restrict__ cu, const double* __restrict__ scale_dev = nullptr,
+                              const int32_t* __restrict__ row_exp = nullptr) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows_pad) return;
   if (scale_dev) scale = *scale_dev;
+  if (r < rows && row_exp) scale = ldexp(scale, row_exp[r]);
   cu[r] = r < rows ? __double2float_ru(norms[r] * scale) : 0.f;
 }
 
@@ -802,6 +806,7 @@ struct FinalizeParams {
   int64_t* out_visited;
   float* row_T0_out;   // prefix mode: certified lower bound for the full-list pass (scaled)
   double t0_scale;     // 2^(su+si)
+  const int32_t* u_exp;  // per-user scale exponents (simdex_pack_f16_rows) or null: t0 also x 2^u_exp[user]
   int64_t* cont_list;  // prefix mode: rows that continue past B
   int32_t* cont_n;
   int64_t* over_list;
@@ -1344,7 +1349,7 @@ __global__ void __launch_bounds__(256) finalize_warp_kernel(const FinalizeParams
           // pass starts from it (rounded down, 2^-40 relative guard)
           float t0 = -INFINITY;
           if (held == p.k_eff) {
-            const double sk = kth * p.t0_scale;
+            const double sk = p.u_exp ? ldexp(kth * p.t0_scale, p.u_exp[user]) : kth * p.t0_scale;
             t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
           }
           p.row_T0_out[r] = t0;
@@ -1852,13 +1857,26 @@ void read_ws_stats(int64_t* out) {
   if (g_ws_cont_slot) out[1] = *g_ws_cont_slot;
 }
 
+// rows of this thread's last serving call that took the exact float64
+// fallback (band wider than the candidate buffer); pinned host slot 1 of the
+// context, valid once the stream has synchronised
+static thread_local const int64_t* g_fallback_slot = nullptr;
+int record_fallback_count(Ctx* ctx, const int32_t* over_n, cudaStream_t s) {
+  int64_t* host = ctx_host_slots(ctx);
+  g_fallback_slot = &host[1];
+  SIMDEX_CUDA(cudaMemcpyAsync(&host[1], over_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  return SIMDEX_OK;
+}
+int64_t read_fallback_count() { return g_fallback_slot ? *g_fallback_slot : 0; }
+
 // Brute-force fused path (topk_matmul).  No allocation, no host round trip
 // (options & SIMDEX_MM_NORM_AUTO excepted: it reads two norms to decide the
 // early exit).
 int gemm_topk_brute(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
                     const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
-                    int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
-                    int64_t* heap_ops, float* debug_out, int32_t options, Ctx* ctx, cudaStream_t s) {
+                    int32_t f, int32_t kp, int32_t su, const int32_t* u_exp, int32_t si, int32_t k, int32_t* out_ids,
+                    double* out_scores, int64_t* heap_ops, float* debug_out, int32_t options, Ctx* ctx,
+                    cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
   GemmGeometry g;
   int rc = geometry(kp, &g);
@@ -1889,7 +1907,8 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, nu, ni, units, n_units,
                                                                           nunits);
   SIMDEX_LAUNCH_CHECK("units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(u_norm, nu, nu_pad, eps * std::ldexp(1.0, su), cu);
+  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(u_norm, nu, nu_pad, eps * std::ldexp(1.0, su), cu,
+                                                                nullptr, u_exp);
   SIMDEX_LAUNCH_CHECK("row_cu");
   item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm,
                                                                       inmax);
@@ -1946,6 +1965,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   fp.item_perm = item_perm;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   if ((rc = launch_finalize(fp, nu, "finalize", s))) return rc;
+  if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
   // band overflow (rare): exact float64 rows, the count read on the device
   return exact_topk_devcount(users, users32, items, items32, ni, f, over_list, nullptr, over_n, k, over_out,
                              out_ids, out_scores, slab, s);
@@ -1961,7 +1981,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
 // device: the call enqueues its kernels and returns (CUDA-graph capturable).
 int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
-                 int32_t f, int32_t kp, int32_t su, int32_t si,
+                 int32_t f, int32_t kp, int32_t su, const int32_t* u_exp, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
@@ -2033,7 +2053,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
 
   ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off, units, n_units);
   SIMDEX_LAUNCH_CHECK("ws_units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu);
+  row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu, nullptr,
+                                                            u_exp);
   SIMDEX_LAUNCH_CHECK("row_cu");
   // rows past a_off[c] stay "padding" (row_user = -1) and are skipped by finalize
   SIMDEX_CUDA(cudaMemsetAsync(row_user, 0xff, sizeof(int64_t) * rows_max, s));
@@ -2109,6 +2130,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.out_visited = out_visited;
   fp.row_T0_out = t0;
   fp.t0_scale = std::ldexp(1.0, su + si);
+  fp.u_exp = u_exp;
   fp.cont_list = cont;
   fp.cont_n = cont_n;
   fp.over_list = over_list;
@@ -2193,6 +2215,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   f2.cont_n = nullptr;
   f2.item_perm = item_perm;
   if ((rc = launch_finalize(f2, rows2, "finalize_full", s))) return rc;
+  if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
   record_ws_stats(nq, &host[0], -1, bp, ni, f);
   // band overflow on the full list (rare): exact float64 scan for those users
   // and the same visited closed form; counts read on the device

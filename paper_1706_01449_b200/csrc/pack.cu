@@ -26,6 +26,33 @@ __global__ void pack_f16_kernel(const double* __restrict__ x, int64_t rows, int 
   if (lane == 0 && r < rows) norms[r] = sqrt(ss);
 }
 
+// Per-row exact power-of-two scale (users): 2^e_r with max|x_r| 2^e_r in
+// [1, 2), so a small-norm row keeps fp16's full relative precision instead
+// of sinking into the subnormal range of a matrix-wide scale.
+__global__ void pack_f16_rows_kernel(const double* __restrict__ x, int64_t rows, int f, int64_t rows_pad, int kp,
+                                     uint16_t* __restrict__ out, double* __restrict__ norms,
+                                     int32_t* __restrict__ row_exp) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows_pad) return;
+  double m = 0.0;
+  for (int k = lane; k < f; k += 32) m = fmax(m, r < rows ? fabs(x[r * f + k]) : 0.0);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int e = m > 0.0 ? -ilogb(m) : 0;
+  double ss = 0.0;
+  for (int k = lane; k < kp; k += 32) {
+    const double v = (r < rows && k < f) ? x[r * f + k] : 0.0;
+    ss = fma(v, v, ss);
+    __half b = __double2half(ldexp(v, e));
+    out[r * kp + k] = *reinterpret_cast<uint16_t*>(&b);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0 && r < rows) {
+    norms[r] = sqrt(ss);
+    row_exp[r] = e;
+  }
+}
+
 __global__ void gather_prefix_kernel(const uint16_t* __restrict__ ib, const double* __restrict__ inorm, int64_t ni,
                                      int kp, const int32_t* __restrict__ list_ids, int64_t bp, int64_t b_pad,
                                      int64_t n_clusters, uint16_t* __restrict__ out, double* __restrict__ onorm) {
@@ -66,6 +93,13 @@ int launch_pack_f16(const double* x, int64_t rows, int32_t f, int32_t scale_exp,
                      uint16_t* out, double* norms, cudaStream_t s) {
   pack_f16_kernel<<<(unsigned)ceil_div(rows_pad, 8), 256, 0, s>>>(x, rows, f, scale_exp, rows_pad, kp, out, norms);
   SIMDEX_LAUNCH_CHECK("pack_f16");
+  return SIMDEX_OK;
+}
+
+int launch_pack_f16_rows(const double* x, int64_t rows, int32_t f, int64_t rows_pad, int32_t kp, uint16_t* out,
+                         double* norms, int32_t* row_exp, cudaStream_t s) {
+  pack_f16_rows_kernel<<<(unsigned)ceil_div(rows_pad, 8), 256, 0, s>>>(x, rows, f, rows_pad, kp, out, norms, row_exp);
+  SIMDEX_LAUNCH_CHECK("pack_f16_rows");
   return SIMDEX_OK;
 }
 

@@ -5,17 +5,19 @@
 namespace simdex {
 int gemm_topk_brute(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu, const double* items,
                     const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
-                    int32_t f, int32_t kp, int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
-                    int64_t* heap_ops, float* debug_out, int32_t options, Ctx* ctx, cudaStream_t s);
+                    int32_t f, int32_t kp, int32_t su, const int32_t* u_exp, int32_t si, int32_t k, int32_t* out_ids,
+                    double* out_scores, int64_t* heap_ops, float* debug_out, int32_t options, Ctx* ctx,
+                    cudaStream_t s);
 int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, const double* unorm, int64_t nu, const double* items,
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
-                 int32_t f, int32_t kp, int32_t su, int32_t si,
+                 int32_t f, int32_t kp, int32_t su, const int32_t* u_exp, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                  const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
                  double* out_scores, int64_t* out_visited, int32_t options, Ctx* ctx, cudaStream_t s);
 
 void read_ws_stats(int64_t* out);
+int64_t read_fallback_count();
 
 namespace {
 constexpr int kMaxMatmulK = 256;
@@ -41,9 +43,9 @@ using namespace simdex;
 extern "C" int simdex_topk_matmul_ctx(void* ctx, const double* users, const float* users32, const uint16_t* ub,
                                       const double* u_norm, int64_t nu, const double* items, const float* items32,
                                       const uint16_t* ib, const double* i_norm, const int32_t* item_perm,
-                                      int64_t ib_rows, int64_t ni, int32_t f, int32_t kp, int32_t su, int32_t si,
-                                      int32_t k, int32_t* out_ids, double* out_scores, int64_t* heap_ops,
-                                      int32_t options, void* stream) {
+                                      int64_t ib_rows, int64_t ni, int32_t f, int32_t kp, int32_t su,
+                                      const int32_t* u_row_exp, int32_t si, int32_t k, int32_t* out_ids,
+                                      double* out_scores, int64_t* heap_ops, int32_t options, void* stream) {
   SIMDEX_CHECK_ARG(users && items && out_ids && out_scores, "simdex_topk_matmul: null pointer");
   SIMDEX_CHECK_ARG(nu >= 1 && ni >= 1 && f >= 1 && k >= 1 && ni < INT32_MAX, "simdex_topk_matmul: bad sizes");
   const int64_t k_eff = k < ni ? k : ni;
@@ -56,7 +58,7 @@ extern "C" int simdex_topk_matmul_ctx(void* ctx, const double* users, const floa
   Ctx* c = ctx_or_default(ctx);
   SIMDEX_CHECK_ARG(c, "simdex_topk_matmul: no execution context");
   return gemm_topk_brute(users, users32, ub, u_norm, nu, items, items32, ib, i_norm, item_perm, ib_rows, ni, f, kp, su,
-                         si, k, out_ids, out_scores, heap_ops, nullptr, options, c, as_stream(stream));
+                         u_row_exp, si, k, out_ids, out_scores, heap_ops, nullptr, options, c, as_stream(stream));
 }
 
 extern "C" int simdex_topk_matmul(const double* users, const float* users32, const uint16_t* ub, const double* u_norm, int64_t nu,
@@ -65,7 +67,14 @@ extern "C" int simdex_topk_matmul(const double* users, const float* users32, con
                                   int32_t su, int32_t si, int32_t k, int32_t* out_ids, double* out_scores,
                                   int64_t* heap_ops, void* stream) {
   return simdex_topk_matmul_ctx(nullptr, users, users32, ub, u_norm, nu, items, items32, ib, i_norm, item_perm, ib_rows,
-                                ni, f, kp, su, si, k, out_ids, out_scores, heap_ops, SIMDEX_MM_NORM_AUTO, stream);
+                                ni, f, kp, su, nullptr, si, k, out_ids, out_scores, heap_ops, SIMDEX_MM_NORM_AUTO,
+                                stream);
+}
+
+extern "C" int simdex_fallback_rows(int64_t* out) {
+  SIMDEX_CHECK_ARG(out, "simdex_fallback_rows: null pointer");
+  *out = read_fallback_count();
+  return SIMDEX_OK;
 }
 
 extern "C" int simdex_ws_stats(int64_t* out5) {
@@ -85,8 +94,8 @@ extern "C" int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t*
   SIMDEX_CUDA(in.alloc(ni, s));
   SIMDEX_CUDA(cudaMemsetAsync(un.p, 0, sizeof(double) * nu, s));
   SIMDEX_CUDA(cudaMemsetAsync(in.p, 0, sizeof(double) * ni, s));
-  return gemm_topk_brute(nullptr, nullptr, ub, un.p, nu, nullptr, nullptr, ib, in.p, nullptr, 0, ni, f, kp, 0, 0, 1, nullptr, nullptr,
-                         nullptr, out, 0, ctx_or_default(nullptr), s);
+  return gemm_topk_brute(nullptr, nullptr, ub, un.p, nu, nullptr, nullptr, ib, in.p, nullptr, 0, ni, f, kp, 0, nullptr, 0, 1,
+                         nullptr, nullptr, nullptr, out, 0, ctx_or_default(nullptr), s);
 }
 
 extern "C" int simdex_group_queries(const int64_t* q_user, int64_t nq, const int64_t* assign, int32_t c,
@@ -114,7 +123,7 @@ extern "C" int simdex_query_ws_ctx(void* ctx, const double* users, const float* 
                                const double* items, const float* items32, const uint16_t* ib,
                                const double* item_norms,
                                const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
-                               int32_t su, int32_t si, const int32_t* list_ids,
+                               int32_t su, const int32_t* u_row_exp, int32_t si, const int32_t* list_ids,
                                const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
                                const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
                                const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
@@ -134,7 +143,7 @@ extern "C" int simdex_query_ws_ctx(void* ctx, const double* users, const float* 
   if (nq == 0) return SIMDEX_OK;
   Ctx* cx = ctx_or_default(ctx);
   SIMDEX_CHECK_ARG(cx, "simdex_query_ws: no execution context");
-  return gemm_topk_ws(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, si,
+  return gemm_topk_ws(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, u_row_exp, si,
                       list_ids, list_pos,
                       bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
                       out_scores, out_visited, options, cx, as_stream(stream));
@@ -151,7 +160,7 @@ extern "C" int simdex_query_ws_opts(const double* users, const float* users32, c
                                int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options,
                                     void* stream) {
   return simdex_query_ws_ctx(nullptr, users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm,
-                             ib_rows, ni, f, kp, su, si, list_ids, list_pos, bounds, c, block, prefix_b, prefix_norm,
+                             ib_rows, ni, f, kp, su, nullptr, si, list_ids, list_pos, bounds, c, block, prefix_b, prefix_norm,
                              b_pad, q_user, q_perm, q_off, nq, k, out_ids, out_scores, out_visited, options, stream);
 }
 

@@ -484,7 +484,7 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
         if q_users.index is not index:
             raise ValueError("QuerySet was prepared for another index")
         q_users, grouped = q_users.q, q_users.grouped
-    pu, pi = _device.packed(model.users), _device.packed_sorted(model.items)
+    pu, pi = _device.packed_users(model.users), _device.packed_sorted(model.items)
     if min(k, n) <= 256 and pu.kp <= 256:
         # tensor-core path; without work sharing every query takes the full-list
         # pass (block 0) and visited is Algorithm 1's stop position, exactly the walk's
