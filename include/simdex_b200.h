@@ -240,6 +240,20 @@ SIMDEX_API int simdex_walk(const double* users, const double* user_norms, const 
                 const int32_t* warm_ids, const double* warm_scores, const int32_t* warm_count,
                 int32_t no_prune, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
 
+/* simdex_walk reading exact float32 copies of users / items (both or
+ * neither; NULL: the float64 values): half the bytes per scored item, the
+ * arithmetic float64 either way (every float32 value is exact in float64).
+ * Scoring is coalesced: 8-lane groups read one contiguous item row each.
+ * A k_eff whose top-K does not fit a warp's shared memory (k beyond ~16k)
+ * is answered by the exact scan, visited from Algorithm 1's closed form
+ * (start == 0 only). */
+SIMDEX_API int simdex_walk32(const double* users, const double* user_norms, const double* items,
+                const float* users32, const float* items32, int32_t f, int64_t ni,
+                const int32_t* list_ids, const double* bounds,
+                const int64_t* q_user, const int32_t* q_cluster, int64_t nq, int32_t k, int64_t start,
+                const int32_t* warm_ids, const double* warm_scores, const int32_t* warm_count,
+                int32_t no_prune, int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream);
+
 /* index.py:305-389 query_batch with work sharing: every cluster's first B
  * list items scored for all its queried users on tcgen05 (prefix GEMM fused
  * with the certified top-K, as simdex_topk_matmul), then the walk continues

@@ -8,6 +8,7 @@ operand.  Host->device copies go through pinned staging.
 
 from __future__ import annotations
 
+import os
 import warnings
 
 import numpy as np
@@ -69,7 +70,10 @@ def packed_users(matrix) -> _ops.Packed:
     small-norm users keep the band of large ones (simdex_pack_f16_rows)."""
     c = _cache(matrix)
     if "packed_rows" not in c:
-        c["packed_rows"] = _ops.pack_rows(f64(matrix))
+        if os.environ.get("SIMDEX_USER_SCALE") == "matrix":  # A/B: one matrix-wide scale
+            c["packed_rows"] = packed(matrix)
+        else:
+            c["packed_rows"] = _ops.pack_rows(f64(matrix))
     return c["packed_rows"]
 
 

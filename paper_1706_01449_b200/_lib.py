@@ -49,6 +49,7 @@ SIGNATURES = {
     "simdex_build_index": [P, I64, I32, P, P, I32, P, P, P, P, P],
     "simdex_list_positions": [P, I32, I64, P, P],
     "simdex_walk": [P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
+    "simdex_walk32": [P, P, P, P, P, I32, I64, P, P, P, P, I64, I32, I64, P, P, P, I32, P, P, P, P],
     "simdex_query_ws": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64, P,
                         P, P, I64, I32, P, P, P, P],
     "simdex_query_ws_opts": [P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, I32, P, P, P, I32, I64, P, P, I64,

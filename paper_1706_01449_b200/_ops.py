@@ -195,7 +195,8 @@ def list_positions(list_ids):
     return pos
 
 
-def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, warm=None, no_prune=False):
+def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, warm=None, no_prune=False,
+         users32=None, items32=None):
     nq = q_user.shape[0]
     ni, f = items.shape
     k_eff = min(k, ni)
@@ -205,8 +206,8 @@ def walk(users, unorm, items, list_ids, bounds, q_user, q_cluster, k, start=0, w
     wi = ws = wc = None
     if warm is not None:
         wi, ws, wc = (_c(warm[0], I32), _c(warm[1], F64), _c(warm[2], I32))
-    call("simdex_walk", ptr(_c(users, F64)), ptr(_c(unorm, F64)), ptr(_c(items, F64)), f, ni,
-         ptr(_c(list_ids, I32)), ptr(_c(bounds, F64)), ptr(_c(q_user, I64)), ptr(_c(q_cluster, I32)), nq, k,
+    call("simdex_walk32", ptr(_c(users, F64)), ptr(_c(unorm, F64)), ptr(_c(items, F64)), ptr(users32), ptr(items32),
+         f, ni, ptr(_c(list_ids, I32)), ptr(_c(bounds, F64)), ptr(_c(q_user, I64)), ptr(_c(q_cluster, I32)), nq, k,
          int(start), ptr(wi), ptr(ws), ptr(wc), int(bool(no_prune)), ptr(ids), ptr(sc), ptr(vis), stream_ptr())
     return ids, sc, vis
 

@@ -9,6 +9,7 @@ identical results under the shared tie rule (score desc, item id asc).
 
 from __future__ import annotations
 
+import sys
 import time
 from dataclasses import dataclass
 
@@ -105,7 +106,7 @@ def _perpair_scan(model: ModelPair, k: int) -> None:
     q = torch.arange(model.num_users, dtype=torch.int64, device=dev)
     qc = torch.zeros(model.num_users, dtype=torch.int32, device=dev)
     _ops.walk(_device.f64(model.users), _device.norms(model.users), _device.f64(model.items), ids, bounds, q, qc,
-              k, no_prune=True)
+              k, no_prune=True, users32=_device.f32_exact(model.users), items32=_device.f32_exact(model.items))
 
 
 @dataclass(frozen=True)
@@ -144,15 +145,18 @@ def measure_throughput(model: ModelPair, k: int = 1, blocks: BlockSpec | None = 
     model -- or, below CALIBRATION_PAIRS, its users tiled up to that size."""
     m = _calibration_model(model)
     pairs = m.num_users * m.num_items
-    topk_matmul_tensors(m, k)
-    _perpair_scan(m, k)
+    # module-attribute lookups at call time, like the reference (its tests
+    # monkeypatch brute.topk_matmul / _perpair_scan)
+    mod = sys.modules[__name__]
+    mod.topk_matmul(m, k, blocks)
+    mod._perpair_scan(m, k)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    topk_matmul_tensors(m, k)
+    mod.topk_matmul(m, k, blocks)
     torch.cuda.synchronize()
     blocked = max(time.perf_counter() - t0, 1e-9)
     t0 = time.perf_counter()
-    _perpair_scan(m, k)
+    mod._perpair_scan(m, k)
     torch.cuda.synchronize()
     unblocked = max(time.perf_counter() - t0, 1e-9)
     return ThroughputSample(pairs / blocked, pairs / unblocked)

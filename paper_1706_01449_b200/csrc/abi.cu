@@ -181,9 +181,9 @@ int sm_count() {
   return n;
 }
 
-int launch_walk(const double*, const double*, const double*, int32_t, int64_t, const int32_t*, const double*,
-                const int64_t*, const int32_t*, int64_t, int32_t, int64_t, const int32_t*, const double*,
-                const int32_t*, int32_t, int32_t*, double*, int64_t*, cudaStream_t);
+int launch_walk(const double*, const double*, const double*, const float*, const float*, int32_t, int64_t,
+                const int32_t*, const double*, const int64_t*, const int32_t*, int64_t, int32_t, int64_t,
+                const int32_t*, const double*, const int32_t*, int32_t, int32_t*, double*, int64_t*, cudaStream_t);
 int launch_pack_f16(const double*, int64_t, int32_t, int32_t, int64_t, int32_t, uint16_t*, double*, cudaStream_t);
 int launch_pack_f16_rows(const double*, int64_t, int32_t, int64_t, int32_t, uint16_t*, double*, int32_t*,
                          cudaStream_t);
@@ -321,18 +321,30 @@ extern "C" int simdex_pack_f16_rows(const double* x, int64_t rows, int32_t f, in
   return launch_pack_f16_rows(x, rows, f, rows_pad, kp, out_f16, out_norms, out_row_exp, as_stream(stream));
 }
 
-extern "C" int simdex_walk(const double* users, const double* user_norms, const double* items, int32_t f,
-                           int64_t ni, const int32_t* list_ids, const double* bounds, const int64_t* q_user,
-                           const int32_t* q_cluster, int64_t nq, int32_t k, int64_t start, const int32_t* warm_ids,
-                           const double* warm_scores, const int32_t* warm_count, int32_t no_prune,
-                           int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
+extern "C" int simdex_walk32(const double* users, const double* user_norms, const double* items, const float* users32,
+                             const float* items32, int32_t f, int64_t ni, const int32_t* list_ids,
+                             const double* bounds, const int64_t* q_user, const int32_t* q_cluster, int64_t nq,
+                             int32_t k, int64_t start, const int32_t* warm_ids, const double* warm_scores,
+                             const int32_t* warm_count, int32_t no_prune, int32_t* out_ids, double* out_scores,
+                             int64_t* out_visited, void* stream) {
   SIMDEX_CHECK_ARG(users && user_norms && items && list_ids && bounds && q_user && q_cluster && out_ids &&
                        out_scores && out_visited,
                    "simdex_walk: null pointer");
   SIMDEX_CHECK_ARG(ni >= 1 && f >= 1 && k >= 1 && nq >= 0 && start >= 0, "simdex_walk: bad sizes");
   SIMDEX_CHECK_ARG(start == 0 || (warm_ids && warm_scores && warm_count), "simdex_walk: warm start needs warm lists");
-  return launch_walk(users, user_norms, items, f, ni, list_ids, bounds, q_user, q_cluster, nq, k, start, warm_ids,
-                     warm_scores, warm_count, no_prune, out_ids, out_scores, out_visited, as_stream(stream));
+  if (!(users32 && items32)) users32 = items32 = nullptr;  // both or neither
+  return launch_walk(users, user_norms, items, users32, items32, f, ni, list_ids, bounds, q_user, q_cluster, nq, k,
+                     start, warm_ids, warm_scores, warm_count, no_prune, out_ids, out_scores, out_visited,
+                     as_stream(stream));
+}
+
+extern "C" int simdex_walk(const double* users, const double* user_norms, const double* items, int32_t f,
+                           int64_t ni, const int32_t* list_ids, const double* bounds, const int64_t* q_user,
+                           const int32_t* q_cluster, int64_t nq, int32_t k, int64_t start, const int32_t* warm_ids,
+                           const double* warm_scores, const int32_t* warm_count, int32_t no_prune,
+                           int32_t* out_ids, double* out_scores, int64_t* out_visited, void* stream) {
+  return simdex_walk32(users, user_norms, items, nullptr, nullptr, f, ni, list_ids, bounds, q_user, q_cluster, nq, k,
+                       start, warm_ids, warm_scores, warm_count, no_prune, out_ids, out_scores, out_visited, stream);
 }
 
 extern "C" int simdex_build_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,

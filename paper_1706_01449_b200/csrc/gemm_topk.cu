@@ -1110,7 +1110,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
         // full-list pass from it (rounded down, with a 2^-40 relative guard)
         float t0 = -INFINITY;
         if (held == p.k_eff) {
-          const double sk = kth * p.t0_scale;
+          const double sk = p.u_exp ? ldexp(kth * p.t0_scale, p.u_exp[user]) : kth * p.t0_scale;
           t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
         }
         p.row_T0_out[r] = t0;
@@ -1140,230 +1140,6 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
       if (v > p.n) v = p.n;
       if (v < p.prefix) v = p.prefix;
       p.out_visited[out] = v;
-    }
-  }
-}
-
-// First list position j with bounds[j] * unorm < s, found by the whole warp:
-// 32 probes per round (the ceilings are non-increasing, so the probes that
-// still reach s form a prefix), about log32(n) rounds.  Uniform result.
-__device__ int64_t ceiling_count_warp(const double* __restrict__ b, int64_t n, double unorm, double s, int lane) {
-  int64_t lo = 0, hi = n;  // the answer lies in [lo, hi]
-  while (lo < hi) {
-    const int64_t step = (hi - lo + 31) / 32;
-    const int64_t pos = lo + (int64_t)lane * step;
-    const bool ge = pos < hi && b[pos] * unorm >= s;
-    const int g = __popc(__ballot_sync(0xffffffffu, ge));
-    if (g == 0) break;  // answer == lo
-    const int64_t last = lo + (int64_t)(g - 1) * step;
-    const int64_t next = lo + (int64_t)g * step;
-    lo = last + 1;
-    if (next < hi) hi = next;
-  }
-  return lo;
-}
-
-// (score desc, id asc) bitonic sort of one entry per lane across the warp
-__device__ __forceinline__ void warp_sort_desc(double& s, int32_t& id, int lane) {
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const double os = __shfl_xor_sync(0xffffffffu, s, stride);
-      const int32_t oi = __shfl_xor_sync(0xffffffffu, id, stride);
-      const bool lower = (lane & stride) == 0;       // this lane keeps the earlier slot of the pair
-      const bool up = (lane & size) == 0 || size == 32;  // this pair sorts toward "before first"
-      const bool other_first = ranks_before(os, oi, s, id);
-      const bool take = (lower == up) ? other_first : !other_first && !(os == s && oi == id);
-      if (take) {
-        s = os;
-        id = oi;
-      }
-    }
-  }
-}
-
-// Warp per row (finalize v2): the candidate buffer is filtered with coalesced
-// reads and compacted into shared memory; 8-lane groups rescore four
-// candidates at a time in float64 -- lane gl holds the user's factor pairs
-// 2(gl + 8i), 2(gl + 8i) + 1 in registers and reads the same pairs of the
-// candidate's item row, so a group reads one contiguous row (the L1-wavefront
-// cost that bound the lane-per-candidate form); the group's partial sums are
-// reduced in a fixed xor order (identical item rows score identically).  Up
-// to 32 survivors are ordered by a register bitonic sort across the warp,
-// more by a shared-memory bitonic sort.  The work-sharing bookkeeping is the
-// lane-per-candidate finalize's.  ET: float (exact float32 copies) or double.
-template <int NV, class ET>
-__global__ void __launch_bounds__(256) finalize_warp_kernel(const FinalizeParams p, const ET* __restrict__ users,
-                                                            const ET* __restrict__ items) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int gl = lane & 7, grp = lane >> 3;
-  double* ss = reinterpret_cast<double*>(smem) + (size_t)w * p.pow2;
-  int32_t* sid = reinterpret_cast<int32_t*>(reinterpret_cast<double*>(smem) + (size_t)nw * p.pow2) + (size_t)w * p.pow2;
-  const int64_t total = p.n_rows_dev ? (int64_t)*p.n_rows_dev : p.total_rows;
-  const int f = p.f;
-  const bool pairs = (f & 1) == 0;
-  for (int64_t r = (int64_t)blockIdx.x * nw + w; r < total; r += (int64_t)gridDim.x * nw) {
-    const int64_t user = p.row_user ? p.row_user[r] : r;
-    if (user < 0 || user >= p.nu) continue;
-    const int64_t out = p.row_out ? p.row_out[r] : r;
-    const int c = (p.mode == kPrefix || p.mode == kFullList) ? p.row_cluster[r] : 0;
-    if (p.row_flags[r]) {
-      if (lane == 0) overflow_row(p, r, user, out);
-      continue;
-    }
-    const int cnt = p.row_count[r];
-    const float Tr = p.row_T[r];
-    // the user's factor pairs of this lane, as float64
-    double u[2 * NV];
-    const ET* urow = users + user * (int64_t)f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int q = 2 * (gl + 8 * i);
-      u[2 * i] = q < f ? (double)urow[q] : 0.0;
-      u[2 * i + 1] = q + 1 < f ? (double)urow[q + 1] : 0.0;
-    }
-    // keep the candidates whose upper bound reaches the final threshold,
-    // compacted in buffer order, resolved to item ids
-    const int32_t* cid = p.cand_id + r * p.cap;
-    const float* chi = p.cand_hi + r * p.cap;
-    int kept = 0;
-    for (int e0 = 0; e0 < cnt; e0 += 32) {
-      const int e = e0 + lane;
-      const bool keep = e < cnt && chi[e] >= Tr;
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int dst = kept + __popc(m & ((1u << lane) - 1u));
-        if (dst < p.pow2) {
-          const int32_t pos = cid[e];
-          sid[dst] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
-        }
-      }
-      kept += __popc(m);
-    }
-    if (kept > p.pow2) {  // more survivors than the warp's shared-memory slots
-      if (lane == 0) overflow_row(p, r, user, out);
-      continue;
-    }
-    __syncwarp();
-    // exact float64 rescoring, four candidates per step
-    for (int j0 = 0; j0 < kept; j0 += 4) {
-      const int j = j0 + grp;
-      double d = 0.0;
-      if (j < kept) {
-        const ET* x = items + (int64_t)sid[j] * f;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const int q = 2 * (gl + 8 * i);
-          double x0 = 0.0, x1 = 0.0;
-          if (pairs) {
-            if (q < f) {
-              if constexpr (sizeof(ET) == 4) {
-                const float2 v = *reinterpret_cast<const float2*>(x + q);
-                x0 = v.x;
-                x1 = v.y;
-              } else {
-                const double2 v = *reinterpret_cast<const double2*>(x + q);
-                x0 = v.x;
-                x1 = v.y;
-              }
-            }
-          } else {
-            if (q < f) x0 = (double)x[q];
-            if (q + 1 < f) x1 = (double)x[q + 1];
-          }
-          d = fma(x0, u[2 * i], d);
-          d = fma(x1, u[2 * i + 1], d);
-        }
-      }
-      d += __shfl_xor_sync(0xffffffffu, d, 4);
-      d += __shfl_xor_sync(0xffffffffu, d, 2);
-      d += __shfl_xor_sync(0xffffffffu, d, 1);
-      if (gl == 0 && j < kept) ss[j] = d;
-    }
-    __syncwarp();
-    const int held = kept < p.k_eff ? kept : p.k_eff;
-    double kth = -DBL_MAX;
-    int64_t mp = -1;
-    if (kept <= 32) {
-      double sv = lane < kept ? ss[lane] : -DBL_MAX;
-      int32_t iv = lane < kept ? sid[lane] : INT32_MAX;
-      warp_sort_desc(sv, iv, lane);
-      if (lane < held) {  // held <= 32: lane i holds output slot i
-        p.out_ids[out * p.k_eff + lane] = iv;
-        p.out_scores[out * p.k_eff + lane] = sv;
-        if (p.mode == kFullList) mp = (int64_t)p.list_pos[(int64_t)c * p.n + iv];
-      }
-      for (int i = held + lane; i < p.k_eff; i += 32) {
-        p.out_ids[out * p.k_eff + i] = -1;
-        p.out_scores[out * p.k_eff + i] = -DBL_MAX;
-      }
-      const double kv = __shfl_sync(0xffffffffu, sv, (p.k_eff - 1) & 31);
-      if (held == p.k_eff) kth = kv;  // held == k_eff <= kept <= 32
-    } else {
-      int np2 = 64;
-      while (np2 < kept) np2 <<= 1;
-      for (int e = kept + lane; e < np2; e += 32) {
-        ss[e] = -DBL_MAX;
-        sid[e] = INT32_MAX;
-      }
-      for (int size = 2; size <= np2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          __syncwarp();
-          for (int i = lane; i < np2 / 2; i += 32) {
-            const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-            const bool up = (lo & size) == 0;
-            const double a = ss[lo], b = ss[hi];
-            const int32_t ia = sid[lo], ib = sid[hi];
-            if (up ? ranks_before(b, ib, a, ia) : ranks_before(a, ia, b, ib)) {
-              ss[lo] = b;
-              ss[hi] = a;
-              sid[lo] = ib;
-              sid[hi] = ia;
-            }
-          }
-        }
-      }
-      __syncwarp();
-      for (int i = lane; i < p.k_eff; i += 32) {
-        p.out_ids[out * p.k_eff + i] = i < held ? sid[i] : -1;
-        p.out_scores[out * p.k_eff + i] = i < held ? ss[i] : -DBL_MAX;
-        if (p.mode == kFullList && i < held) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + sid[i]]);
-      }
-      if (held == p.k_eff) kth = ss[p.k_eff - 1];
-    }
-    if (p.mode == kBrute) continue;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
-    if (p.mode == kPrefix) {
-      // index.py:372-387: the prefix covers the list -> n; the K-th beats the
-      // ceiling at B -> B; otherwise the user continues past B
-      if (lane == 0) {
-        if (p.prefix >= p.n) {
-          p.out_visited[out] = p.n;
-        } else if (held == p.k_eff && kth > p.bounds[(int64_t)c * p.n + p.prefix] * p.unorm[user]) {
-          p.out_visited[out] = p.prefix;
-        } else {
-          // the prefix's exact K-th lower-bounds the catalogue's: the full-list
-          // pass starts from it (rounded down, 2^-40 relative guard)
-          float t0 = -INFINITY;
-          if (held == p.k_eff) {
-            const double sk = p.u_exp ? ldexp(kth * p.t0_scale, p.u_exp[user]) : kth * p.t0_scale;
-            t0 = __double2float_rd(sk - fabs(sk) * 0x1p-40);
-          }
-          p.row_T0_out[r] = t0;
-          p.cont_list[atomicAdd(p.cont_n, 1)] = r;
-        }
-      }
-    } else {  // kFullList: Algorithm 1's stop position in closed form ("visited")
-      const int64_t q = ceiling_count_warp(p.bounds + (int64_t)c * p.n, p.n, p.unorm[user], kth, lane);
-      if (lane == 0) {
-        int64_t v = max(max(mp + 1, (int64_t)p.k_eff), q);
-        if (v > p.n) v = p.n;
-        if (v < p.prefix) v = p.prefix;
-        p.out_visited[out] = v;
-      }
     }
   }
 }
@@ -1731,7 +1507,8 @@ int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, const char* prof
   int dev = 0;
   cudaGetDevice(&dev);
   if (smem > set_for[dev & 15]) {
-    SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SIMDEX_CUDA(cudaFuncSetAttribute(finalize_kernel<LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
     set_for[dev & 15] = smem;
   }
   ProfileScope _prof(prof, s);
@@ -1741,44 +1518,7 @@ int launch_finalize_lpr(const FinalizeParams& fp, int64_t rows, const char* prof
   return SIMDEX_OK;
 }
 
-template <int NV, class ET>
-int launch_finalize_warp(const FinalizeParams& fp, int64_t rows, const ET* users, const ET* items, const char* prof,
-                         cudaStream_t s) {
-  constexpr int kWarps = 8;
-  const size_t smem = (size_t)fp.pow2 * 12 * kWarps;
-  static size_t set_for[16] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (smem > 48 * 1024 && smem > set_for[dev & 15]) {
-    SIMDEX_CUDA(cudaFuncSetAttribute(finalize_warp_kernel<NV, ET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    set_for[dev & 15] = smem;
-  }
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, kWarps), 16 * (int64_t)sm_count()));
-  ProfileScope _prof(prof, s);
-  finalize_warp_kernel<NV, ET><<<(unsigned)blocks, 32 * kWarps, smem, s>>>(fp, users, items);
-  _prof.end();
-  SIMDEX_LAUNCH_CHECK("finalize");
-  return SIMDEX_OK;
-}
-
-template <class ET>
-int launch_finalize_et(const FinalizeParams& fp, int64_t rows, const ET* users, const ET* items, const char* prof,
-                       cudaStream_t s) {
-  const int pairs = (fp.f + 1) / 2;  // factor pairs; 8 lanes per candidate
-  if (pairs <= 8) return launch_finalize_warp<1, ET>(fp, rows, users, items, prof, s);
-  if (pairs <= 16) return launch_finalize_warp<2, ET>(fp, rows, users, items, prof, s);
-  if (pairs <= 32) return launch_finalize_warp<4, ET>(fp, rows, users, items, prof, s);
-  if (pairs <= 64) return launch_finalize_warp<8, ET>(fp, rows, users, items, prof, s);
-  return launch_finalize_warp<16, ET>(fp, rows, users, items, prof, s);
-}
-
 int launch_finalize(const FinalizeParams& fp, int64_t rows, const char* prof, cudaStream_t s) {
-  static const bool v2 = getenv("SIMDEX_FINALIZE_V2") != nullptr;  // warp-per-row form (A/B only)
-  if (fp.mode != kAssign && v2) {
-    if (fp.users32 && fp.items32) return launch_finalize_et<float>(fp, rows, fp.users32, fp.items32, prof, s);
-    return launch_finalize_et<double>(fp, rows, fp.users, fp.items, prof, s);
-  }
   return fp.k_eff > 32 ? launch_finalize_lpr<32>(fp, rows, prof, s) : launch_finalize_lpr<8>(fp, rows, prof, s);
 }
 

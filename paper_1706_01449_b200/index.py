@@ -353,7 +353,14 @@ def build_index(model: ModelPair, clustering: Clustering, block_size: int = DEFA
     if block_size < 1:
         raise ValueError("block_size must be >= 1")
     norms, ids, bounds = _device_build(model, clustering.device_centroids(), clustering.device_max_angle())
-    return CentroidIndex(None, None, None, block_size, clustering, _dev={"ids": ids, "bounds": bounds, "norms": norms})
+    index = CentroidIndex(None, None, None, block_size, clustering, _dev={"ids": ids, "bounds": bounds, "norms": norms})
+    # the serving layout is part of the build (not of the first query): the
+    # inverse list positions (visited in closed form) and, when the tensor-core
+    # path will serve this index, every cluster's prefix operand
+    index.device_list_pos()
+    if model.factors <= 256:
+        index.device_prefix(model)
+    return index
 
 
 def _check_k(k):
@@ -371,7 +378,8 @@ def _walk_rows(index, model, q_users_np, k, q_clusters=None):
         qc = index.device_assignment().index_select(0, q).to(torch.int32)
     else:
         qc = q_clusters
-    return _ops.walk(users, unorm, items, ids, bounds, q, qc, k)
+    return _ops.walk(users, unorm, items, ids, bounds, q, qc, k, users32=_device.f32_exact(model.users),
+                     items32=_device.f32_exact(model.items))
 
 
 def query_user(index: CentroidIndex, model: ModelPair, user_id: int, k: int) -> TopKResult:
@@ -428,7 +436,10 @@ def query_vector(index: CentroidIndex, model: ModelPair, vector, k: int) -> TopK
         ids, bounds = _cluster_list(model, cvals[c], theta)
         qc = torch.zeros(1, dtype=torch.int32, device=dev)
     q = torch.zeros(1, dtype=torch.int64, device=dev)
-    oi, os_, ov = _ops.walk(ut, un, _device.f64(model.items), ids, bounds, q, qc, k)
+    u32 = u.astype(np.float32)
+    ut32 = torch.as_tensor(u32[None, :], device=dev) if np.array_equal(u32.astype(np.float64), u) else None
+    oi, os_, ov = _ops.walk(ut, un, _device.f64(model.items), ids, bounds, q, qc, k, users32=ut32,
+                            items32=_device.f32_exact(model.items))
     return TopKResult(-1, _device.to_host(oi[0]).astype(np.int64), _device.to_host(os_[0]), int(ov[0].item()))
 
 
@@ -496,7 +507,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
                              items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
                              options=_ws_options(index, k, n, work_sharing))
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
-    out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k)
+    out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k,
+                    users32=_device.f32_exact(model.users), items32=_device.f32_exact(model.items))
     if work_sharing:  # k beyond the tensor-core envelope: WS visited = n if B >= n else max(B, walk visited)
         vis = out[2].fill_(n) if index.block_size >= n else out[2].clamp_(min=index.block_size)
         out = (out[0], out[1], vis)
