@@ -323,6 +323,14 @@ SIMDEX_API int simdex_ws_stats(int64_t* out5);
  * float64 fallback (host int64; read after the call's stream synchronised). */
 SIMDEX_API int simdex_fallback_rows(int64_t* out);
 
+/* (user, item) pairs the tensor-core launches of this thread's last
+ * simdex_topk_matmul* / simdex_query_ws* call actually multiplied (valid rows
+ * x valid items of every tile issued; the early exits skip tiles): host
+ * int64[2] = [brute-force or prefix launch, catalogue launch (0 if none)].
+ * Read after the call's stream synchronised.  The roofline's "executed" flop
+ * count is 2 f x these pairs. */
+SIMDEX_API int simdex_executed_pairs(int64_t* out2);
+
 /* Group queries by their cluster (index.py:346-348), stable in query order:
  * out_q_user int64[nq] grouped user rows, out_perm int64[nq] original query
  * position of each grouped entry, out_off int64[c+1] cluster offsets. */

@@ -57,6 +57,7 @@ SIGNATURES = {
     "simdex_query_ws_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, P, I32, P, P, P, I32, I64, P,
                             P, I64, P, P, P, I64, I32, P, P, P, I32, P],
     "simdex_fallback_rows": [P],
+    "simdex_executed_pairs": [P],
     "simdex_ws_stats": [P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
@@ -144,6 +145,14 @@ def fallback_rows() -> int:
     out = C.c_int64(0)
     call("simdex_fallback_rows", C.byref(out))
     return out.value
+
+
+def executed_pairs():
+    """(user, item) pairs the tensor-core launches of this thread's last
+    serving call multiplied: (first launch, second launch)."""
+    buf = (C.c_int64 * 2)()
+    call("simdex_executed_pairs", C.cast(buf, C.c_void_p))
+    return int(buf[0]), int(buf[1])
 
 
 def workspace_bytes() -> int:

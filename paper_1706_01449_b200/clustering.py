@@ -219,10 +219,16 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
     objs = [obj]  # read back once at the end (no per-iteration sync for the history)
     for _ in range(max_iters):
         counts, _, _ = _ops.kmeans_update(pts, assign, centers, points32=p32)
-        assign, _ = repair(assign, d2, counts)
+        d2_before = d2
         new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
+        # one host read per iteration: "a cluster went empty" and "changed"
+        empty, n_changed = torch.stack([(counts == 0).any().to(torch.int64), changed.view(())]).tolist()
+        if empty:  # rare (clustering.py:125-138): repair, then redo this assignment
+            assign, _ = repair(assign, d2_before, counts)
+            new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
+            n_changed = int(changed.item())
         objs.append(obj)
-        if int(changed.item()) == 0:
+        if n_changed == 0:
             break
         assign = new_assign
     counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)

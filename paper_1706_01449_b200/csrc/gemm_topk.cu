@@ -122,6 +122,7 @@ struct TopkParams {
   // norm of the tile's first item
   const float* exit_c;
   const float* exit_m;
+  unsigned long long* pairs_out;  // optional: (user row, item) pairs actually multiplied (valid rows x items)
 };
 
 // three-input max (sm_100 FMNMX3)
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint64_t b_desc0 = umma_desc_sw128(smem_u32(b_sm));
       const int ksteps = p.k_steps;
       int32_t seq = 0;  // stages consumed so far
+      unsigned long long pairs = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++iter) {
         const Unit un = p.units[u];
         const int ntile_a = un.rows > kTileM ? 2 : 1;
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             break;
           }
           ++seq;
+          pairs += (unsigned long long)un.rows * (unsigned long long)min(kTileN, un.n_items - t * kTileN);
           const uint64_t bd0 = b_desc0 + (uint64_t)((stage * KB * kSlab) >> 4);
           for (int h = 0; h < ntile_a; ++h) {
             const uint32_t d = tbase + (buf * kMTiles + h) * kTileN;
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
         mma_commit(a_empty);
       }
+      if (p.pairs_out && pairs) atomicAdd(p.pairs_out, pairs);
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -1609,6 +1613,21 @@ int record_fallback_count(Ctx* ctx, const int32_t* over_n, cudaStream_t s) {
 }
 int64_t read_fallback_count() { return g_fallback_slot ? *g_fallback_slot : 0; }
 
+// (user, item) pairs the tensor-core launches of this thread's last serving
+// call actually multiplied (early exits skip tiles): [first launch, second
+// launch] -- pinned host slots 2, 3 of the context, valid after synchronisation
+static thread_local const int64_t* g_pairs_slot = nullptr;
+int record_pairs(Ctx* ctx, const unsigned long long* dev2, cudaStream_t s) {
+  int64_t* host = ctx_host_slots(ctx);
+  g_pairs_slot = &host[2];
+  SIMDEX_CUDA(cudaMemcpyAsync(&host[2], dev2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  return SIMDEX_OK;
+}
+void read_pairs(int64_t* out2) {
+  out2[0] = g_pairs_slot ? g_pairs_slot[0] : 0;
+  out2[1] = g_pairs_slot ? g_pairs_slot[1] : 0;
+}
+
 // Brute-force fused path (topk_matmul).  No allocation, no host round trip
 // (options & SIMDEX_MM_NORM_AUTO excepted: it reads two norms to decide the
 // early exit).
@@ -1642,7 +1661,10 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   ws.add(&over_list, nu);
   ws.add(&over_out, nu);
   if (fallback) ws.add(&slab, (size_t)exact_slab_ctas(ni) * ni);
+  unsigned long long* pairs;
+  ws.add(&pairs, 2);
   if ((rc = ws.commit())) return rc;
+  SIMDEX_CUDA(cudaMemsetAsync(pairs, 0, 2 * sizeof(unsigned long long), s));
   const double eps = eps_for(kp);
   units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, nu, ni, units, n_units,
                                                                           nunits);
@@ -1660,6 +1682,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   p.heap_ops = heap_ops;
   p.debug_out = debug_out;
   p.debug_ld = ni;
+  p.pairs_out = pairs;
   // early exit pays when the catalogue's norms are skewed (the streaming
   // kernel with exit checks is slower when no tile can be skipped): the
   // caller decides once per operand (SIMDEX_MM_NORM_EXIT); NORM_AUTO reads
@@ -1706,6 +1729,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
   if ((rc = launch_finalize(fp, nu, "finalize", s))) return rc;
   if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
+  if ((rc = record_pairs(ctx, pairs, s))) return rc;
   // band overflow (rare): exact float64 rows, the count read on the device
   return exact_topk_devcount(users, users32, items, items32, ni, f, over_list, nullptr, over_n, k, over_out,
                              out_ids, out_scores, slab, s);
@@ -1788,8 +1812,11 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     ws.add(&inmax, ni_pad / 32);
     ws.add(&slab, (size_t)exact_slab_ctas(ni) * ni);
   }
+  unsigned long long* pairs;
+  ws.add(&pairs, 2);
   if ((rc = ws.commit())) return rc;
   int64_t* host = ctx_host_slots(ctx);
+  SIMDEX_CUDA(cudaMemsetAsync(pairs, 0, 2 * sizeof(unsigned long long), s));
 
   ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off, units, n_units);
   SIMDEX_LAUNCH_CHECK("ws_units");
@@ -1810,6 +1837,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     if ((rc = make_map(&ma, a_pk, rows_max, kp))) return rc;
     if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
     TopkParams p = make_params(st, units, n_units, pnrm, pnmax, cu, g, f, k_eff);
+    p.pairs_out = pairs;
     // early exit on the cluster ceilings (Algorithm 1's own stop bound): a
     // unit stops once every row's threshold exceeds ||u|| x the next tile's
     // ceiling; the prefix top-K is unchanged (later items cannot reach it)
@@ -1886,7 +1914,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   }
   if (!stage2) {  // the prefix was the whole list
     record_ws_stats(nq, nullptr, 0, bp, ni, f);
-    return SIMDEX_OK;
+    return record_pairs(ctx, pairs, s);
   }
 
   // ---- stage 2: continuing users x the whole catalogue.  Buffers are sized
@@ -1928,6 +1956,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   TopkParams p2 = make_params(st, units, n_units, inrm, inmax, cu2, g, f, k_eff);
   p2.row_T0 = t02;
   p2.norm_sorted = item_perm != nullptr && !getenv("SIMDEX_NO_EARLY_EXIT");
+  p2.pairs_out = pairs + 1;
   Scratch<int64_t> hops2;
   if (stats) {
     SIMDEX_CUDA(hops2.alloc(rows2, s));
@@ -1956,6 +1985,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   f2.item_perm = item_perm;
   if ((rc = launch_finalize(f2, rows2, "finalize_full", s))) return rc;
   if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
+  if ((rc = record_pairs(ctx, pairs, s))) return rc;
   record_ws_stats(nq, &host[0], -1, bp, ni, f);
   // band overflow on the full list (rare): exact float64 scan for those users
   // and the same visited closed form; counts read on the device

@@ -18,6 +18,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
 
 void read_ws_stats(int64_t* out);
 int64_t read_fallback_count();
+void read_pairs(int64_t* out2);
 
 namespace {
 constexpr int kMaxMatmulK = 256;
@@ -74,6 +75,12 @@ extern "C" int simdex_topk_matmul(const double* users, const float* users32, con
 extern "C" int simdex_fallback_rows(int64_t* out) {
   SIMDEX_CHECK_ARG(out, "simdex_fallback_rows: null pointer");
   *out = read_fallback_count();
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_executed_pairs(int64_t* out2) {
+  SIMDEX_CHECK_ARG(out2, "simdex_executed_pairs: null pointer");
+  read_pairs(out2);
   return SIMDEX_OK;
 }
 
