@@ -122,9 +122,19 @@ int Workspace::commit() {
     return SIMDEX_EINVAL;
   }
   // order this call after the context's previous call when the stream changed
-  if (c_->have_done && c_->last != s_) SIMDEX_CUDA(cudaStreamWaitEvent(s_, c_->done, 0));
+  // (not while the stream is being captured into a CUDA graph: a capture may
+  // not depend on outside work; the capturing caller orders it, e.g.
+  // torch.cuda.graph synchronises first)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  SIMDEX_CUDA(cudaStreamIsCapturing(s_, &cs));
+  capturing_ = cs != cudaStreamCaptureStatusNone;
+  if (c_->have_done && c_->last != s_ && !capturing_) SIMDEX_CUDA(cudaStreamWaitEvent(s_, c_->done, 0));
   size_t need = 0;
   for (auto& r : reqs_) need += (r.bytes + 255) & ~size_t(255);
+  if (need > c_->cap && capturing_) {
+    set_error("execution context: the workspace must be grown (run the call once) before graph capture");
+    return SIMDEX_EINVAL;
+  }
   if (need > c_->cap) {
     size_t grow = (need + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
     if (c_->arena) SIMDEX_CUDA(cudaFreeAsync(c_->arena, s_));
@@ -147,6 +157,7 @@ int Workspace::commit() {
 Workspace::~Workspace() {
   if (!committed_) return;
   c_->busy = false;
+  if (capturing_) return;  // a replayed graph is ordered by its launch stream
   c_->last = s_;
   c_->have_done = cudaEventRecord(c_->done, s_) == cudaSuccess;
 }

@@ -120,6 +120,7 @@ class Workspace {
   cudaStream_t s_;
   std::vector<Req> reqs_;
   bool committed_ = false;
+  bool capturing_ = false;
 };
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,35 @@
+"""CUDA-graph replay of a fixed serving call.
+
+A serving call (`index.query_batch_tensors` for a fixed query set, or
+`brute.topk_matmul_tensors`) enqueues ~20 kernels, copies and memsets with
+no host synchronisation and no allocation once the context workspace has
+grown (include/simdex_b200.h, "execution contexts"), so it can be captured
+once and replayed: the host then submits a step with one graph launch
+instead of ~20 launches, and the GPU runs the kernels back to back.
+
+The outputs of a replay are the tensors captured the first time: every
+replay overwrites them (copy them if they must outlive the next replay).
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+class GraphedCall:
+    """Capture ``fn()`` (returning a tuple of device tensors) into a CUDA
+    graph after ``warmup`` eager calls; calling the object replays it on the
+    current stream and returns the captured outputs."""
+
+    def __init__(self, fn, warmup: int = 2):
+        for _ in range(warmup):  # grows the workspace arena, fills the tensor-map and attribute caches
+            fn()
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            self.outputs = fn()
+        torch.cuda.synchronize()
+
+    def __call__(self):
+        self.graph.replay()
+        return self.outputs

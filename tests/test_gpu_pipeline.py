@@ -126,3 +126,24 @@ def test_calibration_entry_points(sx, tmp_path):
         assert optimizer.resolve_h0() == pytest.approx(h0)
     finally:
         del os.environ[optimizer.CONFIG_ENV]
+
+
+def test_graph_replay_equals_eager(sx):
+    """graphs.GraphedCall: the captured serving call (work-sharing query of a
+    fixed query set; blocked product) replays to the eager answer."""
+    import torch
+    from paper_1706_01449_b200 import graphs, index as I, sharding
+    spec = sx.SyntheticSpec(6000, 3000, 24, archetype_count=12, angular_spread=0.3, seed=9)
+    m = sx.generate_synthetic(spec)
+    cl = sx.kmeans(m.users, 10, max_iters=5, seed=1)
+    idx = sx.build_index(m, cl, 512)
+    shard = sharding.IndexShard(idx, m, 1, 3)
+    for fn in (lambda: I.query_batch_tensors(idx, m, None, 10), lambda: shard.topk_tensors(7),
+               lambda: sx.brute.topk_matmul_tensors(m, 5)[:2]):
+        eager = [t.clone() for t in fn()]
+        g = graphs.GraphedCall(fn)
+        for _ in range(2):
+            out = g()
+            torch.cuda.synchronize()
+            for a, b in zip(eager, out):
+                assert torch.equal(a, b)
