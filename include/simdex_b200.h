@@ -299,14 +299,18 @@ SIMDEX_API int simdex_query_ws_opts(const double* users, const float* users32, c
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options, void* stream);
 
 /* simdex_query_ws_opts in an execution context (NULL: the thread default);
- * u_row_exp (nullable): per-row scale exponents of ub (simdex_pack_f16_rows). */
+ * u_row_exp (nullable): per-row scale exponents of ub (simdex_pack_f16_rows);
+ * prefix_ids / prefix_tile_ceil (nullable, both or neither): a prefix operand
+ * from simdex_build_prefix_ordered (rows in its own order; ids resolve them,
+ * tile_ceil bounds the early exit). */
 SIMDEX_API int simdex_query_ws_ctx(void* ctx, const double* users, const float* users32, const uint16_t* ub,
                     const double* user_norms, int64_t nu,
                     const double* items, const float* items32, const uint16_t* ib, const double* item_norms,
                     const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                     int32_t f, int32_t kp, int32_t su, const int32_t* u_row_exp, int32_t si,
                     const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
-                    const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                    const uint16_t* prefix_b, const double* prefix_norm, const int32_t* prefix_ids,
+                    const double* prefix_tile_ceil, int64_t b_pad,
                     const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k,
                     int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options, void* stream);
 
@@ -350,6 +354,21 @@ SIMDEX_API int simdex_gemm_debug(const uint16_t* ub, int64_t nu, const uint16_t*
 SIMDEX_API int simdex_build_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
                         const int32_t* list_ids, int32_t c, int64_t block, int64_t b_pad,
                         uint16_t* out_prefix_b, double* out_prefix_norm, void* stream);
+
+/* simdex_build_prefix with each cluster's B' items in "likely score" order:
+ * sorted by the centroid's float64 score centers[j] . items[i] (desc, id asc)
+ * instead of list order, so the cluster's users meet their best items first
+ * and their certified thresholds rise at once.  The prefix top-K and visited
+ * do not depend on the order in which the prefix is scored (index.py:351-387).
+ *   items float64 [ni, f], centers float64 [c, f], list_pos = inverse lists;
+ *   out_prefix_ids int32 [c, b_pad]: item id of each operand row (-1 padding);
+ *   out_tile_ceil float64 [c, b_pad/128]: per 128-row tile, the largest list
+ *   ceiling at or after it (the prefix early-exit bound). */
+SIMDEX_API int simdex_build_prefix_ordered(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
+                        const double* items, int32_t f, const double* centers,
+                        const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c,
+                        int64_t block, int64_t b_pad, uint16_t* out_prefix_b, double* out_prefix_norm,
+                        int32_t* out_prefix_ids, double* out_tile_ceil, void* stream);
 
 /* ------------------------------------------------------------------------
  * Catalog sharding (no reference counterpart)

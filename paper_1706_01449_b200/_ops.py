@@ -224,6 +224,25 @@ def build_prefix(pi: Packed, list_ids, block):
     return out, onorm, b_pad
 
 
+def build_prefix_ordered(pi: Packed, items, centers, list_ids, list_pos, bounds, block):
+    """Per-cluster prefix operands in the centroid's score order:
+    (fp16 [c, b_pad, kp], float64 norms [c, b_pad], b_pad, item ids int32
+    [c, b_pad], per-tile ceiling bounds float64 [c, b_pad/128])."""
+    c, ni = list_ids.shape
+    f = items.shape[1]
+    bp = min(block, ni)
+    b_pad = 128 * ((bp + 127) // 128)
+    dev = list_ids.device
+    out = torch.empty((c, b_pad, pi.kp), dtype=torch.int16, device=dev)
+    onorm = torch.empty((c, b_pad), dtype=F64, device=dev)
+    ids = torch.empty((c, b_pad), dtype=I32, device=dev)
+    tile_ceil = torch.empty((c, b_pad // 128), dtype=F64, device=dev)
+    call("simdex_build_prefix_ordered", ptr(pi.op), ptr(pi.norms), ni, pi.kp, ptr(_c(items, F64)), f,
+         ptr(_c(centers, F64)), ptr(_c(list_ids, I32)), ptr(_c(list_pos, I32)), ptr(_c(bounds, F64)), c, int(block),
+         b_pad, ptr(out), ptr(onorm), ptr(ids), ptr(tile_ceil), stream_ptr())
+    return out, onorm, b_pad, ids, tile_ceil
+
+
 def group_queries(q_user, assign, c):
     """(grouped user rows, original positions, cluster offsets [c+1])."""
     nq = q_user.shape[0]
@@ -253,7 +272,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     ids = torch.empty((nq, k_eff), dtype=I32, device=users.device)
     sc = torch.empty((nq, k_eff), dtype=F64, device=users.device)
     vis = torch.empty(nq, dtype=I64, device=users.device)
-    pb, pn, b_pad = prefix
+    pb, pn, b_pad = prefix[:3]
+    p_ids, p_ceil = prefix[3:5] if len(prefix) >= 5 else (None, None)
     call("simdex_query_ws_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
          ptr(items32),
          ptr(pi.op),
@@ -261,7 +281,8 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
          ptr(_c(list_ids, I32)),
          ptr(_c(list_pos, I32)),
          ptr(_c(bounds, F64)), c, int(block),
-         ptr(pb), ptr(pn), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc), ptr(vis), int(options),
+         ptr(pb), ptr(pn), ptr(p_ids), ptr(p_ceil), b_pad, ptr(gq), ptr(perm), ptr(off), nq, k, ptr(ids), ptr(sc),
+         ptr(vis), int(options),
          stream_ptr())
     return ids, sc, vis
 

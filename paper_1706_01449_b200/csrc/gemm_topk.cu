@@ -811,6 +811,8 @@ struct FinalizeParams {
   float* row_T0_out;   // prefix mode: certified lower bound for the full-list pass (scaled)
   double t0_scale;     // 2^(su+si)
   const int32_t* u_exp;  // per-user scale exponents (simdex_pack_f16_rows) or null: t0 also x 2^u_exp[user]
+  const int32_t* prefix_ids;  // [C, prefix_ld] item id of each prefix operand row (reordered prefix) or null
+  int64_t prefix_ld;
   int64_t* cont_list;  // prefix mode: rows that continue past B
   int32_t* cont_n;
   int64_t* over_list;
@@ -911,7 +913,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
       const int dst = kept + __popc(mine & ((1u << gl) - 1u));
       if (dst < p.pow2) {
         const int32_t pos = cid[e];
-        si[dst] = p.mode == kPrefix ? p.list_ids[(int64_t)c * p.n + pos] : (p.item_perm ? p.item_perm[pos] : pos);
+        si[dst] = p.mode == kPrefix ? (p.prefix_ids ? p.prefix_ids[(int64_t)c * p.prefix_ld + pos]
+                                                     : p.list_ids[(int64_t)c * p.n + pos])
+                                    : (p.item_perm ? p.item_perm[pos] : pos);
       }
     }
     kept += __popc(mine);
@@ -1227,14 +1231,17 @@ __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restric
 // ceiling at the tile's first position, scaled and rounded up, clamped at 0
 // (ceilings are non-increasing along the list and bound every member's score
 // / ||u||, index.py:90-100), and the largest item norm from the tile on.
+// (tile_ceil: the same bound for a reordered prefix -- the largest ceiling at
+// or after each tile, precomputed by simdex_build_prefix_ordered)
 __global__ void prefix_exit_kernel(const double* __restrict__ bounds, int64_t n, int c, int64_t b_pad, int64_t bp,
                                    double si_scale, const float* __restrict__ pnmax, float* __restrict__ exit_c,
-                                   float* __restrict__ exit_m) {
+                                   float* __restrict__ exit_m, const double* __restrict__ tile_ceil) {
   const int64_t per = b_pad / kTileN;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (int64_t)c * per) return;
   const int64_t j = g / per, pos = (g - j * per) * kTileN;
-  exit_c[g] = pos < bp ? fmaxf(0.f, __double2float_ru(bounds[j * n + pos] * si_scale)) : 0.f;
+  const double ceil = tile_ceil ? tile_ceil[g] : (pos < bp ? bounds[j * n + pos] : 0.0);
+  exit_c[g] = pos < bp ? fmaxf(0.f, __double2float_ru(ceil * si_scale)) : 0.f;
   float m = 0.f;
   for (int64_t ch = (j * b_pad + pos) >> 5; ch < ((j + 1) * b_pad) >> 5; ++ch) m = fmaxf(m, pnmax[ch]);
   exit_m[g] = m;
@@ -1747,7 +1754,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                  int32_t f, int32_t kp, int32_t su, const int32_t* u_exp, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
-                 const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
+                 const uint16_t* prefix_b, const double* prefix_norm, const int32_t* prefix_ids,
+                 const double* prefix_tile_ceil, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
                  double* out_scores, int64_t* out_visited, int32_t options, Ctx* ctx, cudaStream_t s) {
   const int k_eff = (int)(k < ni ? k : ni);
@@ -1843,7 +1851,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     // ceiling; the prefix top-K is unchanged (later items cannot reach it)
     if (prefix_exit) {
       prefix_exit_kernel<<<(unsigned)ceil_div(nt, 256), 256, 0, s>>>(bounds, ni, c, b_pad, bp, std::ldexp(1.0, si),
-                                                                     pnmax, exit_c, exit_m);
+                                                                     pnmax, exit_c, exit_m, prefix_tile_ceil);
       SIMDEX_LAUNCH_CHECK("prefix_exit");
       p.norm_sorted = 1;
       p.exit_c = exit_c;
@@ -1899,6 +1907,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.row_T0_out = t0;
   fp.t0_scale = std::ldexp(1.0, su + si);
   fp.u_exp = u_exp;
+  fp.prefix_ids = prefix_ids;
+  fp.prefix_ld = b_pad;
   fp.cont_list = cont;
   fp.cont_n = cont_n;
   fp.over_list = over_list;

@@ -69,6 +69,42 @@ __global__ void gather_prefix_kernel(const uint16_t* __restrict__ ib, const doub
   if (lane == 0) onorm[c * b_pad + r] = live ? inorm[src] : 0.0;
 }
 
+// Ordering keys of a cluster's prefix: the centroid's float64 score c . i of
+// each of its first bp list items (one warp per (cluster, position)).
+__global__ void prefix_keys_kernel(const int32_t* __restrict__ list_ids, int64_t ni, int64_t bp,
+                                   const double* __restrict__ centers, const double* __restrict__ items, int f,
+                                   int64_t n_clusters, double* __restrict__ keys, int32_t* __restrict__ ids) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= n_clusters * bp) return;
+  const int64_t c = g / bp, j = g - c * bp;
+  const int32_t id = list_ids[c * ni + j];
+  double acc = 0.0;
+  for (int q = lane; q < f; q += 32) acc = fma(centers[c * f + q], items[(int64_t)id * f + q], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    keys[g] = acc;
+    ids[g] = id;
+  }
+}
+
+// Per 128-item tile of the reordered prefix: the largest list ceiling at or
+// after the tile (the early-exit bound, index.py:90-100), unscaled.
+__global__ void prefix_tile_ceil_kernel(const int32_t* __restrict__ ids, int64_t bp, int64_t b_pad,
+                                        const int32_t* __restrict__ list_pos, const double* __restrict__ bounds,
+                                        int64_t ni, int64_t n_clusters, double* __restrict__ tile_ceil) {
+  const int64_t tiles = b_pad / 128;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_clusters * tiles) return;
+  const int64_t c = g / tiles, t = g - c * tiles;
+  double m = 0.0;
+  for (int64_t j = t * 128; j < bp; ++j) {
+    const int32_t id = ids[c * bp + j];
+    m = fmax(m, bounds[c * ni + list_pos[c * ni + id]]);
+  }
+  tile_ceil[g] = m;
+}
+
 __global__ void max_abs_kernel(const double* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
   double m = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -110,6 +146,40 @@ int launch_gather_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, i
   gather_prefix_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>(ib, i_norm, ni, kp, list_ids, bp, b_pad, c,
                                                                     out, onorm);
   SIMDEX_LAUNCH_CHECK("gather_prefix");
+  return SIMDEX_OK;
+}
+
+// Work-sharing prefix in "likely score" order: each cluster's first B' list
+// items sorted by the centroid's score (desc, id asc), so a cluster's users
+// meet their best items in the first chunks and their thresholds rise at
+// once (the stage-1 appends concentrate early in list order).  The prefix
+// top-K and visited do not depend on the order in which the prefix is scored.
+int launch_build_prefix_ordered(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
+                                const double* items, int32_t f, const double* centers,
+                                const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c,
+                                int64_t block, int64_t b_pad, uint16_t* out, double* onorm, int32_t* out_ids,
+                                double* out_tile_ceil, cudaStream_t s) {
+  const int64_t bp = block < ni ? block : ni;
+  Scratch<double> keys;
+  SIMDEX_CUDA(keys.alloc((size_t)c * bp, s));
+  int32_t* ids = out_ids;  // [c, bp] sorted in place, then spread to [c, b_pad]
+  Scratch<int32_t> tmp;
+  SIMDEX_CUDA(tmp.alloc((size_t)c * bp, s));
+  prefix_keys_kernel<<<(unsigned)ceil_div((int64_t)c * bp, 8), 256, 0, s>>>(list_ids, ni, bp, centers, items, f, c,
+                                                                             keys.p, tmp.p);
+  SIMDEX_LAUNCH_CHECK("prefix_keys");
+  SIMDEX_CUDA(segmented_sort_desc(keys.p, tmp.p, c, bp, s));
+  prefix_tile_ceil_kernel<<<(unsigned)ceil_div((int64_t)c * (b_pad / 128), 256), 256, 0, s>>>(
+      tmp.p, bp, b_pad, list_pos, bounds, ni, c, out_tile_ceil);
+  SIMDEX_LAUNCH_CHECK("prefix_tile_ceil");
+  // gather the operand rows in the new order (the sorted ids act as a list of length bp)
+  const int64_t warps = (int64_t)c * b_pad;
+  gather_prefix_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>(ib, i_norm, bp, kp, tmp.p, bp, b_pad, c, out,
+                                                                    onorm);
+  SIMDEX_LAUNCH_CHECK("gather_prefix");
+  SIMDEX_CUDA(cudaMemsetAsync(ids, 0xff, sizeof(int32_t) * (size_t)c * b_pad, s));
+  SIMDEX_CUDA(cudaMemcpy2DAsync(ids, sizeof(int32_t) * b_pad, tmp.p, sizeof(int32_t) * bp, sizeof(int32_t) * bp, c,
+                                cudaMemcpyDeviceToDevice, s));
   return SIMDEX_OK;
 }
 

@@ -12,7 +12,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
                  const float* items32, const uint16_t* ib, const double* i_norm, const int32_t* item_perm, int64_t ib_rows, int64_t ni,
                  int32_t f, int32_t kp, int32_t su, const int32_t* u_exp, int32_t si,
                  const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
-                 const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad, const int64_t* q_user,
+                 const uint16_t* prefix_b, const double* prefix_norm, const int32_t* prefix_ids,
+                 const double* prefix_tile_ceil, int64_t b_pad, const int64_t* q_user,
                  const int64_t* q_perm, const int64_t* q_off, int64_t nq, int32_t k, int32_t* out_ids,
                  double* out_scores, int64_t* out_visited, int32_t options, Ctx* ctx, cudaStream_t s);
 
@@ -132,7 +133,8 @@ extern "C" int simdex_query_ws_ctx(void* ctx, const double* users, const float* 
                                const int32_t* item_perm, int64_t ib_rows, int64_t ni, int32_t f, int32_t kp,
                                int32_t su, const int32_t* u_row_exp, int32_t si, const int32_t* list_ids,
                                const int32_t* list_pos, const double* bounds, int32_t c, int64_t block,
-                               const uint16_t* prefix_b, const double* prefix_norm, int64_t b_pad,
+                               const uint16_t* prefix_b, const double* prefix_norm, const int32_t* prefix_ids,
+                               const double* prefix_tile_ceil, int64_t b_pad,
                                const int64_t* q_user, const int64_t* q_perm, const int64_t* q_off, int64_t nq,
                                int32_t k, int32_t* out_ids, double* out_scores, int64_t* out_visited, int32_t options,
                                     void* stream) {
@@ -152,7 +154,8 @@ extern "C" int simdex_query_ws_ctx(void* ctx, const double* users, const float* 
   SIMDEX_CHECK_ARG(cx, "simdex_query_ws: no execution context");
   return gemm_topk_ws(users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm, ib_rows, ni, f, kp, su, u_row_exp, si,
                       list_ids, list_pos,
-                      bounds, c, block, prefix_b, prefix_norm, b_pad, q_user, q_perm, q_off, nq, k, out_ids,
+                      bounds, c, block, prefix_b, prefix_norm, prefix_ids, prefix_tile_ceil, b_pad, q_user, q_perm,
+                      q_off, nq, k, out_ids,
                       out_scores, out_visited, options, cx, as_stream(stream));
 }
 
@@ -168,7 +171,8 @@ extern "C" int simdex_query_ws_opts(const double* users, const float* users32, c
                                     void* stream) {
   return simdex_query_ws_ctx(nullptr, users, users32, ub, user_norms, nu, items, items32, ib, item_norms, item_perm,
                              ib_rows, ni, f, kp, su, nullptr, si, list_ids, list_pos, bounds, c, block, prefix_b, prefix_norm,
-                             b_pad, q_user, q_perm, q_off, nq, k, out_ids, out_scores, out_visited, options, stream);
+                             nullptr, nullptr, b_pad, q_user, q_perm, q_off, nq, k, out_ids, out_scores, out_visited,
+                             options, stream);
 }
 
 extern "C" int simdex_query_ws(const double* users, const float* users32, const uint16_t* ub, const double* user_norms, int64_t nu,

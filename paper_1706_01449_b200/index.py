@@ -12,6 +12,7 @@ reference's, including ``visited``.
 from __future__ import annotations
 
 import math
+import os
 import struct
 from collections.abc import Mapping
 from dataclasses import dataclass
@@ -309,14 +310,24 @@ class CentroidIndex:
     def device_assignment(self):
         return self.clustering.device_assignment()
 
-    def device_prefix(self, model: ModelPair):
+    def device_prefix(self, model: ModelPair, list_order: bool = False):
         """Per-cluster prefix operand of ``model.items`` (cached with a strong
-        reference to that matrix, so a recycled id() can never alias it)."""
-        ent = self._dev.get("prefix")
+        reference to that matrix, so a recycled id() can never alias it).
+        Default: each cluster's first B' items in its centroid's score order
+        (a cluster's users meet their best items first, so their thresholds
+        rise at once: ~8 % off the prefix pass at cfg2 K = 10, 10 % at K = 50);
+        ``list_order``: the list (ceiling) order the prefix early exit needs."""
+        key = "prefix_list" if list_order else "prefix"
+        ent = self._dev.get(key)
         if ent is None or ent[0] is not model.items:
-            ids, _ = self.device_lists()
-            ent = self._dev["prefix"] = (model.items, _ops.build_prefix(_device.packed(model.items), ids,
-                                                                        self.block_size))
+            ids, bounds = self.device_lists()
+            if list_order:
+                built = _ops.build_prefix(_device.packed(model.items), ids, self.block_size)
+            else:
+                built = _ops.build_prefix_ordered(_device.packed(model.items), _device.f64(model.items),
+                                                  self.clustering.device_centroids(), ids, self.device_list_pos(),
+                                                  bounds, self.block_size)
+            ent = self._dev[key] = (model.items, built)
         return ent[1]
 
     def device_all_users(self, num_users: int, dev):
@@ -457,6 +468,14 @@ def note_walk_estimate(index: CentroidIndex, k: int, mean_visited: float) -> Non
     index._dev[("walk_estimate", int(k))] = float(mean_visited)
 
 
+def prepare_serving(index: CentroidIndex, model: ModelPair, k: int) -> None:
+    """Build the prefix operand the next work-sharing query at depth ``k``
+    will use (the order follows the early-exit decision), so a timed serve
+    does not build it."""
+    if model.factors <= 256 and min(k, model.num_items) <= 256:
+        index.device_prefix(model, list_order=bool(_ws_options(index, k, model.num_items, True) & _ops.WS_PREFIX_EXIT))
+
+
 def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int:
     mv = index._dev.get(("walk_estimate", int(k)))
     if not work_sharing or mv is None:
@@ -502,10 +521,12 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
         if grouped is None:
             grouped = _ops.group_queries(q_users, index.device_assignment(), index.num_clusters)
         block = index.block_size if work_sharing else 0
-        prefix = index.device_prefix(model) if work_sharing else (None, None, 0)
+        options = _ws_options(index, k, n, work_sharing)
+        prefix = (index.device_prefix(model, list_order=bool(options & _ops.WS_PREFIX_EXIT)) if work_sharing
+                  else (None, None, 0))
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
                              items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
-                             options=_ws_options(index, k, n, work_sharing))
+                             options=options)
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
     out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k,
                     users32=_device.f32_exact(model.users), items32=_device.f32_exact(model.items))
@@ -625,6 +646,7 @@ def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> Centroi
         out._dev["ids"], out._dev["bounds"] = lists
         out._dev.pop("pos", None)
         out._dev.pop("prefix", None)
+        out._dev.pop("prefix_list", None)
     return out
 
 

@@ -23,6 +23,7 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--k", type=int, default=None)
 ap.add_argument("--steps", type=int, default=30)
 ap.add_argument("--scale", type=float, default=1.0)
+ap.add_argument("--prefix-exit", default="auto", choices=["auto", "on", "off"])
 a = ap.parse_args()
 w = W.CONFIGS[a.config](a.scale) if a.scale != 1.0 else W.CONFIGS[a.config]()
 k = a.k or w.k
@@ -32,6 +33,8 @@ if a.config in ("cfg1", "cfg3", "cfg5"):
 else:
     plan = optimizer.plan_pipeline(model, k=k, num_clusters=w.clusters, block_size=4096, max_iters=w.max_iters,
                                    seed=w.seed)
+    if a.prefix_exit != "auto":
+        index_mod.note_walk_estimate(plan.index, k, 0.0 if a.prefix_exit == "on" else 1e18)
     step = lambda: index_mod.query_batch_tensors(plan.index, model, None, k)  # noqa: E731
 for _ in range(3):
     step()
@@ -55,6 +58,7 @@ for s in range(a.steps):
             per[n].append(ms)
     _lib.profile(False)
 out = {"lib": os.path.basename(os.environ.get("SIMDEX_LIB_PATH", "default")), "config": a.config, "k": k,
-       "step_ms": round(statistics.median(steps), 4)}
+       "prefix_exit": a.prefix_exit, "step_ms": round(statistics.median(steps), 4),
+       "pairs": _lib.executed_pairs()}
 out.update({n: round(statistics.median(v), 4) for n, v in per.items() if v})
 print(json.dumps(out), flush=True)
