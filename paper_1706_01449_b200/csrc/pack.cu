@@ -89,20 +89,33 @@ __global__ void prefix_keys_kernel(const int32_t* __restrict__ list_ids, int64_t
 }
 
 // Per 128-item tile of the reordered prefix: the largest list ceiling at or
-// after the tile (the early-exit bound, index.py:90-100), unscaled.
-__global__ void prefix_tile_ceil_kernel(const int32_t* __restrict__ ids, int64_t bp, int64_t b_pad,
-                                        const int32_t* __restrict__ list_pos, const double* __restrict__ bounds,
-                                        int64_t ni, int64_t n_clusters, double* __restrict__ tile_ceil) {
-  const int64_t tiles = b_pad / 128;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n_clusters * tiles) return;
-  const int64_t c = g / tiles, t = g - c * tiles;
-  double m = 0.0;
-  for (int64_t j = t * 128; j < bp; ++j) {
-    const int32_t id = ids[c * bp + j];
-    m = fmax(m, bounds[c * ni + list_pos[c * ni + id]]);
+// after the tile (the early-exit bound, index.py:90-100), unscaled.  One CTA
+// per cluster: a warp per tile takes the tile's maximum, then a suffix scan.
+__global__ void __launch_bounds__(1024) prefix_tile_ceil_kernel(const int32_t* __restrict__ ids, int64_t bp,
+                                                                int64_t b_pad, const int32_t* __restrict__ list_pos,
+                                                                const double* __restrict__ bounds, int64_t ni,
+                                                                double* __restrict__ tile_ceil) {
+  extern __shared__ double tmax[];  // [tiles]
+  const int64_t c = blockIdx.x;
+  const int tiles = (int)(b_pad / 128);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = w; t < tiles; t += nw) {
+    double m = 0.0;
+    for (int64_t j = (int64_t)t * 128 + lane; j < (int64_t)(t + 1) * 128 && j < bp; j += 32) {
+      const int32_t id = ids[c * bp + j];
+      m = fmax(m, bounds[c * ni + list_pos[c * ni + id]]);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) tmax[t] = m;
   }
-  tile_ceil[g] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int t = tiles - 1; t >= 0; --t) {
+      m = fmax(m, tmax[t]);
+      tile_ceil[c * tiles + t] = m;
+    }
+  }
 }
 
 __global__ void max_abs_kernel(const double* __restrict__ x, int64_t n, unsigned long long* __restrict__ out) {
@@ -169,8 +182,12 @@ int launch_build_prefix_ordered(const uint16_t* ib, const double* i_norm, int64_
                                                                              keys.p, tmp.p);
   SIMDEX_LAUNCH_CHECK("prefix_keys");
   SIMDEX_CUDA(segmented_sort_desc(keys.p, tmp.p, c, bp, s));
-  prefix_tile_ceil_kernel<<<(unsigned)ceil_div((int64_t)c * (b_pad / 128), 256), 256, 0, s>>>(
-      tmp.p, bp, b_pad, list_pos, bounds, ni, c, out_tile_ceil);
+  const size_t tsm = (size_t)(b_pad / 128) * sizeof(double);
+  if (tsm > 48 * 1024) {
+    set_error("simdex_build_prefix_ordered: prefix longer than %d tiles", 48 * 1024 / 8);
+    return SIMDEX_EUNSUPPORTED;
+  }
+  prefix_tile_ceil_kernel<<<(unsigned)c, 1024, tsm, s>>>(tmp.p, bp, b_pad, list_pos, bounds, ni, out_tile_ceil);
   SIMDEX_LAUNCH_CHECK("prefix_tile_ceil");
   // gather the operand rows in the new order (the sorted ids act as a list of length bp)
   const int64_t warps = (int64_t)c * b_pad;
