@@ -856,6 +856,18 @@ __device__ __forceinline__ void overflow_row(const FinalizeParams& p, int64_t r,
   }
 }
 
+#ifdef SIMDEX_FIN_STATS
+// diagnostic build only: per finalize mode, sum over the rows' lanes of
+// buffered candidates, of survivors of the final threshold, and of lanes
+__device__ unsigned long long g_fin_stats[12];
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int simdex_dbg_fin_stats(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_fin_stats, sizeof(g_fin_stats));
+  static const unsigned long long z[12] = {};
+  return (int)cudaMemcpyToSymbol(g_fin_stats, z, sizeof(z));
+}
+namespace {
+#endif
 // 4 rows per warp, 8 lanes per row: exact float64 rescoring of the row's
 // certified candidates, (score desc, id asc) bitonic sort, output; plus the
 // work-sharing bookkeeping of the mode.
@@ -920,6 +932,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     }
     kept += __popc(mine);
   }
+#ifdef SIMDEX_FIN_STATS
+  if (act) {
+    atomicAdd(&g_fin_stats[p.mode * 3], (unsigned long long)cnt);
+    atomicAdd(&g_fin_stats[p.mode * 3 + 1], (unsigned long long)kept);
+    atomicAdd(&g_fin_stats[p.mode * 3 + 2], 1ull);
+  }
+#endif
   if (act && kept > p.pow2) {  // more survivors than the row's shared-memory slots
     if (gl == 0) overflow_row(p, r, user, out);
     act = false;
