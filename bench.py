@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="replay the serving step as a CUDA graph")
+    ap.add_argument("--graph", action="store_true", help="(default) replay the serving step as a CUDA graph")
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of the graph replay")
     return ap.parse_args()
 
 
@@ -366,24 +367,54 @@ def run_ours(args):
         def step():
             return shard.topk_tensors(k) if shard is not None else sx.brute.topk_matmul_tensors(model, k)[:2]
 
-    # --graph: the serving step captured once into a CUDA graph and replayed
-    # (one host launch per step).  The default is eager, so the per-kernel
-    # CUDA events that feed the roofline are recorded live in the timed region.
-    graphed = args.graph and served != "catalog"
-    if graphed:
-        from paper_1706_01449_b200 import graphs
-        n0 = _lib.launch_count()
-        step = graphs.GraphedCall(step)
-        graph_kernels = (_lib.launch_count() - n0) // 3  # 2 warm-up calls + the captured one
     flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
+
+    def kernel_pass(fn, steps):
+        """per-kernel times: CUDA events recorded by the library on the
+        launching stream around each launch, over `steps` eager steps with the
+        L2 flushed before each (as in the timed region)"""
+        _lib.profile(True)  # (resets the counters)
+        for s in range(steps):
+            flush.fill_(s & 0x7F)
+            fn()
+        torch.cuda.synchronize()
+        out = {}
+        for name in ("gemm_topk", "gemm_topk_prefix", "gemm_topk_full", "finalize", "finalize_prefix",
+                     "finalize_full", "walk", "select_rows", "score_f64"):
+            ms, n = _lib.profile_read(name)
+            if n:
+                out[name] = {"ms_per_step": ms / steps, "launches_per_step": n / steps}
+        _lib.profile(False)
+        return out
+
+    # The serving step is captured once into a CUDA graph and replayed (one
+    # host launch per step; --eager times eager launches).  The per-kernel
+    # launch times that feed the roofline come from an eager pass of the same
+    # number of steps just before the timed region (events cannot be recorded
+    # between the kernels of a graph replay).
+    graphed = not args.eager and served != "catalog"
+    graph_note = None
+    kernels = None
+    if graphed:
+        from paper_1706_01449_b200 import graphs
+        for _ in range(args.warmup):
+            step()
+        kernels = kernel_pass(step, args.steps)
+        try:
+            n0 = _lib.launch_count()
+            step = graphs.GraphedCall(step)
+            graph_kernels = (_lib.launch_count() - n0) // 3  # 2 warm-up calls + the captured one
+        except Exception as exc:  # noqa: BLE001 -- capture refused: time eager launches instead
+            graphed, graph_note, kernels = False, f"graph capture failed ({type(exc).__name__}): eager", None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = Clocks(local)
-    _lib.profile(True)
+    if not graphed:
+        _lib.profile(True)
     launches0 = _lib.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
@@ -409,15 +440,15 @@ def run_ours(args):
     ms_per_step = float(total_ms.item()) / args.steps
     value = nu / (ms_per_step / 1000.0)  # the fixed user set, all ranks together
 
-    # ---- per-kernel times: CUDA events recorded by the library on the
-    # launching stream around each launch during the timed steps
-    kernels = {}
-    for name in ("gemm_topk", "gemm_topk_prefix", "gemm_topk_full", "finalize", "finalize_prefix", "finalize_full",
-                 "walk", "select_rows", "score_f64"):
-        ms, n = _lib.profile_read(name)
-        if n:
-            kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": n / args.steps}
-    _lib.profile(False)
+    # ---- per-kernel times (eager: recorded during the timed steps)
+    if kernels is None:
+        kernels = {}
+        for name in ("gemm_topk", "gemm_topk_prefix", "gemm_topk_full", "finalize", "finalize_prefix",
+                     "finalize_full", "walk", "select_rows", "score_f64"):
+            ms, n = _lib.profile_read(name)
+            if n:
+                kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": n / args.steps}
+        _lib.profile(False)
     kern_ms = sum(v["ms_per_step"] for name, v in kernels.items() if name.startswith(("gemm", "finalize")))
     roof = roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, _lib)
 
@@ -448,7 +479,8 @@ def run_ours(args):
                                        [served]) if world > 1 else "1 GPU",
                        "rank0_shard": shard_info or None,
                        "l2": "flushed (256 MB write) before every timed step",
-                       "launch": "CUDA graph replay of the serving call" if graphed else "eager",
+                       "launch": ("CUDA graph replay of the serving call (kernel times: eager pass of the same "
+                                  "steps before the timed region)") if graphed else (graph_note or "eager"),
                        "setup_seconds": setup},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "e2e_serve": e2e_serve,
             "clocks": clk, "gpu_launches": launches,
