@@ -64,6 +64,9 @@ using namespace sm100;
 #define SIMDEX_WAIT_MMA mbar_wait
 #endif
 
+#ifndef SIMDEX_SPLIT_TARGET
+#define SIMDEX_SPLIT_TARGET 8  // stage-2 units aimed at per CTA slot when catalogue segments are cut
+#endif
 #ifndef SIMDEX_M_TILES
 #define SIMDEX_M_TILES 1
 #endif
@@ -85,6 +88,8 @@ constexpr uint32_t kIdesc = idesc_f16_f32(kTileM, kTileN);
 struct Unit {
   int64_t a_row0;   // first packed user row (multiple of 256)
   int64_t b_row0;   // first item-operand row (multiple of 128)
+  int64_t s_row0;   // first row of the per-row state (candidate buffers, counts, thresholds); a_row0
+                    // except for catalogue segments of a split row block (their own state rows)
   int32_t rows;     // valid user rows, 1..256
   int32_t n_items;  // valid item rows
 };
@@ -408,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const int ntile_a = un.rows > kTileM ? 2 : 1;
       const bool live = row_local < un.rows;
       const int64_t grow = un.a_row0 + row_local;
+      const int64_t srow = un.s_row0 + row_local;  // this (row, catalogue segment)'s state
       const float cu = live ? p.row_cu[grow] : 0.f;
       float T = (live && p.row_T0) ? p.row_T0[grow] : -INFINITY;
       float top[KTT];
@@ -415,9 +421,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       for (int i = 0; i < KTT; ++i) top[i] = -INFINITY;
       int cnt = 0, flags = 0;
       int64_t hops = 0;
-      int32_t* my_id = p.cand_id + grow * p.cap;
-      float* my_lo = p.cand_lo + grow * p.cap;
-      float* my_hi = p.cand_hi + grow * p.cap;
+      int32_t* my_id = p.cand_id + srow * p.cap;
+      float* my_lo = p.cand_lo + srow * p.cap;
+      float* my_hi = p.cand_hi + srow * p.cap;
       const int n_tiles = (un.n_items + kTileN - 1) / kTileN;
       // the tile's four 32-item norm maxima, loaded one tile ahead (off the critical path)
       const float4* nm4p = reinterpret_cast<const float4*>(p.item_nmax32 + (un.b_row0 >> 5));
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 while (full) {
                   const int who = __ffs(full) - 1;
                   full &= full - 1;
-                  const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+                  const int64_t g_w = __shfl_sync(0xffffffffu, srow, who);
                   const int c_w = __shfl_sync(0xffffffffu, cnt, who);
                   const float t_w = __shfl_sync(0xffffffffu, T, who);
                   const int nc = warp_filter(p.cand_hi + g_w * p.cap, p.cand_id + g_w * p.cap, c_w, t_w, lane);
@@ -613,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 while (need) {
                   const int who = __ffs(need) - 1;
                   need &= need - 1;
-                  const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+                  const int64_t g_w = __shfl_sync(0xffffffffu, srow, who);
                   const int c_w = __shfl_sync(0xffffffffu, cnt, who);
                   const float t_w = __shfl_sync(0xffffffffu, T, who);
                   int nc;
@@ -653,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           while (need) {
             const int who = __ffs(need) - 1;
             need &= need - 1;
-            const int64_t g_w = __shfl_sync(0xffffffffu, grow, who);
+            const int64_t g_w = __shfl_sync(0xffffffffu, srow, who);
             const int c_w = __shfl_sync(0xffffffffu, cnt, who);
             const float t_w = __shfl_sync(0xffffffffu, T, who);
             int nc;
@@ -670,10 +676,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       if (live && h < ntile_a && !kDebug) {
         // the buffer may still hold entries admitted before T reached its final
         // value; finalize drops those against row_T_out in parallel
-        p.row_count[grow] = cnt;
-        p.row_flags[grow] = flags;
-        p.row_T_out[grow] = T;
-        if (p.heap_ops) p.heap_ops[grow] = hops;
+        p.row_count[srow] = cnt;
+        p.row_flags[srow] = flags;
+        p.row_T_out[srow] = T;
+        if (p.heap_ops) p.heap_ops[srow] = hops;
       }
     }
   }
@@ -1233,6 +1239,7 @@ __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restric
     for (int64_t r = 0; r < cnt; r += kUnitRows) {
       Unit un;
       un.a_row0 = acc + r;
+      un.s_row0 = un.a_row0;
       un.b_row0 = (int64_t)j * b_pad;
       un.rows = (int32_t)min((int64_t)kUnitRows, cnt - r);
       un.n_items = (int32_t)bp;
@@ -1353,19 +1360,133 @@ __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t
   }
 }
 
+// Units of `nr` packed rows (count on the device or the host) over the whole
+// catalogue.  With seg_out given and fewer row blocks than half the CTA
+// slots, the catalogue is cut into S contiguous segments (>= kMinSegTiles
+// tiles each) so the units fill the GPU: S brings the unit count to about
+// SIMDEX_SPLIT_TARGET units per slot, bounded by the state rows available;
+// segment s of row block b keeps its own state rows s * (row blocks * 128) +
+// b * 128 + l (segment 0 = the row itself), merged by merge_segments_kernel.
+// A segment starts from the rows' initial thresholds, not from what the
+// earlier segments reached, so splitting costs work and only pays when the
+// unsplit units would leave most CTAs idle (measured: N = 4, 8 shards).
+constexpr int kMinSegTiles = 8;
 __global__ void units_from_count_kernel(const int32_t* __restrict__ n_rows_dev, int64_t n_rows_host, int64_t ni,
-                                        Unit* __restrict__ units, int32_t* __restrict__ n_units, int64_t units_max) {
+                                        Unit* __restrict__ units, int32_t* __restrict__ n_units, int64_t units_max,
+                                        int32_t* __restrict__ seg_out = nullptr, int64_t slots = 0,
+                                        int64_t state_rows = 0) {
   const int64_t nr = n_rows_dev ? (int64_t)*n_rows_dev : n_rows_host;
-  const int64_t nunits = (nr + kUnitRows - 1) / kUnitRows;
+  const int64_t nblk = (nr + kUnitRows - 1) / kUnitRows;
+  const int64_t tiles = (ni + kTileN - 1) / kTileN;
+  int64_t S = 1;
+  if (seg_out && nblk > 0 && 2 * nblk < slots) {  // fewer row blocks than half the CTA slots
+    S = (int64_t)SIMDEX_SPLIT_TARGET * slots / nblk;
+    S = min(S, tiles / kMinSegTiles);
+    S = min(S, state_rows / (nblk * kUnitRows));
+    S = min(S, units_max / nblk);
+    S = max(S, (int64_t)1);
+  }
+  const int64_t seg_tiles = (tiles + S - 1) / S;
+  S = (tiles + seg_tiles - 1) / seg_tiles;  // every segment non-empty
+  const int64_t nunits = nblk * S;
   const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (u == 0) *n_units = (int32_t)nunits;
+  if (u == 0) {
+    *n_units = (int32_t)nunits;
+    if (seg_out) {
+      seg_out[0] = (int32_t)S;
+      seg_out[1] = (int32_t)seg_tiles;
+    }
+  }
   if (u >= nunits || u >= units_max) return;
+  const int64_t b = u / S, sg = u - b * S;
   Unit un;
-  un.a_row0 = u * kUnitRows;
-  un.b_row0 = 0;
-  un.rows = (int32_t)min((int64_t)kUnitRows, nr - u * kUnitRows);
-  un.n_items = (int32_t)ni;
+  un.a_row0 = b * kUnitRows;
+  un.s_row0 = sg * nblk * kUnitRows + b * kUnitRows;
+  un.b_row0 = sg * seg_tiles * kTileN;
+  un.rows = (int32_t)min((int64_t)kUnitRows, nr - b * kUnitRows);
+  un.n_items = (int32_t)min(seg_tiles * kTileN, ni - un.b_row0);
   units[u] = un;
+}
+
+// Drop the catalogue segments no row of a block can take anything from (the
+// norm-sorted catalogue's early-exit bound of EXM = 1 evaluated at the
+// segment's first item against the rows' starting thresholds); their state
+// rows are set empty for the merge.  One warp per unit; kept units are
+// compacted into `out` (order free).
+__global__ void prune_units_kernel(const Unit* __restrict__ in, const int32_t* __restrict__ n_in,
+                                   Unit* __restrict__ out, int32_t* __restrict__ n_out, const float* __restrict__ cu,
+                                   const float* __restrict__ T0, const float* __restrict__ nmax32, float g_mul,
+                                   float e_abs, int32_t* __restrict__ cnt, int32_t* __restrict__ flags,
+                                   float* __restrict__ rowT) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n = *n_in;
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n; u += nw) {
+    const Unit un = in[u];
+    bool need = un.b_row0 == 0;
+    if (!need) {
+      const float nm = nmax32[un.b_row0 >> 5];
+      for (int l = lane; l < un.rows; l += 32) {
+        const float gu = cu[un.a_row0 + l] * g_mul;
+        const float bound = fmaf(gu, nm, 2.f * e_abs) * (1.f + 0x1p-20f);
+        if (!(bound < T0[un.a_row0 + l])) need = true;
+      }
+    }
+    need = __any_sync(0xffffffffu, need);
+    if (need) {
+      if (lane == 0) out[atomicAdd(n_out, 1)] = un;
+    } else {
+      for (int l = lane; l < un.rows; l += 32) {
+        cnt[un.s_row0 + l] = 0;
+        flags[un.s_row0 + l] = 0;
+        rowT[un.s_row0 + l] = -INFINITY;
+      }
+    }
+  }
+}
+
+// Segment merge (split row blocks): for every row, the threshold is the
+// largest of its segments' (each a valid lower bound of the K-th score), the
+// segments' candidates reaching it are appended to segment 0's buffer (the
+// row's own) with their positions made absolute (a unit stores positions
+// relative to its first item row), a row whose candidates do not fit is
+// flagged (exact fallback).
+__global__ void merge_segments_kernel(const int32_t* __restrict__ n_rows_dev, const int32_t* __restrict__ seg,
+                                      int cap, int32_t* __restrict__ cid, float* __restrict__ chi,
+                                      int32_t* __restrict__ cnt, int32_t* __restrict__ flags, float* __restrict__ rowT) {
+  const int S = seg[0];
+  if (S <= 1) return;
+  const int32_t seg_items = seg[1] * kTileN;
+  const int64_t nr = *n_rows_dev;
+  const int64_t stride = ((nr + kUnitRows - 1) / kUnitRows) * kUnitRows;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+    float T = rowT[r];
+    int fl = flags[r];
+    for (int s = 1; s < S; ++s) {
+      T = fmaxf(T, rowT[r + s * stride]);
+      fl |= flags[r + s * stride];
+    }
+    int c = cnt[r];
+    for (int s = 1; s < S && !fl; ++s) {
+      const int64_t q = r + s * stride;
+      const int cq = cnt[q];
+      for (int e = 0; e < cq; ++e) {
+        const float h = chi[q * cap + e];
+        if (h >= T) {
+          if (c >= cap) {
+            fl = 1;
+            break;
+          }
+          chi[r * cap + c] = h;
+          cid[r * cap + c] = cid[q * cap + e] + s * seg_items;
+          ++c;
+        }
+      }
+    }
+    cnt[r] = c;
+    flags[r] = fl;
+    rowT[r] = T;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1807,6 +1928,11 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   double* slab = nullptr;
   ws.add(&units, units_max > units2 ? units_max : units2);
   ws.add(&n_units, 1);
+  int32_t *seg_n, *n_units_raw;
+  Unit* units_raw;
+  ws.add(&seg_n, 2);
+  ws.add(&n_units_raw, 1);
+  ws.add(&units_raw, units_max > units2 ? units_max : units2);
   ws.add(&a_off, c + 1);
   ws.add(&a_pk, (size_t)rows_max * kp);
   ws.add(&cu, rows_max);
@@ -1979,7 +2105,12 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 8), 8 * sm_count()), 256, 0, s>>>(
       cont, cont_n, rows2, row_user, row_out, rclus, cu, t0, a_pk, kp, a2, cu2, t02, user2, out2, clus2);
   SIMDEX_LAUNCH_CHECK("cont_rows");
-  units_from_count_kernel<<<(unsigned)ceil_div(units2, 256), 256, 0, s>>>(cont_n, 0, ni, units, n_units, units2);
+  // few continuing rows: catalogue segments spread them over the CTAs
+  const bool split = !stats && !getenv("SIMDEX_NO_SPLIT");
+  const int64_t units2_cap = units_max > units2 ? units_max : units2;
+  units_from_count_kernel<<<(unsigned)ceil_div(units2_cap, 256), 256, 0, s>>>(
+      cont_n, 0, ni, split ? units_raw : units, split ? n_units_raw : n_units, units2_cap, split ? seg_n : nullptr,
+      (int64_t)g.ctas_per_sm * sm_count(), rows_max);
   SIMDEX_LAUNCH_CHECK("units");
   item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm,
                                                                       inmax);
@@ -1990,6 +2121,17 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   TopkParams p2 = make_params(st, units, n_units, inrm, inmax, cu2, g, f, k_eff);
   p2.row_T0 = t02;
   p2.norm_sorted = item_perm != nullptr && !getenv("SIMDEX_NO_EARLY_EXIT");
+  if (split) {
+    SIMDEX_CUDA(cudaMemsetAsync(n_units, 0, sizeof(int32_t), s));
+    if (p2.norm_sorted) {
+      prune_units_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units2_cap, 8), 8 * sm_count()), 256, 0, s>>>(
+          units_raw, n_units_raw, units, n_units, cu2, t02, inmax, p2.g_mul, p2.e_abs, st.cnt, st.flags, st.rowT);
+    } else {  // no bound to prune with: keep every unit
+      prune_units_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units2_cap, 8), 8 * sm_count()), 256, 0, s>>>(
+          units_raw, n_units_raw, units, n_units, cu2, t02, inmax, 0.f, INFINITY, st.cnt, st.flags, st.rowT);
+    }
+    SIMDEX_LAUNCH_CHECK("prune_units");
+  }
   p2.pairs_out = pairs + 1;
   Scratch<int64_t> hops2;
   if (stats) {
@@ -1997,8 +2139,13 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     SIMDEX_CUDA(cudaMemsetAsync(hops2.p, 0, sizeof(int64_t) * rows2, s));
     p2.heap_ops = hops2.p;
   }
-  grid = (int)(units2 < g.ctas_per_sm * sm_count() ? units2 : g.ctas_per_sm * sm_count());
+  grid = (int)(units2_cap < g.ctas_per_sm * sm_count() ? units2_cap : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma2, mb2, p2, g, grid, "gemm_topk_full", s))) return rc;
+  if (split) {
+    merge_segments_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 256), 4 * sm_count()), 256, 0, s>>>(
+        cont_n, seg_n, st.cap, st.cid, st.hi, st.cnt, st.flags, st.rowT);
+    SIMDEX_LAUNCH_CHECK("merge_segments");
+  }
   if (stats) {
     std::vector<int64_t> hh(rows2);
     SIMDEX_CUDA(cudaMemcpy(hh.data(), hops2.p, sizeof(int64_t) * rows2, cudaMemcpyDeviceToHost));
