@@ -26,10 +26,14 @@ def device():
 
 
 def to_device(a: np.ndarray, dtype=None) -> torch.Tensor:
+    """Stream-ordered upload through pinned staging (torch's caching host
+    allocator keeps the buffer until the copy has run).  A copy from pageable
+    memory would synchronise the stream first, idling the GPU while the host
+    queues the next launches, so even small arrays are staged."""
     t = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None:
         t = t.to(dtype)
-    if t.numel() * t.element_size() >= (1 << 20):
+    if t.numel():
         t = t.pin_memory()
     return t.to(device(), non_blocking=True)
 

@@ -259,7 +259,7 @@ MM_NORM_EXIT = 2    # SIMDEX_MM_NORM_EXIT
 
 
 def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, block, prefix, grouped, k,
-             items32=None, users32=None, options=0):
+             items32=None, users32=None, options=0, ctx=None):
     """Work-sharing batch query; ``grouped`` = group_queries(...) output.
     Returns (ids, scores, visited) in the original query order.  ``options``:
     WS_PREFIX_EXIT ends prefix units early on the list ceilings."""
@@ -274,7 +274,7 @@ def query_ws(users, pu: Packed, items, pi: Packed, list_ids, list_pos, bounds, b
     vis = torch.empty(nq, dtype=I64, device=users.device)
     pb, pn, b_pad = prefix[:3]
     p_ids, p_ceil = prefix[3:5] if len(prefix) >= 5 else (None, None)
-    call("simdex_query_ws_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
+    call("simdex_query_ws_ctx", ctx, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu, ptr(_c(items, F64)),
          ptr(items32),
          ptr(pi.op),
          ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp, pu.scale_exp, ptr(pu.row_exp), pi.scale_exp,

@@ -22,6 +22,7 @@ from .model_io import FactorMatrix
 
 DEFAULT_NUM_CLUSTERS = 8
 DEFAULT_MAX_ITERS = 100
+_LLOYD_BATCH = 3  # Lloyd iterations queued per host read (see kmeans)
 
 # Angle used when a vector has zero norm; the most conservative choice
 # (clustering.py:21-23).
@@ -217,27 +218,83 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
 
     assign, d2, _, obj = _ops.kmeans_assign(pts, centers, points32=p32)
     objs = [obj]  # read back once at the end (no per-iteration sync for the history)
-    for _ in range(max_iters):
-        counts, _, _ = _ops.kmeans_update(pts, assign, centers, points32=p32)
-        d2_before = d2
-        new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
-        # one host read per iteration: "a cluster went empty" and "changed"
-        empty, n_changed = torch.stack([(counts == 0).any().to(torch.int64), changed.view(())]).tolist()
-        if empty:  # rare (clustering.py:125-138): repair, then redo this assignment
-            assign, _ = repair(assign, d2_before, counts)
-            new_assign, d2, changed, obj = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
-            n_changed = int(changed.item())
-        objs.append(obj)
-        if n_changed == 0:
-            break
-        assign = new_assign
+
+    def lloyd_step(a_cur):
+        counts, _, _ = _ops.kmeans_update(pts, a_cur, centers, points32=p32)
+        new_assign, d_new, changed, ob = _ops.kmeans_assign(pts, centers, prev=a_cur, points32=p32)
+        flag = torch.stack([(counts == 0).any().to(torch.int64), changed.view(())])
+        return counts, new_assign, d_new, flag, ob
+
+    # Lloyd iterations in speculative batches with one host read per batch
+    # ("a cluster went empty", "assignment changed" for every iteration of
+    # the batch).  Iterations queued after convergence recompute the same
+    # centres (means of the same assignment, deterministic) and the same
+    # assignment, so the state is the converged one; only their objective
+    # entries are dropped.  A batch in which a cluster went empty (rare) is
+    # rolled back and replayed one iteration per read with the host repair
+    # (clustering.py:125-138).
+    it = 0
+    done = False
+    while it < max_iters and not done:
+        batch = min(max_iters - it, _LLOYD_BATCH)
+        snap = (assign.clone(), centers.clone(), d2) if batch > 1 else None
+        steps, a_cur = [], assign
+        for _ in range(batch):
+            counts, new_assign, d_new, flag, ob = lloyd_step(a_cur)
+            steps.append((a_cur, counts, new_assign, d_new, ob))
+            a_cur = new_assign
+            steps[-1] = steps[-1] + (flag,)
+        flags = torch.stack([st[5] for st in steps]).tolist()
+        used = next((i + 1 for i, (_, ch) in enumerate(flags) if ch == 0), batch)  # iterations that count
+        if batch > 1 and any(e for e, _ in flags[:used]):
+            # roll back and replay this batch one iteration per read, with the repair
+            assign, d2 = snap[0], snap[2]
+            centers.copy_(snap[1])
+            for _ in range(batch):
+                d2_before = d2
+                counts, new_assign, d2, flag, ob = lloyd_step(assign)
+                empty, n_changed = flag.tolist()
+                if empty:
+                    assign, _ = repair(assign, d2_before, counts)
+                    new_assign, d2, changed, ob = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
+                    n_changed = int(changed.item())
+                objs.append(ob)
+                it += 1
+                if n_changed == 0:
+                    done = True
+                    break
+                assign = new_assign
+            continue
+        if batch == 1 and flags[0][0]:  # a single iteration emptied a cluster: repair, redo the assignment
+            a_prev, counts = steps[0][0], steps[0][1]
+            assign, _ = repair(a_prev, d2, counts)
+            new_assign, d2, changed, ob = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
+            objs.append(ob)
+            it += 1
+            if int(changed.item()) == 0:
+                done = True
+            else:
+                assign = new_assign
+            continue
+        for i in range(used):
+            a_prev, _, new_assign, d_new, ob, _ = steps[i]
+            objs.append(ob)
+            d2 = d_new
+            it += 1
+            if flags[i][1] == 0:
+                done = True
+                assign = a_prev
+                break
+            assign = new_assign
     counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
-    assign, fixed = repair(assign, d2, counts)
-    if fixed:
-        counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
     theta = _ops.max_angles(pts, centers, assign)
     cen_h, theta_h, off_h, objective = (a.copy() for a in _device.to_host_pinned_many(
         centers, theta, offsets, torch.cat(objs)))
+    if (np.diff(off_h) == 0).any():  # rare: an empty cluster after the last iteration
+        assign, fixed = repair(assign, d2, counts)
+        counts, members, offsets = _ops.kmeans_update(pts, assign, None, num_clusters)
+        theta = _ops.max_angles(pts, centers, assign)
+        cen_h, theta_h, off_h = (a.copy() for a in _device.to_host_pinned_many(centers, theta, offsets))
     for a in (theta_h, objective):
         a.setflags(write=False)
     out = _DeviceClustering(FactorMatrix(cen_h), theta_h, objective, seed, assign.contiguous(), members, off_h)

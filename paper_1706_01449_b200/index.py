@@ -499,7 +499,8 @@ class QuerySet:
         return int(self.user_ids.shape[0])
 
 
-def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int, work_sharing: bool = True):
+def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int, work_sharing: bool = True,
+                        ctx=None):
     """Device form of query_batch: int64 user rows in (a device tensor, a
     QuerySet of this index, or None for every user), (ids int32 [n, k_eff],
     scores float64, visited int64) out, all on the device, in query order."""
@@ -526,7 +527,7 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
                   else (None, None, 0))
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
                              items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
-                             options=options)
+                             options=options, ctx=ctx)
     qc = index.device_assignment().index_select(0, q_users).to(torch.int32)
     out = _ops.walk(users, _device.norms(model.users), items, ids, bounds, q_users, qc, k,
                     users32=_device.f32_exact(model.users), items32=_device.f32_exact(model.items))
