@@ -130,3 +130,36 @@ def test_seeding_degenerate_branch(env):
     import simdex_oracle as O
     ref = O.kmeans(users, 6, max_iters=5, seed=2)
     np.testing.assert_array_equal(cl.assignment, ref["assignment"])
+
+
+@pytest.mark.parametrize("n,f,c,iters,seed", [(3000, 8, 20, 7, 1), (2000, 50, 64, 3, 4), (800, 3, 40, 100, 9),
+                                             (500, 6, 6, 5, 2)])
+def test_lloyd_batches_equal_sequential(env, n, f, c, iters, seed):
+    """Lloyd iterations queued in speculative batches (one host read per
+    batch) give exactly the sequential loop's clustering: assignment,
+    centroids, objective history (iterations after convergence dropped) and
+    theta_b; also against the oracle's restatement of clustering.py."""
+    pkg, _ops, torch = env
+    from paper_1706_01449_b200 import clustering
+    rng = np.random.default_rng(seed)
+    if seed == 2:  # duplicates: the degenerate seeding branch and the final repair
+        users = rng.normal(size=(4, f))[rng.integers(0, 4, n)]
+    else:
+        users = rng.normal(size=(n, f)) * rng.lognormal(0.0, 1.0, size=(n, 1))
+    m = pkg.FactorMatrix(users)
+    old = clustering._LLOYD_BATCH
+    try:
+        clustering._LLOYD_BATCH = 1
+        a = pkg.kmeans(m, c, max_iters=iters, seed=seed)
+        clustering._LLOYD_BATCH = 3
+        b = pkg.kmeans(pkg.FactorMatrix(users), c, max_iters=iters, seed=seed)
+    finally:
+        clustering._LLOYD_BATCH = old
+    np.testing.assert_array_equal(a.assignment, b.assignment)
+    np.testing.assert_array_equal(a.centroids.values, b.centroids.values)
+    np.testing.assert_array_equal(a.objective, b.objective)
+    np.testing.assert_array_equal(a.max_angle, b.max_angle)
+    import simdex_oracle as O
+    ref = O.kmeans(users, c, max_iters=iters, seed=seed)
+    np.testing.assert_array_equal(b.assignment, ref["assignment"])
+    assert b.objective.shape == ref["objective"].shape
