@@ -450,7 +450,8 @@ def run_ours(args):
                 kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": n / args.steps}
         _lib.profile(False)
     kern_ms = sum(v["ms_per_step"] for name, v in kernels.items() if name.startswith(("gemm", "finalize")))
-    roof = roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, _lib)
+    roof = roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, _lib,
+                    stats=shard.stats() if hasattr(shard, "stats") else None)
 
     # ---- e2e: public API from host buffers, per step
     e2e = e2e_serve = None
@@ -490,7 +491,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib):
+def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib, stats=None):
     """Tensor-bound roofline of the dominant kernel, gemm_topk.  Work = 2 f
     flops per scored (user, item) pair, f unpadded.  ``frac``
     counts only the pairs the launch actually multiplied
@@ -504,6 +505,8 @@ def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib):
     p1, p2 = lib.executed_pairs()
     if served == "index":
         nq, n_cont, bp, _, _ = lib.ws_stats()
+        if stats is not None:  # a rank serving its share as several concurrent calls: their sums
+            nq, n_cont, p1, p2 = stats
         s1 = kernels.get("gemm_topk_prefix")
         s2 = kernels.get("gemm_topk_full")
         if not s1:
@@ -530,6 +533,8 @@ def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib):
     g = kernels.get("gemm_topk")
     if not g:
         return None
+    if stats is not None:
+        p1 = stats[2]
     n_users = nu / world if served == "matmul" else nu
     n_items = ni if served == "matmul" else ni / world
     credited = 2.0 * f * n_items * n_users

@@ -335,6 +335,13 @@ SIMDEX_API int simdex_fallback_rows(int64_t* out);
  * count is 2 f x these pairs. */
 SIMDEX_API int simdex_executed_pairs(int64_t* out2);
 
+/* The same counts for the last serving call made on execution context `ctx`
+ * (NULL: this thread's default), so a caller running several calls on their
+ * own contexts can add them up: host int64[4] = [queries that went on past B
+ * (simdex_query_ws_ctx), band-overflow rows, pairs of the first launch, pairs
+ * of the catalogue launch].  Read after the calls' streams synchronised. */
+SIMDEX_API int simdex_ctx_stats(void* ctx, int64_t* out4);
+
 /* Group queries by their cluster (index.py:346-348), stable in query order:
  * out_q_user int64[nq] grouped user rows, out_perm int64[nq] original query
  * position of each grouped entry, out_off int64[c+1] cluster offsets. */

@@ -60,6 +60,7 @@ SIGNATURES = {
     "simdex_fallback_rows": [P],
     "simdex_executed_pairs": [P],
     "simdex_ws_stats": [P],
+    "simdex_ctx_stats": [P, P],
     "simdex_group_queries": [P, I64, P, I32, P, P, P, P],
     "simdex_gemm_debug": [P, I64, P, I64, I32, I32, P, P],
     "simdex_build_prefix": [P, P, I64, I32, P, I32, I64, I64, P, P, P],
@@ -154,6 +155,33 @@ def executed_pairs():
     buf = (C.c_int64 * 2)()
     call("simdex_executed_pairs", C.cast(buf, C.c_void_p))
     return int(buf[0]), int(buf[1])
+
+
+class Context:
+    """An execution context of its own (simdex_ctx_create): a workspace
+    arena and statistic slots, for serving calls that run concurrently on
+    different streams of one thread (the default context is per thread)."""
+
+    def __init__(self, device: int | None = None):
+        import torch
+        self.handle = C.c_void_p()
+        call("simdex_ctx_create", torch.cuda.current_device() if device is None else device, C.byref(self.handle))
+
+    def stats(self):
+        """(continued past B, band-overflow rows, pairs launch 1, pairs launch 2)
+        of the last call on this context; valid once its stream synchronised."""
+        buf = (C.c_int64 * 4)()
+        call("simdex_ctx_stats", self.handle, C.cast(buf, C.c_void_p))
+        return tuple(int(x) for x in buf)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.simdex_ctx_destroy(h)
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
+
 
 
 def workspace_bytes() -> int:

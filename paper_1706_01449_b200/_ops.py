@@ -104,14 +104,14 @@ def topk_exact(users, items, k, rows=None):
     return ids, sc
 
 
-def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32=None, users32=None):
+def topk_matmul(users, pu: Packed, items, pi: Packed, k, heap_ops=False, items32=None, users32=None, ctx=None):
     nu, f = users.shape
     ni = items.shape[0]
     k_eff = min(k, ni)
     ids = torch.empty((nu, k_eff), dtype=I32, device=users.device)
     sc = torch.empty((nu, k_eff), dtype=F64, device=users.device)
     hops = torch.zeros(nu, dtype=I64, device=users.device) if heap_ops else None
-    call("simdex_topk_matmul_ctx", None, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu,
+    call("simdex_topk_matmul_ctx", ctx, ptr(_c(users, F64)), ptr(users32), ptr(pu.op), ptr(pu.norms), nu,
          ptr(_c(items, F64)), ptr(items32), ptr(pi.op), ptr(pi.norms), ptr(pi.perm), pi.rows_pad, ni, f, pu.kp,
          pu.scale_exp, ptr(pu.row_exp), pi.scale_exp, k, ptr(ids), ptr(sc), ptr(hops),
          MM_NORM_EXIT if pi.norm_exit else 0, stream_ptr())

@@ -63,14 +63,16 @@ def topk_naive(model: ModelPair, k: int) -> TopKResults:
     return _results(ids, sc, model.num_items, model.num_users)
 
 
-def topk_matmul_tensors(model: ModelPair, k: int, heap_ops: bool = False):
-    """Device form: (ids int32 [U, k_eff], scores float64, heap_ops|None)."""
+def topk_matmul_tensors(model: ModelPair, k: int, heap_ops: bool = False, ctx=None):
+    """Device form: (ids int32 [U, k_eff], scores float64, heap_ops|None);
+    ``ctx``: an execution context of the caller's (_lib.Context().handle)."""
     users, items = _device.f64(model.users), _device.f64(model.items)
     if min(k, model.num_items) > MATMUL_MAX_K:
         ids, sc = _ops.topk_exact(users, items, k)
         return ids, sc, None
     return _ops.topk_matmul(users, _device.packed_users(model.users), items, _device.packed_sorted(model.items), k,
-                            heap_ops, items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users))
+                            heap_ops, items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
+                            ctx=ctx)
 
 
 def topk_matmul(model: ModelPair, k: int, blocks: BlockSpec | None = None, counters: dict | None = None) -> TopKResults:

@@ -2074,6 +2074,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   }
   if (!stage2) {  // the prefix was the whole list
     record_ws_stats(nq, nullptr, 0, bp, ni, f);
+    SIMDEX_CUDA(cudaMemcpyAsync(&host[0], cont_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
     return record_pairs(ctx, pairs, s);
   }
 

@@ -85,6 +85,18 @@ extern "C" int simdex_executed_pairs(int64_t* out2) {
   return SIMDEX_OK;
 }
 
+extern "C" int simdex_ctx_stats(void* ctx, int64_t* out4) {
+  SIMDEX_CHECK_ARG(out4, "simdex_ctx_stats: null pointer");
+  Ctx* c = ctx_or_default(ctx);
+  if (!c) return SIMDEX_ECUDA;
+  const int64_t* h = ctx_host_slots(c);
+  out4[0] = (int64_t)(int32_t)(h[0] & 0xffffffffll);
+  out4[1] = h[1];
+  out4[2] = h[2];
+  out4[3] = h[3];
+  return SIMDEX_OK;
+}
+
 extern "C" int simdex_ws_stats(int64_t* out5) {
   SIMDEX_CHECK_ARG(out5, "simdex_ws_stats: null pointer");
   read_ws_stats(out5);

@@ -30,11 +30,13 @@ gloo with host copies (the CPU tests, and two processes sharing one GPU).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import _device, _ops, brute
+from . import _lib, _device, _ops, brute
 from . import index as index_mod
 from .model_io import FactorMatrix, ModelPair
 
@@ -62,19 +64,62 @@ def user_shard(model: ModelPair, rank: int, world: int) -> tuple[ModelPair, int]
     return ModelPair(FactorMatrix(model.users.values[lo:hi]), model.items), lo
 
 
+# concurrent serving calls per rank (IndexShard, UserShard), each on its own
+# stream and context (SIMDEX_SHARD_PARTS overrides: A/B timing only)
+_SHARD_PARTS = int(os.environ.get("SIMDEX_SHARD_PARTS", "2"))
+
+
 class UserShard:
     """A rank's resident block of users for repeated blocked-product serving
     (the sub-model keeps its device copies between calls; when the parent
-    model is already on the device, the block is a view of its rows)."""
+    model is already on the device, the block is a view of its rows).  At
+    N > 1 the block is served as ``_SHARD_PARTS`` concurrent calls on their
+    own streams and contexts (the last wave of units of one call leaves the
+    GPU partly idle; see IndexShard)."""
 
-    def __init__(self, model: ModelPair, rank: int, world: int):
+    def __init__(self, model: ModelPair, rank: int, world: int, parts: int | None = None):
         self.model, self.lo = user_shard(model, rank, world)
         self.hi = self.lo + self.model.num_users
         _device.share_rows(model.users, self.model.users, self.lo, self.hi)
+        n_parts = (_SHARD_PARTS if world > 1 else 1) if parts is None else parts
+        nu = self.model.num_users
+        self.parts, self.contexts, self.streams = [], [], []
+        if n_parts > 1 and nu >= 1024 * n_parts:
+            cuts = [nu * i // n_parts for i in range(n_parts + 1)]
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                sub = ModelPair(FactorMatrix(self.model.users.values[a:b]), self.model.items)
+                _device.share_rows(self.model.users, sub.users, a, b)
+                self.parts.append(sub)
+                self.contexts.append(_lib.Context())
+                self.streams.append(torch.cuda.Stream())
 
     def topk_tensors(self, k: int):
-        ids, sc, _ = brute.topk_matmul_tensors(self.model, k)
-        return ids, sc
+        if not self.parts:
+            ids, sc, _ = brute.topk_matmul_tensors(self.model, k)
+            return ids, sc
+        main = torch.cuda.current_stream()
+        fork = torch.cuda.Event()
+        fork.record(main)
+        outs = []
+        for sub, ctx, st in zip(self.parts, self.contexts, self.streams):
+            st.wait_event(fork)
+            with torch.cuda.stream(st):
+                outs.append(brute.topk_matmul_tensors(sub, k, ctx=ctx.handle)[:2])
+        for st in self.streams:
+            join = torch.cuda.Event()
+            join.record(st)
+            main.wait_event(join)
+        for o in outs:
+            for t in o:
+                t.record_stream(main)
+        return tuple(torch.cat([o[i] for o in outs]) for i in range(2))
+
+    def stats(self):
+        """(users, 0, executed pairs, 0) summed over this rank's serving calls
+        (after the stream synchronised)."""
+        if not self.parts:
+            return self.model.num_users, 0, _lib.executed_pairs()[0], 0
+        return self.model.num_users, 0, sum(ctx.stats()[2] for ctx in self.contexts), 0
 
 
 def user_sharded_topk(model: ModelPair, k: int, group=None, rank=None, world=None):
@@ -131,26 +176,83 @@ def partition_users_by_cluster(assignment, num_clusters: int, world: int, costs=
 
 class IndexShard:
     """A rank's users for the index path: the cluster-routed range of the
-    (cluster, id) order, prepared once (index.QuerySet) for repeated serving."""
+    (cluster, id) order, prepared once (index.QuerySet) for repeated serving.
 
-    def __init__(self, index, model: ModelPair, rank: int, world: int, estimate=None):
+    At N > 1 a rank's share is small enough that one serving call leaves
+    the GPU partly idle (the last wave of units, the catalogue pass of the
+    few continuing users, the small setup kernels), so the share is cut into
+    ``_SHARD_PARTS`` cost-balanced contiguous parts served concurrently, each
+    on its own stream and execution context (fork / join by events, CUDA-graph
+    capturable); their outputs concatenate to ``user_ids`` order."""
+
+    def __init__(self, index, model: ModelPair, rank: int, world: int, estimate=None, parts: int | None = None):
         costs = cluster_costs(index, model.num_items, estimate)
-        order, cuts = partition_users_by_cluster(index.clustering.assignment, index.num_clusters, world, costs)
+        assign = np.asarray(index.clustering.assignment)
+        order, cuts = partition_users_by_cluster(assign, index.num_clusters, world, costs)
         self.user_ids = order[cuts[rank]:cuts[rank + 1]]
-        self.share = float(costs[np.asarray(index.clustering.assignment)[self.user_ids]].sum() /
-                           max(costs[np.asarray(index.clustering.assignment)].sum(), 1e-30))
+        self.share = float(costs[assign[self.user_ids]].sum() / max(costs[assign].sum(), 1e-30))
         self.index, self.model = index, model
-        self.queries = index_mod.QuerySet(index, self.user_ids) if self.user_ids.size else None
+        n_parts = (_SHARD_PARTS if world > 1 else 1) if parts is None else parts
+        if self.user_ids.size < 1024 * n_parts:
+            n_parts = 1
+        self.parts, self.contexts, self.streams = [], [], []
+        self.queries = None
+        if self.user_ids.size and n_parts == 1:
+            self.queries = index_mod.QuerySet(index, self.user_ids)
+        elif self.user_ids.size:
+            cum = np.cumsum(costs[assign[self.user_ids]])
+            inner = np.searchsorted(cum, cum[-1] * np.arange(1, n_parts) / n_parts, side="left") + 1
+            pc = np.concatenate([[0], np.minimum(inner, self.user_ids.size), [self.user_ids.size]])
+            pc = np.maximum.accumulate(pc)
+            for a, b in zip(pc[:-1], pc[1:]):
+                if b > a:
+                    self.parts.append(index_mod.QuerySet(index, self.user_ids[a:b]))
+                    self.contexts.append(_lib.Context())
+                    self.streams.append(torch.cuda.Stream())
 
     def topk_tensors(self, k: int, work_sharing: bool = True):
         """(ids, scores, visited) of this rank's users, in ``user_ids`` order."""
-        if self.queries is None:
+        if self.queries is not None:
+            return index_mod.query_batch_tensors(self.index, self.model, self.queries, k, work_sharing)
+        if not self.parts:
             dev = _device.device()
             k_eff = min(k, self.model.num_items)
             return (torch.empty((0, k_eff), dtype=torch.int32, device=dev),
                     torch.empty((0, k_eff), dtype=torch.float64, device=dev),
                     torch.empty(0, dtype=torch.int64, device=dev))
-        return index_mod.query_batch_tensors(self.index, self.model, self.queries, k, work_sharing)
+        main = torch.cuda.current_stream()
+        fork = torch.cuda.Event()
+        fork.record(main)
+        outs = []
+        for q, ctx, st in zip(self.parts, self.contexts, self.streams):
+            st.wait_event(fork)
+            with torch.cuda.stream(st):
+                outs.append(index_mod.query_batch_tensors(self.index, self.model, q, k, work_sharing,
+                                                          ctx=ctx.handle))
+        for st in self.streams:
+            join = torch.cuda.Event()
+            join.record(st)
+            main.wait_event(join)
+        # the parts' tensors were made on their streams: keep them alive for main's use
+        for o, st in zip(outs, self.streams):
+            for t in o:
+                t.record_stream(main)
+        return tuple(torch.cat([o[i] for o in outs]) for i in range(3))
+
+    def stats(self):
+        """(queries, continued past B, executed pairs launch 1, launch 2) summed
+        over this rank's serving calls (after the stream synchronised)."""
+        if not self.parts:
+            nq, n_cont, _, _, _ = _lib.ws_stats()
+            p1, p2 = _lib.executed_pairs()
+            return nq, n_cont, p1, p2
+        tot = [int(self.user_ids.size), 0, 0, 0]
+        for ctx in self.contexts:
+            n_cont, _, p1, p2 = ctx.stats()
+            tot[1] += n_cont
+            tot[2] += p1
+            tot[3] += p2
+        return tuple(tot)
 
 
 # ---------------------------------------------------------------------------
