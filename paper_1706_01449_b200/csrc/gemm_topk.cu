@@ -2144,7 +2144,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   grid = (int)(units2_cap < g.ctas_per_sm * sm_count() ? units2_cap : g.ctas_per_sm * sm_count());
   if ((rc = launch_gemm(ma2, mb2, p2, g, grid, "gemm_topk_full", s))) return rc;
   if (split) {
-    merge_segments_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 256), 4 * sm_count()), 256, 0, s>>>(
+    // (segments exist only for fewer than ~19k continuing rows: a small grid-stride grid)
+    merge_segments_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 256), sm_count() / 2), 256, 0, s>>>(
         cont_n, seg_n, st.cap, st.cid, st.hi, st.cnt, st.flags, st.rowT);
     SIMDEX_LAUNCH_CHECK("merge_segments");
   }
