@@ -130,6 +130,15 @@ struct TopkParams {
   unsigned long long* pairs_out;  // optional: (user row, item) pairs actually multiplied (valid rows x items)
 };
 
+#ifdef SIMDEX_EPI_TIMING
+// diagnostic build only: clock64 cycle sums of CTA 0's warps 0 (producer),
+// 1 (MMA), 2 (first epilogue warp), lane 0: [0] epilogue wait for full
+// accumulators, [1] TMEM loads + wait, [2] tile processing, [3] tiles,
+// [5] MMA wait for an empty accumulator buffer, [6] MMA wait for a full
+// operand stage, [7] MMA tiles, [8] producer wait for an empty stage
+__device__ unsigned long long g_epi_t[16];
+#define EPI_T(i, v) atomicAdd(&g_epi_t[i], (unsigned long long)(v))
+#endif
 // three-input max (sm_100 FMNMX3)
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -320,7 +329,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const long long e = wdone[w];
             stop = (int)(e >> 32) == u && (int)(e & 0xffffffffll) < t;
           }
+#ifdef SIMDEX_EPI_TIMING
+          const long long tp0 = clock64();
+#endif
           SIMDEX_WAIT_PRODUCER(empty + stage, phase ^ 1);
+#ifdef SIMDEX_EPI_TIMING
+          if (blockIdx.x == 0) EPI_T(8, clock64() - tp0);
+#endif
           if (stop) {  // every epilogue warp is done with this unit: end marker instead of tile t
             stage_end[stage] = seq;
             mbar_arrive(full + stage);
@@ -361,8 +376,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const int n_tiles = (un.n_items + kTileN - 1) / kTileN;
         for (int t = 0; t < n_tiles; ++t, ++acc) {
           const uint32_t buf = acc & 1, use = acc >> 1;
+#ifdef SIMDEX_EPI_TIMING
+          const long long tw0 = clock64();
+#endif
           SIMDEX_WAIT_MMA(t_empty + buf, (use & 1) ^ 1);
+#ifdef SIMDEX_EPI_TIMING
+          const long long tw1 = clock64();
+#endif
           SIMDEX_WAIT_MMA(full + stage, phase);
+#ifdef SIMDEX_EPI_TIMING
+          if (blockIdx.x == 0) {
+            EPI_T(5, tw1 - tw0);
+            EPI_T(6, clock64() - tw1);
+            EPI_T(7, 1);
+          }
+#endif
           tc_fence_after();
           if (EX && (t & XM) == 0 && t > 0 && stage_end[stage] == seq) {  // end marker: pass it on to the epilogue
             mbar_arrive(empty + stage);
@@ -446,7 +474,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           ec_next = __ldg(p.exit_c + tile0 + t + 2);
           em_next = __ldg(p.exit_m + tile0 + t + 2);
         }
+#ifdef SIMDEX_EPI_TIMING
+        const bool tme = blockIdx.x == 0 && warp == 2 && lane == 0;
+        const long long te0 = clock64();
+        long long te_ld = 0;
+#endif
         mbar_wait(t_full + buf, use & 1);
+#ifdef SIMDEX_EPI_TIMING
+        const long long te1 = clock64();
+#endif
         tc_fence_after();
         if (EX && (t & XM) == 0 && t > 0 && buf_end[buf] == (int32_t)use) {  // the unit ended early
           __syncwarp();
@@ -465,9 +501,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             if (cg * 32 >= tile_valid) break;
             uint32_t raw[LDC][32];
 #pragma unroll
+#ifdef SIMDEX_EPI_TIMING
+            const long long tl0 = clock64();
+#endif
             for (int c = 0; c < LDC; ++c)
               tmem_ld32_nowait(tbase + lane_off + (buf * kMTiles + h) * kTileN + (cg + c) * 32, raw[c]);
             tmem_wait_ld();
+#ifdef SIMDEX_EPI_TIMING
+            te_ld += clock64() - tl0;
+#endif
             if (cg + LDC >= kTileN / 32) {
               tc_fence_before();
               __syncwarp();
@@ -641,6 +683,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           __syncwarp();
           if (lane == 0) mbar_arrive(t_empty + buf);
         }
+#ifdef SIMDEX_EPI_TIMING
+        if (tme) {
+          EPI_T(0, te1 - te0);
+          EPI_T(1, te_ld);
+          EPI_T(2, clock64() - te1 - te_ld);
+          EPI_T(3, 1);
+        }
+#endif
         if (EX && !done && ((t + 1) & XM) == 0 && t + 1 < n_tiles) {
           // every later item has ||i|| <= the next tile's first norm, so its
           // upper bound is at most ||u|| n + 2 (eps ||u|| n + e_abs)
@@ -862,6 +912,15 @@ __device__ __forceinline__ void overflow_row(const FinalizeParams& p, int64_t r,
   }
 }
 
+#ifdef SIMDEX_EPI_TIMING
+}  // namespace
+extern "C" __attribute__((visibility("default"))) int simdex_dbg_epi_timing(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_epi_t, sizeof(g_epi_t));
+  static const unsigned long long z[16] = {};
+  return (int)cudaMemcpyToSymbol(g_epi_t, z, sizeof(z));
+}
+namespace {
+#endif
 #ifdef SIMDEX_FIN_STATS
 // diagnostic build only: per finalize mode, sum over the rows' lanes of
 // buffered candidates, of survivors of the final threshold, and of lanes
