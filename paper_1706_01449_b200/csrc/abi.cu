@@ -78,6 +78,8 @@ struct Ctx {
   bool have_done = false;
   bool busy = false;
   int64_t* host = nullptr;  // pinned statistics slots
+  uint64_t arena_gen = 0;   // bumped whenever the arena is (re)allocated
+  CtxSetup setup;
 };
 
 namespace {
@@ -109,6 +111,8 @@ Ctx* ctx_or_default(void* ctx) {
 }
 
 int64_t* ctx_host_slots(Ctx* c) { return c->host; }
+CtxSetup* ctx_setup(Ctx* c) { return &c->setup; }
+uint64_t ctx_arena_gen(Ctx* c) { return c->arena_gen; }
 
 Workspace::Workspace(Ctx* c, cudaStream_t s) : c_(c), s_(s) {}
 
@@ -143,6 +147,7 @@ int Workspace::commit() {
     keep_pool_warm();
     SIMDEX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c_->arena), grow, s_));
     c_->cap = grow;
+    ++c_->arena_gen;
   }
   size_t off = 0;
   for (auto& r : reqs_) {
@@ -227,6 +232,12 @@ extern "C" int simdex_ctx_create(int device, void** out_ctx) {
     return rc;
   }
   *out_ctx = c;
+  return SIMDEX_OK;
+}
+
+extern "C" int simdex_ctx_set_query_token(void* ctx, int64_t token) {
+  SIMDEX_CHECK_ARG(ctx, "simdex_ctx_set_query_token: a context of the caller's is required");
+  reinterpret_cast<Ctx*>(ctx)->setup.query_token = token;
   return SIMDEX_OK;
 }
 

@@ -96,6 +96,17 @@ struct Ctx;
 Ctx* ctx_or_default(void* ctx);
 // pinned host int64 slots of the context (valid after the stream synchronises)
 int64_t* ctx_host_slots(Ctx* c);
+// Reuse of a serving call's per-query-set setup (simdex_ctx_set_query_token):
+// the caller's token for the query set served next on this context, and what
+// the context's arena currently holds (token, arena generation, signature of
+// the call's inputs); the arena generation changes whenever the arena moves.
+struct CtxSetup {
+  int64_t query_token = 0;
+  int64_t held_token = 0;
+  uint64_t held_gen = 0, held_sig = 0;
+};
+CtxSetup* ctx_setup(Ctx* c);
+uint64_t ctx_arena_gen(Ctx* c);
 
 // Typed buffers carved out of the context arena for ONE call: add() every
 // buffer first, then commit() (grows the arena stream-ordered when needed,

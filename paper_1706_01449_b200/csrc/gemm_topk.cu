@@ -1987,8 +1987,10 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   double* slab = nullptr;
   ws.add(&units, units_max > units2 ? units_max : units2);
   ws.add(&n_units, 1);
-  int32_t *seg_n, *n_units_raw;
-  Unit* units_raw;
+  int32_t *seg_n, *n_units_raw, *n_units_s2;
+  Unit *units_raw, *units_s2;  // stage 2's own unit lists (stage 1's are kept for a reused setup)
+  ws.add(&units_s2, units_max > units2 ? units_max : units2);
+  ws.add(&n_units_s2, 1);
   ws.add(&seg_n, 2);
   ws.add(&n_units_raw, 1);
   ws.add(&units_raw, units_max > units2 ? units_max : units2);
@@ -2030,21 +2032,45 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   int64_t* host = ctx_host_slots(ctx);
   SIMDEX_CUDA(cudaMemsetAsync(pairs, 0, 2 * sizeof(unsigned long long), s));
 
-  ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off, units, n_units);
-  SIMDEX_LAUNCH_CHECK("ws_units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu, nullptr,
-                                                            u_exp);
-  SIMDEX_LAUNCH_CHECK("row_cu");
-  // rows past a_off[c] stay "padding" (row_user = -1) and are skipped by finalize
-  SIMDEX_CUDA(cudaMemsetAsync(row_user, 0xff, sizeof(int64_t) * rows_max, s));
-  ws_rows_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off, c, rows_max, ub, kp,
-                                                                   ucu, a_pk, cu, row_user, row_out, rclus);
-  SIMDEX_LAUNCH_CHECK("ws_rows");
+  // per-query-set setup (units, packed rows and their bands, prefix norms):
+  // skipped when the context holds it for this query set (its token), these
+  // inputs and this arena (simdex_ctx_set_query_token)
+  CtxSetup* cs = ctx_setup(ctx);
+  uint64_t sig = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { sig = (sig ^ v) * 1099511628211ull; };
+  for (const void* ptrv : {(const void*)q_user, (const void*)q_perm, (const void*)q_off, (const void*)ub,
+                           (const void*)unorm, (const void*)u_exp, (const void*)prefix_norm})
+    mix((uint64_t)(uintptr_t)ptrv);
+  for (int64_t v : {nq, nu, (int64_t)c, b_pad, bp, (int64_t)kp, (int64_t)su, (int64_t)si, rows_max, ni,
+                    (int64_t)k_eff, (int64_t)no_ws})
+    mix((uint64_t)v);
+  const bool reuse = cs->query_token != 0 && cs->held_token == cs->query_token &&
+                     cs->held_gen == ctx_arena_gen(ctx) && cs->held_sig == sig && !getenv("SIMDEX_NO_SETUP_REUSE");
+  if (!reuse) {
+    cs->held_token = 0;
+    ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off, units, n_units);
+    SIMDEX_LAUNCH_CHECK("ws_units");
+    row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu,
+                                                              nullptr, u_exp);
+    SIMDEX_LAUNCH_CHECK("row_cu");
+    // rows past a_off[c] stay "padding" (row_user = -1) and are skipped by finalize
+    SIMDEX_CUDA(cudaMemsetAsync(row_user, 0xff, sizeof(int64_t) * rows_max, s));
+    ws_rows_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(q_user, q_perm, q_off, a_off, c, rows_max, ub,
+                                                                     kp, ucu, a_pk, cu, row_user, row_out, rclus);
+    SIMDEX_LAUNCH_CHECK("ws_rows");
+    if (!no_ws) {
+      item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
+          prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm, pnmax);
+      SIMDEX_LAUNCH_CHECK("item_nrm");
+    }
+    if (cs->query_token != 0) {
+      cs->held_token = cs->query_token;
+      cs->held_gen = ctx_arena_gen(ctx);
+      cs->held_sig = sig;
+    }
+  }
   int grid = 0;
   if (!no_ws) {
-    item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
-        prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm, pnmax);
-    SIMDEX_LAUNCH_CHECK("item_nrm");
     CUtensorMap ma, mb;
     if ((rc = make_map(&ma, a_pk, rows_max, kp))) return rc;
     if ((rc = make_map(&mb, prefix_b, (int64_t)c * b_pad, kp))) return rc;
@@ -2170,7 +2196,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   const bool split = !stats && !getenv("SIMDEX_NO_SPLIT");
   const int64_t units2_cap = units_max > units2 ? units_max : units2;
   units_from_count_kernel<<<(unsigned)ceil_div(units2_cap, 256), 256, 0, s>>>(
-      cont_n, 0, ni, split ? units_raw : units, split ? n_units_raw : n_units, units2_cap, split ? seg_n : nullptr,
+      cont_n, 0, ni, split ? units_raw : units_s2, split ? n_units_raw : n_units_s2, units2_cap,
+      split ? seg_n : nullptr,
       (int64_t)g.ctas_per_sm * sm_count(), rows_max);
   SIMDEX_LAUNCH_CHECK("units");
   item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm,
@@ -2179,17 +2206,18 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   CUtensorMap ma2, mb2;
   if ((rc = make_map(&ma2, a2, rows2, kp))) return rc;
   if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
-  TopkParams p2 = make_params(st, units, n_units, inrm, inmax, cu2, g, f, k_eff);
+  TopkParams p2 = make_params(st, units_s2, n_units_s2, inrm, inmax, cu2, g, f, k_eff);
   p2.row_T0 = t02;
   p2.norm_sorted = item_perm != nullptr && !getenv("SIMDEX_NO_EARLY_EXIT");
   if (split) {
-    SIMDEX_CUDA(cudaMemsetAsync(n_units, 0, sizeof(int32_t), s));
+    SIMDEX_CUDA(cudaMemsetAsync(n_units_s2, 0, sizeof(int32_t), s));
     if (p2.norm_sorted) {
       prune_units_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units2_cap, 8), 8 * sm_count()), 256, 0, s>>>(
-          units_raw, n_units_raw, units, n_units, cu2, t02, inmax, p2.g_mul, p2.e_abs, st.cnt, st.flags, st.rowT);
+          units_raw, n_units_raw, units_s2, n_units_s2, cu2, t02, inmax, p2.g_mul, p2.e_abs, st.cnt, st.flags,
+          st.rowT);
     } else {  // no bound to prune with: keep every unit
       prune_units_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units2_cap, 8), 8 * sm_count()), 256, 0, s>>>(
-          units_raw, n_units_raw, units, n_units, cu2, t02, inmax, 0.f, INFINITY, st.cnt, st.flags, st.rowT);
+          units_raw, n_units_raw, units_s2, n_units_s2, cu2, t02, inmax, 0.f, INFINITY, st.cnt, st.flags, st.rowT);
     }
     SIMDEX_LAUNCH_CHECK("prune_units");
   }

@@ -11,6 +11,9 @@ reference's, including ``visited``.
 
 from __future__ import annotations
 
+import ctypes as C
+import itertools
+
 import math
 import os
 import struct
@@ -20,7 +23,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _device, _ops
+from . import _device, _lib, _ops
 from .clustering import DEGENERATE_ANGLE, Clustering, angular_distance
 from .model_io import DimensionMismatchError, FactorMatrix, FormatError, ModelPair, NonFiniteValueError
 
@@ -333,11 +336,17 @@ class CentroidIndex:
     def device_all_users(self, num_users: int, dev):
         """(arange(num_users) on the device, its cluster grouping), cached per
         user count (a model grown by add_user gets a fresh entry)."""
+        qs = self.all_users_queries(num_users, dev)
+        return qs.q, qs.grouped
+
+    def all_users_queries(self, num_users: int, dev) -> "QuerySet":
+        """Every user as a QuerySet (its own execution context, so repeated
+        serves skip the per-query-set setup), cached per user count."""
         key = ("all_users", int(num_users))
         ent = self._dev.get(key)
         if ent is None:
             q = torch.arange(num_users, dtype=torch.int64, device=dev)
-            ent = self._dev[key] = (q, _ops.group_queries(q, self.device_assignment(), self.num_clusters))
+            ent = self._dev[key] = QuerySet(self, None, q=q)
         return ent
 
 
@@ -483,20 +492,42 @@ def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int
     return _ops.WS_PREFIX_EXIT if mv < PREFIX_EXIT_FRACTION * min(index.block_size, n) else 0
 
 
+_QUERY_TOKENS = itertools.count(1)
+
+
 class QuerySet:
     """A fixed set of user rows prepared for repeated serving on one index:
     the device id tensor and its grouping by cluster (simdex_group_queries),
-    computed once.  Used by the multi-GPU shards, whose user sets are fixed."""
+    computed once, and an execution context of its own tagged with a token
+    unique to this object (simdex_ctx_set_query_token), so a serve after the
+    first skips the per-query-set setup kernels (units, packed query rows,
+    prefix norms).  Used by the all-users serve and the multi-GPU shards."""
 
-    def __init__(self, index: CentroidIndex, user_ids):
-        ids = np.asarray(user_ids, dtype=np.int64)
+    def __init__(self, index: CentroidIndex, user_ids, q=None):
         self.index = index
-        self.user_ids = ids
-        self.q = _device.to_device(ids)
+        if q is None:
+            ids = np.asarray(user_ids, dtype=np.int64)
+            self.user_ids = ids
+            self.q = _device.to_device(ids)
+        else:
+            self.user_ids = None if user_ids is None else np.asarray(user_ids, dtype=np.int64)
+            self.q = q
         self.grouped = _ops.group_queries(self.q, index.device_assignment(), index.num_clusters)
+        self.token = next(_QUERY_TOKENS)
+        self._ctx = None
+
+    def context(self, ctx=None):
+        """The context handle to serve this set on (``ctx``, a caller's
+        context, or this set's own), tagged with this set's token."""
+        if ctx is None:
+            if self._ctx is None:
+                self._ctx = _lib.Context()
+            ctx = self._ctx.handle
+        _lib.call("simdex_ctx_set_query_token", ctx, C.c_int64(self.token))
+        return ctx
 
     def __len__(self):
-        return int(self.user_ids.shape[0])
+        return int(self.q.shape[0])
 
 
 def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int, work_sharing: bool = True,
@@ -509,12 +540,15 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
     ids, bounds = index.device_lists()
     n = model.num_items
     grouped = None
+    qs = None
     if q_users is None:
-        q_users, grouped = index.device_all_users(model.num_users, users.device)
+        qs = index.all_users_queries(model.num_users, users.device)
     elif isinstance(q_users, QuerySet):
         if q_users.index is not index:
             raise ValueError("QuerySet was prepared for another index")
-        q_users, grouped = q_users.q, q_users.grouped
+        qs = q_users
+    if qs is not None:
+        q_users, grouped = qs.q, qs.grouped
     pu, pi = _device.packed_users(model.users), _device.packed_sorted(model.items)
     if min(k, n) <= 256 and pu.kp <= 256:
         # tensor-core path; without work sharing every query takes the full-list
@@ -525,6 +559,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
         options = _ws_options(index, k, n, work_sharing)
         prefix = (index.device_prefix(model, list_order=bool(options & _ops.WS_PREFIX_EXIT)) if work_sharing
                   else (None, None, 0))
+        if qs is not None:
+            ctx = qs.context(ctx)
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
                              items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
                              options=options, ctx=ctx)

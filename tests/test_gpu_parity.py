@@ -383,3 +383,38 @@ def test_cfg1_full_size(sx):
     for fn in (sx.topk_matmul, sx.topk_naive):
         res = fn(model, 10)
         assert_same_topk(_ids(res), _scores(res), g["ids"].astype(np.int64), g["scores"], ctx=fn.__name__)
+
+
+def test_query_set_setup_reuse(sx):
+    """Query sets served repeatedly on their own contexts skip the
+    per-query-set setup (simdex_ctx_set_query_token): alternating two sets,
+    two depths, the all-users serve and a caller context reused across sets
+    all give exactly the answers of a serve that rebuilds the setup."""
+    import os
+    from paper_1706_01449_b200 import _lib
+    from paper_1706_01449_b200 import index as I
+    rng = np.random.default_rng(5)
+    users = rng.normal(size=(3000, 24)) * rng.lognormal(0, 0.5, size=(3000, 1))
+    items = rng.normal(size=(5000, 24)) * rng.lognormal(0, 0.5, size=(5000, 1))
+    m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    idx = sx.build_index(m, sx.kmeans(m.users, 12, max_iters=4, seed=1), 512)
+    a = I.QuerySet(idx, rng.choice(3000, 700, replace=False))
+    b = I.QuerySet(idx, np.arange(0, 3000, 3))
+    shared = _lib.Context()
+
+    def serve(q, k, ctx=None):
+        return [t.cpu().numpy() for t in I.query_batch_tensors(idx, m, q, k, ctx=ctx)]
+
+    os.environ["SIMDEX_NO_SETUP_REUSE"] = "1"
+    try:
+        want = {(n, k): serve(q, k) for n, q in (("a", a), ("b", b), ("all", None)) for k in (10, 5)}
+    finally:
+        del os.environ["SIMDEX_NO_SETUP_REUSE"]
+    for _ in range(2):
+        for n, q in (("a", a), ("b", b), ("all", None)):
+            for k in (10, 5, 10):
+                for got, exp in zip(serve(q, k), want[(n, k)]):
+                    np.testing.assert_array_equal(got, exp)
+                if q is not None:
+                    for got, exp in zip(serve(q, k, ctx=shared.handle), want[(n, k)]):
+                        np.testing.assert_array_equal(got, exp)
