@@ -1399,17 +1399,18 @@ __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t
                                  const uint16_t* __restrict__ a_in, int kp, uint16_t* __restrict__ a2,
                                  float* __restrict__ cu2, float* __restrict__ t02, int64_t* __restrict__ user2,
                                  int64_t* __restrict__ out2, int32_t* __restrict__ clus2) {
-  const int lane = threadIdx.x & 31;
+  // 8 lanes per row (a 64-factor fp16 row is 8 x 16 bytes), 4 rows per warp
+  const int gl = threadIdx.x & 7;
   const int64_t nc = *n_cont;
   const int64_t lim = min(rows_max, ((nc + kUnitRows - 1) / kUnitRows) * kUnitRows);
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < lim;
-       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); r < lim;
+       r += (int64_t)gridDim.x * (blockDim.x >> 3)) {
   const bool live = r < nc;
   const int64_t src_row = live ? cont[r] : 0;
   const uint4* s = reinterpret_cast<const uint4*>(a_in + src_row * kp);
   uint4* d = reinterpret_cast<uint4*>(a2 + r * kp);
-  for (int v = lane; v < kp / 8; v += 32) d[v] = live ? s[v] : make_uint4(0, 0, 0, 0);
-  if (lane == 0) {
+  for (int v = gl; v < kp / 8; v += 8) d[v] = live ? s[v] : make_uint4(0, 0, 0, 0);
+  if (gl == 0) {
     cu2[r] = live ? cu_in[src_row] : 0.f;
     t02[r] = live ? t0_in[src_row] : -INFINITY;
     user2[r] = live ? row_user[src_row] : -1;
@@ -1829,6 +1830,16 @@ int record_pairs(Ctx* ctx, const unsigned long long* dev2, cudaStream_t s) {
   SIMDEX_CUDA(cudaMemcpyAsync(&host[2], dev2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   return SIMDEX_OK;
 }
+// the four statistic slots of a work-sharing call in ONE copy: a device block
+// laid out as the host slots [continuing rows, overflow rows, pairs 1, pairs 2]
+// (the counts int32 in the low halves of zeroed int64 slots)
+int record_stat_block(Ctx* ctx, const int64_t* blk, cudaStream_t s) {
+  int64_t* host = ctx_host_slots(ctx);
+  g_fallback_slot = &host[1];
+  g_pairs_slot = &host[2];
+  SIMDEX_CUDA(cudaMemcpyAsync(host, blk, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  return SIMDEX_OK;
+}
 void read_pairs(int64_t* out2) {
   out2[0] = g_pairs_slot ? g_pairs_slot[0] : 0;
   out2[1] = g_pairs_slot ? g_pairs_slot[1] : 0;
@@ -2003,8 +2014,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   ws.add(&rclus, rows_max);
   ws.add(&cont, rows_max);
   ws.add(&t0, rows_max);
-  ws.add(&cont_n, 1);
-  ws.add(&over_n, 1);
+  int64_t* statblk;  // [cont_n, over_n, pairs[2]] as host slots (record_stat_block)
+  ws.add(&statblk, 4);
   ws.add(&over_list, rows_max);
   ws.add(&over_out, rows_max);
   if (!no_ws) {
@@ -2026,11 +2037,12 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     ws.add(&inmax, ni_pad / 32);
     ws.add(&slab, (size_t)exact_slab_ctas(ni) * ni);
   }
-  unsigned long long* pairs;
-  ws.add(&pairs, 2);
   if ((rc = ws.commit())) return rc;
   int64_t* host = ctx_host_slots(ctx);
-  SIMDEX_CUDA(cudaMemsetAsync(pairs, 0, 2 * sizeof(unsigned long long), s));
+  cont_n = reinterpret_cast<int32_t*>(statblk);
+  over_n = reinterpret_cast<int32_t*>(statblk + 1);
+  unsigned long long* pairs = reinterpret_cast<unsigned long long*>(statblk + 2);
+  SIMDEX_CUDA(cudaMemsetAsync(statblk, 0, 4 * sizeof(int64_t), s));
 
   // per-query-set setup (units, packed rows and their bands, prefix norms):
   // skipped when the context holds it for this query set (its token), these
@@ -2039,9 +2051,9 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   uint64_t sig = 1469598103934665603ull;
   auto mix = [&](uint64_t v) { sig = (sig ^ v) * 1099511628211ull; };
   for (const void* ptrv : {(const void*)q_user, (const void*)q_perm, (const void*)q_off, (const void*)ub,
-                           (const void*)unorm, (const void*)u_exp, (const void*)prefix_norm})
+                           (const void*)unorm, (const void*)u_exp, (const void*)prefix_norm, (const void*)i_norm})
     mix((uint64_t)(uintptr_t)ptrv);
-  for (int64_t v : {nq, nu, (int64_t)c, b_pad, bp, (int64_t)kp, (int64_t)su, (int64_t)si, rows_max, ni,
+  for (int64_t v : {nq, nu, (int64_t)c, b_pad, bp, (int64_t)kp, (int64_t)su, (int64_t)si, rows_max, ni, ni_pad,
                     (int64_t)k_eff, (int64_t)no_ws})
     mix((uint64_t)v);
   const bool reuse = cs->query_token != 0 && cs->held_token == cs->query_token &&
@@ -2109,8 +2121,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     }
   }
 
-  SIMDEX_CUDA(cudaMemsetAsync(cont_n, 0, sizeof(int32_t), s));
-  SIMDEX_CUDA(cudaMemsetAsync(over_n, 0, sizeof(int32_t), s));
+  // (cont_n and over_n were zeroed with the statistics block)
   FinalizeParams fp{};
   fp.mode = kPrefix;
   fp.total_rows = rows_max;
@@ -2159,17 +2170,15 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   }
   if (!stage2) {  // the prefix was the whole list
     record_ws_stats(nq, nullptr, 0, bp, ni, f);
-    SIMDEX_CUDA(cudaMemcpyAsync(&host[0], cont_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
-    return record_pairs(ctx, pairs, s);
+    return record_stat_block(ctx, statblk, s);
   }
 
   // ---- stage 2: continuing users x the whole catalogue.  Buffers are sized
   // for every row; the row and unit counts are read on the device; the count
   // reaches the host statistics slot asynchronously.
   // (slot 0 holds the int32 count in its low half; the high half stays 0)
-  SIMDEX_CUDA(cudaMemcpyAsync(&host[0], cont_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   if (stats) {
+    SIMDEX_CUDA(cudaMemcpyAsync(&host[0], cont_n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SIMDEX_CUDA(cudaStreamSynchronize(s));
     std::vector<int32_t> hc(rows_max);
     SIMDEX_CUDA(cudaMemcpy(hc.data(), st.cnt, sizeof(int32_t) * rows_max, cudaMemcpyDeviceToHost));
@@ -2189,7 +2198,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
             (long long)nq, (long long)host[0], live ? (double)tot / live : 0.0, (long long)mx, (long long)hist[0],
             (long long)hist[1], (long long)hist[2], (long long)hist[3]);
   }
-  cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 8), 8 * sm_count()), 256, 0, s>>>(
+  cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 32), 8 * sm_count()), 256, 0, s>>>(
       cont, cont_n, rows2, row_user, row_out, rclus, cu, t0, a_pk, kp, a2, cu2, t02, user2, out2, clus2);
   SIMDEX_LAUNCH_CHECK("cont_rows");
   // few continuing rows: catalogue segments spread them over the CTAs
@@ -2200,9 +2209,11 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
       split ? seg_n : nullptr,
       (int64_t)g.ctas_per_sm * sm_count(), rows_max);
   SIMDEX_LAUNCH_CHECK("units");
-  item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si), inrm,
-                                                                      inmax);
-  SIMDEX_LAUNCH_CHECK("item_nrm");
+  if (!reuse) {  // the catalogue's scaled norms: part of the reusable setup
+    item_nrm_kernel<<<(unsigned)ceil_div(ni_pad / 32, 8), 256, 0, s>>>(i_norm, ni, ni_pad, std::ldexp(1.0, si),
+                                                                        inrm, inmax);
+    SIMDEX_LAUNCH_CHECK("item_nrm");
+  }
   CUtensorMap ma2, mb2;
   if ((rc = make_map(&ma2, a2, rows2, kp))) return rc;
   if ((rc = make_map(&mb2, ib, ni_pad, kp))) return rc;
@@ -2255,8 +2266,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   f2.cont_n = nullptr;
   f2.item_perm = item_perm;
   if ((rc = launch_finalize(f2, rows2, "finalize_full", s))) return rc;
-  if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
-  if ((rc = record_pairs(ctx, pairs, s))) return rc;
+  if ((rc = record_stat_block(ctx, statblk, s))) return rc;
   record_ws_stats(nq, &host[0], -1, bp, ni, f);
   // band overflow on the full list (rare): exact float64 scan for those users
   // and the same visited closed form; counts read on the device
