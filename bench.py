@@ -559,7 +559,7 @@ def measure_e2e(sx, sharding, model, w, k, served, rank, world, dev, torch, dist
     host_u = torch.from_numpy(model.users.values).pin_memory()
     host_i = torch.from_numpy(model.items.values).pin_memory()
     times, rep, n_mine = [], None, nu
-    for s in range(4):
+    for s in range(8):
         m2 = sx.ModelPair(sx.FactorMatrix(model.users.values), sx.FactorMatrix(model.items.values))
         torch.cuda.synchronize()
         if world > 1:
@@ -578,13 +578,16 @@ def measure_e2e(sx, sharding, model, w, k, served, rank, world, dev, torch, dist
         torch.cuda.synchronize()
         if s >= 2:  # the first passes pay one-time costs (pinned pools, tensor maps, arena growth)
             times.append(time.perf_counter() - t0)
-    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    # median of 6 host-timed passes (a pass is ~20 ms of mostly host-driven
+    # orchestration; single passes vary by tens of percent with host noise)
+    t = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     k_eff = min(k, ni)
     return {"value": nu / float(t.item()), "unit": "users/s",
             "h2d_bytes_per_step": int(model.users.values.nbytes + model.items.values.nbytes),
             "d2h_bytes_per_step": int(n_mine * (k_eff * (4 + 8) + 8)),
+            "passes": len(times), "pass_ms": [round(x * 1e3, 3) for x in times],
             "what": ("run_pipeline" if world == 1 else "sharding.run_pipeline_shard (max over ranks)") +
                     " from host float64 matrices: H2D, k-means, build, estimate, decide, serve, D2H [U,K]",
             "stage_seconds": {"cluster": rep.cluster_seconds, "build": rep.build_seconds,

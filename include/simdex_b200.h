@@ -76,13 +76,14 @@ SIMDEX_API int simdex_profile_reset(void);
  * reference (brute.py:86-107, index.py:351-389) with one resident arena. */
 SIMDEX_API int simdex_ctx_create(int device, void** out_ctx);
 SIMDEX_API int simdex_ctx_destroy(void* ctx);
-/* Declare that the following simdex_query_ws_ctx calls on `ctx` (a context of
- * the caller's, not NULL) serve the query set identified by `token` (nonzero,
+/* Declare that the next simdex_query_ws_ctx call on `ctx` (NULL: this thread's
+ * default context) serves the query set identified by `token` (nonzero,
  * unique for the lifetime of that query set and of the operands it is served
- * with; 0 = none).  A call that finds its setup for the same token, inputs
- * and arena already in the context's workspace skips it: the grouping of the
+ * with; 0 = none); the call consumes the token.  A call that finds its setup
+ * for the same token, inputs and arena still in the context's workspace (no
+ * other call has used the context since) skips it: the grouping of the
  * queries into 128-row units, the packed query rows and their bands, and the
- * prefix norms (index.py:346-357 done once per query set). */
+ * prefix and catalogue norms (index.py:346-357 done once per query set). */
 SIMDEX_API int simdex_ctx_set_query_token(void* ctx, int64_t token);
 /* current arena size of `ctx` in bytes (host output) */
 SIMDEX_API int simdex_ctx_workspace_bytes(void* ctx, int64_t* out_bytes);

@@ -156,6 +156,9 @@ int Workspace::commit() {
   }
   c_->busy = true;
   committed_ = true;
+  // whatever this call leaves in the arena is not a reusable query setup
+  // unless the call itself records one (gemm_topk_ws)
+  c_->setup.held_token = 0;
   return SIMDEX_OK;
 }
 
@@ -236,8 +239,9 @@ extern "C" int simdex_ctx_create(int device, void** out_ctx) {
 }
 
 extern "C" int simdex_ctx_set_query_token(void* ctx, int64_t token) {
-  SIMDEX_CHECK_ARG(ctx, "simdex_ctx_set_query_token: a context of the caller's is required");
-  reinterpret_cast<Ctx*>(ctx)->setup.query_token = token;
+  Ctx* c = ctx_or_default(ctx);
+  if (!c) return SIMDEX_ECUDA;
+  c->setup.query_token = token;
   return SIMDEX_OK;
 }
 

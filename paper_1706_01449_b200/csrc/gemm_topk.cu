@@ -1986,6 +1986,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   const int64_t units2 = rows2 / kUnitRows;
   const int64_t nt = (int64_t)c * (b_pad / kTileN);
 
+  const CtxSetup held_before = *ctx_setup(ctx);  // what the previous call on this context left
   Workspace ws(ctx, s);
   RowState st;
   st.add(ws, rows_max, k_eff);
@@ -2048,6 +2049,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   // skipped when the context holds it for this query set (its token), these
   // inputs and this arena (simdex_ctx_set_query_token)
   CtxSetup* cs = ctx_setup(ctx);
+  const int64_t qtok = cs->query_token;
+  cs->query_token = 0;  // consumed by this call
   uint64_t sig = 1469598103934665603ull;
   auto mix = [&](uint64_t v) { sig = (sig ^ v) * 1099511628211ull; };
   for (const void* ptrv : {(const void*)q_user, (const void*)q_perm, (const void*)q_off, (const void*)ub,
@@ -2056,10 +2059,11 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   for (int64_t v : {nq, nu, (int64_t)c, b_pad, bp, (int64_t)kp, (int64_t)su, (int64_t)si, rows_max, ni, ni_pad,
                     (int64_t)k_eff, (int64_t)no_ws})
     mix((uint64_t)v);
-  const bool reuse = cs->query_token != 0 && cs->held_token == cs->query_token &&
-                     cs->held_gen == ctx_arena_gen(ctx) && cs->held_sig == sig && !getenv("SIMDEX_NO_SETUP_REUSE");
+  // (the held setup is what the previous call on this context left: commit()
+  // cleared it, so compare against the value saved before the commit)
+  const bool reuse = qtok != 0 && held_before.held_token == qtok && held_before.held_gen == ctx_arena_gen(ctx) &&
+                     held_before.held_sig == sig && !getenv("SIMDEX_NO_SETUP_REUSE");
   if (!reuse) {
-    cs->held_token = 0;
     ws_units_kernel<<<1, 1024, 0, s>>>(q_off, c, b_pad, bp, a_off, units, n_units);
     SIMDEX_LAUNCH_CHECK("ws_units");
     row_cu_kernel<<<(unsigned)ceil_div(nu, 256), 256, 0, s>>>(unorm, nu, nu, eps * std::ldexp(1.0, su), ucu,
@@ -2075,11 +2079,11 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
           prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm, pnmax);
       SIMDEX_LAUNCH_CHECK("item_nrm");
     }
-    if (cs->query_token != 0) {
-      cs->held_token = cs->query_token;
-      cs->held_gen = ctx_arena_gen(ctx);
-      cs->held_sig = sig;
-    }
+  }
+  if (qtok != 0) {  // the arena now holds this query set's setup
+    cs->held_token = qtok;
+    cs->held_gen = ctx_arena_gen(ctx);
+    cs->held_sig = sig;
   }
   int grid = 0;
   if (!no_ws) {

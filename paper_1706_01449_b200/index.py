@@ -498,10 +498,11 @@ _QUERY_TOKENS = itertools.count(1)
 class QuerySet:
     """A fixed set of user rows prepared for repeated serving on one index:
     the device id tensor and its grouping by cluster (simdex_group_queries),
-    computed once, and an execution context of its own tagged with a token
-    unique to this object (simdex_ctx_set_query_token), so a serve after the
-    first skips the per-query-set setup kernels (units, packed query rows,
-    prefix norms).  Used by the all-users serve and the multi-GPU shards."""
+    computed once, and a token unique to this object
+    (simdex_ctx_set_query_token): a serve that finds this set's setup still
+    in its execution context's workspace (no other call in between) skips
+    the per-query-set setup kernels (units, packed query rows, norms).  Used
+    by the all-users serve and the multi-GPU shards."""
 
     def __init__(self, index: CentroidIndex, user_ids, q=None):
         self.index = index
@@ -514,15 +515,10 @@ class QuerySet:
             self.q = q
         self.grouped = _ops.group_queries(self.q, index.device_assignment(), index.num_clusters)
         self.token = next(_QUERY_TOKENS)
-        self._ctx = None
 
     def context(self, ctx=None):
-        """The context handle to serve this set on (``ctx``, a caller's
-        context, or this set's own), tagged with this set's token."""
-        if ctx is None:
-            if self._ctx is None:
-                self._ctx = _lib.Context()
-            ctx = self._ctx.handle
+        """Tag the context the next serve runs on (``ctx``, or None for the
+        thread's default) with this set's token; returns ``ctx``."""
         _lib.call("simdex_ctx_set_query_token", ctx, C.c_int64(self.token))
         return ctx
 
