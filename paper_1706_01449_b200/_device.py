@@ -25,6 +25,9 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_SMALL_PAGEABLE = os.environ.get("SIMDEX_SMALL_PAGEABLE") == "1"  # A/B timing only
+
+
 def to_device(a: np.ndarray, dtype=None) -> torch.Tensor:
     """Stream-ordered upload through pinned staging (torch's caching host
     allocator keeps the buffer until the copy has run).  A copy from pageable
@@ -33,7 +36,7 @@ def to_device(a: np.ndarray, dtype=None) -> torch.Tensor:
     t = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None:
         t = t.to(dtype)
-    if t.numel():
+    if t.numel() and (t.numel() * t.element_size() >= (1 << 20) or not _SMALL_PAGEABLE):
         t = t.pin_memory()
     return t.to(device(), non_blocking=True)
 
