@@ -85,6 +85,16 @@ SIMDEX_API int simdex_ctx_destroy(void* ctx);
  * queries into 128-row units, the packed query rows and their bands, and the
  * prefix and catalogue norms (index.py:346-357 done once per query set). */
 SIMDEX_API int simdex_ctx_set_query_token(void* ctx, int64_t token);
+/* Hand the next simdex_query_ws_ctx call on `ctx` (NULL: this thread's
+ * default) every cluster's whole list as a packed operand in list order
+ * (simdex_build_prefix with block = n: fp16 [c, bf_pad, kp] and float64 norms
+ * [c, bf_pad], bf_pad % 128 == 0); consumed by that call.  With it, the users
+ * that go on past B are grouped by cluster and scan their own cluster's list
+ * from B in ceiling order, stopping on the list ceilings (Algorithm 1's own
+ * bound, index.py:225-227) instead of scanning the norm-sorted catalogue; the
+ * prefix top-K joins their candidates.  Same results, less work.  NULL
+ * pointers: the norm-sorted catalogue pass. */
+SIMDEX_API int simdex_ctx_set_full_lists(void* ctx, const uint16_t* full_b, const double* full_norm, int64_t bf_pad);
 /* current arena size of `ctx` in bytes (host output) */
 SIMDEX_API int simdex_ctx_workspace_bytes(void* ctx, int64_t* out_bytes);
 

@@ -33,6 +33,7 @@ SIGNATURES = {
     "simdex_ctx_create": [C.c_int, P],
     "simdex_ctx_destroy": [P],
     "simdex_ctx_set_query_token": [P, I64],
+    "simdex_ctx_set_full_lists": [P, P, P, I64],
     "simdex_ctx_workspace_bytes": [P, P],
     "simdex_topk_exact": [P, I64, P, I64, I32, P, I64, I32, P, P, P],
     "simdex_max_abs": [P, I64, P, P],

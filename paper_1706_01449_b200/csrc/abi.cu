@@ -245,6 +245,17 @@ extern "C" int simdex_ctx_set_query_token(void* ctx, int64_t token) {
   return SIMDEX_OK;
 }
 
+extern "C" int simdex_ctx_set_full_lists(void* ctx, const uint16_t* full_b, const double* full_norm, int64_t bf_pad) {
+  Ctx* c = ctx_or_default(ctx);
+  if (!c) return SIMDEX_ECUDA;
+  SIMDEX_CHECK_ARG((full_b == nullptr) == (full_norm == nullptr) && bf_pad % 128 == 0 && bf_pad >= 0,
+                   "simdex_ctx_set_full_lists: bad arguments");
+  c->setup.full_b = full_b;
+  c->setup.full_norm = full_norm;
+  c->setup.bf_pad = full_b ? bf_pad : 0;
+  return SIMDEX_OK;
+}
+
 extern "C" int simdex_ctx_destroy(void* ctx) {
   if (!ctx) return SIMDEX_OK;
   Ctx* c = reinterpret_cast<Ctx*>(ctx);

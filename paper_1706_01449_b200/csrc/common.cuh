@@ -104,6 +104,10 @@ struct CtxSetup {
   int64_t query_token = 0;
   int64_t held_token = 0;
   uint64_t held_gen = 0, held_sig = 0;
+  // per-cluster full lists for the next work-sharing call (simdex_ctx_set_full_lists)
+  const uint16_t* full_b = nullptr;
+  const double* full_norm = nullptr;
+  int64_t bf_pad = 0;
 };
 CtxSetup* ctx_setup(Ctx* c);
 uint64_t ctx_arena_gen(Ctx* c);

@@ -67,6 +67,12 @@ using namespace sm100;
 #ifndef SIMDEX_SPLIT_TARGET
 #define SIMDEX_SPLIT_TARGET 8  // stage-2 units aimed at per CTA slot when catalogue segments are cut
 #endif
+#ifndef SIMDEX_LIST_STAGE2
+#define SIMDEX_LIST_STAGE2 1
+#endif
+#ifndef SIMDEX_LIST_MIN_K
+#define SIMDEX_LIST_MIN_K 8
+#endif
 #ifndef SIMDEX_M_TILES
 #define SIMDEX_M_TILES 1
 #endif
@@ -875,6 +881,15 @@ struct FinalizeParams {
   int64_t* over_out;
   int32_t* over_n;
   int pow2;
+  // list-order catalogue pass (full-list mode): candidate positions are list
+  // positions from list_off on, and the row's prefix top-K (already in
+  // out_ids, exact) joins the candidates; prefix rows whose band overflowed
+  // go to the exact fallback list over1_* instead of continuing
+  int64_t list_off;
+  int merge_prefix;
+  int64_t* over1_list;
+  int64_t* over1_out;
+  int32_t* over1_n;
   // k-means assignment mode (items = centers): d2 = (p2 + c2) - 2 p.c in
   // float64, first minimum over the certified candidates
   const float* users32;  // exact float32 copy of users or null
@@ -902,7 +917,11 @@ __device__ int64_t ceiling_count(const double* b, int64_t n, double unorm, doubl
 // a row whose candidates do not fit: prefix rows redo the full list (stage
 // 2 from T0 = -inf), other rows go to the exact float64 path
 __device__ __forceinline__ void overflow_row(const FinalizeParams& p, int64_t r, int64_t user, int64_t out) {
-  if (p.mode == kPrefix) {
+  if (p.mode == kPrefix && p.over1_list) {  // list-order catalogue pass: the exact fallback takes the row
+    const int sl = atomicAdd(p.over1_n, 1);
+    p.over1_list[sl] = r;
+    p.over1_out[sl] = out;
+  } else if (p.mode == kPrefix) {
     p.row_T0_out[r] = -INFINITY;
     p.cont_list[atomicAdd(p.cont_n, 1)] = r;
   } else {
@@ -992,10 +1011,27 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
         const int32_t pos = cid[e];
         si[dst] = p.mode == kPrefix ? (p.prefix_ids ? p.prefix_ids[(int64_t)c * p.prefix_ld + pos]
                                                      : p.list_ids[(int64_t)c * p.n + pos])
-                                    : (p.item_perm ? p.item_perm[pos] : pos);
+                  : p.merge_prefix ? p.list_ids[(int64_t)c * p.n + p.list_off + pos]
+                                   : (p.item_perm ? p.item_perm[pos] : pos);
       }
     }
     kept += __popc(mine);
+  }
+  if (p.merge_prefix) {
+    // the prefix's exact top-K (positions < list_off, never among the
+    // candidates) joins the rescoring
+    for (int i0 = 0; i0 < p.k_eff; i0 += LPR) {
+      const int i = i0 + gl;
+      const int32_t id = (act && i < p.k_eff) ? p.out_ids[out * p.k_eff + i] : -1;
+      const bool keep = id >= 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      const unsigned mine = (bal & gmask) >> (grp * LPR);
+      if (keep) {
+        const int dst = kept + __popc(mine & ((1u << gl) - 1u));
+        if (dst < p.pow2) si[dst] = id;
+      }
+      kept += __popc(mine);
+    }
   }
 #ifdef SIMDEX_FIN_STATS
   if (act) {
@@ -1265,7 +1301,8 @@ __global__ void fallback_visited_kernel(const int64_t* __restrict__ rows, const 
 // list; thread t owns a contiguous run of clusters, runs are scanned in order
 __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restrict__ q_off, int c, int64_t b_pad,
                                                         int64_t bp, int64_t* __restrict__ a_off,
-                                                        Unit* __restrict__ units, int32_t* __restrict__ n_units) {
+                                                        Unit* __restrict__ units, int32_t* __restrict__ n_units,
+                                                        int64_t b_off = 0, int32_t* __restrict__ rows_out = nullptr) {
   __shared__ int64_t s_rows[1024];
   __shared__ int s_units[1024];
   const int t = threadIdx.x;
@@ -1299,7 +1336,7 @@ __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restric
       Unit un;
       un.a_row0 = acc + r;
       un.s_row0 = un.a_row0;
-      un.b_row0 = (int64_t)j * b_pad;
+      un.b_row0 = (int64_t)j * b_pad + b_off;
       un.rows = (int32_t)min((int64_t)kUnitRows, cnt - r);
       un.n_items = (int32_t)bp;
       units[nu++] = un;
@@ -1309,6 +1346,7 @@ __global__ void __launch_bounds__(1024) ws_units_kernel(const int64_t* __restric
   if (t == 1023) {
     a_off[c] = s_rows[1023];
     *n_units = s_units[1023];
+    if (rows_out) *rows_out = (int32_t)s_rows[1023];
   }
 }
 
@@ -1392,6 +1430,73 @@ __global__ void all_rows_continue_kernel(const int64_t* __restrict__ row_user, i
 }
 
 // stage 2: pack the continuing rows densely (rows past the count are zero)
+// List-order catalogue pass: the continuing rows grouped by cluster.
+// Per-cluster counts (one atomic per row), their exclusive scan (one CTA),
+// then each continuing row takes a slot in its cluster's 128-padded range.
+__global__ void cont_count_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
+                                  const int32_t* __restrict__ row_cluster, int32_t* __restrict__ cnt) {
+  const int64_t nc = *n_cont;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + row_cluster[cont[i]], 1);
+}
+__global__ void __launch_bounds__(1024) count_scan_kernel(const int32_t* __restrict__ cnt, int c,
+                                                          int64_t* __restrict__ off) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int per = (c + 1023) / 1024;
+  const int j0 = min(c, t * per), j1 = min(c, j0 + per);
+  int64_t v = 0;
+  for (int j = j0; j < j1; ++j) v += cnt[j];
+  part[t] = v;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t add = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += add;
+    __syncthreads();
+  }
+  int64_t acc = part[t] - v;
+  for (int j = j0; j < j1; ++j) {
+    off[j] = acc;
+    acc += cnt[j];
+  }
+  if (t == 1023) off[c] = part[1023];
+}
+// a warp per 4 continuing rows, 8 lanes per row: the row's slot in its
+// cluster's range a_off2[cl] + (arrival order), operand row and bookkeeping
+__global__ void cont_group_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
+                                  const int64_t* __restrict__ row_user, const int64_t* __restrict__ row_out,
+                                  const int32_t* __restrict__ row_cluster, const float* __restrict__ cu_in,
+                                  const float* __restrict__ t0_in, const uint16_t* __restrict__ a_in, int kp,
+                                  const int64_t* __restrict__ a_off2, int32_t* __restrict__ cursor,
+                                  uint16_t* __restrict__ a2, float* __restrict__ cu2, float* __restrict__ t02,
+                                  int64_t* __restrict__ user2, int64_t* __restrict__ out2, int32_t* __restrict__ clus2) {
+  const int lane = threadIdx.x & 31, gl = lane & 7;
+  const int64_t nc = *n_cont;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; base < nc;
+       base += nw * 4) {  // warp-uniform trip count (the shuffle below needs the whole warp)
+    const int64_t i = base + (lane >> 3);
+    const bool v = i < nc;
+    const int64_t src = v ? cont[i] : 0;
+    const int cl = v ? row_cluster[src] : 0;
+    int64_t dst = 0;
+    if (v && gl == 0) dst = a_off2[cl] + atomicAdd(cursor + cl, 1);
+    dst = __shfl_sync(0xffffffffu, dst, lane & ~7);
+    if (!v) continue;
+    const uint4* sr = reinterpret_cast<const uint4*>(a_in + src * kp);
+    uint4* d = reinterpret_cast<uint4*>(a2 + dst * kp);
+    for (int q = gl; q < kp / 8; q += 8) d[q] = sr[q];
+    if (gl == 0) {
+      cu2[dst] = cu_in[src];
+      t02[dst] = t0_in[src];
+      user2[dst] = row_user[src];
+      out2[dst] = row_out[src];
+      clus2[dst] = cl;
+    }
+  }
+}
+
 __global__ void cont_rows_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
                                  int64_t rows_max, const int64_t* __restrict__ row_user,
                                  const int64_t* __restrict__ row_out, const int32_t* __restrict__ row_cluster,
@@ -1987,6 +2092,19 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   const int64_t nt = (int64_t)c * (b_pad / kTileN);
 
   const CtxSetup held_before = *ctx_setup(ctx);  // what the previous call on this context left
+  // per-cluster full lists handed to this call (simdex_ctx_set_full_lists): the
+  // continuing users scan their own cluster's list from B' in list order
+  const uint16_t* full_b = held_before.full_b;
+  const double* full_norm = held_before.full_norm;
+  const int64_t bf_pad = held_before.bf_pad;
+  ctx_setup(ctx)->full_b = nullptr;
+  ctx_setup(ctx)->full_norm = nullptr;
+  ctx_setup(ctx)->bf_pad = 0;
+  // (from K = 8 on: at K = 1, 5 the continuing users are few and the grouping
+  // and per-cluster units cost more than the shorter scan saves -- measured)
+  const bool list2 = SIMDEX_LIST_STAGE2 && stage2 && !no_ws && full_b && full_norm && bf_pad >= ni && bp % kTileN == 0 &&
+                     k_eff >= SIMDEX_LIST_MIN_K && !getenv("SIMDEX_NO_LIST_STAGE2") && !getenv("SIMDEX_STATS");
+  const int64_t rows_s2 = list2 ? rows_max : rows2;  // stage-2 packed rows (cluster-padded in list mode)
   Workspace ws(ctx, s);
   RowState st;
   st.add(ws, rows_max, k_eff);
@@ -2027,13 +2145,30 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     ws.add(&exit_c, nt);
     ws.add(&exit_m, nt);
   }
+  int64_t *q_off2 = nullptr, *a_off2 = nullptr, *over1_list = nullptr, *over1_out = nullptr;
+  int32_t *cnt2 = nullptr, *cur2 = nullptr, *rows2_n = nullptr, *over1_n = nullptr;
+  float *fnrm = nullptr, *fnmax = nullptr, *exit_c2 = nullptr, *exit_m2 = nullptr;
+  const int64_t nt2 = list2 ? (int64_t)c * (bf_pad / kTileN) : 0;
+  if (list2) {
+    ws.add(&q_off2, c + 1);
+    ws.add(&a_off2, c + 1);
+    ws.add(&cnt2, c);
+    ws.add(&cur2, c);
+    ws.add(&rows2_n, 4);  // [0] grouped rows, [1] prefix-overflow rows
+    ws.add(&over1_list, rows_max);
+    ws.add(&over1_out, rows_max);
+    ws.add(&fnrm, (size_t)c * bf_pad);
+    ws.add(&fnmax, (size_t)c * bf_pad / 32);
+    ws.add(&exit_c2, nt2);
+    ws.add(&exit_m2, nt2);
+  }
   if (stage2) {
-    ws.add(&a2, (size_t)rows2 * kp);
-    ws.add(&cu2, rows2);
-    ws.add(&t02, rows2);
-    ws.add(&user2, rows2);
-    ws.add(&out2, rows2);
-    ws.add(&clus2, rows2);
+    ws.add(&a2, (size_t)rows_s2 * kp);
+    ws.add(&cu2, rows_s2);
+    ws.add(&t02, rows_s2);
+    ws.add(&user2, rows_s2);
+    ws.add(&out2, rows_s2);
+    ws.add(&clus2, rows_s2);
     ws.add(&inrm, ni_pad);
     ws.add(&inmax, ni_pad / 32);
     ws.add(&slab, (size_t)exact_slab_ctas(ni) * ni);
@@ -2054,10 +2189,11 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   uint64_t sig = 1469598103934665603ull;
   auto mix = [&](uint64_t v) { sig = (sig ^ v) * 1099511628211ull; };
   for (const void* ptrv : {(const void*)q_user, (const void*)q_perm, (const void*)q_off, (const void*)ub,
-                           (const void*)unorm, (const void*)u_exp, (const void*)prefix_norm, (const void*)i_norm})
+                           (const void*)unorm, (const void*)u_exp, (const void*)prefix_norm, (const void*)i_norm,
+                           (const void*)full_b, (const void*)full_norm})
     mix((uint64_t)(uintptr_t)ptrv);
   for (int64_t v : {nq, nu, (int64_t)c, b_pad, bp, (int64_t)kp, (int64_t)su, (int64_t)si, rows_max, ni, ni_pad,
-                    (int64_t)k_eff, (int64_t)no_ws})
+                    (int64_t)k_eff, (int64_t)no_ws, bf_pad, (int64_t)list2})
     mix((uint64_t)v);
   // (the held setup is what the previous call on this context left: commit()
   // cleared it, so compare against the value saved before the commit)
@@ -2078,6 +2214,14 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
       item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * b_pad / 32, 8), 256, 0, s>>>(
           prefix_norm, (int64_t)c * b_pad, (int64_t)c * b_pad, std::ldexp(1.0, si), pnrm, pnmax);
       SIMDEX_LAUNCH_CHECK("item_nrm");
+    }
+    if (list2) {  // the full lists' scaled norms and per-tile stop bounds (list ceilings)
+      item_nrm_kernel<<<(unsigned)ceil_div((int64_t)c * bf_pad / 32, 8), 256, 0, s>>>(
+          full_norm, (int64_t)c * bf_pad, (int64_t)c * bf_pad, std::ldexp(1.0, si), fnrm, fnmax);
+      SIMDEX_LAUNCH_CHECK("item_nrm");
+      prefix_exit_kernel<<<(unsigned)ceil_div(nt2, 256), 256, 0, s>>>(bounds, ni, c, bf_pad, ni, std::ldexp(1.0, si),
+                                                                      fnmax, exit_c2, exit_m2, nullptr);
+      SIMDEX_LAUNCH_CHECK("prefix_exit");
     }
   }
   if (qtok != 0) {  // the arena now holds this query set's setup
@@ -2165,6 +2309,13 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.over_out = over_out;
   fp.over_n = over_n;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
+  if (list2) {
+    SIMDEX_CUDA(cudaMemsetAsync(rows2_n, 0, 4 * sizeof(int32_t), s));
+    over1_n = rows2_n + 1;
+    fp.over1_list = over1_list;
+    fp.over1_out = over1_out;
+    fp.over1_n = over1_n;
+  }
   if (no_ws) {
     fp.prefix = 0;  // no floor: visited is the stop position from 0
     all_rows_continue_kernel<<<(unsigned)ceil_div(rows_max, 256), 256, 0, s>>>(row_user, rows_max, cont, cont_n, t0);
@@ -2201,6 +2352,68 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
             "<16:%lld <32:%lld <64:%lld >=64:%lld\n",
             (long long)nq, (long long)host[0], live ? (double)tot / live : 0.0, (long long)mx, (long long)hist[0],
             (long long)hist[1], (long long)hist[2], (long long)hist[3]);
+  }
+  if (list2) {
+    // continuing rows grouped by cluster, each cluster's range 128-padded
+    SIMDEX_CUDA(cudaMemsetAsync(cnt2, 0, sizeof(int32_t) * c, s));
+    SIMDEX_CUDA(cudaMemsetAsync(cur2, 0, sizeof(int32_t) * c, s));
+    SIMDEX_CUDA(cudaMemsetAsync(user2, 0xff, sizeof(int64_t) * rows_s2, s));  // padding rows: no user
+    cont_count_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 256), 4 * sm_count()), 256, 0, s>>>(
+        cont, cont_n, rclus, cnt2);
+    SIMDEX_LAUNCH_CHECK("cont_count");
+    count_scan_kernel<<<1, 1024, 0, s>>>(cnt2, c, q_off2);
+    SIMDEX_LAUNCH_CHECK("count_scan");
+    // units: each cluster's rows x its list from B' (list order, stop bounds per tile)
+    ws_units_kernel<<<1, 1024, 0, s>>>(q_off2, c, bf_pad, ni - bp, a_off2, units_s2, n_units_s2, bp, rows2_n);
+    SIMDEX_LAUNCH_CHECK("ws_units");
+    cont_group_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 32), 8 * sm_count()), 256, 0, s>>>(
+        cont, cont_n, row_user, row_out, rclus, cu, t0, a_pk, kp, a_off2, cur2, a2, cu2, t02, user2, out2, clus2);
+    SIMDEX_LAUNCH_CHECK("cont_group");
+    CUtensorMap ma2, mb2;
+    if ((rc = make_map(&ma2, a2, rows_s2, kp))) return rc;
+    if ((rc = make_map(&mb2, full_b, (int64_t)c * bf_pad, kp))) return rc;
+    TopkParams p2 = make_params(st, units_s2, n_units_s2, fnrm, fnmax, cu2, g, f, k_eff);
+    p2.row_T0 = t02;
+    p2.norm_sorted = 1;
+    p2.exit_c = exit_c2;
+    p2.exit_m = exit_m2;
+    p2.pairs_out = pairs + 1;
+    grid = (int)(units_max < g.ctas_per_sm * sm_count() ? units_max : g.ctas_per_sm * sm_count());
+    if ((rc = launch_gemm(ma2, mb2, p2, g, grid, "gemm_topk_full", s))) return rc;
+    FinalizeParams f2 = fp;
+    f2.mode = kFullList;
+    f2.total_rows = rows_s2;
+    f2.n_rows_dev = rows2_n;
+    f2.row_user = user2;
+    f2.row_out = out2;
+    f2.row_cluster = clus2;
+    f2.cont_list = nullptr;
+    f2.cont_n = nullptr;
+    f2.item_perm = nullptr;
+    f2.list_off = bp;
+    f2.merge_prefix = 1;
+    f2.over1_list = nullptr;
+    f2.over1_out = nullptr;
+    f2.over1_n = nullptr;
+    if ((rc = launch_finalize(f2, rows_s2, "finalize_full", s))) return rc;
+    if ((rc = record_stat_block(ctx, statblk, s))) return rc;
+    record_ws_stats(nq, &host[0], -1, bp, ni, f);
+    // band overflow (rare): exact float64 scan and the visited closed form, for
+    // the catalogue-pass rows and for the prefix rows that overflowed
+    if ((rc = exact_topk_devcount(users, users32, items, items32, ni, f, over_list, user2, over_n, k, over_out,
+                                  out_ids, out_scores, slab, s)))
+      return rc;
+    fallback_visited_kernel<<<kFallbackGrid, 256, 0, s>>>(over_list, over_n, user2, out2, clus2, list_pos, bounds,
+                                                          unorm, ni, bp, k_eff, out_ids, out_scores, out_visited);
+    SIMDEX_LAUNCH_CHECK("fallback_visited");
+    if ((rc = exact_topk_devcount(users, users32, items, items32, ni, f, over1_list, row_user, over1_n, k, over1_out,
+                                  out_ids, out_scores, slab, s)))
+      return rc;
+    fallback_visited_kernel<<<kFallbackGrid, 256, 0, s>>>(over1_list, over1_n, row_user, row_out, rclus, list_pos,
+                                                          bounds, unorm, ni, bp, k_eff, out_ids, out_scores,
+                                                          out_visited);
+    SIMDEX_LAUNCH_CHECK("fallback_visited");
+    return SIMDEX_OK;
   }
   cont_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 32), 8 * sm_count()), 256, 0, s>>>(
       cont, cont_n, rows2, row_user, row_out, rclus, cu, t0, a_pk, kp, a2, cu2, t02, user2, out2, clus2);

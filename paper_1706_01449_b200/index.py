@@ -333,6 +333,26 @@ class CentroidIndex:
             ent = self._dev[key] = (model.items, built)
         return ent[1]
 
+    def device_full_lists(self, model: ModelPair):
+        """Every cluster's whole list as a packed operand in list order
+        (simdex_build_prefix with block = n; cached with a strong reference to
+        ``model.items``): the users that go on past B scan their own cluster's
+        list from B and stop on its ceilings (Algorithm 1's bound) instead of
+        scanning the norm-sorted catalogue.  None when it would take more than
+        FULL_LIST_BYTES (cfg4: 17.9 GB), or when the prefix is the whole list."""
+        ent = self._dev.get("full_lists")
+        if ent is None or ent[0] is not model.items:
+            n, c = model.num_items, self.num_clusters
+            pi = _device.packed(model.items)
+            bf_pad = 128 * ((n + 127) // 128)
+            built = None
+            if min(self.block_size, n) < n and min(self.block_size, n) % 128 == 0 and \
+                    c * bf_pad * pi.kp * 2 <= FULL_LIST_BYTES:
+                ids, _ = self.device_lists()
+                built = _ops.build_prefix(pi, ids, n)
+            ent = self._dev["full_lists"] = (model.items, built)
+        return ent[1]
+
     def device_all_users(self, num_users: int, dev):
         """(arange(num_users) on the device, its cluster grouping), cached per
         user count (a model grown by add_user gets a fresh entry)."""
@@ -483,6 +503,7 @@ def prepare_serving(index: CentroidIndex, model: ModelPair, k: int) -> None:
     does not build it."""
     if model.factors <= 256 and min(k, model.num_items) <= 256:
         index.device_prefix(model, list_order=bool(_ws_options(index, k, model.num_items, True) & _ops.WS_PREFIX_EXIT))
+        index.device_full_lists(model)
 
 
 def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int:
@@ -493,6 +514,8 @@ def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int
 
 
 _QUERY_TOKENS = itertools.count(1)
+# largest per-cluster full-list operand built for the list-order catalogue pass
+FULL_LIST_BYTES = int(os.environ.get("SIMDEX_FULL_LIST_BYTES", str(4 << 30)))
 
 
 class QuerySet:
@@ -557,6 +580,10 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
                   else (None, None, 0))
         if qs is not None:
             ctx = qs.context(ctx)
+        if work_sharing and block < n:
+            fl = index.device_full_lists(model)
+            if fl is not None:
+                _lib.call("simdex_ctx_set_full_lists", ctx, _lib.ptr(fl[0]), _lib.ptr(fl[1]), fl[2])
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,
                              items32=_device.f32_exact(model.items), users32=_device.f32_exact(model.users),
                              options=options, ctx=ctx)
@@ -680,6 +707,7 @@ def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> Centroi
         out._dev.pop("pos", None)
         out._dev.pop("prefix", None)
         out._dev.pop("prefix_list", None)
+        out._dev.pop("full_lists", None)
     return out
 
 
