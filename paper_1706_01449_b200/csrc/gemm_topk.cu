@@ -73,6 +73,9 @@ using namespace sm100;
 #ifndef SIMDEX_LIST_MIN_K
 #define SIMDEX_LIST_MIN_K 8
 #endif
+#ifndef SIMDEX_LIST_MIN_Q
+#define SIMDEX_LIST_MIN_Q 100000
+#endif
 #ifndef SIMDEX_M_TILES
 #define SIMDEX_M_TILES 1
 #endif
@@ -2100,10 +2103,14 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   ctx_setup(ctx)->full_b = nullptr;
   ctx_setup(ctx)->full_norm = nullptr;
   ctx_setup(ctx)->bf_pad = 0;
-  // (from K = 8 on: at K = 1, 5 the continuing users are few and the grouping
-  // and per-cluster units cost more than the shorter scan saves -- measured)
+  // (from K = 8 on and for large query sets: at K = 1, 5 the continuing users
+  // are few and the grouping and per-cluster units cost more than the shorter
+  // scan saves; for a multi-GPU share of ~30k users a few per-cluster units
+  // running to their longest walk set the time, where the norm-sorted pass
+  // cuts the catalogue into segments -- measured)
   const bool list2 = SIMDEX_LIST_STAGE2 && stage2 && !no_ws && full_b && full_norm && bf_pad >= ni && bp % kTileN == 0 &&
-                     k_eff >= SIMDEX_LIST_MIN_K && !getenv("SIMDEX_NO_LIST_STAGE2") && !getenv("SIMDEX_STATS");
+                     k_eff >= SIMDEX_LIST_MIN_K && nq >= SIMDEX_LIST_MIN_Q && !getenv("SIMDEX_NO_LIST_STAGE2") &&
+                     !getenv("SIMDEX_STATS");
   const int64_t rows_s2 = list2 ? rows_max : rows2;  // stage-2 packed rows (cluster-padded in list mode)
   Workspace ws(ctx, s);
   RowState st;
