@@ -1436,11 +1436,20 @@ __global__ void all_rows_continue_kernel(const int64_t* __restrict__ row_user, i
 // List-order catalogue pass: the continuing rows grouped by cluster.
 // Per-cluster counts (one atomic per row), their exclusive scan (one CTA),
 // then each continuing row takes a slot in its cluster's 128-padded range.
+// (warp-aggregated: the continuing rows arrive in packed order, i.e. mostly
+// grouped by cluster, so one atomic per run of equal clusters in a warp)
 __global__ void cont_count_kernel(const int64_t* __restrict__ cont, const int32_t* __restrict__ n_cont,
                                   const int32_t* __restrict__ row_cluster, int32_t* __restrict__ cnt) {
   const int64_t nc = *n_cont;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(cnt + row_cluster[cont[i]], 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); b < nc; b += stride) {
+    const int64_t i = b + lane;
+    const bool v = i < nc;
+    const int cl = v ? row_cluster[cont[i]] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, cl);
+    if (v && lane == __ffs(same) - 1) atomicAdd(cnt + cl, __popc(same));
+  }
 }
 __global__ void __launch_bounds__(1024) count_scan_kernel(const int32_t* __restrict__ cnt, int c,
                                                           int64_t* __restrict__ off) {
@@ -1474,28 +1483,39 @@ __global__ void cont_group_kernel(const int64_t* __restrict__ cont, const int32_
                                   const int64_t* __restrict__ a_off2, int32_t* __restrict__ cursor,
                                   uint16_t* __restrict__ a2, float* __restrict__ cu2, float* __restrict__ t02,
                                   int64_t* __restrict__ user2, int64_t* __restrict__ out2, int32_t* __restrict__ clus2) {
+  // a warp takes 32 continuing rows: slots by one warp-aggregated atomic per
+  // run of equal clusters, then the rows are copied 4 at a time (8 lanes each)
   const int lane = threadIdx.x & 31, gl = lane & 7;
   const int64_t nc = *n_cont;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4; base < nc;
-       base += nw * 4) {  // warp-uniform trip count (the shuffle below needs the whole warp)
-    const int64_t i = base + (lane >> 3);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nc;
+       base += nw * 32) {  // warp-uniform trip count (shuffles below)
+    const int64_t i = base + lane;
     const bool v = i < nc;
     const int64_t src = v ? cont[i] : 0;
-    const int cl = v ? row_cluster[src] : 0;
-    int64_t dst = 0;
-    if (v && gl == 0) dst = a_off2[cl] + atomicAdd(cursor + cl, 1);
-    dst = __shfl_sync(0xffffffffu, dst, lane & ~7);
-    if (!v) continue;
-    const uint4* sr = reinterpret_cast<const uint4*>(a_in + src * kp);
-    uint4* d = reinterpret_cast<uint4*>(a2 + dst * kp);
-    for (int q = gl; q < kp / 8; q += 8) d[q] = sr[q];
-    if (gl == 0) {
+    const int cl = v ? row_cluster[src] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, cl);
+    const int leader = __ffs(same) - 1;
+    int64_t first = 0;
+    if (v && lane == leader) first = a_off2[cl] + atomicAdd(cursor + cl, __popc(same));
+    first = __shfl_sync(0xffffffffu, first, leader);
+    const int64_t dst = first + __popc(same & ((1u << lane) - 1u));
+    if (v) {
       cu2[dst] = cu_in[src];
       t02[dst] = t0_in[src];
       user2[dst] = row_user[src];
       out2[dst] = row_out[src];
       clus2[dst] = cl;
+    }
+    for (int j = 0; j < 32; j += 4) {
+      const int who = j + (lane >> 3);
+      const int64_t s_w = __shfl_sync(0xffffffffu, src, who);
+      const int64_t d_w = __shfl_sync(0xffffffffu, dst, who);
+      if (base + who < nc) {
+        const uint4* sr = reinterpret_cast<const uint4*>(a_in + s_w * kp);
+        uint4* d = reinterpret_cast<uint4*>(a2 + d_w * kp);
+        for (int q = gl; q < kp / 8; q += 8) d[q] = sr[q];
+      }
     }
   }
 }
@@ -2373,7 +2393,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
     // units: each cluster's rows x its list from B' (list order, stop bounds per tile)
     ws_units_kernel<<<1, 1024, 0, s>>>(q_off2, c, bf_pad, ni - bp, a_off2, units_s2, n_units_s2, bp, rows2_n);
     SIMDEX_LAUNCH_CHECK("ws_units");
-    cont_group_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 32), 8 * sm_count()), 256, 0, s>>>(
+    cont_group_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows2, 256), 8 * sm_count()), 256, 0, s>>>(
         cont, cont_n, row_user, row_out, rclus, cu, t0, a_pk, kp, a_off2, cur2, a2, cu2, t02, user2, out2, clus2);
     SIMDEX_LAUNCH_CHECK("cont_group");
     CUtensorMap ma2, mb2;
