@@ -74,7 +74,7 @@ using namespace sm100;
 #define SIMDEX_LIST_MIN_K 8
 #endif
 #ifndef SIMDEX_LIST_MIN_Q
-#define SIMDEX_LIST_MIN_Q 100000
+#define SIMDEX_LIST_MIN_Q 50000
 #endif
 #ifndef SIMDEX_M_TILES
 #define SIMDEX_M_TILES 1
