@@ -694,10 +694,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
 #ifdef SIMDEX_EPI_TIMING
         if (tme) {
+          const long long tproc = clock64() - te1 - te_ld;
           EPI_T(0, te1 - te0);
           EPI_T(1, te_ld);
-          EPI_T(2, clock64() - te1 - te_ld);
+          EPI_T(2, tproc);
           EPI_T(3, 1);
+          // processing cycles by the tile's place in its unit: t = 0, 1-3, 4-7, >= 8
+          EPI_T(9 + (t == 0 ? 0 : t < 4 ? 1 : t < 8 ? 2 : 3), tproc);
         }
 #endif
         if (EX && !done && ((t + 1) & XM) == 0 && t + 1 < n_tiles) {

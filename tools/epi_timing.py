@@ -38,5 +38,7 @@ tot = v[0] + v[1] + v[2]
 print(f"{cfg} k={k}: epilogue warp 2 of CTA 0 over {v[3]} tiles: per tile {tot / tiles:.0f} cycles = wait full "
       f"{v[0] / tiles:.0f} + TMEM loads {v[1] / tiles:.0f} + processing {v[2] / tiles:.0f}")
 mt = max(v[7], 1)
+print(f"  processing cycles by tile place in the unit: t=0 {v[9]}, 1-3 {v[10]}, 4-7 {v[11]}, >=8 {v[12]} "
+      f"(shares {v[9] / max(v[2], 1):.2f} / {v[10] / max(v[2], 1):.2f} / {v[11] / max(v[2], 1):.2f} / {v[12] / max(v[2], 1):.2f})")
 print(f"  MMA warp over {v[7]} tiles: per tile wait empty accumulator {v[5] / mt:.0f}, wait operand stage "
       f"{v[6] / mt:.0f} cycles; producer wait for an empty stage {v[8] / mt:.0f} cycles per tile")

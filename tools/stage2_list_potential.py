@@ -44,3 +44,37 @@ for c in range(idx.num_clusters):
     rows_tiles += int(np.ceil(ext / 128).sum()) if ext.size else 0
 print(f"  list order: warp-tiles {tiles} (x 32 rows x 128 items = {tiles * 32 * 128} pairs); "
       f"per-row tiles {rows_tiles} ({rows_tiles * 128} pairs)")
+
+# stage 1 (the prefix): with list order and a per-warp stop on the ceilings,
+# a warp of 32 consecutive packed rows of a cluster needs min(B', its longest
+# walk) items; the prefix pass multiplies B' for every row
+tiles1 = 0
+full1 = 0
+for c in range(idx.num_clusters):
+    ids = np.flatnonzero(a == c)
+    ext = np.minimum(wu[ids], B)
+    for s in range(0, ext.size, 32):
+        tiles1 += int(np.ceil(ext[s:s + 32].max() / 128))
+        full1 += B // 128
+print(f"  stage 1: per-warp stop on the ceilings needs {tiles1} warp-tiles of {full1} ({tiles1 / full1:.2f})")
+for grp in (32, 128):
+    for sort in (False, True):
+        t = 0
+        for c in range(idx.num_clusters):
+            ext = np.minimum(wu[np.flatnonzero(a == c)], B)
+            if sort:
+                ext = np.sort(ext)
+            for s in range(0, ext.size, grp):
+                t += int(np.ceil(ext[s:s + grp].max() / 128)) * (grp // 32)
+        print(f"  stage 1, groups of {grp} rows {'sorted by walk' if sort else 'packed order'}: {t / full1:.2f} of the warp-tiles")
+# a cheap proxy for the walk: the user's angle to its centroid
+cen = np.asarray(idx.clustering.centroids.values)
+U = m.users.values
+cosv = np.einsum('ij,ij->i', U, cen[a]) / (np.linalg.norm(U, axis=1) * np.linalg.norm(cen[a], axis=1) + 1e-300)
+t = 0
+for c in range(idx.num_clusters):
+    ids = np.flatnonzero(a == c)
+    ext = np.minimum(wu[ids], B)[np.argsort(-cosv[ids])]
+    for s in range(0, ext.size, 128):
+        t += int(np.ceil(ext[s:s + 128].max() / 128)) * 4
+print(f"  stage 1, units of 128 sorted by angle to the centroid: {t / full1:.2f}")
