@@ -395,6 +395,16 @@ SIMDEX_API int simdex_build_prefix_ordered(const uint16_t* ib, const double* i_n
                         const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c,
                         int64_t block, int64_t b_pad, uint16_t* out_prefix_b, double* out_prefix_norm,
                         int32_t* out_prefix_ids, double* out_tile_ceil, void* stream);
+/* The same with a hybrid order: each cluster's `head` prefix items with the
+ * best centroid scores first, then the rest of the prefix in list (ceiling)
+ * order, so that out_tile_ceil falls like the list's ceilings past the head
+ * and the early exit (SIMDEX_WS_PREFIX_EXIT) can end a warp inside the
+ * prefix (index.py:225-227).  head = 0: simdex_build_prefix_ordered. */
+SIMDEX_API int simdex_build_prefix_hybrid(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
+                        const double* items, int32_t f, const double* centers,
+                        const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c,
+                        int64_t block, int64_t b_pad, int64_t head, uint16_t* out_prefix_b, double* out_prefix_norm,
+                        int32_t* out_prefix_ids, double* out_tile_ceil, void* stream);
 
 /* ------------------------------------------------------------------------
  * Catalog sharding (no reference counterpart)

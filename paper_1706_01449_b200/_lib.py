@@ -59,6 +59,7 @@ SIGNATURES = {
     "simdex_query_ws_ctx": [P, P, P, P, P, I64, P, P, P, P, P, I64, I64, I32, I32, I32, P, I32, P, P, P, I32, I64, P,
                             P, P, P, I64, P, P, P, I64, I32, P, P, P, I32, P],
     "simdex_build_prefix_ordered": [P, P, I64, I32, P, I32, P, P, P, P, I32, I64, I64, P, P, P, P, P],
+    "simdex_build_prefix_hybrid": [P, P, I64, I32, P, I32, P, P, P, P, I32, I64, I64, I64, P, P, P, P, P],
     "simdex_fallback_rows": [P],
     "simdex_executed_pairs": [P],
     "simdex_ws_stats": [P],

@@ -243,6 +243,24 @@ def build_prefix_ordered(pi: Packed, items, centers, list_ids, list_pos, bounds,
     return out, onorm, b_pad, ids, tile_ceil
 
 
+def build_prefix_hybrid(pi: Packed, items, centers, list_ids, list_pos, bounds, block, head):
+    """build_prefix_ordered with the best ``head`` items (centroid score)
+    first and the rest of the prefix in list order (simdex_build_prefix_hybrid)."""
+    c, ni = list_ids.shape
+    f = items.shape[1]
+    bp = min(block, ni)
+    b_pad = 128 * ((bp + 127) // 128)
+    dev = list_ids.device
+    out = torch.empty((c, b_pad, pi.kp), dtype=torch.int16, device=dev)
+    onorm = torch.empty((c, b_pad), dtype=F64, device=dev)
+    ids = torch.empty((c, b_pad), dtype=I32, device=dev)
+    tile_ceil = torch.empty((c, b_pad // 128), dtype=F64, device=dev)
+    call("simdex_build_prefix_hybrid", ptr(pi.op), ptr(pi.norms), ni, pi.kp, ptr(_c(items, F64)), f,
+         ptr(_c(centers, F64)), ptr(_c(list_ids, I32)), ptr(_c(list_pos, I32)), ptr(_c(bounds, F64)), c, int(block),
+         b_pad, int(head), ptr(out), ptr(onorm), ptr(ids), ptr(tile_ceil), stream_ptr())
+    return out, onorm, b_pad, ids, tile_ceil
+
+
 def group_queries(q_user, assign, c):
     """(grouped user rows, original positions, cluster offsets [c+1])."""
     nq = q_user.shape[0]

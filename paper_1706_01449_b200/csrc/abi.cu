@@ -208,7 +208,7 @@ int launch_pack_f16_rows(const double*, int64_t, int32_t, int64_t, int32_t, uint
                          cudaStream_t);
 int launch_build_prefix_ordered(const uint16_t*, const double*, int64_t, int32_t, const double*, int32_t,
                                 const double*, const int32_t*, const int32_t*, const double*, int32_t, int64_t,
-                                int64_t, uint16_t*, double*, int32_t*, double*, cudaStream_t);
+                                int64_t, uint16_t*, double*, int32_t*, double*, cudaStream_t, int64_t);
 int launch_gather_prefix(const uint16_t*, const double*, int64_t, int32_t, const int32_t*, int32_t, int64_t,
                          int64_t, uint16_t*, double*, cudaStream_t);
 
@@ -411,7 +411,24 @@ extern "C" int simdex_build_prefix_ordered(const uint16_t* ib, const double* i_n
                    "simdex_build_prefix_ordered: bad sizes");
   return launch_build_prefix_ordered(ib, i_norm, ni, kp, items, f, centers, list_ids, list_pos, bounds, c, block,
                                      b_pad, out_prefix_b, out_prefix_norm, out_prefix_ids, out_tile_ceil,
-                                     as_stream(stream));
+                                     as_stream(stream), 0);
+}
+
+extern "C" int simdex_build_prefix_hybrid(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
+                                          const double* items, int32_t f, const double* centers,
+                                          const int32_t* list_ids, const int32_t* list_pos, const double* bounds,
+                                          int32_t c, int64_t block, int64_t b_pad, int64_t head,
+                                          uint16_t* out_prefix_b, double* out_prefix_norm, int32_t* out_prefix_ids,
+                                          double* out_tile_ceil, void* stream) {
+  SIMDEX_CHECK_ARG(ib && i_norm && items && centers && list_ids && list_pos && bounds && out_prefix_b &&
+                       out_prefix_norm && out_prefix_ids && out_tile_ceil,
+                   "simdex_build_prefix_hybrid: null pointer");
+  SIMDEX_CHECK_ARG(ni >= 1 && c >= 1 && block >= 1 && f >= 1 && head >= 0 && b_pad >= (block < ni ? block : ni) &&
+                       b_pad % 128 == 0 && kp % 64 == 0,
+                   "simdex_build_prefix_hybrid: bad sizes");
+  return launch_build_prefix_ordered(ib, i_norm, ni, kp, items, f, centers, list_ids, list_pos, bounds, c, block,
+                                     b_pad, out_prefix_b, out_prefix_norm, out_prefix_ids, out_tile_ceil,
+                                     as_stream(stream), head);
 }
 
 extern "C" int simdex_merge_topk(const int32_t* in_ids, const double* in_scores, int32_t parts, int64_t nu,

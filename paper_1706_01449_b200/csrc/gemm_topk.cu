@@ -125,6 +125,7 @@ struct TopkParams {
   int64_t* heap_ops;
   float* debug_out;
   int64_t debug_ld;
+  int first_all;  // EXM = 2: a unit's first chunk stored whole with vector stores (list-order prefix)
   // item operand in descending-norm order: a unit stops streaming once no row
   // can take another candidate (Cauchy-Schwarz against the remaining norms)
   int norm_sorted;
@@ -566,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) push_top<KTT>(top, v[i] - em);
                     T = fmaxf(T, KTT == kk + 1 ? top[KTT - 1] : top_at<KTT>(top, kk));
-                    if constexpr (EXM == 2) {
+                    if (EXM == 2 && p.first_all) {
                       // prefix units that end within a few tiles: plain vector
                       // stores of all 32 (finalize drops those below T)
                       float4* dh = reinterpret_cast<float4*>(my_hi);
@@ -2276,6 +2277,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
       p.norm_sorted = 1;
       p.exit_c = exit_c;
       p.exit_m = exit_m;
+      p.first_all = prefix_ids == nullptr;  // list-order prefix; a hybrid one keeps the threshold-filtered stores
       // a two-stage ring for the exit kernel: the tiles already in flight when
       // a unit ends are wasted work, and the epilogue (not the loads) sets the
       // pace (prefix pass at cfg4 K=10: 0.55 -> 0.46 ms, K=1: 0.36 -> 0.27 ms

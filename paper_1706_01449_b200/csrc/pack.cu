@@ -167,11 +167,52 @@ int launch_gather_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, i
 // meet their best items in the first chunks and their thresholds rise at
 // once (the stage-1 appends concentrate early in list order).  The prefix
 // top-K and visited do not depend on the order in which the prefix is scored.
+// Hybrid order: a cluster's `head` best prefix items by the centroid's score
+// first (the thresholds rise at once), then the rest of the prefix in list
+// (ceiling) order, so the per-tile suffix maxima of the ceilings fall like
+// the list's and the early exit can stop a warp inside the tail.  One CTA per
+// cluster: head items marked by list position, the tail compacted in list
+// order by a CTA scan.
+__global__ void __launch_bounds__(1024) prefix_hybrid_kernel(const int32_t* __restrict__ sorted, int64_t bp,
+                                                             int64_t head, const int32_t* __restrict__ list_ids,
+                                                             const int32_t* __restrict__ list_pos, int64_t ni,
+                                                             int32_t* __restrict__ out) {
+  extern __shared__ unsigned char flag[];  // [bp]
+  __shared__ int wsum[32];
+  const int64_t c = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int64_t p = t; p < bp; p += blockDim.x) flag[p] = 0;
+  __syncthreads();
+  for (int64_t i = t; i < head; i += blockDim.x) {
+    const int32_t id = sorted[c * bp + i];
+    flag[list_pos[c * ni + id]] = 1;
+    out[c * bp + i] = id;
+  }
+  __syncthreads();
+  // tail: list positions without a flag, in order (chunks of blockDim.x positions)
+  int64_t base = head;
+  for (int64_t p0 = 0; p0 < bp; p0 += blockDim.x) {
+    const int64_t p = p0 + t;
+    const int keep = (p < bp && !flag[p]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      if (q < w) before += wsum[q];
+      tot += wsum[q];
+    }
+    if (keep) out[c * bp + base + before + __popc(bal & ((1u << lane) - 1u))] = list_ids[c * ni + p];
+    base += tot;
+    __syncthreads();
+  }
+}
+
 int launch_build_prefix_ordered(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp,
                                 const double* items, int32_t f, const double* centers,
                                 const int32_t* list_ids, const int32_t* list_pos, const double* bounds, int32_t c,
                                 int64_t block, int64_t b_pad, uint16_t* out, double* onorm, int32_t* out_ids,
-                                double* out_tile_ceil, cudaStream_t s) {
+                                double* out_tile_ceil, cudaStream_t s, int64_t head) {
   const int64_t bp = block < ni ? block : ni;
   Scratch<double> keys;
   SIMDEX_CUDA(keys.alloc((size_t)c * bp, s));
@@ -182,6 +223,13 @@ int launch_build_prefix_ordered(const uint16_t* ib, const double* i_norm, int64_
                                                                              keys.p, tmp.p);
   SIMDEX_LAUNCH_CHECK("prefix_keys");
   SIMDEX_CUDA(segmented_sort_desc(keys.p, tmp.p, c, bp, s));
+  Scratch<int32_t> hyb;
+  if (head > 0 && head < bp && bp <= 48 * 1024) {
+    SIMDEX_CUDA(hyb.alloc((size_t)c * bp, s));
+    prefix_hybrid_kernel<<<(unsigned)c, 1024, (size_t)bp, s>>>(tmp.p, bp, head, list_ids, list_pos, ni, hyb.p);
+    SIMDEX_LAUNCH_CHECK("prefix_hybrid");
+    SIMDEX_CUDA(cudaMemcpyAsync(tmp.p, hyb.p, sizeof(int32_t) * (size_t)c * bp, cudaMemcpyDeviceToDevice, s));
+  }
   const size_t tsm = (size_t)(b_pad / 128) * sizeof(double);
   if (tsm > 48 * 1024) {
     set_error("simdex_build_prefix_ordered: prefix longer than %d tiles", 48 * 1024 / 8);

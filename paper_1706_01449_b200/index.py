@@ -313,18 +313,24 @@ class CentroidIndex:
     def device_assignment(self):
         return self.clustering.device_assignment()
 
-    def device_prefix(self, model: ModelPair, list_order: bool = False):
+    def device_prefix(self, model: ModelPair, list_order: bool = False, head: int = 0):
         """Per-cluster prefix operand of ``model.items`` (cached with a strong
         reference to that matrix, so a recycled id() can never alias it).
         Default: each cluster's first B' items in its centroid's score order
         (a cluster's users meet their best items first, so their thresholds
         rise at once: ~8 % off the prefix pass at cfg2 K = 10, 10 % at K = 50);
-        ``list_order``: the list (ceiling) order the prefix early exit needs."""
-        key = "prefix_list" if list_order else "prefix"
+        ``list_order``: the list (ceiling) order the prefix early exit needs,
+        after the ``head`` best items by centroid score (hybrid) when head > 0."""
+        head = head if list_order else 0
+        key = (("prefix_hybrid", head) if head else "prefix_list") if list_order else "prefix"
         ent = self._dev.get(key)
         if ent is None or ent[0] is not model.items:
             ids, bounds = self.device_lists()
-            if list_order:
+            if list_order and head:
+                built = _ops.build_prefix_hybrid(_device.packed(model.items), _device.f64(model.items),
+                                                 self.clustering.device_centroids(), ids, self.device_list_pos(),
+                                                 bounds, self.block_size, head)
+            elif list_order:
                 built = _ops.build_prefix(_device.packed(model.items), ids, self.block_size)
             else:
                 built = _ops.build_prefix_ordered(_device.packed(model.items), _device.f64(model.items),
@@ -490,7 +496,14 @@ def query_vector(index: CentroidIndex, model: ModelPair, vector, k: int) -> TopK
 # bookkeeping costs (tools/exit_ab.py, all-user serve: cfg4 K=10, mean walk
 # 47 of 4,096, 2.95 -> 2.10 ms; cfg2 K=5, walk 0.30 B', 0.97 -> 0.95 ms;
 # cfg2 K=10, walk 0.44 B', break-even; cfg2 K=50, walk B', +2 %).
-PREFIX_EXIT_FRACTION = 0.4
+# Round 2: between PREFIX_LIST_FRACTION and PREFIX_EXIT_FRACTION the prefix is
+# laid out "hybrid" -- its PREFIX_HEAD best items by centroid score first (the
+# thresholds rise at once), the rest in list order (the exit can end a warp
+# inside the prefix): cfg2 K=10 gemm 0.457 -> 0.402 ms, K=5 0.390 -> 0.300
+# (tools/ab_run_hybrid.sh); below PREFIX_LIST_FRACTION (cfg4: walks of 0.015
+# B') the pure list order stays faster (0.479 vs 0.584 ms).
+PREFIX_EXIT_FRACTION = 0.6
+PREFIX_LIST_FRACTION = 0.1
 
 
 def note_walk_estimate(index: CentroidIndex, k: int, mean_visited: float) -> None:
@@ -502,7 +515,9 @@ def prepare_serving(index: CentroidIndex, model: ModelPair, k: int) -> None:
     will use (the order follows the early-exit decision), so a timed serve
     does not build it."""
     if model.factors <= 256 and min(k, model.num_items) <= 256:
-        index.device_prefix(model, list_order=bool(_ws_options(index, k, model.num_items, True) & _ops.WS_PREFIX_EXIT))
+        opts = _ws_options(index, k, model.num_items, True)
+        index.device_prefix(model, list_order=bool(opts & _ops.WS_PREFIX_EXIT),
+                            head=_prefix_head(index, k, model.num_items))
         index.device_full_lists(model)
 
 
@@ -513,7 +528,17 @@ def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int
     return _ops.WS_PREFIX_EXIT if mv < PREFIX_EXIT_FRACTION * min(index.block_size, n) else 0
 
 
+def _prefix_head(index: CentroidIndex, k: int, n: int) -> int:
+    """Head of the hybrid prefix layout for the exit (0: pure list order)."""
+    mv = index._dev.get(("walk_estimate", int(k)))
+    if mv is None or mv < PREFIX_LIST_FRACTION * min(index.block_size, n):
+        return 0
+    return PREFIX_HEAD
+
+
 _QUERY_TOKENS = itertools.count(1)
+# the hybrid prefix's head (see PREFIX_EXIT_FRACTION)
+PREFIX_HEAD = int(os.environ.get("SIMDEX_PREFIX_HEAD", "256"))
 # largest per-cluster full-list operand built for the list-order catalogue pass
 FULL_LIST_BYTES = int(os.environ.get("SIMDEX_FULL_LIST_BYTES", str(4 << 30)))
 
@@ -576,8 +601,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
             grouped = _ops.group_queries(q_users, index.device_assignment(), index.num_clusters)
         block = index.block_size if work_sharing else 0
         options = _ws_options(index, k, n, work_sharing)
-        prefix = (index.device_prefix(model, list_order=bool(options & _ops.WS_PREFIX_EXIT)) if work_sharing
-                  else (None, None, 0))
+        prefix = (index.device_prefix(model, list_order=bool(options & _ops.WS_PREFIX_EXIT),
+                                      head=_prefix_head(index, k, n)) if work_sharing else (None, None, 0))
         if qs is not None:
             ctx = qs.context(ctx)
         if work_sharing and block < n:
@@ -707,6 +732,8 @@ def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> Centroi
         out._dev.pop("pos", None)
         out._dev.pop("prefix", None)
         out._dev.pop("prefix_list", None)
+        for key in [key for key in out._dev if isinstance(key, tuple) and key[0] == "prefix_hybrid"]:
+            out._dev.pop(key)
         out._dev.pop("full_lists", None)
     return out
 
