@@ -497,7 +497,7 @@ def query_vector(index: CentroidIndex, model: ModelPair, vector, k: int) -> TopK
 # 47 of 4,096, 2.95 -> 2.10 ms; cfg2 K=5, walk 0.30 B', 0.97 -> 0.95 ms;
 # cfg2 K=10, walk 0.44 B', break-even; cfg2 K=50, walk B', +2 %).
 # Round 2: between PREFIX_LIST_FRACTION and PREFIX_EXIT_FRACTION the prefix is
-# laid out "hybrid" -- its PREFIX_HEAD best items by centroid score first (the
+# laid out "hybrid" -- its PREFIX_HEAD (128) best items by centroid score first (the
 # thresholds rise at once), the rest in list order (the exit can end a warp
 # inside the prefix): cfg2 K=10 gemm 0.457 -> 0.402 ms, K=5 0.390 -> 0.300
 # (tools/ab_run_hybrid.sh); below PREFIX_LIST_FRACTION (cfg4: walks of 0.015
@@ -538,7 +538,7 @@ def _prefix_head(index: CentroidIndex, k: int, n: int) -> int:
 
 _QUERY_TOKENS = itertools.count(1)
 # the hybrid prefix's head (see PREFIX_EXIT_FRACTION)
-PREFIX_HEAD = int(os.environ.get("SIMDEX_PREFIX_HEAD", "256"))
+PREFIX_HEAD = int(os.environ.get("SIMDEX_PREFIX_HEAD", "128"))
 # largest per-cluster full-list operand built for the list-order catalogue pass
 FULL_LIST_BYTES = int(os.environ.get("SIMDEX_FULL_LIST_BYTES", str(4 << 30)))
 
