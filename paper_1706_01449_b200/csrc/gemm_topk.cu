@@ -2277,7 +2277,8 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
       p.norm_sorted = 1;
       p.exit_c = exit_c;
       p.exit_m = exit_m;
-      p.first_all = prefix_ids == nullptr;  // list-order prefix; a hybrid one keeps the threshold-filtered stores
+      p.first_all = prefix_ids == nullptr && !getenv("SIMDEX_FIRST_FILTERED");  // list-order prefix; a hybrid one
+                                                                               // keeps the threshold-filtered stores
       // a two-stage ring for the exit kernel: the tiles already in flight when
       // a unit ends are wasted work, and the epilogue (not the loads) sets the
       // pace (prefix pass at cfg4 K=10: 0.55 -> 0.46 ms, K=1: 0.36 -> 0.27 ms
