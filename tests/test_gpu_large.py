@@ -186,3 +186,34 @@ def test_heavy_tailed_user_norms_stay_exact(sx, path):
     sample = np.sort(rng.choice(nu, 1500, replace=False))
     _check(res.item_ids, res.scores, users, items, k, sample, f"heavy-tailed norms {path}")
     assert fb <= nu // 1000
+
+
+@pytest.mark.parametrize("k,mode", [(10, "hybrid"), (16, "hybrid"), (10, "list"), (12, "none"), (50, "hybrid")])
+def test_work_sharing_prefix_layouts_and_list_catalogue_pass(sx, k, mode):
+    """The prefix layouts of the work-sharing pass (centroid order without an
+    exit, hybrid head + list order with the exit, list order with the exit)
+    and the list-order catalogue pass (query sets of 50k+ users, K >= 8) give
+    the exact top-K of every user, and visited = max(B', the walk's visited)
+    (index.py:372-387) against the walk kernel without work sharing."""
+    from paper_1706_01449_b200 import index as I
+    rng = np.random.default_rng(7 + k)
+    nu, ni, f, c = 64000, 6000, 32, 48
+    centers = rng.normal(size=(c, f))
+    users = centers[rng.integers(0, c, nu)] + rng.normal(0, 0.4, (nu, f))
+    d = rng.normal(size=(ni, f))
+    items = d / np.linalg.norm(d, axis=1, keepdims=True) * rng.lognormal(0, 0.5, (ni, 1))
+    users, items = users.astype(np.float32).astype(np.float64), items.astype(np.float32).astype(np.float64)
+    m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    block = 1024
+    idx = sx.build_index(m, sx.kmeans(m.users, c, max_iters=3, seed=2), block)
+    est = {"hybrid": 0.3, "list": 0.05, "none": 0.9}[mode] * block
+    I.note_walk_estimate(idx, k, est)
+    assert bool(I._ws_options(idx, k, ni, True)) == (mode != "none")
+    if mode != "none":
+        assert (I._prefix_head(idx, k, ni) > 0) == (mode == "hybrid")
+    ids, sc, vis = (t.cpu().numpy() for t in I.query_batch_tensors(idx, m, None, k, work_sharing=True))
+    sample = rng.choice(nu, 800, replace=False)
+    _check(ids, sc, users, items, k, sample, f"{mode} K={k}")
+    ids0, sc0, vis0 = (t.cpu().numpy() for t in I.query_batch_tensors(idx, m, None, k, work_sharing=False))
+    np.testing.assert_array_equal(vis, np.maximum(min(block, ni), vis0))
+    np.testing.assert_array_equal(ids, ids0)
