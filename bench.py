@@ -172,6 +172,17 @@ def _import_reference():
     return mipserve
 
 
+def _import_oracle():
+    """The oracle port (oracle/simdex_oracle.py): the stand-in CPU arm when
+    baseline/_ref is not installed (bench.py's cpu_baseline / reference arm are
+    the only non-test callers of oracle/)."""
+    opath = os.path.join(ROOT, "oracle")
+    if opath not in sys.path:
+        sys.path.insert(0, opath)
+    import simdex_oracle
+    return simdex_oracle
+
+
 def _ref_worker(args):
     """One worker's share of a step (reference state inherited through fork)."""
     sample, k = args
@@ -179,7 +190,13 @@ def _ref_worker(args):
     M = _REF["M"]
     with threadpool_limits(1):
         t0 = time.perf_counter()
-        if _REF["index"] is not None:
+        if _REF.get("port"):
+            users, items = _REF["model"]
+            if _REF["index"] is not None:
+                M.query_batch(_REF["index"], items, users, sample.tolist(), k, 4096)
+            else:
+                M.topk_matmul(users[sample], items, k)
+        elif _REF["index"] is not None:
             M.query_batch(_REF["index"], _REF["model"], sample.tolist(), k)
         else:
             sub = M.ModelPair(M.FactorMatrix(_REF["model"].users.values[sample]), _REF["model"].items)
@@ -191,7 +208,23 @@ def reference_setup(w, clustering=None):
     """mipserve model (+ index for the index path).  ``clustering`` = (centroids,
     assignment) to build the reference index from (its own build_index); None
     runs the reference's own kmeans."""
-    M = _import_reference()
+    try:
+        M = _import_reference()
+    except Exception:  # noqa: BLE001 -- baseline/_ref absent: the oracle port stands in
+        O = _import_oracle()
+        users, items = w.users.astype(np.float64), w.items.astype(np.float64)
+        idx = None
+        if w.expected_path == "index":
+            if clustering is None:
+                cl = O.kmeans(users, w.clusters, max_iters=w.max_iters, seed=w.seed)
+                cen, assign, theta = cl["centroids"], cl["assignment"], cl["max_angle"]
+            else:
+                cen, assign = clustering
+                theta = O.compute_max_angles(users, cen, assign)
+            ids, bnd, _ = O.build_index(items, cen, theta)
+            idx = (ids, bnd, assign)
+        _REF.update(M=O, model=(users, items), index=idx, port=True)
+        return (users, items), idx
     model = M.ModelPair(M.FactorMatrix(w.users.astype(np.float64)), M.FactorMatrix(w.items.astype(np.float64)))
     idx = None
     if w.expected_path == "index":
@@ -204,7 +237,7 @@ def reference_setup(w, clustering=None):
             cl = M.Clustering(M.FactorMatrix(cen), assign, theta,
                               tuple(np.flatnonzero(assign == j) for j in range(c)), np.empty(0), w.seed)
         idx = M.build_index(model, cl, 4096)
-    _REF.update(M=M, model=model, index=idx)
+    _REF.update(M=M, model=model, index=idx, port=False)
     return model, idx
 
 
@@ -235,9 +268,10 @@ def run_reference(args):
     k = args.k or w.k
     try:
         M = _import_reference()
-    except Exception as e:  # noqa: BLE001
-        print(json.dumps({"impl": "reference", "unavailable": f"mipserve not importable from baseline/_ref: {e}"}))
-        return
+        kind = "reference"
+    except Exception:  # noqa: BLE001 -- the oracle port always exists
+        M = None
+        kind = "port"
     cores = len(os.sched_getaffinity(0))
     path = workload_path(w)
     t0 = time.perf_counter()
@@ -250,8 +284,10 @@ def run_reference(args):
     v = users / wall
     nu, ni, f = w.users.shape[0], w.items.shape[0], w.users.shape[1]
     what = "query_batch work_sharing=True (B=4096)" if w.expected_path == "index" else "topk_matmul"
-    sample = (f"mipserve {getattr(M, '__version__', '?')} (baseline/_ref, unmodified) {what} on {per} random "
-              f"users per process per step, {cores} processes x 1 BLAS thread; setup (reference kmeans + "
+    who = (f"mipserve {getattr(M, '__version__', '?')} (baseline/_ref, unmodified)" if kind == "reference"
+           else "oracle port (oracle/simdex_oracle.py; baseline/_ref not installed)")
+    sample = (f"{who} {what} on {per} random "
+              f"users per process per step, {cores} processes x 1 BLAS thread; setup (kmeans + "
               f"build_index) {setup_s:.1f} s, untimed")
     line = {
         "impl": "reference", "metric": f"exact top-K users/sec (f={f}, K={k})", "value": v, "unit": "users/s",
@@ -262,7 +298,7 @@ def run_reference(args):
         "config": {"workload": f"{w.name}: {nu}x{ni}x{f}, K={k}" + (f", C={w.clusters}, B=4096"
                                                                      if w.expected_path == "index" else ""),
                    "path": path},
-        "cpu_baseline": {"value": v, "unit": "users/s", "cores": cores, "kind": "reference", "sample": sample,
+        "cpu_baseline": {"value": v, "unit": "users/s", "cores": cores, "kind": kind, "sample": sample,
                          "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "users/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -283,9 +319,11 @@ def cpu_baseline_ours(w, k, cl_host):
     users = sum(n for n, _ in steps)
     wall = sum(t for _, t in steps)
     what = "query_batch work_sharing=True (B=4096)" if idx is not None else "topk_matmul"
-    return {"value": users / wall, "unit": "users/s", "cores": 1, "kind": "reference",
-            "sample": f"mipserve {what} on {per} random users, 1 process x 1 BLAS thread, {wall:.1f} s"
-                      + ("; index by mipserve.build_index from the GPU clustering" if idx is not None else ""),
+    port = bool(_REF.get("port"))
+    return {"value": users / wall, "unit": "users/s", "cores": 1, "kind": "port" if port else "reference",
+            "sample": f"{'oracle port' if port else 'mipserve'} {what} on {per} random users, 1 process x 1 BLAS "
+                      f"thread, {wall:.1f} s"
+                      + ("; index by its build_index from the GPU clustering" if idx is not None else ""),
             "cpu_model": cpu_model()}
 
 
