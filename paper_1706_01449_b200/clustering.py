@@ -194,11 +194,13 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
     if max_iters < 1:
         raise ValueError("max_iters must be >= 1")
     pts = _device.f64(users)
-    p32 = _device.f32_exact(users)  # exact float32 copy (half the bytes) or None
     dev = pts.device
     rng = np.random.default_rng(seed)
     first = int(rng.integers(0, n))
     unif = _device.to_device(rng.random(num_clusters - 1)) if num_clusters > 1 else None
+    # (the draws are uploaded before f32_exact's flag read-back: the seeding
+    # launch then follows that synchronisation at once)
+    p32 = _device.f32_exact(users)  # exact float32 copy (half the bytes) or None
     rows, centers, deg = _ops.kmeans_seed(pts, num_clusters, first, unif, points32=p32)
     deg_pass = int(deg.item())
     if deg_pass >= 0:
@@ -297,6 +299,8 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
         cen_h, theta_h, off_h = (a.copy() for a in _device.to_host_pinned_many(centers, theta, offsets))
     for a in (theta_h, objective):
         a.setflags(write=False)
-    out = _DeviceClustering(FactorMatrix(cen_h), theta_h, objective, seed, assign.contiguous(), members, off_h)
+    cen_fm = FactorMatrix(cen_h)
+    _device._cache(cen_fm)["f64"] = centers  # resident already: build_index reads it without an upload
+    out = _DeviceClustering(cen_fm, theta_h, objective, seed, assign.contiguous(), members, off_h)
     out._dev()["theta"] = theta
     return out

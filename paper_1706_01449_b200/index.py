@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import weakref
 
 import math
 import os
@@ -400,12 +401,11 @@ def build_index(model: ModelPair, clustering: Clustering, block_size: int = DEFA
         raise ValueError("block_size must be >= 1")
     norms, ids, bounds = _device_build(model, clustering.device_centroids(), clustering.device_max_angle())
     index = CentroidIndex(None, None, None, block_size, clustering, _dev={"ids": ids, "bounds": bounds, "norms": norms})
-    # the serving layout is part of the build (not of the first query): the
-    # inverse list positions (visited in closed form) and, when the tensor-core
-    # path will serve this index, every cluster's prefix operand
+    # the inverse list positions (visited in closed form) are part of the
+    # build; the prefix operand is built by prepare_serving / the first
+    # work-sharing query, in the layout the walk estimate selects (building the
+    # default layout here cost run_pipeline 0.5 ms for an operand it replaced)
     index.device_list_pos()
-    if model.factors <= 256:
-        index.device_prefix(model)
     return index
 
 
@@ -518,7 +518,6 @@ def prepare_serving(index: CentroidIndex, model: ModelPair, k: int) -> None:
         opts = _ws_options(index, k, model.num_items, True)
         index.device_prefix(model, list_order=bool(opts & _ops.WS_PREFIX_EXIT),
                             head=_prefix_head(index, k, model.num_items))
-        index.device_full_lists(model)
 
 
 def _ws_options(index: CentroidIndex, k: int, n: int, work_sharing: bool) -> int:
@@ -534,6 +533,26 @@ def _prefix_head(index: CentroidIndex, k: int, n: int) -> int:
     if mv is None or mv < PREFIX_LIST_FRACTION * min(index.block_size, n):
         return 0
     return PREFIX_HEAD
+
+
+# the list-order catalogue pass (csrc/gemm_topk.cu: SIMDEX_LIST_MIN_K,
+# SIMDEX_LIST_MIN_Q) serves query sets of 50k users or more from K = 8 on; its
+# per-cluster full-list operand (0.8 ms, 583 MB at cfg2) is built once an
+# index has served FULL_LISTS_AFTER such batches -- a one-shot run_pipeline
+# saves 0.11 ms per serve with it and would pay 0.8 ms to build it
+LIST_MIN_K, LIST_MIN_Q = 8, 50000
+FULL_LISTS_AFTER = int(os.environ.get("SIMDEX_FULL_LISTS_AFTER", "1"))
+
+
+def _full_lists_for(index: CentroidIndex, model: ModelPair, k: int, nq: int):
+    ent = index._dev.get("full_lists")
+    if ent is not None and ent[0] is model.items:
+        return ent[1]
+    if min(k, model.num_items) < LIST_MIN_K or nq < LIST_MIN_Q:
+        return None
+    served = index._dev.get("list_pass_serves", 0)
+    index._dev["list_pass_serves"] = served + 1
+    return index.device_full_lists(model) if served >= FULL_LISTS_AFTER else None
 
 
 _QUERY_TOKENS = itertools.count(1)
@@ -553,7 +572,10 @@ class QuerySet:
     by the all-users serve and the multi-GPU shards."""
 
     def __init__(self, index: CentroidIndex, user_ids, q=None):
-        self.index = index
+        # weak: the index caches its all-users set, and a reference cycle would
+        # keep a dropped index's device tensors (lists, operands) alive until
+        # the cyclic collector runs -- every rebuild would then cudaMalloc anew
+        self._index = weakref.ref(index)
         if q is None:
             ids = np.asarray(user_ids, dtype=np.int64)
             self.user_ids = ids
@@ -563,6 +585,10 @@ class QuerySet:
             self.q = q
         self.grouped = _ops.group_queries(self.q, index.device_assignment(), index.num_clusters)
         self.token = next(_QUERY_TOKENS)
+
+    @property
+    def index(self):
+        return self._index()
 
     def context(self, ctx=None):
         """Tag the context the next serve runs on (``ctx``, or None for the
@@ -606,7 +632,7 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
         if qs is not None:
             ctx = qs.context(ctx)
         if work_sharing and block < n:
-            fl = index.device_full_lists(model)
+            fl = _full_lists_for(index, model, k, int(q_users.shape[0]))
             if fl is not None:
                 _lib.call("simdex_ctx_set_full_lists", ctx, _lib.ptr(fl[0]), _lib.ptr(fl[1]), fl[2])
         return _ops.query_ws(users, pu, items, pi, ids, index.device_list_pos(), bounds, block, prefix, grouped, k,

@@ -211,6 +211,7 @@ def test_work_sharing_prefix_layouts_and_list_catalogue_pass(sx, k, mode):
     assert bool(I._ws_options(idx, k, ni, True)) == (mode != "none")
     if mode != "none":
         assert (I._prefix_head(idx, k, ni) > 0) == (mode == "hybrid")
+    assert idx.device_full_lists(m) is not None  # (a serving index builds it after its first large batch)
     ids, sc, vis = (t.cpu().numpy() for t in I.query_batch_tensors(idx, m, None, k, work_sharing=True))
     sample = rng.choice(nu, 800, replace=False)
     _check(ids, sc, users, items, k, sample, f"{mode} K={k}")

@@ -12,7 +12,7 @@ from torch.profiler import ProfilerActivity, profile
 import paper_1706_01449_b200 as sx
 from paper_1706_01449_b200 import workloads as W
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "cfg2"
 w = W.CONFIGS[cfg]()
 model = sx.ModelPair(sx.FactorMatrix(w.users), sx.FactorMatrix(w.items))
 dev = torch.device("cuda", 0)
@@ -61,3 +61,8 @@ gaps.sort(reverse=True)
 print("idle total %.2f ms; largest gaps:" % (sum(g[0] for g in gaps) / 1e3))
 for g, a, b, at in gaps[:25]:
     print(f"  {g / 1e3:7.3f} ms at {at / 1e3:7.2f} ms  after {a}  before {b}")
+if "--seq" in sys.argv:
+    print("timeline (start ms, dur ms, name):")
+    t00 = ev[0].time_range.start
+    for e in ev:
+        print(f"  {(e.time_range.start - t00) / 1e3:8.3f} {(e.time_range.end - e.time_range.start) / 1e3:7.3f}  {e.name[:90]}")
