@@ -79,6 +79,14 @@ using namespace sm100;
 #ifndef SIMDEX_M_TILES
 #define SIMDEX_M_TILES 1
 #endif
+// finalize: two survivors per lane in one rescoring pass; resident CTAs per SM
+// the register allocation is held to
+#ifndef SIMDEX_FIN_TWO
+#define SIMDEX_FIN_TWO 1
+#endif
+#ifndef SIMDEX_FIN_MINB
+#define SIMDEX_FIN_MINB 5
+#endif
 // 128-row M tiles per unit and CTAs per SM: one M tile per CTA with two CTAs
 // per SM (each CTA: 2 accumulator buffers x 128 columns of TMEM, 4 epilogue
 // warps), so one CTA's slow epilogue warp never gates the other's hand-off
@@ -964,7 +972,7 @@ namespace {
 // work-sharing bookkeeping of the mode.
 // LPR lanes per row: 8 (4 rows per warp) for small k, 32 for k > 32
 template <int LPR>
-__global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
+__global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const FinalizeParams p) {
   constexpr int RPW = 32 / LPR;
   extern __shared__ unsigned char smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -974,9 +982,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) * RPW + slot;
   const size_t per_row = ((size_t)p.pow2 * 12 + (size_t)p.f * 8 + 15) & ~size_t(15);
   unsigned char* mine = smem + slot * per_row;
-  double* us = reinterpret_cast<double*>(mine);
-  double* ss = us + p.f;
-  int32_t* si = reinterpret_cast<int32_t*>(ss + p.pow2);
+  // scores first (16-byte aligned rows: the rank loop and the rescoring read
+  // pairs of doubles with one shared-memory load), then the user row, the ids
+  double* ss = reinterpret_cast<double*>(mine);
+  double* us = ss + p.pow2;
+  int32_t* si = reinterpret_cast<int32_t*>(us + p.f);
   const int64_t total = p.n_rows_dev ? (int64_t)*p.n_rows_dev : p.total_rows;
   int64_t user = -1, out = -1;
   int c = 0, cnt = 0;
@@ -999,8 +1009,18 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
   if (__all_sync(0xffffffffu, !act)) return;
   int np2 = 2;
   while (np2 < cmax) np2 <<= 1;
-  if (act)
-    for (int i = gl; i < p.f; i += LPR) us[i] = p.users32 ? (double)p.users32[user * p.f + i] : p.users[user * p.f + i];
+  if (act) {
+    if (p.users32 && (p.f & 1) == 0) {  // two factors per load (rows of an even f are 8-byte aligned)
+      const float2* u2 = reinterpret_cast<const float2*>(p.users32 + user * p.f);
+      for (int i = gl; i < p.f / 2; i += LPR) {
+        const float2 v = u2[i];
+        *reinterpret_cast<double2*>(us + 2 * i) = make_double2((double)v.x, (double)v.y);
+      }
+    } else {
+      for (int i = gl; i < p.f; i += LPR)
+        us[i] = p.users32 ? (double)p.users32[user * p.f + i] : p.users[user * p.f + i];
+    }
+  }
   const int32_t* cid = p.cand_id + r * p.cap;
   const float* chi = p.cand_hi + r * p.cap;
   // keep the candidates whose upper bound reaches the row's final threshold
@@ -1147,7 +1167,32 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     part += __shfl_xor_sync(0xffffffffu, part, 1);
     if (act && sl == 0 && e < cnt) ss[e] = part;
   }
-  for (int e = gl; e < (lane_per_cand ? cmax2 : 0); e += LPR) {
+  // up to two survivors per lane (the common case at K = 10: 9..16 per row):
+  // one pass, the two candidates of a lane sharing the user-row loads; each
+  // candidate's arithmetic is that of the single-candidate loop below
+  const bool two_per_lane = SIMDEX_FIN_TWO && lane_per_cand && cmax2 > LPR && cmax2 <= 2 * LPR && p.items32 && (p.f & 1) == 0;
+  if (two_per_lane) {
+    const int e0 = gl, e1 = gl + LPR;
+    if (act && e0 < cnt) {
+      const bool has1 = e1 < cnt;
+      const float2* xa = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[e0] * p.f);
+      const float2* xb = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[has1 ? e1 : e0] * p.f);
+      const double2* u2 = reinterpret_cast<const double2*>(us);
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll 5
+      for (int q = 0; q < p.f / 2; ++q) {
+        const float2 va = xa[q], vb = xb[q];
+        const double2 u = u2[q];
+        a0 = fma((double)va.x, u.x, a0);
+        a1 = fma((double)va.y, u.y, a1);
+        b0 = fma((double)vb.x, u.x, b0);
+        b1 = fma((double)vb.y, u.y, b1);
+      }
+      ss[e0] = a0 + a1;
+      if (has1) ss[e1] = b0 + b1;
+    }
+  }
+  for (int e = gl; e < (lane_per_cand && !two_per_lane ? cmax2 : 0); e += LPR) {
     if (act && e < cnt) {
       double d0 = 0.0, d1 = 0.0;
       const int64_t id = si[e];
@@ -1181,8 +1226,16 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
       if (act && e < cnt) {
         const double se = ss[e];
         const int32_t ie = si[e];
+        // over the warp-uniform padded count: slots [cnt, np2) hold
+        // (-DBL_MAX, INT32_MAX), which ranks before no candidate
         int rank = 0;
-        for (int o = 0; o < cnt; ++o) rank += ranks_before(ss[o], si[o], se, ie) ? 1 : 0;
+#pragma unroll 2
+        for (int o = 0; o < np2; o += 2) {
+          const double2 s2 = *reinterpret_cast<const double2*>(ss + o);
+          const int2 i2 = *reinterpret_cast<const int2*>(si + o);
+          rank += ranks_before(s2.x, i2.x, se, ie) ? 1 : 0;
+          rank += ranks_before(s2.y, i2.y, se, ie) ? 1 : 0;
+        }
         if (rank < p.k_eff) {
           p.out_ids[out * p.k_eff + rank] = ie;
           p.out_scores[out * p.k_eff + rank] = se;
