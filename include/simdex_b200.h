@@ -76,7 +76,7 @@ SIMDEX_API int simdex_profile_reset(void);
  * reference (brute.py:86-107, index.py:351-389) with one resident arena. */
 SIMDEX_API int simdex_ctx_create(int device, void** out_ctx);
 SIMDEX_API int simdex_ctx_destroy(void* ctx);
-/* Declare that the next simdex_query_ws_ctx call on `ctx` (NULL: this thread's
+/* Declare that the next simdex_query_ws_ctx (or simdex_kmeans_assign) call on `ctx` (NULL: this thread's
  * default context) serves the query set identified by `token` (nonzero,
  * unique for the lifetime of that query set and of the operands it is served
  * with; 0 = none); the call consumes the token.  A call that finds its setup
@@ -197,7 +197,12 @@ SIMDEX_API int simdex_kmeans_seed(const double* points, const float* points32, i
  * center as ||p||^2 + ||c||^2 - 2 p.c clipped at 0, first minimum wins.
  * prev_assign (nullable) is compared to count changed rows.
  * out_assign int64[n], out_d2 float64[n] (distance to the assigned center),
- * out_changed int64[1], out_objective float64[1] = sum(out_d2). */
+ * out_changed int64[1], out_objective float64[1] = sum(out_d2).
+ * Runs on the thread's default context; a token set with
+ * simdex_ctx_set_query_token(NULL, t) (t unique to one run over the same,
+ * unchanged points, e.g. the Lloyd loop of clustering.py:160-190) lets
+ * consecutive calls reuse the point side of the product (squared norms,
+ * packed operand, bands) while nothing else has used that context. */
 SIMDEX_API int simdex_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f,
                          const double* centers, int32_t c,
                          const int64_t* prev_assign, int64_t* out_assign, double* out_d2,

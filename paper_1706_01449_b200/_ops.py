@@ -7,6 +7,7 @@ stream.  Nothing here computes on the host.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 from dataclasses import dataclass
 
@@ -135,20 +136,25 @@ def to_f32(x):
 def kmeans_seed(points, k, first, uniforms, points32=None):
     n, f = points.shape
     rows = torch.empty(k, dtype=I64, device=points.device)
-    centers = torch.empty((k, f), dtype=F64, device=points.device)
+    centers = torch.zeros((k, f), dtype=F64, device=points.device)  # (defined rows even when the seeding stops early)
     deg = torch.empty(1, dtype=I32, device=points.device)
     call("simdex_kmeans_seed", ptr(_c(points, F64)), ptr(points32), n, f, k, int(first),
          ptr(None if uniforms is None else _c(uniforms, F64)), ptr(rows), ptr(centers), ptr(deg), stream_ptr())
     return rows, centers, deg
 
 
-def kmeans_assign(points, centers, prev=None, points32=None):
+def kmeans_assign(points, centers, prev=None, points32=None, token=0):
+    """``token`` != 0 (unique to one run over fixed points, e.g. a Lloyd loop):
+    tags the thread's default context so that consecutive assignments reuse
+    the point side of the product (simdex_ctx_set_query_token)."""
     n, f = points.shape
     c = centers.shape[0]
     assign = torch.empty(n, dtype=I64, device=points.device)
     d2 = torch.empty(n, dtype=F64, device=points.device)
     changed = torch.empty(1, dtype=I64, device=points.device)
     obj = torch.empty(1, dtype=F64, device=points.device)
+    if token:
+        call("simdex_ctx_set_query_token", None, C.c_int64(token))
     call("simdex_kmeans_assign", ptr(_c(points, F64)), ptr(points32), n, f, ptr(_c(centers, F64)), c,
          ptr(None if prev is None else _c(prev, I64)), ptr(assign), ptr(d2), ptr(changed), ptr(obj), stream_ptr())
     return assign, d2, changed, obj

@@ -11,6 +11,7 @@ convergence test and the empty-cluster check.
 
 from __future__ import annotations
 
+import itertools
 import math
 from dataclasses import dataclass
 
@@ -27,6 +28,9 @@ _LLOYD_BATCH = 3  # Lloyd iterations queued per host read (see kmeans)
 # Angle used when a vector has zero norm; the most conservative choice
 # (clustering.py:21-23).
 DEGENERATE_ANGLE = math.pi
+
+
+_RUN_TOKENS = itertools.count(1)
 
 
 @dataclass(frozen=True, eq=False)
@@ -183,6 +187,16 @@ def _repair_empty_host(points_h, centers_h, assign_h, d2_h):
     return changed
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(dev) -> "torch.cuda.Stream":
+    s = _SIDE_STREAMS.get(dev.index)
+    if s is None:
+        s = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
 def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_iters: int = DEFAULT_MAX_ITERS,
            seed: int = 0) -> Clustering:
     """Lloyd iterations with k-means++ seeding, stopping on a stable
@@ -202,11 +216,19 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
     # launch then follows that synchronisation at once)
     p32 = _device.f32_exact(users)  # exact float32 copy (half the bytes) or None
     rows, centers, deg = _ops.kmeans_seed(pts, num_clusters, first, unif, points32=p32)
-    deg_pass = int(deg.item())
-    if deg_pass >= 0:
-        rows_h = _device.to_host(rows).copy()
-        rows_h = _finish_seeds_on_degenerate(users.values, rows_h, deg_pass)
-        centers = torch.as_tensor(users.values[rows_h], device=dev).contiguous()
+    # the degenerate-seeding flag is read through a side stream while the first
+    # assignment (queued at once, speculatively) runs: the host wait ends when
+    # the seeding does, and the GPU does not idle while the loop is queued
+    seeded = torch.cuda.Event()
+    seeded.record()
+    side = _side_stream(dev)
+    deg_h = torch.empty(1, dtype=deg.dtype, pin_memory=True)
+    with torch.cuda.stream(side):
+        side.wait_event(seeded)
+        deg_h.copy_(deg, non_blocking=True)
+        deg_read = torch.cuda.Event()
+        deg_read.record()
+    deg.record_stream(side)
 
     def repair(assign_t, d2_t, counts_t):
         if not (_device.to_host(counts_t) == 0).any():
@@ -218,12 +240,20 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
         centers.copy_(torch.as_tensor(c_h, device=dev))
         return torch.as_tensor(a_h, device=dev), True
 
-    assign, d2, _, obj = _ops.kmeans_assign(pts, centers, points32=p32)
+    tok = -next(_RUN_TOKENS)  # this run's assignments share the point side of the product (negative: not a query set's)
+    assign, d2, _, obj = _ops.kmeans_assign(pts, centers, points32=p32, token=tok)
+    deg_read.synchronize()
+    deg_pass = int(deg_h.item())
+    if deg_pass >= 0:  # fewer distinct points than seeds: finish on the host, redo the first assignment
+        rows_h = _device.to_host(rows).copy()
+        rows_h = _finish_seeds_on_degenerate(users.values, rows_h, deg_pass)
+        centers = torch.as_tensor(users.values[rows_h], device=dev).contiguous()
+        assign, d2, _, obj = _ops.kmeans_assign(pts, centers, points32=p32, token=tok)
     objs = [obj]  # read back once at the end (no per-iteration sync for the history)
 
     def lloyd_step(a_cur):
         counts, _, _ = _ops.kmeans_update(pts, a_cur, centers, points32=p32)
-        new_assign, d_new, changed, ob = _ops.kmeans_assign(pts, centers, prev=a_cur, points32=p32)
+        new_assign, d_new, changed, ob = _ops.kmeans_assign(pts, centers, prev=a_cur, points32=p32, token=tok)
         flag = torch.stack([(counts == 0).any().to(torch.int64), changed.view(())])
         return counts, new_assign, d_new, flag, ob
 
@@ -258,7 +288,7 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
                 empty, n_changed = flag.tolist()
                 if empty:
                     assign, _ = repair(assign, d2_before, counts)
-                    new_assign, d2, changed, ob = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
+                    new_assign, d2, changed, ob = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32, token=tok)
                     n_changed = int(changed.item())
                 objs.append(ob)
                 it += 1
@@ -270,7 +300,7 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
         if batch == 1 and flags[0][0]:  # a single iteration emptied a cluster: repair, redo the assignment
             a_prev, counts = steps[0][0], steps[0][1]
             assign, _ = repair(a_prev, d2, counts)
-            new_assign, d2, changed, ob = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32)
+            new_assign, d2, changed, ob = _ops.kmeans_assign(pts, centers, prev=assign, points32=p32, token=tok)
             objs.append(ob)
             it += 1
             if int(changed.item()) == 0:

@@ -110,6 +110,8 @@ struct CtxSetup {
   int64_t bf_pad = 0;
 };
 CtxSetup* ctx_setup(Ctx* c);
+// fills out[0..n) with the squared norms of the n points (k-means assignment)
+using P2Fill = int (*)(const void* points, int64_t n, int f, double* out, cudaStream_t s);
 uint64_t ctx_arena_gen(Ctx* c);
 
 // Typed buffers carved out of the context arena for ONE call: add() every

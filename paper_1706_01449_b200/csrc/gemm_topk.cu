@@ -2639,9 +2639,9 @@ __global__ void __launch_bounds__(256) assign_finalize_kernel(const FinalizePara
 // *n_over) for the float64 SIMT kernel.  Needs f + 1 <= 256.
 template <class P>
 int gemm_assign_impl(const double* points, const P* px, const float* points32, int64_t n, int32_t f,
-                     const double* p2, const double* centers, const double* c2, int32_t c, const int64_t* prev,
-                     int64_t* out_assign, double* out_d2, unsigned long long* changed, int64_t* over_rows,
-                     int32_t* n_over, cudaStream_t s) {
+                     P2Fill fill_p2, const double** p2_out, const double* centers, const double* c2, int32_t c,
+                     const int64_t* prev, int64_t* out_assign, double* out_d2, unsigned long long* changed,
+                     int64_t* over_rows, int32_t* n_over, cudaStream_t s) {
   const int kp = ((f + 1 + 63) / 64) * 64;
   GemmGeometry g;
   int rc = geometry(kp, &g);
@@ -2649,13 +2649,28 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   const int64_t nu_pad = ceil_div(n, 256) * 256, nc_pad = ceil_div(c, 256) * 256;
   const int64_t nunits = nu_pad / kUnitRows;
   const int k_eff = 1;
-  Workspace ws(ctx_or_default(nullptr), s);
+  Ctx* ctx = ctx_or_default(nullptr);
+  // The point side of the product (squared norms, scale, packed operand,
+  // bands, unit list) depends on the points only.  A caller that runs several
+  // assignments over the same points (Lloyd iterations) tags the context with
+  // a token (simdex_ctx_set_query_token); a call that finds the arena still
+  // holding that token's point side -- no other call has used the context
+  // since, the arena has not moved, same pointers and sizes -- skips it
+  // (0.1 ms of 0.65 per iteration at cfg2).
+  const CtxSetup held_before = *ctx_setup(ctx);
+  const int64_t qtok = ctx_setup(ctx)->query_token;
+  ctx_setup(ctx)->query_token = 0;  // consumed by this call
+  uint64_t sig = 1469598103934665603ull;
+  for (uint64_t v : {(uint64_t)(uintptr_t)px, (uint64_t)n, (uint64_t)f, (uint64_t)c, (uint64_t)kp,
+                     (uint64_t)sizeof(P), (uint64_t)0x6b6d65616e73ull})
+    sig = (sig ^ v) * 1099511628211ull;
+  Workspace ws(ctx, s);
   unsigned long long* mx;
   int* sexp;
   double* sfac;
   RowState st;
   uint16_t *ua, *ca;
-  double *un, *cn;
+  double *un, *cn, *p2w;
   Unit* units;
   int32_t *n_units, *over_n;
   float *cu, *inrm, *inmax;
@@ -2663,6 +2678,7 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   ws.add(&mx, 3);
   ws.add(&sexp, 2);
   ws.add(&sfac, 2);
+  ws.add(&p2w, nu_pad);
   st.add(ws, nu_pad, k_eff);
   ws.add(&ua, (size_t)nu_pad * kp);
   ws.add(&ca, (size_t)nc_pad * kp);
@@ -2676,9 +2692,16 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   ws.add(&inrm, nc_pad);
   ws.add(&inmax, nc_pad / 32);
   if ((rc = ws.commit())) return rc;
-  SIMDEX_CUDA(cudaMemsetAsync(mx, 0, 3 * sizeof(unsigned long long), s));
+  const bool reuse = qtok != 0 && held_before.held_token == qtok && held_before.held_gen == ctx_arena_gen(ctx) &&
+                     held_before.held_sig == sig && !getenv("SIMDEX_NO_SETUP_REUSE");
+  const double* p2 = p2w;
+  *p2_out = p2w;
+  SIMDEX_CUDA(cudaMemsetAsync(mx + (reuse ? 1 : 0), 0, (reuse ? 2 : 3) * sizeof(unsigned long long), s));
   const int64_t nf = n * (int64_t)f;
-  max_abs_any_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(nf, 256), 4 * 148), 256, 0, s>>>(px, nf, 1.0, mx);
+  if (!reuse) {
+    if ((rc = fill_p2(px, n, f, p2w, s))) return rc;
+    max_abs_any_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(nf, 256), 4 * 148), 256, 0, s>>>(px, nf, 1.0, mx);
+  }
   max_abs_any_kernel<double><<<(unsigned)std::min<int64_t>(ceil_div((int64_t)c * f, 256), 64), 256, 0, s>>>(
       centers, (int64_t)c * f, 1.0, mx + 1);
   max_abs_any_kernel<double><<<1, 256, 0, s>>>(c2, c, 0.5, mx + 2);
@@ -2686,16 +2709,25 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   assign_scales_kernel<<<1, 32, 0, s>>>(mx, eps_for(kp), sexp, sfac);
   SIMDEX_LAUNCH_CHECK("assign_scales");
   ProfileScope _prof("assign_pack", s);
-  pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, sexp, nu_pad, kp,
-                                                                          ua, un);
+  if (!reuse)
+    pack_aug_kernel<P><<<(unsigned)ceil_div(nu_pad * 8, 256), 256, 0, s>>>(px, p2, n, f, 0, sexp, nu_pad, kp,
+                                                                            ua, un);
   pack_aug_kernel<double><<<(unsigned)ceil_div(nc_pad * 8, 256), 256, 0, s>>>(centers, c2, c, f, 1, sexp + 1,
                                                                                nc_pad, kp, ca, cn);
   _prof.end();
   SIMDEX_LAUNCH_CHECK("pack_aug");
-  units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units, n_units, nunits);
-  SIMDEX_LAUNCH_CHECK("units");
-  row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un, n, nu_pad, 0.0, cu, sfac);
-  SIMDEX_LAUNCH_CHECK("row_cu");
+  if (!reuse) {
+    units_from_count_kernel<<<(unsigned)ceil_div(nunits, 256), 256, 0, s>>>(nullptr, n, c, units, n_units, nunits);
+    SIMDEX_LAUNCH_CHECK("units");
+    row_cu_kernel<<<(unsigned)ceil_div(nu_pad, 256), 256, 0, s>>>(un, n, nu_pad, 0.0, cu, sfac);
+    SIMDEX_LAUNCH_CHECK("row_cu");
+  }
+  if (qtok != 0) {  // the arena now holds this token's point side
+    CtxSetup* cs = ctx_setup(ctx);
+    cs->held_token = qtok;
+    cs->held_gen = ctx_arena_gen(ctx);
+    cs->held_sig = sig;
+  }
   item_nrm_kernel<<<(unsigned)ceil_div(nc_pad / 32, 8), 256, 0, s>>>(cn, c, nc_pad, 0.0, inrm, inmax,
                                                                       sfac + 1);
   SIMDEX_LAUNCH_CHECK("item_nrm");
@@ -2740,15 +2772,15 @@ int gemm_assign_impl(const double* points, const P* px, const float* points32, i
   return SIMDEX_OK;
 }
 
-int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, const double* p2,
-                       const double* centers, const double* c2, int32_t c, const int64_t* prev, int64_t* out_assign,
-                       double* out_d2, unsigned long long* changed, int64_t* over_rows, int32_t* n_over,
-                       cudaStream_t s) {
+int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, P2Fill fill_p2,
+                       const double** p2_out, const double* centers, const double* c2, int32_t c,
+                       const int64_t* prev, int64_t* out_assign, double* out_d2, unsigned long long* changed,
+                       int64_t* over_rows, int32_t* n_over, cudaStream_t s) {
   if (points32)
-    return gemm_assign_impl<float>(points, points32, points32, n, f, p2, centers, c2, c, prev, out_assign, out_d2,
-                                   changed, over_rows, n_over, s);
-  return gemm_assign_impl<double>(points, points, nullptr, n, f, p2, centers, c2, c, prev, out_assign, out_d2,
-                                  changed, over_rows, n_over, s);
+    return gemm_assign_impl<float>(points, points32, points32, n, f, fill_p2, p2_out, centers, c2, c, prev,
+                                   out_assign, out_d2, changed, over_rows, n_over, s);
+  return gemm_assign_impl<double>(points, points, nullptr, n, f, fill_p2, p2_out, centers, c2, c, prev, out_assign,
+                                  out_d2, changed, over_rows, n_over, s);
 }
 
 }  // namespace simdex

@@ -21,10 +21,10 @@
 
 namespace simdex {
 
-int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, const double* p2,
-                       const double* centers, const double* c2, int32_t c, const int64_t* prev, int64_t* out_assign,
-                       double* out_d2, unsigned long long* changed, int64_t* over_rows, int32_t* n_over_dev,
-                       cudaStream_t s);
+int gemm_kmeans_assign(const double* points, const float* points32, int64_t n, int32_t f, P2Fill fill_p2,
+                       const double** p2_out, const double* centers, const double* c2, int32_t c,
+                       const int64_t* prev, int64_t* out_assign, double* out_d2, unsigned long long* changed,
+                       int64_t* over_rows, int32_t* n_over_dev, cudaStream_t s);
 
 namespace {
 
@@ -1232,30 +1232,40 @@ __global__ void to_f32_kernel(const double* __restrict__ x, int64_t n, float* __
 // launchers (float64 or exact float32 points)
 // ---------------------------------------------------------------------------
 template <class P>
+int fill_sqnorm(const void* px, int64_t n, int f, double* out, cudaStream_t s) {
+  sqnorm_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(static_cast<const P*>(px), n, f, out);
+  SIMDEX_LAUNCH_CHECK("sqnorm");
+  return SIMDEX_OK;
+}
+
+template <class P>
 int assign_impl(const double* points, const float* points32, const P* px, int64_t n, int32_t f,
                 const double* centers, int32_t c, const int64_t* prev, int64_t* out_assign, double* out_d2,
                 int64_t* out_changed, double* out_objective, cudaStream_t s) {
   Scratch<double> p2, c2, part;
-  SIMDEX_CUDA(p2.alloc(n, s));
   SIMDEX_CUDA(c2.alloc(c, s));
-  sqnorm_kernel<P><<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(px, n, f, p2.p);
-  SIMDEX_LAUNCH_CHECK("sqnorm");
+  const bool tc = f + 1 <= kAssignGemmMaxF;  // (the tensor-core path keeps the squared norms in its workspace)
+  if (!tc) {
+    SIMDEX_CUDA(p2.alloc(n, s));
+    if (int rc = fill_sqnorm<P>(px, n, f, p2.p, s)) return rc;
+  }
   sqnorm_kernel<double><<<(unsigned)ceil_div(c, 256), 256, 0, s>>>(centers, c, f, c2.p);
   SIMDEX_LAUNCH_CHECK("sqnorm");
   SIMDEX_CUDA(cudaMemsetAsync(out_changed, 0, sizeof(int64_t), s));
   auto* changed = reinterpret_cast<unsigned long long*>(out_changed);
-  if (f + 1 <= kAssignGemmMaxF) {
+  if (tc) {
     // tensor-core candidates + exact float64 d2; overflowing bands go to the SIMT kernel
     Scratch<int64_t> over;
     Scratch<int32_t> n_over;
     SIMDEX_CUDA(over.alloc(n, s));
     SIMDEX_CUDA(n_over.alloc(1, s));
-    int rc = gemm_kmeans_assign(points, points32, n, f, p2.p, centers, c2.p, c, prev, out_assign, out_d2, changed,
-                                over.p, n_over.p, s);
+    const double* p2w = nullptr;  // in the context workspace: valid until the context's next call
+    int rc = gemm_kmeans_assign(points, points32, n, f, &fill_sqnorm<P>, &p2w, centers, c2.p, c, prev, out_assign,
+                                out_d2, changed, over.p, n_over.p, s);
     if (rc) return rc;
     // rows whose band overflowed (rare): exact SIMT kernel, count read on the device
     assign_kernel<P><<<(unsigned)std::min<int64_t>(ceil_div(n, kAssignThreads), 2 * sm_count()), kAssignThreads, 0,
-                       s>>>(px, p2.p, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, over.p, n_over.p);
+                       s>>>(px, p2w, n, f, centers, c2.p, c, prev, out_assign, out_d2, changed, over.p, n_over.p);
     SIMDEX_LAUNCH_CHECK("assign");
   } else {
     ProfileScope _prof("kmeans_assign", s);
