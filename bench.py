@@ -331,10 +331,11 @@ def cpu_baseline_ours(w, k, cl_host):
 # our arm
 # ---------------------------------------------------------------------------
 
-def committed_traffic(kernel):
+def committed_traffic(kernel, workload, k, world):
     """DRAM bytes per launch of ``kernel`` from the committed ncu --set full
     capture (profiles/gemm_topk_traffic.json), only when it was taken on the
-    current kernel sources (hash match); else None."""
+    current kernel sources (hash match) and on this workload and depth at one
+    GPU; else None."""
     try:
         with open(TRAFFIC_FILE) as fh:
             t = json.load(fh)
@@ -342,6 +343,8 @@ def committed_traffic(kernel):
         return None, "no committed capture"
     if t.get("kernel_source_hash") != kernel_source_hash():
         return None, "committed capture is from other kernel sources"
+    if (t.get("workload", "cfg2"), int(t.get("k", 10))) != (workload, int(k)) or world != 1:
+        return None, f"committed capture is of {t.get('workload', 'cfg2')} K={t.get('k', 10)} on one GPU"
     ent = t.get("launches", {}).get(kernel)
     if not ent:
         return None, f"no capture of {kernel}"
@@ -556,7 +559,7 @@ def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib, st
         t12 = t1 + (s2["ms_per_step"] / 1e3 if s2 else 0.0)
         e1, e2 = 2.0 * f * p1, 2.0 * f * p2
         c1, c2 = 2.0 * f * nq * bp, 2.0 * f * n_cont * ni
-        traffic, src = committed_traffic("gemm_topk_prefix")
+        traffic, src = committed_traffic("gemm_topk_prefix", w.name, k, world)
         # the algorithmic work of the prefix launch is 2 f B' per
         # user (work sharing scores every user's first B' list items); the
         # early exit skips tiles that cannot change the answer, so the launch
@@ -586,7 +589,7 @@ def roofline(w, k, served, world, kernels, ms_per_step, bf16, peak_kind, lib, st
     credited = 2.0 * f * n_items * n_users
     executed = 2.0 * f * p1
     t = g["ms_per_step"] / 1e3
-    traffic, src = committed_traffic("gemm_topk")
+    traffic, src = committed_traffic("gemm_topk", w.name, k, world)
     return {"kernel": "gemm_topk_kernel (blocked product, tcgen05 fp16 -> fp32 TMEM, fused certified top-K)",
             "bound": "tensor", "achieved": executed / t / 1e12, "peak": bf16, "peak_kind": peak_note,
             "unit": "TFLOP/s", "frac": executed / t / 1e12 / bf16, "traffic": traffic, "traffic_source": src,

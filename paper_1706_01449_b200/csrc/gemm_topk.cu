@@ -84,6 +84,9 @@ using namespace sm100;
 #ifndef SIMDEX_FIN_TWO
 #define SIMDEX_FIN_TWO 1
 #endif
+#ifndef SIMDEX_FIN_ITEMS64
+#define SIMDEX_FIN_ITEMS64 0
+#endif
 #ifndef SIMDEX_FIN_MINB
 #define SIMDEX_FIN_MINB 5
 #endif
@@ -1175,10 +1178,24 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
     const int e0 = gl, e1 = gl + LPR;
     if (act && e0 < cnt) {
       const bool has1 = e1 < cnt;
-      const float2* xa = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[e0] * p.f);
-      const float2* xb = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[has1 ? e1 : e0] * p.f);
       const double2* u2 = reinterpret_cast<const double2*>(us);
       double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#if SIMDEX_FIN_ITEMS64
+      // (A/B: the float64 item rows, twice the bytes, no conversions)
+      const double2* xa = reinterpret_cast<const double2*>(p.items + (int64_t)si[e0] * p.f);
+      const double2* xb = reinterpret_cast<const double2*>(p.items + (int64_t)si[has1 ? e1 : e0] * p.f);
+#pragma unroll 5
+      for (int q = 0; q < p.f / 2; ++q) {
+        const double2 va = xa[q], vb = xb[q];
+        const double2 u = u2[q];
+        a0 = fma(va.x, u.x, a0);
+        a1 = fma(va.y, u.y, a1);
+        b0 = fma(vb.x, u.x, b0);
+        b1 = fma(vb.y, u.y, b1);
+      }
+#else
+      const float2* xa = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[e0] * p.f);
+      const float2* xb = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[has1 ? e1 : e0] * p.f);
 #pragma unroll 5
       for (int q = 0; q < p.f / 2; ++q) {
         const float2 va = xa[q], vb = xb[q];
@@ -1188,6 +1205,7 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
         b0 = fma((double)vb.x, u.x, b0);
         b1 = fma((double)vb.y, u.y, b1);
       }
+#endif
       ss[e0] = a0 + a1;
       if (has1) ss[e1] = b0 + b1;
     }

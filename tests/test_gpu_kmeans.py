@@ -163,3 +163,28 @@ def test_lloyd_batches_equal_sequential(env, n, f, c, iters, seed):
     ref = O.kmeans(users, c, max_iters=iters, seed=seed)
     np.testing.assert_array_equal(b.assignment, ref["assignment"])
     assert b.objective.shape == ref["objective"].shape
+
+
+def test_assign_reuses_point_side_under_a_token(env):
+    """Consecutive assignments over the same points under one context token
+    (the Lloyd loop) skip the point side of the product; the results are those
+    of untagged calls, for changed centres too, and another call on the
+    context in between invalidates the held setup."""
+    pkg, _ops, torch = env
+    rng = np.random.default_rng(5)
+    n, f, c = 40000, 24, 64
+    centers = rng.normal(size=(c, f))
+    points = (centers[rng.integers(0, c, n)] + 0.4 * rng.normal(size=(n, f))).astype(np.float32).astype(np.float64)
+    pts = _dev(torch, points)
+    p32 = pts.to(torch.float32)
+    tok = -987654
+    for it in range(4):
+        cen = _dev(torch, centers + 0.05 * it * rng.normal(size=(c, f)))
+        a0, d0, _, o0 = _ops.kmeans_assign(pts, cen, points32=p32)
+        a1, d1, _, o1 = _ops.kmeans_assign(pts, cen, points32=p32, token=tok)
+        assert torch.equal(a0, a1) and torch.equal(d0, d1) and torch.equal(o0, o1)
+        if it == 2:  # a different problem on the same context: the held point side must not be reused after it
+            other = _dev(torch, rng.normal(size=(n, f)))
+            _ops.kmeans_assign(other, cen)
+    want, _ = _np_assign(points, cen.cpu().numpy())
+    assert np.array_equal(a1.cpu().numpy(), want)

@@ -218,3 +218,26 @@ def test_work_sharing_prefix_layouts_and_list_catalogue_pass(sx, k, mode):
     ids0, sc0, vis0 = (t.cpu().numpy() for t in I.query_batch_tensors(idx, m, None, k, work_sharing=False))
     np.testing.assert_array_equal(vis, np.maximum(min(block, ni), vis0))
     np.testing.assert_array_equal(ids, ids0)
+
+
+def test_full_list_operand_is_built_after_the_first_large_batch(sx):
+    """The list-order catalogue pass's operand is built once an index has
+    served a large batch (index.FULL_LISTS_AFTER), not by build_index or a
+    one-shot run_pipeline; the answers before and after are identical."""
+    from paper_1706_01449_b200 import index as I
+    rng = np.random.default_rng(3)
+    nu, ni, f, c, k = 52000, 3000, 16, 24, 10
+    centers = rng.normal(size=(c, f))
+    users = (centers[rng.integers(0, c, nu)] + rng.normal(0, 0.5, (nu, f))).astype(np.float32).astype(np.float64)
+    items = rng.normal(size=(ni, f)).astype(np.float32).astype(np.float64)
+    m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    idx = sx.build_index(m, sx.kmeans(m.users, c, max_iters=2, seed=1), 512)
+    assert "full_lists" not in idx._dev and "prefix" not in idx._dev
+    first = [t.clone() for t in I.query_batch_tensors(idx, m, None, k)]
+    assert "full_lists" not in idx._dev
+    for _ in range(I.FULL_LISTS_AFTER):
+        second = [t.clone() for t in I.query_batch_tensors(idx, m, None, k)]
+    assert idx._dev.get("full_lists") is not None
+    import torch
+    for a, b in zip(first, second):
+        assert torch.equal(a, b)

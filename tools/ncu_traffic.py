@@ -21,6 +21,8 @@ ap.add_argument("rep")
 ap.add_argument("--path", default="index")
 ap.add_argument("--capture", default="")
 ap.add_argument("--out", default=bench.TRAFFIC_FILE)
+ap.add_argument("--workload", default="cfg2")
+ap.add_argument("--k", type=int, default=10)
 a = ap.parse_args()
 raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv", "--metrics",
                       "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
@@ -42,7 +44,7 @@ for r in rows[2:]:
 labels = ["gemm_topk_prefix", "gemm_topk_full"] if a.path == "index" else ["gemm_topk"]
 for (name, rd, wr), lab in zip(order, labels):
     launches[lab] = {"kernel_name": name, "dram_bytes": rd + wr, "dram_read": rd, "dram_write": wr}
-out = {"kernel_source_hash": bench.kernel_source_hash(), "capture": a.capture or os.path.basename(a.rep),
+out = {"kernel_source_hash": bench.kernel_source_hash(), "workload": a.workload, "k": a.k, "capture": a.capture or os.path.basename(a.rep),
        "launches": launches}
 json.dump(out, open(a.out, "w"), indent=1)
 print(json.dumps(out, indent=1))
