@@ -117,6 +117,17 @@ def drop(matrix):
     matrix.__dict__.get("_device", {}).clear()
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def side_stream(dev) -> "torch.cuda.Stream":
+    """One extra stream per device for copies that overlap the main stream's kernels."""
+    s = _SIDE_STREAMS.get(dev.index)
+    if s is None:
+        s = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
+    return s
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy()
 

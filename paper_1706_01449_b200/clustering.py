@@ -187,16 +187,6 @@ def _repair_empty_host(points_h, centers_h, assign_h, d2_h):
     return changed
 
 
-_SIDE_STREAMS: dict = {}
-
-
-def _side_stream(dev) -> "torch.cuda.Stream":
-    s = _SIDE_STREAMS.get(dev.index)
-    if s is None:
-        s = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
-    return s
-
-
 def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_iters: int = DEFAULT_MAX_ITERS,
            seed: int = 0) -> Clustering:
     """Lloyd iterations with k-means++ seeding, stopping on a stable
@@ -221,7 +211,7 @@ def kmeans(users: FactorMatrix, num_clusters: int = DEFAULT_NUM_CLUSTERS, max_it
     # the seeding does, and the GPU does not idle while the loop is queued
     seeded = torch.cuda.Event()
     seeded.record()
-    side = _side_stream(dev)
+    side = _device.side_stream(dev)
     deg_h = torch.empty(1, dtype=deg.dtype, pin_memory=True)
     with torch.cuda.stream(side):
         side.wait_event(seeded)

@@ -647,6 +647,56 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
     return out
 
 
+# Serving every user and returning the results to the host: the users are cut
+# into contiguous id ranges served one after the other, each range's results
+# copied to pinned host memory on a side stream while the next range is
+# served (58 MB of results take 1.2 ms over PCIe against a 0.95 ms serve at
+# cfg2).  Ranges keep 100k users or more so that each still takes the
+# list-order catalogue pass.
+D2H_PARTS = int(os.environ.get("SIMDEX_D2H_PARTS", "2"))
+D2H_MIN_USERS_PER_PART = 100_000
+
+
+def _d2h_parts(model: ModelPair, k: int) -> int:
+    if min(k, model.num_items) > 256 or model.factors > 256:
+        return 1
+    return max(1, min(D2H_PARTS, model.num_users // D2H_MIN_USERS_PER_PART))
+
+
+def _serve_all_users_overlapped(index: CentroidIndex, model: ModelPair, k: int, work_sharing: bool, parts: int):
+    """query_batch_tensors over ``parts`` contiguous user ranges (cached
+    QuerySets, each with its own execution context so their setups stay
+    reusable), device -> pinned host copies of a range overlapped with the
+    next range's kernels.  Returns host (ids, scores, visited) in user order."""
+    n, k_eff = model.num_users, min(k, model.num_items)
+    dev = _device.f64(model.users).device
+    key = ("user_ranges", n, parts)
+    ranges = index._dev.get(key)
+    if ranges is None:
+        cuts = [n * i // parts for i in range(parts + 1)]
+        ranges = index._dev[key] = [
+            (lo, hi, QuerySet(index, None, q=torch.arange(lo, hi, dtype=torch.int64, device=dev)), _lib.Context())
+            for lo, hi in zip(cuts[:-1], cuts[1:])]
+    ids_h = torch.empty((n, k_eff), dtype=torch.int32, pin_memory=True)
+    sc_h = torch.empty((n, k_eff), dtype=torch.float64, pin_memory=True)
+    vis_h = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    main = torch.cuda.current_stream()
+    side = _device.side_stream(dev)
+    for lo, hi, qs, ctx in ranges:
+        ids, sc, vis = query_batch_tensors(index, model, qs, k, work_sharing, ctx=ctx.handle)
+        served = torch.cuda.Event()
+        served.record(main)
+        with torch.cuda.stream(side):
+            side.wait_event(served)
+            ids_h[lo:hi].copy_(ids, non_blocking=True)
+            sc_h[lo:hi].copy_(sc, non_blocking=True)
+            vis_h[lo:hi].copy_(vis, non_blocking=True)
+        for t in (ids, sc, vis):
+            t.record_stream(side)
+    side.synchronize()
+    return ids_h.numpy(), sc_h.numpy(), vis_h.numpy()
+
+
 def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 1, work_sharing: bool = True,
                 precomputed: dict | None = None) -> TopKResults:
     """Top-K for many users (index.py:305-389); identical entries with work
@@ -680,6 +730,15 @@ def query_batch(index: CentroidIndex, model: ModelPair, user_ids=None, k: int = 
     if len(reused) * 2 <= n_q:
         # few reused entries: serve every position on the device (the reused
         # positions still return the precomputed objects), no host gather
+        if all_users and _d2h_parts(model, k) > 1:
+            # from an index's second all-user serve on (the ranges' query sets
+            # and contexts are one-time costs a one-shot run_pipeline would only pay)
+            served = index._dev.get("all_user_serves", 0)
+            index._dev["all_user_serves"] = served + 1
+            if served >= 1:
+                ids_h, sc_h, vis_h = _serve_all_users_overlapped(index, model, k, work_sharing,
+                                                                 _d2h_parts(model, k))
+                return TopKResults(uids, ids_h, sc_h, vis_h, reused)
         q = None if all_users else _device.to_device(uids)
         ids, sc, vis = query_batch_tensors(index, model, q, k, work_sharing)
         ids_h, sc_h, vis_h = _device.to_host_pinned_many(ids, sc, vis)
@@ -750,7 +809,7 @@ def _derive(index: CentroidIndex, clustering: Clustering, lists=None) -> Centroi
     # prefix operand and list positions on the lists; walk estimates stay
     # (they only pick an option, the results are identical either way)
     out._dev = {key: val for key, val in index._dev.items()
-                if not (isinstance(key, tuple) and key[0] == "all_users")}
+                if not (isinstance(key, tuple) and key[0] in ("all_users", "user_ranges"))}
     if lists is not None:
         out._host.pop("item_ids", None)
         out._host.pop("bounds", None)

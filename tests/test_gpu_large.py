@@ -241,3 +241,25 @@ def test_full_list_operand_is_built_after_the_first_large_batch(sx):
     import torch
     for a, b in zip(first, second):
         assert torch.equal(a, b)
+
+
+def test_all_user_serve_with_overlapped_copies_equals_one_batch(sx):
+    """query_batch(None) serves large models in contiguous user ranges with
+    the device->host copies overlapped; the results are those of one batch."""
+    from paper_1706_01449_b200 import index as I
+    rng = np.random.default_rng(11)
+    nu, ni, f, c, k = 210000, 2500, 16, 16, 10
+    centers = rng.normal(size=(c, f))
+    users = (centers[rng.integers(0, c, nu)] + rng.normal(0, 0.5, (nu, f))).astype(np.float32).astype(np.float64)
+    items = rng.normal(size=(ni, f)).astype(np.float32).astype(np.float64)
+    m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    idx = sx.build_index(m, sx.kmeans(m.users, c, max_iters=2, seed=1), 512)
+    assert I._d2h_parts(m, k) == 2
+    for _ in range(3):  # (one batch first; then the ranges, whose second serve takes the list-order catalogue pass)
+        res = sx.query_batch(idx, m, None, k)
+    assert ("user_ranges", nu, 2) in idx._dev
+    ids, sc, vis = (t.cpu().numpy() for t in I.query_batch_tensors(idx, m, None, k))
+    np.testing.assert_array_equal(res.item_ids, ids)
+    np.testing.assert_array_equal(res.scores, sc)
+    np.testing.assert_array_equal(np.asarray(res.visited), vis)
+    assert len(res) == nu and res[nu - 1].item_ids.tolist() == ids[-1].tolist()
