@@ -141,11 +141,18 @@ int Workspace::commit() {
   }
   if (need > c_->cap) {
     size_t grow = (need + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
-    if (c_->arena) SIMDEX_CUDA(cudaFreeAsync(c_->arena, s_));
+    // Growth is rare (the first calls of a process) and takes a plain
+    // cudaFree + cudaMalloc, which synchronise the device.  An arena regrown
+    // through the stream-ordered pool (cudaFreeAsync + cudaMallocAsync, which
+    // may stitch the new block from the freed ones) left about one process in
+    // eight with a catalogue pass twice as slow for its whole life
+    // (tools/full_pass_variation.py; a context whose arena was allocated
+    // once was never slow).
+    if (c_->arena) SIMDEX_CUDA(cudaFree(c_->arena));
     c_->arena = nullptr;
     c_->cap = 0;
     keep_pool_warm();
-    SIMDEX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c_->arena), grow, s_));
+    SIMDEX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c_->arena), grow));
     c_->cap = grow;
     ++c_->arena_gen;
   }
