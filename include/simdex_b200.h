@@ -67,7 +67,9 @@ SIMDEX_API int simdex_profile_enable(int on);
 SIMDEX_API int simdex_profile_read(const char* name, double* total_ms, int64_t* launches);
 SIMDEX_API int simdex_profile_reset(void);
 /* Execution contexts.  A context owns a device workspace arena (grown on
- * demand, stream-ordered, reused by every later call) and pinned host
+ * demand with cudaFree + cudaMalloc -- a growing call synchronises the
+ * device, which happens only in a process's first calls -- and reused by
+ * every later call) and pinned host
  * statistic slots; calls that take `ctx` carve their scratch from it instead
  * of allocating.  ctx == NULL selects the calling thread's default context
  * for the current device (what the legacy entry points use).  A context
