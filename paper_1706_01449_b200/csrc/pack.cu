@@ -56,17 +56,18 @@ __global__ void pack_f16_rows_kernel(const double* __restrict__ x, int64_t rows,
 __global__ void gather_prefix_kernel(const uint16_t* __restrict__ ib, const double* __restrict__ inorm, int64_t ni,
                                      int kp, const int32_t* __restrict__ list_ids, int64_t bp, int64_t b_pad,
                                      int64_t n_clusters, uint16_t* __restrict__ out, double* __restrict__ onorm) {
-  // one warp per (cluster, prefix row)
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  const int64_t c = g / b_pad, r = g % b_pad;
+  // one thread per 16-byte piece of a (cluster, prefix row): the stores of a
+  // warp are contiguous (a warp per row kept 8 of 32 lanes busy at kp = 64)
+  const int vpr = kp / 8;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = g / vpr;
+  const int v = (int)(g - row * vpr);
+  const int64_t c = row / b_pad, r = row - c * b_pad;
   if (c >= n_clusters) return;
   const bool live = r < bp;
   const int64_t src = live ? list_ids[c * ni + r] : 0;
-  const uint4* s = reinterpret_cast<const uint4*>(ib + src * kp);
-  uint4* d = reinterpret_cast<uint4*>(out + (c * b_pad + r) * kp);
-  for (int v = lane; v < kp / 8; v += 32) d[v] = live ? s[v] : make_uint4(0, 0, 0, 0);
-  if (lane == 0) onorm[c * b_pad + r] = live ? inorm[src] : 0.0;
+  reinterpret_cast<uint4*>(out)[g] = live ? reinterpret_cast<const uint4*>(ib + src * kp)[v] : make_uint4(0, 0, 0, 0);
+  if (v == 0) onorm[row] = live ? inorm[src] : 0.0;
 }
 
 // Ordering keys of a cluster's prefix: the centroid's float64 score c . i of
@@ -173,9 +174,9 @@ int launch_pack_f16_rows(const double* x, int64_t rows, int32_t f, int64_t rows_
 int launch_gather_prefix(const uint16_t* ib, const double* i_norm, int64_t ni, int32_t kp, const int32_t* list_ids,
                          int32_t c, int64_t block, int64_t b_pad, uint16_t* out, double* onorm, cudaStream_t s) {
   const int64_t bp = block < ni ? block : ni;
-  const int64_t warps = (int64_t)c * b_pad;
-  gather_prefix_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>(ib, i_norm, ni, kp, list_ids, bp, b_pad, c,
-                                                                    out, onorm);
+  const int64_t pieces = (int64_t)c * b_pad * (kp / 8);
+  gather_prefix_kernel<<<(unsigned)ceil_div(pieces, 256), 256, 0, s>>>(ib, i_norm, ni, kp, list_ids, bp, b_pad, c,
+                                                                       out, onorm);
   SIMDEX_LAUNCH_CHECK("gather_prefix");
   return SIMDEX_OK;
 }
@@ -256,9 +257,9 @@ int launch_build_prefix_ordered(const uint16_t* ib, const double* i_norm, int64_
   prefix_tile_ceil_kernel<<<(unsigned)c, 1024, tsm, s>>>(tmp.p, bp, b_pad, list_pos, bounds, ni, out_tile_ceil);
   SIMDEX_LAUNCH_CHECK("prefix_tile_ceil");
   // gather the operand rows in the new order (the sorted ids act as a list of length bp)
-  const int64_t warps = (int64_t)c * b_pad;
-  gather_prefix_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, s>>>(ib, i_norm, bp, kp, tmp.p, bp, b_pad, c, out,
-                                                                    onorm);
+  const int64_t pieces = (int64_t)c * b_pad * (kp / 8);
+  gather_prefix_kernel<<<(unsigned)ceil_div(pieces, 256), 256, 0, s>>>(ib, i_norm, bp, kp, tmp.p, bp, b_pad, c, out,
+                                                                       onorm);
   SIMDEX_LAUNCH_CHECK("gather_prefix");
   SIMDEX_CUDA(cudaMemsetAsync(ids, 0xff, sizeof(int32_t) * (size_t)c * b_pad, s));
   SIMDEX_CUDA(cudaMemcpy2DAsync(ids, sizeof(int32_t) * b_pad, tmp.p, sizeof(int32_t) * bp, sizeof(int32_t) * bp, c,
