@@ -79,6 +79,8 @@ struct Ctx {
   bool busy = false;
   int64_t* host = nullptr;  // pinned statistics slots
   uint64_t arena_gen = 0;   // bumped whenever the arena is (re)allocated
+  bool captured = false;    // a CUDA graph holds pointers into the current arena
+  std::vector<char*> retired;  // arenas captured into graphs and outgrown since: kept until the context dies
   CtxSetup setup;
 };
 
@@ -148,7 +150,13 @@ int Workspace::commit() {
     // eight with a catalogue pass twice as slow for its whole life
     // (tools/full_pass_variation.py; a context whose arena was allocated
     // once was never slow).
-    if (c_->arena) SIMDEX_CUDA(cudaFree(c_->arena));
+    // (an arena a CUDA graph was captured over stays allocated: the graph's
+    // kernels hold its addresses and may be replayed after this growth)
+    if (c_->arena && c_->captured)
+      c_->retired.push_back(c_->arena);
+    else if (c_->arena)
+      SIMDEX_CUDA(cudaFree(c_->arena));
+    c_->captured = false;
     c_->arena = nullptr;
     c_->cap = 0;
     keep_pool_warm();
@@ -163,6 +171,7 @@ int Workspace::commit() {
   }
   c_->busy = true;
   committed_ = true;
+  if (capturing_) c_->captured = true;
   // whatever this call leaves in the arena is not a reusable query setup
   // unless the call itself records one (gemm_topk_ws)
   c_->setup.held_token = 0;
@@ -272,6 +281,7 @@ extern "C" int simdex_ctx_destroy(void* ctx) {
   SIMDEX_CUDA(cudaSetDevice(c->device));
   if (c->have_done) cudaEventSynchronize(c->done);
   if (c->arena) cudaFree(c->arena);
+  for (char* old : c->retired) cudaFree(old);
   if (c->done) cudaEventDestroy(c->done);
   if (c->host) cudaFreeHost(c->host);
   cudaSetDevice(prev);

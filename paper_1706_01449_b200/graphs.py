@@ -9,6 +9,17 @@ instead of ~20 launches, and the GPU runs the kernels back to back.
 
 The outputs of a replay are the tensors captured the first time: every
 replay overwrites them (copy them if they must outlive the next replay).
+
+What a captured call relies on.  Its kernels hold addresses inside its
+execution context's workspace arena: the library keeps an arena a graph was
+captured over allocated even when a later, larger call outgrows it.  A
+work-sharing query captured for a fixed query set also relies on that set's
+setup staying in the workspace (the capture happens after warm-up serves, so
+it records the reuse path without the setup kernels): serve the set on a
+context nothing else uses -- the all-users set does so by itself from its
+second serve on, the concurrent parts of a `sharding` shard own theirs, for an explicit `QuerySet`
+pass `ctx=` -- and do not serve the same set with other arguments on that
+context between replays.
 """
 
 from __future__ import annotations

@@ -585,10 +585,24 @@ class QuerySet:
             self.q = q
         self.grouped = _ops.group_queries(self.q, index.device_assignment(), index.num_clusters)
         self.token = next(_QUERY_TOKENS)
+        self._serves = 0
+        self._own_ctx = None
 
     @property
     def index(self):
         return self._index()
+
+    def serving_context(self):
+        """The execution context this set is served on when the caller names
+        none: the thread's default for its first serve (a one-shot pipeline
+        allocates nothing), its own from the second serve on -- nothing else
+        then disturbs the setup the set keeps in that context's workspace
+        (which a CUDA graph captured from a serve relies on), and the arena
+        is allocated once at its final size."""
+        self._serves += 1
+        if self._serves >= 2 and self._own_ctx is None:
+            self._own_ctx = _lib.Context()
+        return None if self._own_ctx is None else self._own_ctx.handle
 
     def context(self, ctx=None):
         """Tag the context the next serve runs on (``ctx``, or None for the
@@ -613,6 +627,8 @@ def query_batch_tensors(index: CentroidIndex, model: ModelPair, q_users, k: int,
     qs = None
     if q_users is None:
         qs = index.all_users_queries(model.num_users, users.device)
+        if ctx is None:
+            ctx = qs.serving_context()
     elif isinstance(q_users, QuerySet):
         if q_users.index is not index:
             raise ValueError("QuerySet was prepared for another index")

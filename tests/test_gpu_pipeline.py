@@ -147,3 +147,33 @@ def test_graph_replay_equals_eager(sx):
             torch.cuda.synchronize()
             for a, b in zip(eager, out):
                 assert torch.equal(a, b)
+
+
+def test_graph_replay_survives_other_calls_and_arena_growth(sx):
+    """Replays stay correct when other library calls run in between: the
+    all-users query set serves on its own context (its captured setup is not
+    disturbed by calls on the default context), and an arena a graph was
+    captured over is retired, not freed, when a larger call outgrows it."""
+    import torch
+    from paper_1706_01449_b200 import graphs, index as I
+    small = sx.generate_synthetic(sx.SyntheticSpec(3000, 1500, 16, archetype_count=8, angular_spread=0.3, seed=4))
+    idx = sx.build_index(small, sx.kmeans(small.users, 6, max_iters=3, seed=1), 256)
+    calls = [lambda: I.query_batch_tensors(idx, small, None, 10),        # own context from its second serve
+             lambda: sx.brute.topk_matmul_tensors(small, 5)[:2]]         # the thread's default context
+    eager = [[t.clone() for t in fn()] for fn in calls]
+    graphed = [graphs.GraphedCall(fn) for fn in calls]
+    # far larger calls on the default context: its arena is outgrown (or, if an
+    # earlier test grew it, overwritten)
+    big = sx.generate_synthetic(sx.SyntheticSpec(150000, 4000, 32, archetype_count=16, angular_spread=0.3, seed=5))
+    sx.brute.topk_matmul_tensors(big, 20)
+    idx_big = sx.build_index(big, sx.kmeans(big.users, 16, max_iters=2, seed=2), 1024)
+    I.query_batch_tensors(idx_big, big, None, 20)
+    scratch = torch.full((64 << 20,), 7, dtype=torch.int32, device="cuda")  # reuse any freed device memory
+    torch.cuda.synchronize()
+    for _ in range(2):
+        for g, want in zip(graphed, eager):
+            out = g()
+            torch.cuda.synchronize()
+            for a, b in zip(want, out):
+                assert torch.equal(a, b)
+    del scratch
