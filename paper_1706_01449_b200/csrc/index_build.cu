@@ -305,14 +305,16 @@ __global__ void __launch_bounds__(128) bounds_kernel(const double* __restrict__ 
 }
 
 // theta_b: per-user angle to its centroid, atomic max on the (non-negative) bits.
+// unit_centers[c, k] = centers[c, k] / ||c|| is divided once per centre
+// (unit_centers_kernel) instead of once per user: the same quotients.
 __global__ void max_angles_kernel(const double* __restrict__ users, int64_t n, int f,
-                                  const double* __restrict__ centers, const double* __restrict__ cnorm,
+                                  const double* __restrict__ unit_centers, const double* __restrict__ cnorm,
                                   const int64_t* __restrict__ assign, unsigned long long* __restrict__ theta_bits) {
   int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n) return;
   const int64_t c = assign[u];
   const double* x = users + u * f;
-  const double* y = centers + c * f;
+  const double* y = unit_centers + c * f;
   const double cn = cnorm[c];
   double s = 0.0;
   for (int k = 0; k < f; ++k) s = fma(x[k], x[k], s);
@@ -323,7 +325,7 @@ __global__ void max_angles_kernel(const double* __restrict__ users, int64_t n, i
   } else {
     double dm = 0.0, dp = 0.0;
     for (int k = 0; k < f; ++k) {
-      double xk = x[k] / un, yk = y[k] / cn;
+      double xk = x[k] / un, yk = y[k];
       double a = xk - yk, b = xk + yk;
       dm = fma(a, a, dm);
       dp = fma(b, b, dp);
@@ -331,6 +333,14 @@ __global__ void max_angles_kernel(const double* __restrict__ users, int64_t n, i
     ang = 2.0 * atan2(sqrt(dm), sqrt(dp));
   }
   atomicMax(theta_bits + c, (unsigned long long)__double_as_longlong(ang));
+}
+
+__global__ void unit_centers_kernel(const double* __restrict__ centers, const double* __restrict__ cnorm, int64_t c,
+                                    int f, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= c * f) return;
+  const double cn = cnorm[t / f];
+  out[t] = cn == 0.0 ? 0.0 : centers[t] / cn;
 }
 
 // pos[c, list_ids[c, j]] = j  (inverse permutation of every cluster's list)
@@ -462,8 +472,12 @@ extern "C" int simdex_max_angles(const double* users, int64_t n, int32_t f, cons
   SIMDEX_CUDA(cn.alloc(c, s));
   center_norms_kernel<<<(unsigned)ceil_div(c, 128), 128, 0, s>>>(centers, c, f, cn.p);
   SIMDEX_LAUNCH_CHECK("center_norms");
+  Scratch<double> unit;
+  SIMDEX_CUDA(unit.alloc((size_t)c * f, s));
+  unit_centers_kernel<<<(unsigned)ceil_div((int64_t)c * f, 256), 256, 0, s>>>(centers, cn.p, c, f, unit.p);
+  SIMDEX_LAUNCH_CHECK("unit_centers");
   SIMDEX_CUDA(cudaMemsetAsync(out_theta, 0, sizeof(double) * c, s));
-  max_angles_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(users, n, f, centers, cn.p, assign,
+  max_angles_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(users, n, f, unit.p, cn.p, assign,
                                                                reinterpret_cast<unsigned long long*>(out_theta));
   SIMDEX_LAUNCH_CHECK("max_angles");
   return SIMDEX_OK;
