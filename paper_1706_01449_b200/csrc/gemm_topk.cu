@@ -84,6 +84,9 @@ using namespace sm100;
 #ifndef SIMDEX_FIN_TWO
 #define SIMDEX_FIN_TWO 1
 #endif
+#ifndef SIMDEX_FIN_COOP
+#define SIMDEX_FIN_COOP 1
+#endif
 #ifndef SIMDEX_FIN_ITEMS64
 #define SIMDEX_FIN_ITEMS64 0
 #endif
@@ -899,6 +902,7 @@ struct FinalizeParams {
   int64_t* over_out;
   int32_t* over_n;
   int pow2;
+  int coop;  // cooperative rescoring (finalize_coop())
   // list-order catalogue pass (full-list mode): candidate positions are list
   // positions from list_off on, and the row's prefix top-K (already in
   // out_ids, exact) joins the candidates; prefix rows whose band overflowed
@@ -1012,7 +1016,16 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
   if (__all_sync(0xffffffffu, !act)) return;
   int np2 = 2;
   while (np2 < cmax) np2 <<= 1;
-  if (act) {
+  // cooperative rescoring (narrow rows, exact float32 copies): the 8 lanes of a
+  // row share each candidate's item row -- every lane keeps its own factor
+  // pairs of the user row in registers and reads the same pairs of the item
+  // row, so a warp's gather touches 4 lines per load instead of up to 32 (the
+  // kernel is bound by the L1 data pipe) -- and the 8 partial sums of a
+  // candidate meet in the row's shared-memory block (the user row is not
+  // staged there in this mode)
+  const bool coop = SIMDEX_FIN_COOP && p.coop && LPR == 8 && p.mode != kAssign && p.items32 && p.users32 &&
+                    (p.f & 1) == 0 && p.f <= 64 && p.f >= 36;
+  if (act && !coop) {
     if (p.users32 && (p.f & 1) == 0) {  // two factors per load (rows of an even f are 8-byte aligned)
       const float2* u2 = reinterpret_cast<const float2*>(p.users32 + user * p.f);
       for (int i = gl; i < p.f / 2; i += LPR) {
@@ -1136,10 +1149,54 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
   // group: one lane per candidate (two partial sums over the even / odd
   // factors, so identical rows still score identically); otherwise LPR/8
   // candidates per round, 8 lanes each (strided partials + xor tree)
-  const bool lane_per_cand = p.f <= 64 && cmax2 > LPR / 2;
+  if (coop) {
+    // this lane's factor pairs: float2 index v = 8 i + gl, i = 0..3
+    double2 uu[4];
+    {
+      const float2* u2 = reinterpret_cast<const float2*>(p.users32 + (act ? user : 0) * p.f);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int v = 8 * i + gl;
+        const float2 t = (act && 2 * v < p.f) ? u2[v] : make_float2(0.f, 0.f);
+        uu[i] = make_double2((double)t.x, (double)t.y);
+      }
+    }
+    double* part = us;  // [4 candidates][9]: 36 doubles of the (unused) user-row block
+    for (int base = 0; base < cmax2; base += 4) {
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int e = base + c4;
+        double a0 = 0.0, a1 = 0.0;
+        if (act && e < cnt) {
+          const float2* x2 = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[e] * p.f);
+          float2 xv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) xv[i] = 2 * (8 * i + gl) < p.f ? x2[8 * i + gl] : make_float2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            a0 = fma((double)xv[i].x, uu[i].x, a0);
+            a1 = fma((double)xv[i].y, uu[i].y, a1);
+          }
+        }
+        part[c4 * 9 + gl] = a0 + a1;
+      }
+      __syncwarp();
+      if (gl < 4) {  // lane c4 adds the candidate's 8 partials in lane order
+        const int e = base + gl;
+        if (act && e < cnt) {
+          double t = part[gl * 9];
+#pragma unroll
+          for (int j = 1; j < 8; ++j) t += part[gl * 9 + j];
+          ss[e] = t;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  const bool lane_per_cand = !coop && p.f <= 64 && cmax2 > LPR / 2;
   constexpr int SG = LPR / 8;
   const int sg = gl >> 3, sl = gl & 7;
-  for (int base = 0; base < (lane_per_cand ? 0 : cmax2); base += SG) {
+  for (int base = 0; base < (lane_per_cand || coop ? 0 : cmax2); base += SG) {
     const int e = base + sg;
     double part = 0.0;
     if (act && e < cnt) {
@@ -1998,6 +2055,16 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   return p;
 }
 
+// Cooperative rescoring pays when the kernel is bound by the L1 data pipe --
+// a catalogue whose hot rows stay in L1 (cfg2: 3.5 MB of float32 rows; -6 %
+// at K = 10, -14 % at K = 1) -- or when a row has only a few survivors (a lane
+// per candidate then idles most lanes: cfg4 K = 1 -16 %); with a large
+// catalogue and a dozen survivors the batches of four candidates serialise
+// L2 latency (cfg4 K = 10: +5 %), and a lane per candidate stays.
+int finalize_coop(int64_t ni, int f, int k_eff) {
+  return (k_eff <= 4 || (int64_t)ni * f * 4 <= (int64_t(8) << 20)) ? 1 : 0;
+}
+
 int pow2_at_least(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -2166,6 +2233,7 @@ int gemm_topk_brute(const double* users, const float* users32, const uint16_t* u
   fp.over_n = over_n;
   fp.item_perm = item_perm;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
+  fp.coop = finalize_coop(ni, f, k_eff);
   if ((rc = launch_finalize(fp, nu, "finalize", s))) return rc;
   if ((rc = record_fallback_count(ctx, over_n, s))) return rc;
   if ((rc = record_pairs(ctx, pairs, s))) return rc;
@@ -2432,6 +2500,7 @@ int gemm_topk_ws(const double* users, const float* users32, const uint16_t* ub, 
   fp.over_out = over_out;
   fp.over_n = over_n;
   fp.pow2 = pow2_at_least(std::min(st.cap, std::max(64, 2 * k_eff + 32)));
+  fp.coop = finalize_coop(ni, f, k_eff);
   if (list2) {
     SIMDEX_CUDA(cudaMemsetAsync(rows2_n, 0, 4 * sizeof(int32_t), s));
     over1_n = rows2_n + 1;
