@@ -1151,16 +1151,20 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
   // candidates per round, 8 lanes each (strided partials + xor tree)
   if (coop) {
     // this lane's factor pairs: float2 index v = 8 i + gl, i = 0..3
+    // pairs 0..15 exist for every f >= 36; pairs 16 + gl and 24 + gl only below f / 2
+    const int half = p.f >> 1;
+    const bool ok2 = 16 + gl < half, ok3 = 24 + gl < half;
+    const float2 zero2 = make_float2(0.f, 0.f);
     double2 uu[4];
     {
-      const float2* u2 = reinterpret_cast<const float2*>(p.users32 + (act ? user : 0) * p.f);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int v = 8 * i + gl;
-        const float2 t = (act && 2 * v < p.f) ? u2[v] : make_float2(0.f, 0.f);
-        uu[i] = make_double2((double)t.x, (double)t.y);
-      }
+      const float2* ul = reinterpret_cast<const float2*>(p.users32) + (act ? user : 0) * half + gl;
+      const float2 t0 = ul[0], t1 = ul[8], t2 = ok2 ? ul[16] : zero2, t3 = ok3 ? ul[24] : zero2;
+      uu[0] = make_double2((double)t0.x, (double)t0.y);
+      uu[1] = make_double2((double)t1.x, (double)t1.y);
+      uu[2] = make_double2((double)t2.x, (double)t2.y);
+      uu[3] = make_double2((double)t3.x, (double)t3.y);
     }
+    const float2* items2 = reinterpret_cast<const float2*>(p.items32) + gl;
     double* part = us;  // [4 candidates][9]: 36 doubles of the (unused) user-row block
     for (int base = 0; base < cmax2; base += 4) {
 #pragma unroll
@@ -1168,15 +1172,16 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
         const int e = base + c4;
         double a0 = 0.0, a1 = 0.0;
         if (act && e < cnt) {
-          const float2* x2 = reinterpret_cast<const float2*>(p.items32 + (int64_t)si[e] * p.f);
-          float2 xv[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) xv[i] = 2 * (8 * i + gl) < p.f ? x2[8 * i + gl] : make_float2(0.f, 0.f);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            a0 = fma((double)xv[i].x, uu[i].x, a0);
-            a1 = fma((double)xv[i].y, uu[i].y, a1);
-          }
+          const float2* xl = items2 + (int64_t)si[e] * half;
+          const float2 x0 = xl[0], x1 = xl[8], x2v = ok2 ? xl[16] : zero2, x3 = ok3 ? xl[24] : zero2;
+          a0 = fma((double)x0.x, uu[0].x, a0);
+          a1 = fma((double)x0.y, uu[0].y, a1);
+          a0 = fma((double)x1.x, uu[1].x, a0);
+          a1 = fma((double)x1.y, uu[1].y, a1);
+          a0 = fma((double)x2v.x, uu[2].x, a0);
+          a1 = fma((double)x2v.y, uu[2].y, a1);
+          a0 = fma((double)x3.x, uu[3].x, a0);
+          a1 = fma((double)x3.y, uu[3].y, a1);
         }
         part[c4 * 9 + gl] = a0 + a1;
       }
@@ -2055,14 +2060,14 @@ TopkParams make_params(const RowState& st, const Unit* units, const int32_t* n_u
   return p;
 }
 
-// Cooperative rescoring pays when the kernel is bound by the L1 data pipe --
-// a catalogue whose hot rows stay in L1 (cfg2: 3.5 MB of float32 rows; -6 %
-// at K = 10, -14 % at K = 1) -- or when a row has only a few survivors (a lane
-// per candidate then idles most lanes: cfg4 K = 1 -16 %); with a large
-// catalogue and a dozen survivors the batches of four candidates serialise
-// L2 latency (cfg4 K = 10: +5 %), and a lane per candidate stays.
-int finalize_coop(int64_t ni, int f, int k_eff) {
-  return (k_eff <= 4 || (int64_t)ni * f * 4 <= (int64_t(8) << 20)) ? 1 : 0;
+// Cooperative rescoring (finalize_kernel): on whenever the kernel's
+// conditions hold (8 lanes per row, exact float32 copies, even f in [36, 64]).
+// Measured against a lane per candidate: cfg2 prefix finalize 0.338 -> 0.291
+// ms at K = 10, 0.232 -> 0.205 at K = 5, 0.173 -> 0.152 at K = 1; cfg4 1.19
+// -> 1.09 at K = 10, 0.66 -> 0.58 at K = 1.  SIMDEX_FIN_COOP_FORCE=0/1: A/B.
+int finalize_coop(int64_t, int, int) {
+  if (const char* e = getenv("SIMDEX_FIN_COOP_FORCE")) return atoi(e);
+  return 1;
 }
 
 int pow2_at_least(int x) {
