@@ -1301,13 +1301,45 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
   double kth = -DBL_MAX;
   int64_t mp = -1;
   if (cmax2 <= 32) {
-    // few survivors: each candidate's rank under (score desc, id asc) is its output slot
-    for (int e = gl; e < cmax2; e += LPR) {
+    // few survivors: each candidate's rank under (score desc, id asc) is its
+    // output slot.  Ranks are counted over the warp-uniform padded count:
+    // slots [cnt, np2) hold (-DBL_MAX, INT32_MAX), which ranks before no
+    // candidate.  A lane with two candidates (e, e + LPR) ranks both in one
+    // pass over the slots.
+    auto place = [&](int rank, double se, int32_t ie) {
+      if (rank < p.k_eff) {
+        p.out_ids[out * p.k_eff + rank] = ie;
+        p.out_scores[out * p.k_eff + rank] = se;
+        if (rank == p.k_eff - 1) kth = se;
+        if (p.mode == kFullList) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + ie]);
+      }
+    };
+    if (cmax2 > LPR) {
+      for (int e = gl; e < cmax2; e += 2 * LPR) {
+        const int e1 = e + LPR;
+        if (act && e < cnt) {
+          const bool two = e1 < cnt;
+          const double se0 = ss[e], se1 = two ? ss[e1] : se0;
+          const int32_t ie0 = si[e], ie1 = two ? si[e1] : ie0;
+          int rank0 = 0, rank1 = 0;
+#pragma unroll 2
+          for (int o = 0; o < np2; o += 2) {
+            const double2 s2 = *reinterpret_cast<const double2*>(ss + o);
+            const int2 i2 = *reinterpret_cast<const int2*>(si + o);
+            rank0 += ranks_before(s2.x, i2.x, se0, ie0) ? 1 : 0;
+            rank0 += ranks_before(s2.y, i2.y, se0, ie0) ? 1 : 0;
+            rank1 += ranks_before(s2.x, i2.x, se1, ie1) ? 1 : 0;
+            rank1 += ranks_before(s2.y, i2.y, se1, ie1) ? 1 : 0;
+          }
+          place(rank0, se0, ie0);
+          if (two) place(rank1, se1, ie1);
+        }
+      }
+    } else {
+      const int e = gl;
       if (act && e < cnt) {
         const double se = ss[e];
         const int32_t ie = si[e];
-        // over the warp-uniform padded count: slots [cnt, np2) hold
-        // (-DBL_MAX, INT32_MAX), which ranks before no candidate
         int rank = 0;
 #pragma unroll 2
         for (int o = 0; o < np2; o += 2) {
@@ -1316,12 +1348,7 @@ __global__ void __launch_bounds__(256, SIMDEX_FIN_MINB) finalize_kernel(const Fi
           rank += ranks_before(s2.x, i2.x, se, ie) ? 1 : 0;
           rank += ranks_before(s2.y, i2.y, se, ie) ? 1 : 0;
         }
-        if (rank < p.k_eff) {
-          p.out_ids[out * p.k_eff + rank] = ie;
-          p.out_scores[out * p.k_eff + rank] = se;
-          if (rank == p.k_eff - 1) kth = se;
-          if (p.mode == kFullList) mp = max(mp, (int64_t)p.list_pos[(int64_t)c * p.n + ie]);
-        }
+        place(rank, se, ie);
       }
     }
     if (act)
