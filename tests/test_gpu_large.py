@@ -263,3 +263,30 @@ def test_all_user_serve_with_overlapped_copies_equals_one_batch(sx):
     np.testing.assert_array_equal(res.scores, sc)
     np.testing.assert_array_equal(np.asarray(res.visited), vis)
     assert len(res) == nu and res[nu - 1].item_ids.tolist() == ids[-1].tolist()
+
+
+@pytest.mark.parametrize("f", [34, 36, 38, 46, 48, 50, 62, 64, 66])
+def test_cooperative_rescoring_factor_edges(sx, f):
+    """finalize's cooperative rescoring (8 lanes share a candidate's item row,
+    factor pairs 8 i + lane) at the edges of its range: f = 36..64 takes it,
+    with the third and fourth pair of a lane present or not; 34 and 66 do not.
+    Blocked product and work-sharing query against the exact float64 top-K,
+    K = 1, 3, 10, 20; inside the range every (user, item) score has one
+    arithmetic, so the two paths return bit-equal scores (outside it the
+    summation order follows the row's survivor count: last-bit differences)."""
+    from paper_1706_01449_b200 import index as I
+    rng = np.random.default_rng(100 + f)
+    nu, ni, c = 6000, 3000, 12
+    centers = rng.normal(size=(c, f))
+    users = (centers[rng.integers(0, c, nu)] + rng.normal(0, 0.5, (nu, f))).astype(np.float32).astype(np.float64)
+    items = (rng.normal(size=(ni, f)) * rng.lognormal(0, 0.4, (ni, 1))).astype(np.float32).astype(np.float64)
+    m = sx.ModelPair(sx.FactorMatrix(users), sx.FactorMatrix(items))
+    idx = sx.build_index(m, sx.kmeans(m.users, c, max_iters=3, seed=2), 512)
+    sample = np.arange(0, nu, 5)
+    for k in (1, 3, 10, 20):
+        b_ids, b_sc = (t.cpu().numpy() for t in sx.brute.topk_matmul_tensors(m, k)[:2])
+        _check(b_ids, b_sc, users, items, k, sample, f"brute f={f} K={k}")
+        ids, sc, _ = (t.cpu().numpy() for t in I.query_batch_tensors(idx, m, None, k))
+        _check(ids, sc, users, items, k, sample, f"index f={f} K={k}")
+        if 36 <= f <= 64:
+            np.testing.assert_array_equal(sc, b_sc)
